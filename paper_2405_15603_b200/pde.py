@@ -1,0 +1,314 @@
+"""Host-side problem catalog, collocation sampler and batch container.
+
+Mirror of `pkg/src/pinnopt/pde.py`.  These objects are *inputs* to the hot
+path: the device step only needs, per batch, the interior points, the boundary
+points/targets and — because every in-scope residual is affine in the network
+output triple — the residual at zero output ``r0(x)`` and the per-sample seed
+row ``[dr/du, dr/dgrad, dr/dLu]`` (see ``affine_residual_terms``).
+
+* ``PdeProblem`` / ``Batch``  ↔ pde.py:33-60 (same fields; duck-type compatible,
+  so the reference's own objects can be passed to ``optimizer_step``);
+* the six catalog problems     ↔ pde.py:67-276;
+* ``sample_batch``             ↔ pde.py:300-341, identical PCG64 draw order, so a
+  seeded batch is bit-identical to the reference's;
+* three BASELINE variants (configs c3/c4/c5 of BASELINE.json, which the
+  reference catalog does not contain verbatim): the 4+1-d heat
+  problem with the product-sine solution, the 10-d cosine-sum Poisson problem,
+  and the 100-d ``||x||^2 / 100`` Poisson problem.  Each reuses the parent
+  problem's residual/seed structure and only changes the solution and source.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable
+
+import numpy as np
+
+from .taylor import OperatorCoeffs
+
+__all__ = [
+    "PdeProblem",
+    "Batch",
+    "PROBLEM_NAMES",
+    "make_problem",
+    "sample_batch",
+    "affine_residual_terms",
+]
+
+
+@dataclass(frozen=True, eq=False)
+class PdeProblem:
+    name: str
+    dim: int
+    coeffs: OperatorCoeffs
+    lower: np.ndarray
+    upper: np.ndarray
+    boundary_kind: str  # "faces" | "heat" | "initial"
+    residual: Callable
+    residual_grads: Callable
+    boundary_target: Callable
+    true_solution: Callable
+
+
+@dataclass
+class Batch:
+    interior: np.ndarray          # (N, d)
+    boundary: np.ndarray          # (Nb, d)
+    boundary_targets: np.ndarray  # (Nb,)
+
+
+def _const_seed_grads(d: int, du: float, dgrad0: float, dop: float):
+    """``residual_grads`` of an affine residual with constant coefficients."""
+
+    def residual_grads(x, u, grad, op):
+        n = x.shape[0]
+        dg = np.zeros((n, d))
+        if dgrad0:
+            dg[:, 0] = dgrad0
+        return np.full(n, float(du)) if du else np.zeros(n), dg, np.full(n, float(dop))
+
+    return residual_grads
+
+
+def _poisson(name, d, solution, source, boundary_target=None):
+    """``-Lap u = f`` on the unit box; residual ``-Lu - f`` (pde.py:74-79 pattern)."""
+
+    def residual(x, u, grad, op):
+        return -op - source(x)
+
+    return PdeProblem(
+        name=name, dim=d, coeffs=OperatorCoeffs.laplacian(d),
+        lower=np.zeros(d), upper=np.ones(d), boundary_kind="faces",
+        residual=residual, residual_grads=_const_seed_grads(d, 0.0, 0.0, -1.0),
+        boundary_target=boundary_target if boundary_target is not None else solution,
+        true_solution=solution,
+    )
+
+
+def _poisson2d_sin() -> PdeProblem:
+    # pde.py:67-92 : u* = sin(pi x) sin(pi y), f = 2 pi^2 u*, zero boundary data
+    def sol(x):
+        return np.sin(np.pi * x[:, 0]) * np.sin(np.pi * x[:, 1])
+
+    def src(x):
+        return 2.0 * np.pi ** 2 * np.sin(np.pi * x[:, 0]) * np.sin(np.pi * x[:, 1])
+
+    return _poisson("poisson2d_sin", 2, sol, src, boundary_target=lambda x: np.zeros(x.shape[0]))
+
+
+def _poisson_cos_sum(dim: int = 5) -> PdeProblem:
+    # pde.py:95-121 (d = 5 there); dim = 10 is BASELINE config c4
+    d = int(dim)
+
+    def sol(x):
+        return np.cos(np.pi * x).sum(axis=1)
+
+    def src(x):
+        return np.pi ** 2 * np.cos(np.pi * x).sum(axis=1)
+
+    return _poisson("poisson_cos_sum", d, sol, src)
+
+
+def _poisson_harmonic_mixed() -> PdeProblem:
+    # pde.py:124-150 : harmonic u* = sum_k x_{2k-1} x_{2k} in d = 10, residual -Lu
+    d = 10
+
+    def sol(x):
+        return np.einsum("nk,nk->n", x[:, 0::2], x[:, 1::2])
+
+    def residual(x, u, grad, op):
+        return -op
+
+    return PdeProblem(
+        name="poisson_harmonic_mixed", dim=d, coeffs=OperatorCoeffs.laplacian(d),
+        lower=np.zeros(d), upper=np.ones(d), boundary_kind="faces",
+        residual=residual, residual_grads=_const_seed_grads(d, 0.0, 0.0, -1.0),
+        boundary_target=sol, true_solution=sol,
+    )
+
+
+def _poisson_norm2(dim: int = 100, divisor: float = 1.0) -> PdeProblem:
+    # pde.py:153-181 : u* = ||x||^2, -Lap u = -2d.  divisor = 100 with dim = 100
+    # is BASELINE config c5 (u* = ||x||^2 / 100, f = -2, residual -Lu + 2).
+    d = int(dim)
+    if d < 1:
+        raise ValueError(f"poisson_norm2 needs dim >= 1, got {dim}")
+    div = float(divisor)
+
+    def sol(x):
+        v = np.einsum("ni,ni->n", x, x)
+        return v if div == 1.0 else v / div
+
+    lap = 2.0 * d / div
+
+    def residual(x, u, grad, op):
+        return -op + lap
+
+    return PdeProblem(
+        name="poisson_norm2", dim=d, coeffs=OperatorCoeffs.laplacian(d),
+        lower=np.zeros(d), upper=np.ones(d), boundary_kind="faces",
+        residual=residual, residual_grads=_const_seed_grads(d, 0.0, 0.0, -1.0),
+        boundary_target=sol, true_solution=sol,
+    )
+
+
+def _heat(spatial_dim: int = 1, kappa: float = 0.25, solution: str = "catalog") -> PdeProblem:
+    # pde.py:184-231 : u_t = kappa Lap_x u on [0,1]^(1+s); residual u_t - kappa Lu.
+    # solution="sine_product" is BASELINE config c3: u* = exp(-pi^2 t) prod_i sin(pi x_i)
+    # (exact for kappa = 1/4, s = 4: kappa * (-4 pi^2) = -pi^2).
+    s = int(spatial_dim)
+    if solution == "catalog" and s not in (1, 4):
+        raise ValueError(f"heat supports spatial_dim in {{1, 4}}, got {spatial_dim}")
+    if kappa != 0.25:
+        raise ValueError("the catalog heat solutions require kappa = 1/4")
+    d = s + 1
+    if solution == "sine_product":
+        if s != 4:
+            raise ValueError("the sine-product heat solution is defined for spatial_dim = 4")
+
+        def sol(x):
+            return np.exp(-np.pi ** 2 * x[:, 0]) * np.prod(np.sin(np.pi * x[:, 1:]), axis=1)
+    elif s == 1:
+        def sol(x):
+            return np.exp(-np.pi ** 2 * x[:, 0] / 4.0) * np.sin(np.pi * x[:, 1])
+    else:
+        def sol(x):
+            return np.exp(-x[:, 0]) * np.sin(2.0 * x[:, 1:]).sum(axis=1)
+
+    def residual(x, u, grad, op):
+        return grad[:, 0] - kappa * op
+
+    return PdeProblem(
+        name="heat", dim=d, coeffs=OperatorCoeffs.partial_laplacian(d, range(1, d)),
+        lower=np.zeros(d), upper=np.ones(d), boundary_kind="heat",
+        residual=residual, residual_grads=_const_seed_grads(d, 0.0, 1.0, -kappa),
+        boundary_target=sol, true_solution=sol,
+    )
+
+
+def _log_fokker_planck() -> PdeProblem:
+    # pde.py:234-276 : nonlinear in grad u -> outside the device path (rejected there)
+    s = 9
+    d = s + 1
+    lower = np.concatenate([[0.0], np.full(s, -5.0)])
+    upper = np.concatenate([[1.0], np.full(s, 5.0)])
+
+    def sol(x):
+        var = 2.0 - np.exp(-x[:, 0])
+        sq = np.einsum("ni,ni->n", x[:, 1:], x[:, 1:])
+        return -0.5 * s * np.log(2.0 * np.pi * var) - sq / (2.0 * var)
+
+    def residual(x, u, grad, op):
+        gx = grad[:, 1:]
+        return (grad[:, 0] - 0.5 * s - 0.5 * np.einsum("ni,ni->n", gx, x[:, 1:])
+                - np.einsum("ni,ni->n", gx, gx) - op)
+
+    def residual_grads(x, u, grad, op):
+        n = x.shape[0]
+        dg = np.zeros((n, d))
+        dg[:, 0] = 1.0
+        dg[:, 1:] = -0.5 * x[:, 1:] - 2.0 * grad[:, 1:]
+        return np.zeros(n), dg, -np.ones(n)
+
+    return PdeProblem(
+        name="log_fokker_planck", dim=d, coeffs=OperatorCoeffs.partial_laplacian(d, range(1, d)),
+        lower=lower, upper=upper, boundary_kind="initial",
+        residual=residual, residual_grads=residual_grads,
+        boundary_target=sol, true_solution=sol,
+    )
+
+
+_FACTORIES = {
+    "poisson2d_sin": _poisson2d_sin,
+    "poisson_cos_sum": _poisson_cos_sum,
+    "poisson_harmonic_mixed": _poisson_harmonic_mixed,
+    "poisson_norm2": _poisson_norm2,
+    "heat": _heat,
+    "log_fokker_planck": _log_fokker_planck,
+}
+
+PROBLEM_NAMES = tuple(sorted(_FACTORIES))
+
+
+def make_problem(name: str, **params) -> PdeProblem:
+    """Catalog lookup (pde.py:291-297); extra keyword params where supported."""
+    if name not in _FACTORIES:
+        raise ValueError(f"unknown problem {name!r}; known: {', '.join(PROBLEM_NAMES)}")
+    return _FACTORIES[name](**params)
+
+
+def _face_points(gen, lo, hi, n):
+    """Uniform on the box faces: a face index first, then a uniform point (pde.py:300-308)."""
+    d = lo.size
+    face = gen.integers(0, 2 * d, size=n)
+    pts = gen.uniform(lo, hi, size=(n, d))
+    axis, upper_side = face // 2, face % 2
+    pts[np.arange(n), axis] = np.where(upper_side == 0, lo[axis], hi[axis])
+    return pts
+
+
+def sample_batch(problem, n_interior: int, n_boundary: int, seed: int) -> Batch:
+    """Seeded collocation batch, reference draw order (pde.py:311-341)."""
+    if n_interior < 1 or n_boundary < 1:
+        raise ValueError("need at least one interior and one boundary point")
+    gen = np.random.default_rng(seed)
+    lo, hi = np.asarray(problem.lower, float), np.asarray(problem.upper, float)
+    d = problem.dim
+    interior = gen.uniform(lo, hi, size=(n_interior, d))
+    kind = problem.boundary_kind
+    if kind == "faces":
+        bnd = _face_points(gen, lo, hi, n_boundary)
+    elif kind == "heat":
+        n_init = (n_boundary + 1) // 2
+        init = gen.uniform(lo, hi, size=(n_init, d))
+        init[:, 0] = 0.0
+        n_side = n_boundary - n_init
+        side = _face_points(gen, lo[1:], hi[1:], n_side)
+        t = gen.uniform(lo[0], hi[0], size=n_side)
+        bnd = np.concatenate([init, np.column_stack([t, side])], axis=0)
+    elif kind == "initial":
+        bnd = gen.uniform(lo, hi, size=(n_boundary, d))
+        bnd[:, 0] = 0.0
+    else:
+        raise ValueError(f"unknown boundary kind {kind!r}")
+    return Batch(interior, bnd, problem.boundary_target(bnd))
+
+
+def affine_residual_terms(problem, x, rtol: float = 1e-12):
+    """Split an affine interior residual into ``r0(x)`` and per-sample seeds.
+
+    Returns ``(r0, seeds)`` with ``r0[n] = residual(x_n, 0, 0, 0)`` and
+    ``seeds[n] = [dr/du, dr/dgrad_1..d, dr/dLu]`` from the problem's own
+    ``residual_grads`` (the reverse-pass seeds of optim.py:157-158).  Affinity is
+    verified at a random output triple; a residual that is not affine with
+    output-independent seeds (log-Fokker-Planck, pde.py:253-263) raises
+    ``NotImplementedError`` — the device path has no CPU fallback.
+    """
+    x = np.asarray(x, dtype=np.float64)
+    n, d = x.shape
+    zu, zg = np.zeros(n), np.zeros((n, d))
+    r0 = np.asarray(problem.residual(x, zu, zg, zu), dtype=np.float64)
+    du, dg, dop = problem.residual_grads(x, zu, zg, zu)
+    du = np.broadcast_to(np.asarray(du, np.float64), (n,))
+    dg = np.broadcast_to(np.asarray(dg, np.float64), (n, d))
+    dop = np.broadcast_to(np.asarray(dop, np.float64), (n,))
+    gen = np.random.default_rng(12345)
+    u1, g1, o1 = gen.standard_normal(n), gen.standard_normal((n, d)), gen.standard_normal(n)
+    du1, dg1, dop1 = problem.residual_grads(x, u1, g1, o1)
+    same = (np.array_equal(np.broadcast_to(du1, (n,)), du)
+            and np.array_equal(np.broadcast_to(dg1, (n, d)), dg)
+            and np.array_equal(np.broadcast_to(dop1, (n,)), dop))
+    r1 = np.asarray(problem.residual(x, u1, g1, o1), dtype=np.float64)
+    pred = r0 + du * u1 + np.einsum("ni,ni->n", dg, g1) + dop * o1
+    scale = np.maximum(np.abs(r1), 1.0)
+    if not same or not np.all(np.abs(r1 - pred) <= rtol * 1e3 * scale):
+        raise NotImplementedError(
+            f"problem {getattr(problem, 'name', '?')!r}: residual is not affine in "
+            "(u, grad u, Lu) with output-independent seeds; the device KFAC path "
+            "supports affine residuals only")
+    seeds = np.empty((n, d + 2))
+    seeds[:, 0] = du
+    seeds[:, 1:d + 1] = dg
+    seeds[:, d + 1] = dop
+    return np.ascontiguousarray(r0), seeds

@@ -1,0 +1,46 @@
+"""Helpers to compare arrays against the golden fixtures (full arrays or summaries)."""
+
+import os
+
+import numpy as np
+
+GOLDEN_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+NAMES = ("c1", "c2", "c3", "c4", "c5", "c1_momentum")
+
+
+def load(name):
+    return dict(np.load(os.path.join(GOLDEN_DIR, f"{name}.npz")))
+
+
+def has(g, key):
+    return key in g or f"{key}#sum" in g
+
+
+def max_rel(a, b):
+    """||a - b||_max / max(||b||_max, tiny) (SURVEY.md §8c parity measure)."""
+    a = np.asarray(a, dtype=np.float64).ravel()
+    b = np.asarray(b, dtype=np.float64).ravel()
+    assert a.shape == b.shape, (a.shape, b.shape)
+    den = max(float(np.max(np.abs(b))) if b.size else 0.0, 1e-300)
+    return float(np.max(np.abs(a - b))) / den if a.size else 0.0
+
+
+def compare(g, key, arr, rtol):
+    """Return the relative discrepancy of ``arr`` vs the golden entry ``key``."""
+    arr = np.asarray(arr, dtype=np.float64).ravel()
+    if key in g:
+        return max_rel(arr, g[key])
+    size = int(g[f"{key}#size"])
+    assert arr.size == size, (key, arr.size, size)
+    idx = g[f"{key}#idx"]
+    errs = [max_rel(arr[idx], g[f"{key}#vals"])]
+    for stat, val in (("abssum", np.abs(arr).sum()), ("sqsum", (arr * arr).sum())):
+        ref = float(g[f"{key}#{stat}"])
+        errs.append(abs(val - ref) / max(abs(ref), 1e-300))
+    scale = float(g[f"{key}#abssum"])
+    errs.append(abs(arr.sum() - float(g[f"{key}#sum"])) / max(scale, 1e-300))
+    return max(errs)
+
+
+def pack_factors(mats):
+    return np.concatenate([np.asarray(m, dtype=np.float64).ravel() for m in mats])

@@ -1,0 +1,64 @@
+"""Pin the CPU oracle (oracle/kfac_oracle.py) to golden vectors made by the reference.
+
+The fixtures come from running the reference implementation itself
+(tests/golden/make_golden.py).  Inputs are regenerated here from seeds by this
+package's host code, which also checks that the package reproduces the
+reference's seeded parameters and batches bit-for-bit.
+"""
+
+import numpy as np
+import pytest
+
+from golden_util import NAMES, compare, load, pack_factors
+from oracle import kfac_oracle as orc
+from paper_2405_15603_b200 import configs as cfgs
+from paper_2405_15603_b200.network import params_to_vec
+
+WL_OF = {"c1": "c1", "c2": "c2", "c3": "c3", "c4": "c4", "c5": "c5", "c1_momentum": "c1"}
+
+
+def build(name):
+    g = load(name)
+    wl = cfgs.WORKLOADS[WL_OF[name]]
+    prob, params, batch = wl.build(0, int(g["n_interior"]), int(g["n_boundary"]))
+    return g, wl, prob, params, batch
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_inputs_bit_identical_to_reference(name):
+    g, wl, prob, params, batch = build(name)
+    assert compare(g, "in/interior", batch.interior, 0) == 0.0
+    assert compare(g, "in/boundary", batch.boundary, 0) == 0.0
+    assert compare(g, "in/targets", batch.boundary_targets, 0) == 0.0
+    assert compare(g, "in/theta", params_to_vec(params), 0) == 0.0
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_oracle_matches_reference_steps(name):
+    g, wl, prob, params, batch = build(name)
+    st = orc.init_state(params.weights, params.biases, ema=float(g["ema"]),
+                        damping=float(g["damping"]), momentum=float(g["momentum"]))
+    t = 1
+    while f"s{t}/alpha" in g:
+        rec = {}
+        alpha, mu, li, lb = orc.kfac_step(st, batch, prob, record=rec)
+        p = f"s{t}/"
+        tol = 1e-10 if t == 1 else 1e-8
+        assert alpha == float(g[p + "alpha"])
+        assert abs(li - float(g[p + "loss_interior"])) <= tol * abs(float(g[p + "loss_interior"]))
+        assert abs(lb - float(g[p + "loss_boundary"])) <= tol * abs(float(g[p + "loss_boundary"]))
+        ls = np.asarray(rec["ls_losses"])
+        assert np.max(np.abs(ls - g[p + "ls_losses"]) / np.maximum(np.abs(g[p + "ls_losses"]), 1e-300)) <= tol
+        from paper_2405_15603_b200.network import mats_to_vec
+        assert compare(g, p + "grad", mats_to_vec(rec["grad_mats"]), tol) <= tol
+        assert compare(g, p + "delta", mats_to_vec(rec["delta"]), tol) <= tol
+        theta = np.concatenate([np.hstack([w, b[:, None]]).ravel(order="F")
+                                for w, b in zip(st.weights, st.biases)])
+        assert compare(g, p + "theta", theta, tol) <= tol
+        assert compare(g, p + "prev_update", mats_to_vec(st.prev_update), tol) <= tol
+        kf = st.kfac
+        for key, mats in (("a_interior", kf.a_int), ("b_interior", kf.b_int),
+                          ("a_boundary", kf.a_bnd), ("b_boundary", kf.b_bnd)):
+            assert compare(g, p + key, pack_factors(mats), tol) <= tol, key
+        t += 1
+    assert t > 1
