@@ -1,0 +1,74 @@
+// Shared device helpers for the KFAC-PINN sm_100a kernels (FP64 throughout).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define KP_CUDA_TRY(expr)                                   \
+  do {                                                      \
+    cudaError_t e__ = (expr);                               \
+    if (e__ != cudaSuccess) return kp::fail_cuda(e__, #expr, __FILE__, __LINE__); \
+  } while (0)
+
+namespace kp {
+
+int fail_cuda(cudaError_t e, const char* what, const char* file, int line);
+
+constexpr int kWarp = 32;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// 8-byte async global->shared copy; zero-fills when !pred (src-size 0).
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool pred) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_addr(dst)), "l"(src),
+               "r"(pred ? 8 : 0));
+}
+
+// 16-byte async copy (cg: bypass L1), zero-fill when !pred.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool pred) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_addr(dst)), "l"(src),
+               "r"(pred ? 16 : 0));
+}
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// FP64 tensor-core MMA: D(8x8) += A(8x4, row) * B(4x8, col); lowers to SASS DMMA.8x8x4.
+// Fragments (PTX ISA, mma.m8n8k4 .f64): a = A[lane/4][lane%4], b = B[lane%4][lane/4],
+// c = {C[lane/4][2*(lane%4)], C[lane/4][2*(lane%4)+1]}.
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// tanh and its derivatives s1 = 1 - s0^2, s2 = -2 s0 s1, s3 = -2 s1^2 - 2 s0 s2
+// (reference src/network.py:54-62; same operation order).
+struct TanhD {
+  double s0, s1, s2, s3;
+};
+
+__device__ __forceinline__ TanhD tanh_derivs(double z, bool third) {
+  TanhD t;
+  t.s0 = tanh(z);
+  t.s1 = 1.0 - t.s0 * t.s0;
+  t.s2 = -2.0 * t.s0 * t.s1;
+  t.s3 = third ? (-2.0 * t.s1 * t.s1 - 2.0 * t.s0 * t.s2) : 0.0;
+  return t;
+}
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace kp

@@ -1,0 +1,129 @@
+// Internal launcher interfaces shared by the kernel translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace kp {
+
+// Host-side count of this library's kernel launches (reported as gpu_launches).
+void count_launch();
+int64_t launch_count();
+
+// ---- FP64 DMMA GEMMs (kp_gemm.cu) -----------------------------------------
+
+// C[M,N] = A[M,K] * B[N,K]^T  (+ bias[n * bias_stride] on rows m with m % S == 0).
+struct GemmNT {
+  const double* A;
+  int64_t lda;
+  const double* B;
+  int64_t ldb;
+  double* C;
+  int64_t ldc;
+  int64_t M;
+  int N;
+  int K;
+  const double* bias;
+  int64_t bias_stride;
+  int S;
+};
+void launch_gemm_nt(const GemmNT& g, cudaStream_t s);
+
+// Row reduction C[p,q] = sum_r Xh[r,p] * w(r) * Yh[r,q] over rows [0,R), split into
+// `splits` row ranges whose partial tiles go to partial[split][P][Q]; then
+// acc[p][q] += sum_split partial (fixed order -> deterministic).
+// Xh = [X | bias] where the virtual bias column (index nx) is 1 on rows r % S == 0.
+// w(r) = w[r / Sw] when w != nullptr.  sym: X == Y, only lower-triangle tiles are
+// computed and acc holds a valid lower triangle.
+struct GemmTN {
+  const double* X;
+  int64_t ldx;
+  int nx;
+  bool x_bias;
+  const double* Y;
+  int64_t ldy;
+  int ny;
+  bool y_bias;
+  const double* w;
+  int Sw;
+  int S;  // bias-row period
+  int64_t R;
+  bool sym;
+};
+size_t gemm_tn_partial_doubles(int64_t R, int P, int Q, bool sym);
+void launch_gemm_tn_accumulate(const GemmTN& g, double* partial, double* acc, cudaStream_t s);
+
+// ---- Taylor-mode elementwise kernels (kp_taylor.cu) ------------------------
+
+struct TaylorDims {
+  int S;       // rows per sample: d + 2 (Taylor) or 1 (plain)
+  int d;       // derivative rows (0 for plain)
+  bool taylor; // operator row present
+};
+
+// Layer 0 fused with its activation: pre-activation value z = x W0^T + b0 -> zval,
+// post-activation state (n*S x h1) -> post.  Derivative rows of the pre-activation
+// are W0[:, i] and its operator row is 0 (reference taylor.py:124-131).
+void launch_first_layer(const double* x, int64_t n, int d, const double* theta0, int h1,
+                        TaylorDims td, const double* cdiag, double* zval, double* post,
+                        cudaStream_t s);
+// Taylor activation (taylor.py:151-169): pre (n*S x h) -> post.
+void launch_act_fwd(const double* pre, double* post, int64_t n, int h, TaylorDims td,
+                    const double* cdiag, cudaStream_t s);
+// Scalar output + residual: u_{n,s} = post[n*S+s,:] . w + (s==0) b;
+// taylor: r_n = r0_n + sum_s seeds[n,s] u_{n,s};  plain: r_n = u_n - target_n.
+void launch_last_layer(const double* post, int64_t n, int h, const double* theta_last,
+                       TaylorDims td, const double* r0, const double* seeds,
+                       const double* targets, double* r, double* u_out, cudaStream_t s);
+// Adjoint of the Taylor activation (taylor.py:206-239).  Pre-activation either a
+// stored state `pre` or (layer 0) zval + W0.  gin either a stored adjoint or the
+// rank-1 seeds (x) w_last (first reverse step, taylor.py:262,271).
+struct ActBwd {
+  const double* pre;      // n*S x h (nullptr -> use zval/theta0)
+  const double* zval;     // n x h
+  const double* theta0;   // [W0 | b0] rows of length d + 1
+  const double* gin;      // n*S x h (nullptr -> rank-1)
+  const double* seeds;    // n*S (rank-1; nullptr -> ones)
+  const double* wlast;    // h (rank-1)
+  double* gout;           // n*S x h
+};
+void launch_act_bwd(const ActBwd& a, int64_t n, int h, TaylorDims td, const double* cdiag,
+                    cudaStream_t s);
+// Layer-0 gradient, derivative-row part: acc[j*(d+1)+i] += sum_n r_n gbar0[n, 1+i, j].
+void launch_grad0_deriv(const double* gbar0, const double* r, int64_t n, int d, int h1,
+                        double* acc, cudaStream_t s);
+// Batched deterministic sum of squares: out[k] = sum_i v[k*stride + i]^2, i < n.
+void launch_sumsq(const double* v, int64_t n, int64_t stride, int nvec, double* out,
+                  int64_t out_stride, cudaStream_t s);
+void launch_transpose(const double* src, int64_t lds, int rows, int cols, double* dst,
+                      cudaStream_t s);
+void launch_fill(double* p, int64_t n, double v, cudaStream_t s);
+// u (n x S) -> value (n), grad (n x d), op (n)
+void launch_split_u(const double* u, int64_t n, int d, double* value, double* grad, double* op,
+                    cudaStream_t s);
+// initial_state (taylor.py:124-131): z (n*S x d) = [x; I; 0]
+void launch_initial_state(const double* x, int64_t n, int d, double* z, cudaStream_t s);
+
+// ---- optimizer bookkeeping (kp_optim.cu) ------------------------------------
+void launch_factor_finalize(const double* acc, double* F, int n, double scale, double ema,
+                            int diag_n, double diag_add, cudaStream_t s);
+void launch_grad_finalize(const double* gi, const double* gb, double ni, double nb,
+                          double* grad, int64_t D, cudaStream_t s);
+void launch_axpy_out(const double* x, const double* y, double a, double* out, int64_t n,
+                     cudaStream_t s);  // out = x + a*y
+void launch_losses(const double* sums, double ni, double nb, double* scalars, cudaStream_t s);
+void launch_candidate(const double* theta, const double* dir, int exp2, double* out, int64_t D,
+                      cudaStream_t s);
+void launch_argmin_update(const double* ls_sums, int ncand, int min_exp, double ni, double nb,
+                          double* theta, double* prev, const double* dir, int64_t D,
+                          double* scalars, double* ls_losses, int32_t* status, double mu,
+                          cudaStream_t s);
+void launch_damped_copy(const double* F, double lam, int n, double* out, cudaStream_t s);
+void launch_eig_status(const double* la, int p, const double* lb, int q, const int* info,
+                       int32_t* status, cudaStream_t s);
+void launch_kron_scale(double* W, const double* la, int p, const double* lb, int q,
+                       cudaStream_t s);
+void launch_set_status(int32_t* status, int32_t code, cudaStream_t s);
+void launch_identity(double* F, int n, double v, cudaStream_t s);
+
+}  // namespace kp

@@ -1,0 +1,232 @@
+// Optimizer bookkeeping kernels: factor EMA, gradient/direction assembly,
+// line-search candidates, device-side grid argmin and parameter update.
+//
+// References (src/ = /root/reference/pkg/src/pinnopt):
+//   factor EMA          src/curvature.py:79-85, 112-117, 133-136
+//   gradient weights    src/optim.py:164-177
+//   direction           src/optim.py:254 (Delta + momentum * prev_update)
+//   line search         src/optim.py:195-211 (ascending grid, finite, strict <)
+//   update              src/optim.py:260-262, non-finite check :398-401
+#include <algorithm>
+
+#include "../../include/kfac_pinn_b200.h"
+#include "kp_common.cuh"
+#include "kp_internal.h"
+
+namespace kp {
+
+static inline unsigned grid1(int64_t n, int t = 256) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, t), 148LL * 32));
+}
+
+__device__ __forceinline__ void set_status(int32_t* status, int32_t code) {
+  atomicCAS(status, 0, code);
+}
+
+// new = lower(acc) (+ diag_add on the first diag_n diagonal entries) / scale;
+// F = ema * F + (1 - ema) * new.  `acc` holds a valid lower triangle.
+__global__ void k_factor_finalize(const double* __restrict__ acc, double* __restrict__ F, int n,
+                                  double scale, double ema, int diag_n, double diag_add) {
+  const int64_t total = (int64_t)n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / n), j = (int)(e % n);
+    const int a = max(i, j), b = min(i, j);
+    double v = acc[(int64_t)a * n + b];
+    if (i == j && i < diag_n) v += diag_add;
+    const double nw = v / scale;
+    F[e] = ema * F[e] + (1.0 - ema) * nw;
+  }
+}
+
+void launch_factor_finalize(const double* acc, double* F, int n, double scale, double ema,
+                            int diag_n, double diag_add, cudaStream_t s) {
+  count_launch();
+  k_factor_finalize<<<grid1((int64_t)n * n), 256, 0, s>>>(acc, F, n, scale, ema, diag_n, diag_add);
+}
+
+__global__ void k_grad_finalize(const double* __restrict__ gi, const double* __restrict__ gb,
+                                double ni, double nb, double* __restrict__ grad, int64_t D) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < D;
+       e += (int64_t)gridDim.x * blockDim.x)
+    grad[e] = gi[e] / ni + gb[e] / nb;
+}
+
+void launch_grad_finalize(const double* gi, const double* gb, double ni, double nb, double* grad,
+                          int64_t D, cudaStream_t s) {
+  count_launch();
+  k_grad_finalize<<<grid1(D), 256, 0, s>>>(gi, gb, ni, nb, grad, D);
+}
+
+__global__ void k_axpy_out(const double* __restrict__ x, const double* __restrict__ y, double a,
+                           double* __restrict__ out, int64_t n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    out[e] = x[e] + a * y[e];
+}
+
+void launch_axpy_out(const double* x, const double* y, double a, double* out, int64_t n,
+                     cudaStream_t s) {
+  count_launch();
+  k_axpy_out<<<grid1(n), 256, 0, s>>>(x, y, a, out, n);
+}
+
+// scalars[0..1] = interior / boundary loss = sum r^2 / (2 N)  (pde.py:351, 359)
+__global__ void k_losses(const double* sums, double ni, double nb, double* scalars) {
+  scalars[0] = sums[0] / (2.0 * ni);
+  scalars[1] = sums[1] / (2.0 * nb);
+}
+
+void launch_losses(const double* sums, double ni, double nb, double* scalars, cudaStream_t s) {
+  count_launch();
+  k_losses<<<1, 1, 0, s>>>(sums, ni, nb, scalars);
+}
+
+// theta_c = theta + 2^e * dir  (add_scaled, network.py:299-305)
+__global__ void k_candidate(const double* __restrict__ th, const double* __restrict__ dir,
+                            double alpha, double* __restrict__ out, int64_t D) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < D;
+       e += (int64_t)gridDim.x * blockDim.x)
+    out[e] = th[e] + alpha * dir[e];
+}
+
+void launch_candidate(const double* theta, const double* dir, int exp2, double* out, int64_t D,
+                      cudaStream_t s) {
+  count_launch();
+  k_candidate<<<grid1(D), 256, 0, s>>>(theta, dir, ldexp(1.0, exp2), out, D);
+}
+
+// Grid argmin (optim.py:195-211) then theta += alpha dir, prev = alpha dir.
+__global__ void k_argmin(const double* __restrict__ ls_sums, int ncand, int min_exp, double ni,
+                         double nb, double* scalars, double* ls_losses, int32_t* status,
+                         double mu) {
+  double best = INFINITY;
+  int best_k = -1;
+  for (int k = 0; k < ncand; ++k) {
+    const double li = ls_sums[2 * k] / (2.0 * ni);
+    const double lb = ls_sums[2 * k + 1] / (2.0 * nb);
+    if (ls_losses) {
+      ls_losses[2 * k] = li;
+      ls_losses[2 * k + 1] = lb;
+    }
+    const double l = li + lb;
+    if (isfinite(l) && l < best) {
+      best = l;
+      best_k = k;
+    }
+  }
+  if (best_k < 0) {
+    set_status(status, KP_ERR_LINE_SEARCH);
+    scalars[2] = 0.0;
+  } else {
+    scalars[2] = ldexp(1.0, min_exp + best_k);
+  }
+  scalars[3] = mu;
+}
+
+__global__ void k_update(double* __restrict__ th, double* __restrict__ prev,
+                         const double* __restrict__ dir, int64_t D,
+                         const double* __restrict__ scalars, int32_t* status) {
+  if (*status != 0) return;  // failed line search: parameters untouched (reference raises)
+  const double alpha = scalars[2];
+  bool bad = false;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < D;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double v = th[e] + alpha * dir[e];
+    th[e] = v;
+    prev[e] = alpha * dir[e];
+    bad |= !isfinite(v);
+  }
+  if (bad) set_status(status, KP_ERR_NONFINITE);
+}
+
+void launch_argmin_update(const double* ls_sums, int ncand, int min_exp, double ni, double nb,
+                          double* theta, double* prev, const double* dir, int64_t D,
+                          double* scalars, double* ls_losses, int32_t* status, double mu,
+                          cudaStream_t s) {
+  count_launch();
+  k_argmin<<<1, 1, 0, s>>>(ls_sums, ncand, min_exp, ni, nb, scalars, ls_losses, status, mu);
+  count_launch();
+  k_update<<<grid1(D), 256, 0, s>>>(theta, prev, dir, D, scalars, status);
+}
+
+// out = F + lam I
+__global__ void k_damped_copy(const double* __restrict__ F, double lam, int n,
+                              double* __restrict__ out) {
+  const int64_t total = (int64_t)n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / n), j = (int)(e % n);
+    out[e] = F[e] + (i == j ? lam : 0.0);
+  }
+}
+
+void launch_damped_copy(const double* F, double lam, int n, double* out, cudaStream_t s) {
+  count_launch();
+  k_damped_copy<<<grid1((int64_t)n * n), 256, 0, s>>>(F, lam, n, out);
+}
+
+// Eigen-solver status: info > n -> second factor not PD (linalg.py:128-132);
+// 0 < info <= n -> no convergence; eigenvalues of the transformed first factor
+// below -PSD_TOL * max|lambda| -> not PSD (linalg.py:79-83, 165-166).
+__global__ void k_eig_status(const double* la, int p, const double* lb, int q, const int* info,
+                             int32_t* status) {
+  const double tol = 1e-6;
+  for (int k = 0; k < 2; ++k) {
+    const int n = k == 0 ? p : q;
+    if (info[k] > n) set_status(status, KP_ERR_NOT_PSD);
+    else if (info[k] != 0) set_status(status, KP_ERR_EIG);
+  }
+  const double* ls[2] = {la, lb};
+  const int ns[2] = {p, q};
+  for (int k = 0; k < 2; ++k) {
+    if (info[k] != 0) continue;
+    const double lo = ls[k][0], hi = ls[k][ns[k] - 1];
+    const double norm = fmax(fabs(lo), fabs(hi));
+    if (lo < -tol * fmax(norm, 1e-300)) set_status(status, KP_ERR_NOT_PSD);
+  }
+}
+
+void launch_eig_status(const double* la, int p, const double* lb, int q, const int* info,
+                       int32_t* status, cudaStream_t s) {
+  count_launch();
+  k_eig_status<<<1, 1, 0, s>>>(la, p, lb, q, info, status);
+}
+
+// W (p x q column-major) /= (lb_i la_j + 1)   (linalg.py:171)
+__global__ void k_kron_scale(double* W, const double* __restrict__ la, int p,
+                             const double* __restrict__ lb, int q) {
+  const int64_t total = (int64_t)p * q;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / p), j = (int)(e % p);
+    W[e] = W[e] / (lb[i] * la[j] + 1.0);
+  }
+}
+
+void launch_kron_scale(double* W, const double* la, int p, const double* lb, int q,
+                       cudaStream_t s) {
+  count_launch();
+  k_kron_scale<<<grid1((int64_t)p * q), 256, 0, s>>>(W, la, p, lb, q);
+}
+
+__global__ void k_set_status(int32_t* status, int32_t code) { set_status(status, code); }
+
+void launch_set_status(int32_t* status, int32_t code, cudaStream_t s) {
+  count_launch();
+  k_set_status<<<1, 1, 0, s>>>(status, code);
+}
+
+__global__ void k_identity(double* F, int n, double v) {
+  const int64_t total = (int64_t)n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x)
+    F[e] = (e / n == e % n) ? v : 0.0;
+}
+
+void launch_identity(double* F, int n, double v, cudaStream_t s) {
+  count_launch();
+  k_identity<<<grid1((int64_t)n * n), 256, 0, s>>>(F, n, v);
+}
+
+}  // namespace kp

@@ -1,0 +1,914 @@
+// KFAC step orchestration and the extern "C" boundary (include/kfac_pinn_b200.h).
+//
+// One KFAC step (reference src/optim.py:251-263) on the device, in four phases:
+//   1. accumulate  — chunked forward-Laplacian forward (taylor.py:172-203), affine
+//      residual, reverse pass (taylor.py:242-276), boundary plain MLP
+//      (network.py:200-232) and the UNNORMALISED sums of the interior/boundary
+//      factors (curvature.py:96-137), the residual-weighted gradient
+//      (optim.py:164-177) and sum r^2 — all into one contiguous reduce buffer
+//      (the only thing multi-GPU ranks must all-reduce).
+//   2. precondition — normalise + EMA, damped Kronecker-sum solve per layer
+//      (curvature.py:140-163 / linalg.py:136-174), direction = Delta + mu prev.
+//   3. line search — 31 forward-only passes at theta + 2^e dir (optim.py:195-211);
+//      per-candidate sums of r^2 into a second small buffer (all-reduce #2).
+//   4. update — device argmin (ascending grid, finite, strict <), theta += a dir,
+//      prev = a dir, non-finite check (optim.py:260-262, 398-401).
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "../../include/kfac_pinn_b200.h"
+#include "kp_common.cuh"
+#include "kp_internal.h"
+
+namespace kp {
+
+static std::atomic<int64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+int64_t launch_count() { return g_launches.load(); }
+
+int fail_cuda(cudaError_t e, const char* what, const char* file, int line) {
+  fprintf(stderr, "[kfac_pinn_b200] CUDA error %s in %s (%s:%d)\n", cudaGetErrorString(e), what,
+          file, line);
+  return KP_ERR_CUDA;
+}
+
+}  // namespace kp
+
+using namespace kp;
+
+struct kp_context {
+  int device = 0;
+  cusolverDnHandle_t solver = nullptr;
+  cublasHandle_t blas = nullptr;
+  bool profile = false;
+  std::vector<cudaEvent_t> ev;  // pairs
+  size_t ev_used = 0;
+  double prof_flops = 0.0;
+  int64_t prof_launches = 0;
+  double prof_ms_done = 0.0;
+};
+
+#define KP_SOLVER_TRY(expr)                                                          \
+  do {                                                                               \
+    cusolverStatus_t s__ = (expr);                                                   \
+    if (s__ != CUSOLVER_STATUS_SUCCESS) {                                            \
+      fprintf(stderr, "[kfac_pinn_b200] cuSOLVER status %d in %s\n", (int)s__, #expr); \
+      return KP_ERR_CUDA;                                                            \
+    }                                                                                \
+  } while (0)
+
+#define KP_BLAS_TRY(expr)                                                            \
+  do {                                                                               \
+    cublasStatus_t s__ = (expr);                                                     \
+    if (s__ != CUBLAS_STATUS_SUCCESS) {                                              \
+      fprintf(stderr, "[kfac_pinn_b200] cuBLAS status %d in %s\n", (int)s__, #expr);  \
+      return KP_ERR_CUDA;                                                            \
+    }                                                                                \
+  } while (0)
+
+#define KP_TRY(expr)          \
+  do {                        \
+    int r__ = (expr);         \
+    if (r__ != KP_OK) return r__; \
+  } while (0)
+
+namespace {
+
+constexpr int MAXL = KP_MAX_LAYERS;
+
+// Static description of the step: shapes, parameter/factor packing, workspace carve.
+struct Plan {
+  int L = 0, d = 0, S = 0, ncand = 0, maxh = 0, maxp = 0, maxq = 0;
+  int h[MAXL + 1] = {};
+  int p[MAXL] = {}, q[MAXL] = {};
+  int64_t N = 0, Nb = 0, Nc = 0;
+  int64_t D = 0, FA = 0, FB = 0;
+  int64_t th[MAXL] = {}, fa[MAXL] = {}, fb[MAXL] = {};
+  // workspace offsets, in doubles
+  int64_t o_wT[MAXL] = {}, o_zval0 = 0, o_post[MAXL] = {}, o_pre[MAXL] = {}, o_gout[MAXL] = {};
+  int64_t o_ping = 0, o_pong = 0;
+  int64_t o_bzval0 = 0, o_bpost[MAXL] = {}, o_bpre[MAXL] = {}, o_bg[MAXL] = {};
+  int64_t o_bping = 0, o_bpong = 0, o_ones = 0;
+  int64_t o_r = 0, o_rb = 0, o_rls = 0, o_rbls = 0, o_u = 0;
+  int64_t o_partial = 0, o_red = 0, o_grad = 0, o_delta = 0, o_dir = 0, o_thc = 0, o_ls = 0;
+  int64_t o_A1 = 0, o_A2 = 0, o_B1 = 0, o_B2 = 0, o_la = 0, o_lb = 0, o_T1 = 0, o_T2 = 0;
+  int64_t o_work = 0, o_info = 0;
+  int64_t lwork = 0;
+  int64_t total = 0;  // doubles
+  // reduce-buffer sub-offsets (relative to o_red)
+  int64_t r_aint = 0, r_bint = 0, r_abnd = 0, r_bbnd = 0, r_gint = 0, r_gbnd = 0, r_ss = 0,
+          r_count = 0;
+};
+
+int check_net(const kp_net* net) {
+  if (!net || net->n_layers < 1 || net->n_layers > MAXL) return KP_ERR_INVALID;
+  for (int l = 0; l <= net->n_layers; ++l)
+    if (net->widths[l] < 1) return KP_ERR_INVALID;
+  if (net->widths[net->n_layers] != 1) return KP_ERR_INVALID;
+  return KP_OK;
+}
+
+// Bytes of chunk-dependent workspace per interior point.
+int64_t per_point_doubles(const kp_net* net) {
+  const int L = net->n_layers, d = net->widths[0], S = d + 2;
+  int maxh = d;
+  for (int l = 1; l < L; ++l) maxh = std::max(maxh, net->widths[l]);
+  int64_t v = net->widths[1];  // zval0
+  for (int l = 1; l < L; ++l) v += (int64_t)S * net->widths[l];           // post
+  for (int l = 1; l + 1 < L; ++l) v += (int64_t)S * net->widths[l + 1];   // pre
+  for (int l = 0; l + 1 < L; ++l) v += (int64_t)S * net->widths[l + 1];   // gout
+  v += 2LL * S * maxh;                                                   // ping/pong
+  v += (int64_t)S;                                                       // u
+  return v;
+}
+
+int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
+  KP_TRY(check_net(&pr->net));
+  if (pr->n_interior < 1 || pr->n_boundary < 1 || pr->n_candidates < 1) return KP_ERR_INVALID;
+  P.L = pr->net.n_layers;
+  for (int l = 0; l <= P.L; ++l) P.h[l] = pr->net.widths[l];
+  P.d = P.h[0];
+  P.S = P.d + 2;
+  P.ncand = pr->n_candidates;
+  P.N = pr->n_interior;
+  P.Nb = pr->n_boundary;
+  P.Nc = (pr->chunk > 0 && pr->chunk < P.N) ? pr->chunk : P.N;
+  P.maxh = P.d;
+  for (int l = 1; l < P.L; ++l) P.maxh = std::max(P.maxh, P.h[l]);
+  int64_t off = 0;
+  for (int l = 0; l < P.L; ++l) {
+    P.p[l] = P.h[l] + 1;
+    P.q[l] = P.h[l + 1];
+    P.maxp = std::max(P.maxp, P.p[l]);
+    P.maxq = std::max(P.maxq, P.q[l]);
+    P.th[l] = off;
+    off += (int64_t)P.p[l] * P.q[l];
+  }
+  P.D = off;
+  for (int l = 0; l < P.L; ++l) {
+    P.fa[l] = P.FA;
+    P.FA += (int64_t)P.p[l] * P.p[l];
+    P.fb[l] = P.FB;
+    P.FB += (int64_t)P.q[l] * P.q[l];
+  }
+  const int64_t Mc = P.Nc * P.S;
+  int64_t o = 0;
+  auto take = [&](int64_t n) {
+    const int64_t at = o;
+    o += (n + 31) / 32 * 32;  // 256-byte alignment
+    return at;
+  };
+  for (int l = 1; l < P.L; ++l) P.o_wT[l] = take((int64_t)P.h[l] * P.q[l]);
+  P.o_zval0 = take(P.Nc * P.h[1]);
+  for (int l = 1; l < P.L; ++l) P.o_post[l] = take(Mc * P.h[l]);
+  for (int l = 1; l + 1 < P.L; ++l) P.o_pre[l] = take(Mc * P.h[l + 1]);
+  for (int l = 0; l + 1 < P.L; ++l) P.o_gout[l] = take(Mc * P.h[l + 1]);
+  P.o_ping = take(Mc * P.maxh);
+  P.o_pong = take(Mc * P.maxh);
+  P.o_u = take(Mc);
+  P.o_bzval0 = take(P.Nb * P.h[1]);
+  for (int l = 1; l < P.L; ++l) P.o_bpost[l] = take(P.Nb * P.h[l]);
+  for (int l = 1; l + 1 < P.L; ++l) P.o_bpre[l] = take(P.Nb * P.h[l + 1]);
+  for (int l = 0; l + 1 < P.L; ++l) P.o_bg[l] = take(P.Nb * P.h[l + 1]);
+  P.o_bping = take(P.Nb * P.maxh);
+  P.o_bpong = take(P.Nb * P.maxh);
+  P.o_ones = take(P.Nb);
+  P.o_r = take(P.N);
+  P.o_rb = take(P.Nb);
+  P.o_rls = take(P.N * P.ncand);
+  P.o_rbls = take(P.Nb * P.ncand);
+  // TN partial buffer: max over every contraction of a step
+  size_t part = 1;
+  auto upd = [&](int64_t R, int Pp, int Qq, bool sym) {
+    part = std::max(part, gemm_tn_partial_doubles(R, Pp, Qq, sym));
+  };
+  for (int64_t R : {P.Nc, P.Nb}) {
+    const bool interior = (R == P.Nc);
+    const int64_t rows = interior ? R * P.S : R;
+    for (int l = 0; l < P.L; ++l) {
+      upd(l == 0 ? R : rows, P.p[l], P.p[l], true);
+      upd(rows, P.q[l], P.q[l], true);
+      upd(l == 0 ? R : rows, P.q[l], P.p[l], false);
+    }
+  }
+  P.o_partial = take((int64_t)part);
+  P.r_aint = 0;
+  P.r_bint = P.r_aint + P.FA;
+  P.r_abnd = P.r_bint + P.FB;
+  P.r_bbnd = P.r_abnd + P.FA;
+  P.r_gint = P.r_bbnd + P.FB;
+  P.r_gbnd = P.r_gint + P.D;
+  P.r_ss = P.r_gbnd + P.D;
+  P.r_count = P.r_ss + 2;
+  P.o_red = take(P.r_count);
+  P.o_grad = take(P.D);
+  P.o_delta = take(P.D);
+  P.o_dir = take(P.D);
+  P.o_thc = take(P.D);
+  P.o_ls = take(2 * (int64_t)P.ncand);
+  P.o_A1 = take((int64_t)P.maxp * P.maxp);
+  P.o_A2 = take((int64_t)P.maxp * P.maxp);
+  P.o_B1 = take((int64_t)P.maxq * P.maxq);
+  P.o_B2 = take((int64_t)P.maxq * P.maxq);
+  P.o_la = take(P.maxp);
+  P.o_lb = take(P.maxq);
+  P.o_T1 = take((int64_t)P.maxp * P.maxq);
+  P.o_T2 = take((int64_t)P.maxp * P.maxq);
+  int lwork = 1;
+  for (int l = 0; l < P.L; ++l) {
+    for (int n : {P.p[l], P.q[l]}) {
+      int lw = 0;
+      KP_SOLVER_TRY(cusolverDnDsygvd_bufferSize(ctx->solver, CUSOLVER_EIG_TYPE_1,
+                                                CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
+                                                n, nullptr, n, nullptr, n, nullptr, &lw));
+      lwork = std::max(lwork, lw);
+    }
+  }
+  P.lwork = lwork;
+  P.o_work = take(lwork);
+  P.o_info = take(8);
+  P.total = o;
+  return KP_OK;
+}
+
+struct Ctx {
+  kp_context* ctx;
+  const Plan& P;
+  double* W;  // workspace base
+  cudaStream_t s;
+  double* at(int64_t off) const { return W + off; }
+};
+
+// Optional CUDA-event timing of the hidden-layer forward GEMMs.
+void prof_gemm(const Ctx& c, const GemmNT& g) {
+  kp_context* ctx = c.ctx;
+  if (!ctx->profile) {
+    launch_gemm_nt(g, c.s);
+    return;
+  }
+  if (ctx->ev_used + 2 > ctx->ev.size()) {
+    for (int k = 0; k < 64; ++k) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ctx->ev.push_back(e);
+    }
+  }
+  cudaEventRecord(ctx->ev[ctx->ev_used], c.s);
+  launch_gemm_nt(g, c.s);
+  cudaEventRecord(ctx->ev[ctx->ev_used + 1], c.s);
+  ctx->ev_used += 2;
+  ctx->prof_flops += 2.0 * (double)g.M * g.N * g.K;
+  ctx->prof_launches += 1;
+}
+
+struct StateBufs {
+  double* zval0;
+  double* post[MAXL];
+  double* pre[MAXL];
+  double* gout[MAXL];
+  double* ping;
+  double* pong;
+};
+
+StateBufs interior_bufs(const Ctx& c) {
+  const Plan& P = c.P;
+  StateBufs b{};
+  b.zval0 = c.at(P.o_zval0);
+  for (int l = 1; l < P.L; ++l) b.post[l] = c.at(P.o_post[l]);
+  for (int l = 1; l + 1 < P.L; ++l) b.pre[l] = c.at(P.o_pre[l]);
+  for (int l = 0; l + 1 < P.L; ++l) b.gout[l] = c.at(P.o_gout[l]);
+  b.ping = c.at(P.o_ping);
+  b.pong = c.at(P.o_pong);
+  return b;
+}
+
+StateBufs boundary_bufs(const Ctx& c) {
+  const Plan& P = c.P;
+  StateBufs b{};
+  b.zval0 = c.at(P.o_bzval0);
+  for (int l = 1; l < P.L; ++l) b.post[l] = c.at(P.o_bpost[l]);
+  for (int l = 1; l + 1 < P.L; ++l) b.pre[l] = c.at(P.o_bpre[l]);
+  for (int l = 0; l + 1 < P.L; ++l) b.gout[l] = c.at(P.o_bg[l]);
+  b.ping = c.at(P.o_bping);
+  b.pong = c.at(P.o_bpong);
+  return b;
+}
+
+// Residual definition for one pass (interior: affine residual; boundary: u - target).
+struct ResidualIn {
+  const double* r0;
+  const double* seeds;
+  const double* targets;
+};
+
+// Forward pass storing every state needed by the reverse pass (taylor.py:172-203;
+// boundary: network.py:200-213).  Writes residuals r[0..n).
+void forward_store(const Ctx& c, const double* theta, const double* x, int64_t n,
+                   const TaylorDims& td, const double* cdiag, const StateBufs& b,
+                   const ResidualIn& ri, double* r, double* u_out) {
+  const Plan& P = c.P;
+  const int L = P.L;
+  const double* last_in;
+  if (L == 1) {
+    if (td.taylor) {
+      launch_initial_state(x, n, P.d, b.ping, c.s);
+      last_in = b.ping;
+    } else {
+      last_in = x;
+    }
+  } else {
+    launch_first_layer(x, n, P.d, theta + P.th[0], P.h[1], td, cdiag, b.zval0, b.post[1], c.s);
+    for (int l = 1; l + 1 < L; ++l) {
+      GemmNT g{b.post[l], P.h[l], theta + P.th[l], P.p[l], b.pre[l], P.h[l + 1],
+               n * td.S, P.h[l + 1], P.h[l], theta + P.th[l] + P.h[l], P.p[l], td.S};
+      prof_gemm(c, g);
+      launch_act_fwd(b.pre[l], b.post[l + 1], n, P.h[l + 1], td, cdiag, c.s);
+    }
+    last_in = b.post[L - 1];
+  }
+  launch_last_layer(last_in, n, P.h[L - 1], theta + P.th[L - 1], td, ri.r0, ri.seeds, ri.targets,
+                    r, u_out, c.s);
+}
+
+// Forward pass for losses only (no stored states): ping-pong buffers, in-place activation.
+void forward_loss(const Ctx& c, const double* theta, const double* x, int64_t n,
+                  const TaylorDims& td, const double* cdiag, double* ping, double* pong,
+                  const ResidualIn& ri, double* r, double* u_out) {
+  const Plan& P = c.P;
+  const int L = P.L;
+  const double* cur;
+  if (L == 1) {
+    if (td.taylor) {
+      launch_initial_state(x, n, P.d, ping, c.s);
+      cur = ping;
+    } else {
+      cur = x;
+    }
+  } else {
+    launch_first_layer(x, n, P.d, theta + P.th[0], P.h[1], td, cdiag, nullptr, ping, c.s);
+    double* a = ping;
+    double* b = pong;
+    for (int l = 1; l + 1 < L; ++l) {
+      GemmNT g{a, P.h[l], theta + P.th[l], P.p[l], b, P.h[l + 1],
+               n * td.S, P.h[l + 1], P.h[l], theta + P.th[l] + P.h[l], P.p[l], td.S};
+      prof_gemm(c, g);
+      launch_act_fwd(b, b, n, P.h[l + 1], td, cdiag, c.s);
+      std::swap(a, b);
+    }
+    cur = a;
+  }
+  launch_last_layer(cur, n, P.h[L - 1], theta + P.th[L - 1], td, ri.r0, ri.seeds, ri.targets, r,
+                    u_out, c.s);
+}
+
+// Reverse pass (taylor.py:242-276 / network.py:216-232): gout[l] for l < L-1.
+void backward(const Ctx& c, const double* theta, int64_t n, const TaylorDims& td,
+              const double* cdiag, const StateBufs& b, const double* seeds) {
+  const Plan& P = c.P;
+  const int L = P.L;
+  if (L < 2) return;
+  {
+    ActBwd a{};
+    a.pre = (L - 2 == 0) ? nullptr : b.pre[L - 2];
+    a.zval = b.zval0;
+    a.theta0 = theta + P.th[0];
+    a.gin = nullptr;
+    a.seeds = seeds;
+    a.wlast = theta + P.th[L - 1];
+    a.gout = b.gout[L - 2];
+    launch_act_bwd(a, n, P.h[L - 1], td, cdiag, c.s);
+  }
+  for (int l = L - 2; l >= 1; --l) {
+    GemmNT g{b.gout[l], P.h[l + 1], c.at(P.o_wT[l]), P.h[l + 1], b.ping, P.h[l],
+             n * td.S, P.h[l], P.h[l + 1], nullptr, 0, td.S};
+    launch_gemm_nt(g, c.s);
+    ActBwd a{};
+    a.pre = (l - 1 == 0) ? nullptr : b.pre[l - 1];
+    a.zval = b.zval0;
+    a.theta0 = theta + P.th[0];
+    a.gin = b.ping;
+    a.gout = b.gout[l - 1];
+    launch_act_bwd(a, n, P.h[l], td, cdiag, c.s);
+  }
+}
+
+// Factor and gradient contractions of one pass into the reduce buffer.
+void accumulate(const Ctx& c, const double* x, int64_t n, const TaylorDims& td,
+                const StateBufs& b, const double* gl_last, const double* r, double* accA,
+                double* accB, double* accG) {
+  const Plan& P = c.P;
+  const int L = P.L;
+  double* part = c.at(P.o_partial);
+  const int64_t rows = n * td.S;
+  for (int l = 0; l < L; ++l) {
+    const int q = P.q[l];
+    const double* G = (l == L - 1) ? gl_last : b.gout[l];
+    // A_l = sum zhat zhat^T over the bias-augmented layer inputs (curvature.py:112-114)
+    if (l == 0) {
+      GemmTN a{x, P.d, P.d, true, x, P.d, P.d, true, nullptr, 1, 1, n, true};
+      launch_gemm_tn_accumulate(a, part, accA + P.fa[0], c.s);
+    } else {
+      GemmTN a{b.post[l], P.h[l], P.h[l], true, b.post[l], P.h[l], P.h[l], true, nullptr, 1,
+               td.S, rows, true};
+      launch_gemm_tn_accumulate(a, part, accA + P.fa[l], c.s);
+    }
+    // B_l = sum g g^T over all rows (curvature.py:113,115)
+    {
+      GemmTN bb{G, q, q, false, G, q, q, false, nullptr, 1, 1, rows, true};
+      launch_gemm_tn_accumulate(bb, part, accB + P.fb[l], c.s);
+    }
+    // gradient = sum_n r_n sum_s g_{n,s} zhat_{n,s}^T (optim.py:170-176)
+    if (l == 0) {
+      GemmTN gg{G, (int64_t)td.S * q, q, false, x, P.d, P.d, true, r, 1, 1, n, false};
+      launch_gemm_tn_accumulate(gg, part, accG + P.th[0], c.s);
+      if (td.taylor) launch_grad0_deriv(G, r, n, P.d, q, accG + P.th[0], c.s);
+    } else {
+      GemmTN gg{G, q, q, false, b.post[l], P.h[l], P.h[l], true, r, td.S, td.S, rows, false};
+      launch_gemm_tn_accumulate(gg, part, accG + P.th[l], c.s);
+    }
+  }
+}
+
+int phase_accumulate(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, const kp_batch* bt) {
+  const Plan& P = c.P;
+  double* red = c.at(P.o_red);
+  KP_CUDA_TRY(cudaMemsetAsync(red, 0, sizeof(double) * P.r_count, c.s));
+  for (int l = 1; l < P.L; ++l)
+    launch_transpose(st->theta + P.th[l], P.p[l], P.q[l], P.h[l], c.at(P.o_wT[l]), c.s);
+  const TaylorDims tdi{P.S, P.d, true};
+  const TaylorDims tdb{1, 0, false};
+  const StateBufs bi = interior_bufs(c);
+  for (int64_t n0 = 0; n0 < P.N; n0 += P.Nc) {
+    const int64_t nc = std::min(P.Nc, P.N - n0);
+    const double* x = bt->x_int + n0 * P.d;
+    const double* seeds = bt->seeds + n0 * P.S;
+    double* r = c.at(P.o_r) + n0;
+    ResidualIn ri{bt->r0 + n0, seeds, nullptr};
+    forward_store(c, st->theta, x, nc, tdi, bt->coeff_diag, bi, ri, r, nullptr);
+    backward(c, st->theta, nc, tdi, bt->coeff_diag, bi, seeds);
+    accumulate(c, x, nc, tdi, bi, seeds, r, red + P.r_aint, red + P.r_bint, red + P.r_gint);
+  }
+  const StateBufs bb = boundary_bufs(c);
+  double* ones = c.at(P.o_ones);
+  launch_fill(ones, P.Nb, 1.0, c.s);
+  ResidualIn rb{nullptr, nullptr, bt->targets};
+  forward_store(c, st->theta, bt->x_bnd, P.Nb, tdb, bt->coeff_diag, bb, rb, c.at(P.o_rb),
+                nullptr);
+  backward(c, st->theta, P.Nb, tdb, bt->coeff_diag, bb, nullptr);
+  accumulate(c, bt->x_bnd, P.Nb, tdb, bb, ones, c.at(P.o_rb), red + P.r_abnd, red + P.r_bbnd,
+             red + P.r_gbnd);
+  launch_sumsq(c.at(P.o_r), P.N, 0, 1, red + P.r_ss, 1, c.s);
+  launch_sumsq(c.at(P.o_rb), P.Nb, 0, 1, red + P.r_ss + 1, 1, c.s);
+  return KP_OK;
+}
+
+// Damped two-term Kronecker-sum solve for one layer (linalg.py:136-174) by the
+// generalised symmetric-definite eigenproblems A1 x = l A2 x, B1 y = m B2 y
+// (Cholesky of A2/B2 + eigh, cuSOLVER sygvd): with T_A^T A2 T_A = I,
+// T_A^T A1 T_A = diag(la) (likewise B), X = T_B [(T_B^T G T_A) / (lb la^T + 1)] T_A^T
+// solves B1 X A1 + B2 X A2 = G — the same unique solution as the reference's
+// inverse-square-root route.  Writes out = sign * X (q x p row-major).
+int kron_solve(kp_context* ctx, const Ctx& c, int p, int q, double* A1, double* A2, double* B1,
+               double* B2, const double* G, double* out, double sign, int* info,
+               int32_t* status) {
+  const Plan& P = c.P;
+  double* la = c.at(P.o_la);
+  double* lb = c.at(P.o_lb);
+  double* T1 = c.at(P.o_T1);
+  double* T2 = c.at(P.o_T2);
+  double* work = c.at(P.o_work);
+  KP_SOLVER_TRY(cusolverDnSetStream(ctx->solver, c.s));
+  KP_BLAS_TRY(cublasSetStream(ctx->blas, c.s));
+  KP_SOLVER_TRY(cusolverDnDsygvd(ctx->solver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
+                                 CUBLAS_FILL_MODE_LOWER, p, A1, p, A2, p, la, work,
+                                 (int)P.lwork, info));
+  KP_SOLVER_TRY(cusolverDnDsygvd(ctx->solver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
+                                 CUBLAS_FILL_MODE_LOWER, q, B1, q, B2, q, lb, work,
+                                 (int)P.lwork, info + 1));
+  launch_eig_status(la, p, lb, q, info, status, c.s);
+  // column-major views: G^T is p x q (ld p); T_A = A1 (p x p), T_B = B1 (q x q)
+  const double one = 1.0, zero = 0.0;
+  KP_BLAS_TRY(cublasDgemm(ctx->blas, CUBLAS_OP_N, CUBLAS_OP_N, p, q, q, &one, G, p, B1, q, &zero,
+                          T1, p));  // G^T T_B
+  KP_BLAS_TRY(cublasDgemm(ctx->blas, CUBLAS_OP_T, CUBLAS_OP_N, p, q, p, &one, A1, p, T1, p, &zero,
+                          T2, p));  // (T_B^T G T_A)^T
+  launch_kron_scale(T2, la, p, lb, q, c.s);
+  KP_BLAS_TRY(cublasDgemm(ctx->blas, CUBLAS_OP_N, CUBLAS_OP_T, p, q, q, &one, T2, p, B1, q, &zero,
+                          T1, p));  // Y^T T_B^T
+  KP_BLAS_TRY(cublasDgemm(ctx->blas, CUBLAS_OP_N, CUBLAS_OP_N, p, q, p, &sign, A1, p, T1, p,
+                          &zero, out, p));  // sign * (T_B Y T_A^T)^T
+  return KP_OK;
+}
+
+int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp_step_out* out) {
+  const Plan& P = c.P;
+  double* red = c.at(P.o_red);
+  const double Ng = cfg->n_interior_global, Nbg = cfg->n_boundary_global;
+  const double ema = cfg->ema;
+  for (int l = 0; l < P.L; ++l) {
+    launch_factor_finalize(red + P.r_aint + P.fa[l], st->a_int + P.fa[l], P.p[l], Ng * P.S, ema,
+                           l == 0 ? P.d : 0, Ng, c.s);
+    launch_factor_finalize(red + P.r_bint + P.fb[l], st->b_int + P.fb[l], P.q[l], Ng, ema, 0, 0.0,
+                           c.s);
+    launch_factor_finalize(red + P.r_abnd + P.fa[l], st->a_bnd + P.fa[l], P.p[l], Nbg, ema, 0,
+                           0.0, c.s);
+    launch_factor_finalize(red + P.r_bbnd + P.fb[l], st->b_bnd + P.fb[l], P.q[l], Nbg, ema, 0,
+                           0.0, c.s);
+  }
+  double* grad = c.at(P.o_grad);
+  launch_grad_finalize(red + P.r_gint, red + P.r_gbnd, Ng, Nbg, grad, P.D, c.s);
+  launch_losses(red + P.r_ss, Ng, Nbg, out->scalars, c.s);
+  double* delta = c.at(P.o_delta);
+  int* info = reinterpret_cast<int*>(c.at(P.o_info));
+  const double lam = cfg->damping;
+  for (int l = 0; l < P.L; ++l) {
+    double* A1 = c.at(P.o_A1);
+    double* A2 = c.at(P.o_A2);
+    double* B1 = c.at(P.o_B1);
+    double* B2 = c.at(P.o_B2);
+    launch_damped_copy(st->a_int + P.fa[l], lam, P.p[l], A1, c.s);
+    launch_damped_copy(st->a_bnd + P.fa[l], lam, P.p[l], A2, c.s);
+    launch_damped_copy(st->b_int + P.fb[l], lam, P.q[l], B1, c.s);
+    launch_damped_copy(st->b_bnd + P.fb[l], lam, P.q[l], B2, c.s);
+    KP_TRY(kron_solve(c.ctx, c, P.p[l], P.q[l], A1, A2, B1, B2, grad + P.th[l], delta + P.th[l],
+                      -1.0, info, out->status));
+  }
+  launch_axpy_out(delta, st->prev_update, cfg->momentum, c.at(P.o_dir), P.D, c.s);
+  if (out->grad) KP_CUDA_TRY(cudaMemcpyAsync(out->grad, grad, sizeof(double) * P.D,
+                                             cudaMemcpyDeviceToDevice, c.s));
+  if (out->delta) KP_CUDA_TRY(cudaMemcpyAsync(out->delta, delta, sizeof(double) * P.D,
+                                              cudaMemcpyDeviceToDevice, c.s));
+  return KP_OK;
+}
+
+int phase_linesearch(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, const kp_batch* bt) {
+  const Plan& P = c.P;
+  const TaylorDims tdi{P.S, P.d, true};
+  const TaylorDims tdb{1, 0, false};
+  double* thc = c.at(P.o_thc);
+  double* dir = c.at(P.o_dir);
+  for (int k = 0; k < P.ncand; ++k) {
+    launch_candidate(st->theta, dir, cfg->ls_min_exp + k, thc, P.D, c.s);
+    for (int64_t n0 = 0; n0 < P.N; n0 += P.Nc) {
+      const int64_t nc = std::min(P.Nc, P.N - n0);
+      ResidualIn ri{bt->r0 + n0, bt->seeds + n0 * P.S, nullptr};
+      forward_loss(c, thc, bt->x_int + n0 * P.d, nc, tdi, bt->coeff_diag, c.at(P.o_ping),
+                   c.at(P.o_pong), ri, c.at(P.o_rls) + k * P.N + n0, nullptr);
+    }
+    ResidualIn rb{nullptr, nullptr, bt->targets};
+    forward_loss(c, thc, bt->x_bnd, P.Nb, tdb, bt->coeff_diag, c.at(P.o_bping), c.at(P.o_bpong),
+                 rb, c.at(P.o_rbls) + k * P.Nb, nullptr);
+  }
+  double* ls = c.at(P.o_ls);
+  launch_sumsq(c.at(P.o_rls), P.N, P.N, P.ncand, ls, 2, c.s);
+  launch_sumsq(c.at(P.o_rbls), P.Nb, P.Nb, P.ncand, ls + 1, 2, c.s);
+  return KP_OK;
+}
+
+int phase_update(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp_step_out* out) {
+  const Plan& P = c.P;
+  launch_argmin_update(c.at(P.o_ls), P.ncand, cfg->ls_min_exp, cfg->n_interior_global,
+                       cfg->n_boundary_global, st->theta, st->prev_update, c.at(P.o_dir), P.D,
+                       out->scalars, out->ls_losses, out->status, cfg->momentum, c.s);
+  return KP_OK;
+}
+
+int validate_cfg(const kp_problem* pr, const kp_kfac_config* cfg) {
+  if (!cfg) return KP_ERR_INVALID;
+  if (!(cfg->ema >= 0.0 && cfg->ema < 1.0)) return KP_ERR_INVALID;
+  if (!(cfg->damping > 0.0)) return KP_ERR_INVALID;
+  if (!(cfg->momentum >= 0.0)) return KP_ERR_INVALID;
+  if (cfg->ls_max_exp - cfg->ls_min_exp + 1 != pr->n_candidates) return KP_ERR_INVALID;
+  if (!(cfg->n_interior_global >= 1.0) || !(cfg->n_boundary_global >= 1.0)) return KP_ERR_INVALID;
+  return KP_OK;
+}
+
+int prepare(kp_context* ctx, const kp_problem* pr, Plan& P, size_t ws_bytes) {
+  if (!ctx || !pr) return KP_ERR_INVALID;
+  KP_TRY(make_plan(ctx, pr, P));
+  if ((size_t)P.total * sizeof(double) > ws_bytes) return KP_ERR_WORKSPACE;
+  return KP_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// extern "C"
+
+extern "C" {
+
+int32_t kp_abi_version(void) { return KP_ABI_VERSION; }
+
+const char* kp_status_string(int32_t s) {
+  switch (s) {
+    case KP_OK: return "ok";
+    case KP_ERR_INVALID: return "invalid argument";
+    case KP_ERR_NOT_PSD: return "matrix not positive (semi)definite";
+    case KP_ERR_LINE_SEARCH: return "loss is non-finite at every line-search step size";
+    case KP_ERR_NONFINITE: return "parameters became non-finite during the step";
+    case KP_ERR_CUDA: return "CUDA/cuSOLVER/cuBLAS failure";
+    case KP_ERR_EIG: return "eigensolver did not converge";
+    case KP_ERR_WORKSPACE: return "workspace too small";
+    default: return "unknown status";
+  }
+}
+
+int32_t kp_context_create(int32_t device, kp_context** out) {
+  if (!out) return KP_ERR_INVALID;
+  KP_CUDA_TRY(cudaSetDevice(device));
+  kp_context* c = new kp_context();
+  c->device = device;
+  if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS) {
+    delete c;
+    return KP_ERR_CUDA;
+  }
+  if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) {
+    cusolverDnDestroy(c->solver);
+    delete c;
+    return KP_ERR_CUDA;
+  }
+  *out = c;
+  return KP_OK;
+}
+
+int32_t kp_context_destroy(kp_context* c) {
+  if (!c) return KP_OK;
+  for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+  if (c->blas) cublasDestroy(c->blas);
+  if (c->solver) cusolverDnDestroy(c->solver);
+  delete c;
+  return KP_OK;
+}
+
+int32_t kp_profile_enable(kp_context* c, int32_t enable) {
+  if (!c) return KP_ERR_INVALID;
+  c->profile = enable != 0;
+  c->ev_used = 0;
+  c->prof_flops = 0.0;
+  c->prof_launches = 0;
+  return KP_OK;
+}
+
+int32_t kp_profile_read(kp_context* c, double* gemm_ms, double* gemm_flops, int64_t* launches,
+                        int64_t* kernel_launches) {
+  if (!c) return KP_ERR_INVALID;
+  double ms = 0.0;
+  for (size_t k = 0; k + 1 < c->ev_used; k += 2) {
+    KP_CUDA_TRY(cudaEventSynchronize(c->ev[k + 1]));
+    float t = 0.f;
+    KP_CUDA_TRY(cudaEventElapsedTime(&t, c->ev[k], c->ev[k + 1]));
+    ms += t;
+  }
+  if (gemm_ms) *gemm_ms = ms;
+  if (gemm_flops) *gemm_flops = c->prof_flops;
+  if (launches) *launches = c->prof_launches;
+  if (kernel_launches) *kernel_launches = kp::launch_count();
+  c->ev_used = 0;
+  c->prof_flops = 0.0;
+  c->prof_launches = 0;
+  return KP_OK;
+}
+
+int64_t kp_param_count(const kp_net* net) {
+  if (check_net(net) != KP_OK) return -1;
+  int64_t D = 0;
+  for (int l = 0; l < net->n_layers; ++l) D += (int64_t)(net->widths[l] + 1) * net->widths[l + 1];
+  return D;
+}
+
+int64_t kp_factor_count(const kp_net* net, int32_t which) {
+  if (check_net(net) != KP_OK) return -1;
+  int64_t n = 0;
+  for (int l = 0; l < net->n_layers; ++l) {
+    const int64_t k = which == 0 ? net->widths[l] + 1 : net->widths[l + 1];
+    n += k * k;
+  }
+  return n;
+}
+
+int32_t kp_workspace_bytes(kp_context* ctx, const kp_problem* pr, size_t* bytes) {
+  if (!ctx || !pr || !bytes) return KP_ERR_INVALID;
+  Plan P;
+  KP_TRY(make_plan(ctx, pr, P));
+  *bytes = (size_t)P.total * sizeof(double);
+  return KP_OK;
+}
+
+int32_t kp_bytes_per_interior_point(const kp_net* net, size_t* bytes) {
+  if (!bytes) return KP_ERR_INVALID;
+  KP_TRY(check_net(net));
+  *bytes = (size_t)per_point_doubles(net) * sizeof(double);
+  return KP_OK;
+}
+
+int32_t kp_init_state(kp_context* ctx, const kp_net* net, kp_state* st, int32_t init_identity,
+                      void* stream) {
+  if (!ctx || !st) return KP_ERR_INVALID;
+  KP_TRY(check_net(net));
+  cudaStream_t s = (cudaStream_t)stream;
+  const double v = init_identity ? 1.0 : 0.0;
+  int64_t oa = 0, ob = 0, D = 0;
+  for (int l = 0; l < net->n_layers; ++l) {
+    const int p = net->widths[l] + 1, q = net->widths[l + 1];
+    launch_identity(st->a_int + oa, p, v, s);
+    launch_identity(st->a_bnd + oa, p, v, s);
+    launch_identity(st->b_int + ob, q, v, s);
+    launch_identity(st->b_bnd + ob, q, v, s);
+    oa += (int64_t)p * p;
+    ob += (int64_t)q * q;
+    D += (int64_t)p * q;
+  }
+  KP_CUDA_TRY(cudaMemsetAsync(st->prev_update, 0, sizeof(double) * D, s));
+  KP_CUDA_TRY(cudaGetLastError());
+  return KP_OK;
+}
+
+int32_t kp_reduce_buffer(kp_context* ctx, const kp_problem* pr, void* ws, double** ptr,
+                         int64_t* count) {
+  Plan P;
+  KP_TRY(make_plan(ctx, pr, P));
+  *ptr = static_cast<double*>(ws) + P.o_red;
+  *count = P.r_count;
+  return KP_OK;
+}
+
+int32_t kp_linesearch_buffer(kp_context* ctx, const kp_problem* pr, void* ws, double** ptr,
+                             int64_t* count) {
+  Plan P;
+  KP_TRY(make_plan(ctx, pr, P));
+  *ptr = static_cast<double*>(ws) + P.o_ls;
+  *count = 2LL * P.ncand;
+  return KP_OK;
+}
+
+#define KP_PHASE_PROLOGUE                                            \
+  Plan P;                                                            \
+  KP_TRY(prepare(ctx, prob, P, ws_bytes));                           \
+  KP_TRY(validate_cfg(prob, cfg));                                   \
+  if (!st || !out || !out->scalars || !out->status) return KP_ERR_INVALID; \
+  Ctx c{ctx, P, static_cast<double*>(ws), (cudaStream_t)stream};
+
+int32_t kp_kfac_phase_accumulate(kp_context* ctx, const kp_problem* prob,
+                                 const kp_kfac_config* cfg, kp_state* st, const kp_batch* bt,
+                                 kp_step_out* out, void* ws, size_t ws_bytes, void* stream) {
+  KP_PHASE_PROLOGUE
+  if (!bt) return KP_ERR_INVALID;
+  KP_CUDA_TRY(cudaMemsetAsync(out->status, 0, sizeof(int32_t), c.s));
+  KP_TRY(phase_accumulate(c, cfg, st, bt));
+  KP_CUDA_TRY(cudaGetLastError());
+  return KP_OK;
+}
+
+int32_t kp_kfac_phase_precondition(kp_context* ctx, const kp_problem* prob,
+                                   const kp_kfac_config* cfg, kp_state* st, kp_step_out* out,
+                                   void* ws, size_t ws_bytes, void* stream) {
+  KP_PHASE_PROLOGUE
+  KP_TRY(phase_precondition(c, cfg, st, out));
+  KP_CUDA_TRY(cudaGetLastError());
+  return KP_OK;
+}
+
+int32_t kp_kfac_phase_linesearch(kp_context* ctx, const kp_problem* prob,
+                                 const kp_kfac_config* cfg, kp_state* st, const kp_batch* bt,
+                                 kp_step_out* out, void* ws, size_t ws_bytes, void* stream) {
+  KP_PHASE_PROLOGUE
+  if (!bt) return KP_ERR_INVALID;
+  KP_TRY(phase_linesearch(c, cfg, st, bt));
+  KP_CUDA_TRY(cudaGetLastError());
+  return KP_OK;
+}
+
+int32_t kp_kfac_phase_update(kp_context* ctx, const kp_problem* prob, const kp_kfac_config* cfg,
+                             kp_state* st, kp_step_out* out, void* ws, size_t ws_bytes,
+                             void* stream) {
+  KP_PHASE_PROLOGUE
+  KP_TRY(phase_update(c, cfg, st, out));
+  KP_CUDA_TRY(cudaGetLastError());
+  return KP_OK;
+}
+
+int32_t kp_kfac_step(kp_context* ctx, const kp_problem* prob, const kp_kfac_config* cfg,
+                     kp_state* st, const kp_batch* bt, kp_step_out* out, void* ws,
+                     size_t ws_bytes, void* stream) {
+  KP_PHASE_PROLOGUE
+  if (!bt) return KP_ERR_INVALID;
+  KP_CUDA_TRY(cudaMemsetAsync(out->status, 0, sizeof(int32_t), c.s));
+  KP_TRY(phase_accumulate(c, cfg, st, bt));
+  KP_TRY(phase_precondition(c, cfg, st, out));
+  KP_TRY(phase_linesearch(c, cfg, st, bt));
+  KP_TRY(phase_update(c, cfg, st, out));
+  KP_CUDA_TRY(cudaGetLastError());
+  return KP_OK;
+}
+
+int32_t kp_taylor_forward(kp_context* ctx, const kp_problem* prob, const double* theta,
+                          const kp_batch* bt, double* value, double* gradient, double* op,
+                          void* ws, size_t ws_bytes, void* stream) {
+  Plan P;
+  KP_TRY(prepare(ctx, prob, P, ws_bytes));
+  if (!theta || !bt || !value || !gradient || !op) return KP_ERR_INVALID;
+  Ctx c{ctx, P, static_cast<double*>(ws), (cudaStream_t)stream};
+  const TaylorDims tdi{P.S, P.d, true};
+  for (int64_t n0 = 0; n0 < P.N; n0 += P.Nc) {
+    const int64_t nc = std::min(P.Nc, P.N - n0);
+    ResidualIn ri{nullptr, nullptr, nullptr};
+    double* u = c.at(P.o_u);
+    forward_loss(c, theta, bt->x_int + n0 * P.d, nc, tdi, bt->coeff_diag, c.at(P.o_ping),
+                 c.at(P.o_pong), ri, nullptr, u);
+    launch_split_u(u, nc, P.d, value + n0, gradient + n0 * P.d, op + n0, c.s);
+  }
+  KP_CUDA_TRY(cudaGetLastError());
+  return KP_OK;
+}
+
+int32_t kp_evaluate_losses(kp_context* ctx, const kp_problem* prob, const double* theta,
+                           const kp_batch* bt, double* losses, void* ws, size_t ws_bytes,
+                           void* stream) {
+  Plan P;
+  KP_TRY(prepare(ctx, prob, P, ws_bytes));
+  if (!theta || !bt || !losses) return KP_ERR_INVALID;
+  Ctx c{ctx, P, static_cast<double*>(ws), (cudaStream_t)stream};
+  const TaylorDims tdi{P.S, P.d, true};
+  const TaylorDims tdb{1, 0, false};
+  for (int64_t n0 = 0; n0 < P.N; n0 += P.Nc) {
+    const int64_t nc = std::min(P.Nc, P.N - n0);
+    ResidualIn ri{bt->r0 + n0, bt->seeds + n0 * P.S, nullptr};
+    forward_loss(c, theta, bt->x_int + n0 * P.d, nc, tdi, bt->coeff_diag, c.at(P.o_ping),
+                 c.at(P.o_pong), ri, c.at(P.o_r) + n0, nullptr);
+  }
+  ResidualIn rb{nullptr, nullptr, bt->targets};
+  forward_loss(c, theta, bt->x_bnd, P.Nb, tdb, bt->coeff_diag, c.at(P.o_bping), c.at(P.o_bpong),
+               rb, c.at(P.o_rb), nullptr);
+  double* ss = c.at(P.o_ls);
+  launch_sumsq(c.at(P.o_r), P.N, 0, 1, ss, 1, c.s);
+  launch_sumsq(c.at(P.o_rb), P.Nb, 0, 1, ss + 1, 1, c.s);
+  launch_losses(ss, (double)P.N, (double)P.Nb, losses, c.s);
+  KP_CUDA_TRY(cudaGetLastError());
+  return KP_OK;
+}
+
+int32_t kp_kron_solve_workspace_bytes(kp_context* ctx, int32_t p, int32_t q, size_t* bytes) {
+  if (!ctx || p < 1 || q < 1 || !bytes) return KP_ERR_INVALID;
+  kp_problem pr{};
+  pr.net.n_layers = 1;
+  pr.net.widths[0] = p - 1 > 0 ? p - 1 : 1;
+  pr.net.widths[1] = 1;
+  (void)pr;
+  int lw = 1;
+  for (int n : {p, q}) {
+    int w = 0;
+    KP_SOLVER_TRY(cusolverDnDsygvd_bufferSize(ctx->solver, CUSOLVER_EIG_TYPE_1,
+                                              CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n,
+                                              nullptr, n, nullptr, n, nullptr, &w));
+    lw = std::max(lw, w);
+  }
+  const int64_t doubles = 2LL * p * p + 2LL * q * q + p + q + 2LL * p * q + lw + 8 + 16 * 32;
+  *bytes = (size_t)doubles * sizeof(double);
+  return KP_OK;
+}
+
+int32_t kp_kron_sum_solve(kp_context* ctx, int32_t p, int32_t q, const double* a1,
+                          const double* b1, const double* a2, const double* b2, const double* g,
+                          double* x, int32_t* status, void* ws, size_t ws_bytes, void* stream) {
+  size_t need = 0;
+  KP_TRY(kp_kron_solve_workspace_bytes(ctx, p, q, &need));
+  if (ws_bytes < need) return KP_ERR_WORKSPACE;
+  if (!a1 || !b1 || !a2 || !b2 || !g || !x || !status) return KP_ERR_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  Plan P;
+  int64_t o = 0;
+  auto take = [&](int64_t n) {
+    const int64_t at = o;
+    o += (n + 31) / 32 * 32;
+    return at;
+  };
+  P.o_A1 = take((int64_t)p * p);
+  P.o_A2 = take((int64_t)p * p);
+  P.o_B1 = take((int64_t)q * q);
+  P.o_B2 = take((int64_t)q * q);
+  P.o_la = take(p);
+  P.o_lb = take(q);
+  P.o_T1 = take((int64_t)p * q);
+  P.o_T2 = take((int64_t)p * q);
+  P.o_info = take(8);
+  P.o_work = o;
+  P.lwork = (int64_t)(ws_bytes / sizeof(double)) - o;
+  Ctx c{ctx, P, static_cast<double*>(ws), s};
+  KP_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int32_t), s));
+  KP_CUDA_TRY(cudaMemcpyAsync(c.at(P.o_A1), a1, sizeof(double) * p * p, cudaMemcpyDeviceToDevice, s));
+  KP_CUDA_TRY(cudaMemcpyAsync(c.at(P.o_A2), a2, sizeof(double) * p * p, cudaMemcpyDeviceToDevice, s));
+  KP_CUDA_TRY(cudaMemcpyAsync(c.at(P.o_B1), b1, sizeof(double) * q * q, cudaMemcpyDeviceToDevice, s));
+  KP_CUDA_TRY(cudaMemcpyAsync(c.at(P.o_B2), b2, sizeof(double) * q * q, cudaMemcpyDeviceToDevice, s));
+  KP_TRY(kron_solve(ctx, c, p, q, c.at(P.o_A1), c.at(P.o_A2), c.at(P.o_B1), c.at(P.o_B2), g, x,
+                    1.0, reinterpret_cast<int*>(c.at(P.o_info)), status));
+  KP_CUDA_TRY(cudaGetLastError());
+  return KP_OK;
+}
+
+}  // extern "C"

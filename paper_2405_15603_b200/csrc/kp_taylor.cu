@@ -1,0 +1,334 @@
+// Taylor-mode (forward-Laplacian) elementwise kernels, FP64, sm_100a.
+//
+// State layout follows the reference (src/taylor.py:3-16): sample n owns rows
+// n*S .. n*S+S-1 of a row-major (N*S, h) matrix — row 0 the value, rows 1..d the
+// directional first derivatives, row d+1 the operator (L z) row.  Every kernel
+// maps one thread to one (sample, unit) pair and walks that sample's S rows, so
+// each row access is a coalesced 32-wide run of consecutive units and the
+// per-sample reductions over the d derivative rows stay in registers.
+#include <algorithm>
+
+#include "kp_common.cuh"
+#include "kp_internal.h"
+
+namespace kp {
+
+static inline unsigned grid_for(int64_t n, int threads) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, threads), 148LL * 64));
+}
+
+// ---------------------------------------------------------------------------
+// layer 0 + first activation (taylor.py:124-169 specialised: Z0 = [x; I; 0])
+
+__global__ void k_first_layer(const double* __restrict__ x, int64_t n, int d,
+                              const double* __restrict__ th0, int h1, TaylorDims td,
+                              const double* __restrict__ cdiag, double* __restrict__ zval,
+                              double* __restrict__ post) {
+  const int p0 = d + 1;
+  const int64_t total = n * h1;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t smp = e / h1;
+    const int j = (int)(e % h1);
+    const double* w = th0 + (int64_t)j * p0;
+    const double* xr = x + smp * d;
+    double z = 0.0;
+    for (int k = 0; k < d; ++k) z = fma(xr[k], w[k], z);
+    z += w[d];  // bias on the value row (taylor.py:147)
+    if (zval) zval[e] = z;
+    const TanhD t = tanh_derivs(z, false);
+    double* out = post + smp * td.S * h1 + j;
+    out[0] = t.s0;
+    if (!td.taylor) continue;
+    double quad = 0.0;
+    for (int i = 0; i < d; ++i) {
+      const double g = w[i];  // derivative row i of the pre-activation is W0[:, i]
+      out[(int64_t)(i + 1) * h1] = t.s1 * g;
+      quad += (g * cdiag[i]) * g;
+    }
+    // operator row: s1 * 0 + s2 * quad (taylor.py:168 with L z_in = 0)
+    out[(int64_t)(d + 1) * h1] = t.s2 * quad;
+  }
+}
+
+void launch_first_layer(const double* x, int64_t n, int d, const double* theta0, int h1,
+                        TaylorDims td, const double* cdiag, double* zval, double* post,
+                        cudaStream_t s) {
+  const int64_t total = n * h1;
+  if (total <= 0) return;
+  count_launch();
+  k_first_layer<<<grid_for(total, 256), 256, 0, s>>>(x, n, d, theta0, h1, td, cdiag, zval, post);
+}
+
+// ---------------------------------------------------------------------------
+// activation forward (taylor.py:151-169)
+
+// pre == post (in-place) is allowed: each thread reads an element before writing it.
+__global__ void k_act_fwd(const double* pre, double* post, int64_t n,
+                          int h, TaylorDims td, const double* __restrict__ cdiag) {
+  const int64_t total = n * h;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t smp = e / h;
+    const int j = (int)(e % h);
+    const int64_t base = smp * td.S * h + j;
+    const TanhD t = tanh_derivs(pre[base], false);
+    post[base] = t.s0;
+    if (!td.taylor) continue;
+    double quad = 0.0;
+    for (int i = 1; i <= td.d; ++i) {
+      const double g = pre[base + (int64_t)i * h];
+      post[base + (int64_t)i * h] = t.s1 * g;
+      quad += (g * cdiag[i - 1]) * g;
+    }
+    const int64_t o = base + (int64_t)(td.d + 1) * h;
+    post[o] = t.s1 * pre[o] + t.s2 * quad;
+  }
+}
+
+void launch_act_fwd(const double* pre, double* post, int64_t n, int h, TaylorDims td,
+                    const double* cdiag, cudaStream_t s) {
+  const int64_t total = n * h;
+  if (total <= 0) return;
+  count_launch();
+  k_act_fwd<<<grid_for(total, 256), 256, 0, s>>>(pre, post, n, h, td, cdiag);
+}
+
+// ---------------------------------------------------------------------------
+// last (h_out = 1) layer + residual (pde.py:344-360 with the affine residual map)
+
+constexpr int LAST_THREADS = 256;
+constexpr int LAST_MAX_ROWS = 1024;
+
+__global__ void __launch_bounds__(LAST_THREADS) k_last_layer(
+    const double* __restrict__ post, int64_t n, int h, const double* __restrict__ th,
+    TaylorDims td, int spb, const double* __restrict__ r0, const double* __restrict__ seeds,
+    const double* __restrict__ targets, double* __restrict__ r, double* __restrict__ u_out) {
+  __shared__ double u[LAST_MAX_ROWS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t s0 = (int64_t)blockIdx.x * spb;
+  const int ns = (int)((n - s0) < spb ? (n - s0) : spb);
+  const int rows = ns * td.S;
+  const double b = th[h];
+  for (int row = warp; row < rows; row += LAST_THREADS / 32) {
+    const double* pr = post + (s0 * td.S + row) * h;
+    double acc = 0.0;
+    for (int j = lane; j < h; j += 32) acc = fma(pr[j], th[j], acc);
+    acc = warp_sum(acc);
+    if (row % td.S == 0) acc += b;
+    if (lane == 0) {
+      u[row] = acc;
+      if (u_out) u_out[s0 * td.S + row] = acc;
+    }
+  }
+  __syncthreads();
+  if (r == nullptr) return;
+  for (int k = threadIdx.x; k < ns; k += LAST_THREADS) {
+    const int64_t smp = s0 + k;
+    double v;
+    if (td.taylor) {
+      v = r0[smp];
+      const double* sd = seeds + smp * td.S;
+      for (int s = 0; s < td.S; ++s) v += sd[s] * u[k * td.S + s];
+    } else {
+      v = u[k] - targets[smp];
+    }
+    r[smp] = v;
+  }
+}
+
+__global__ void k_split_u(const double* __restrict__ u, int64_t n, int d, double* value,
+                          double* grad, double* op) {
+  const int S = d + 2;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * S;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t smp = e / S;
+    const int s = (int)(e % S);
+    if (s == 0) value[smp] = u[e];
+    else if (s <= d) grad[smp * d + s - 1] = u[e];
+    else op[smp] = u[e];
+  }
+}
+
+void launch_split_u(const double* u, int64_t n, int d, double* value, double* grad, double* op,
+                    cudaStream_t s) {
+  if (n <= 0) return;
+  count_launch();
+  count_launch();
+  k_split_u<<<grid_for(n * (d + 2), 256), 256, 0, s>>>(u, n, d, value, grad, op);
+}
+
+__global__ void k_initial_state(const double* __restrict__ x, int64_t n, int d,
+                                double* __restrict__ z) {
+  const int S = d + 2;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * S * d;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t smp = e / ((int64_t)S * d);
+    const int rem = (int)(e % ((int64_t)S * d));
+    const int s = rem / d, k = rem % d;
+    z[e] = s == 0 ? x[smp * d + k] : (s == k + 1 ? 1.0 : 0.0);
+  }
+}
+
+void launch_initial_state(const double* x, int64_t n, int d, double* z, cudaStream_t s) {
+  if (n <= 0) return;
+  count_launch();
+  count_launch();
+  k_initial_state<<<grid_for(n * (d + 2) * d, 256), 256, 0, s>>>(x, n, d, z);
+}
+
+void launch_last_layer(const double* post, int64_t n, int h, const double* theta_last,
+                       TaylorDims td, const double* r0, const double* seeds,
+                       const double* targets, double* r, double* u_out, cudaStream_t s) {
+  if (n <= 0) return;
+  const int spb = std::max(1, std::min(LAST_MAX_ROWS / td.S, 64));
+  const int64_t blocks = ceil_div(n, spb);
+  count_launch();
+  k_last_layer<<<(unsigned)blocks, LAST_THREADS, 0, s>>>(post, n, h, theta_last, td, spb, r0,
+                                                         seeds, targets, r, u_out);
+}
+
+// ---------------------------------------------------------------------------
+// activation backward (taylor.py:206-239)
+
+__global__ void k_act_bwd(ActBwd a, int64_t n, int h, TaylorDims td,
+                          const double* __restrict__ cdiag) {
+  const int64_t total = n * h;
+  const int d = td.d;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t smp = e / h;
+    const int j = (int)(e % h);
+    const int64_t base = smp * td.S * h + j;
+    const double* w0 = a.pre ? nullptr : a.theta0 + (int64_t)j * (d + 1);
+    const double z = a.pre ? a.pre[base] : a.zval[e];
+    const TanhD t = tanh_derivs(z, td.taylor);
+    const double wl = a.gin ? 0.0 : a.wlast[j];
+    auto gin_at = [&](int s) -> double {
+      if (a.gin) return a.gin[base + (int64_t)s * h];
+      const double sd = a.seeds ? a.seeds[smp * td.S + s] : 1.0;
+      return sd * wl;
+    };
+    const double vb = gin_at(0);
+    if (!td.taylor) {
+      a.gout[base] = t.s1 * vb;  // network.py:229-231
+      continue;
+    }
+    const double lb = gin_at(d + 1);
+    const double ell = a.pre ? a.pre[base + (int64_t)(d + 1) * h] : 0.0;
+    double quad = 0.0, ggb = 0.0;
+    const double two_s2 = 2.0 * t.s2;
+    for (int i = 1; i <= d; ++i) {
+      const double g = a.pre ? a.pre[base + (int64_t)i * h] : w0[i - 1];
+      const double gb = gin_at(i);
+      const double cg = g * cdiag[i - 1];
+      quad += cg * g;
+      ggb += g * gb;
+      a.gout[base + (int64_t)i * h] = t.s1 * gb + two_s2 * cg * lb;
+    }
+    a.gout[base + (int64_t)(d + 1) * h] = t.s1 * lb;
+    a.gout[base] = t.s1 * vb + t.s2 * ggb + t.s2 * ell * lb + t.s3 * quad * lb;
+  }
+}
+
+void launch_act_bwd(const ActBwd& a, int64_t n, int h, TaylorDims td, const double* cdiag,
+                    cudaStream_t s) {
+  const int64_t total = n * h;
+  if (total <= 0) return;
+  count_launch();
+  k_act_bwd<<<grid_for(total, 256), 256, 0, s>>>(a, n, h, td, cdiag);
+}
+
+// ---------------------------------------------------------------------------
+// layer-0 gradient, derivative rows: Zhat_0 rows (e_i, 0) pick column i.
+
+__global__ void k_grad0_deriv(const double* __restrict__ gbar0, const double* __restrict__ r,
+                              int64_t n, int d, int h1, double* __restrict__ acc) {
+  const int64_t total = (int64_t)d * h1;
+  const int64_t S = d + 2;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / h1), j = (int)(e % h1);
+    const double* g = gbar0 + (int64_t)(1 + i) * h1 + j;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int64_t k = 0;
+    for (; k + 4 <= n; k += 4) {
+      s0 += r[k] * g[(k)*S * h1];
+      s1 += r[k + 1] * g[(k + 1) * S * h1];
+      s2 += r[k + 2] * g[(k + 2) * S * h1];
+      s3 += r[k + 3] * g[(k + 3) * S * h1];
+    }
+    for (; k < n; ++k) s0 += r[k] * g[k * S * h1];
+    acc[(int64_t)j * (d + 1) + i] += (s0 + s1) + (s2 + s3);
+  }
+}
+
+void launch_grad0_deriv(const double* gbar0, const double* r, int64_t n, int d, int h1,
+                        double* acc, cudaStream_t s) {
+  const int64_t total = (int64_t)d * h1;
+  if (total <= 0 || n <= 0) return;
+  count_launch();
+  k_grad0_deriv<<<(unsigned)ceil_div(total, 128), 128, 0, s>>>(gbar0, r, n, d, h1, acc);
+}
+
+// ---------------------------------------------------------------------------
+// small utilities
+
+__global__ void k_sumsq(const double* __restrict__ v, int64_t n, int64_t stride,
+                        double* __restrict__ out, int64_t out_stride) {
+  __shared__ double red[512];
+  const double* x = v + (int64_t)blockIdx.x * stride;
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) acc = fma(x[i], x[i], acc);
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[(int64_t)blockIdx.x * out_stride] = red[0];
+}
+
+void launch_sumsq(const double* v, int64_t n, int64_t stride, int nvec, double* out,
+                  int64_t out_stride, cudaStream_t s) {
+  if (nvec <= 0) return;
+  count_launch();
+  k_sumsq<<<nvec, 512, 0, s>>>(v, n, stride, out, out_stride);
+}
+
+__global__ void k_transpose(const double* __restrict__ src, int64_t lds, int rows, int cols,
+                            double* __restrict__ dst) {
+  __shared__ double tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int r = by + k, c = bx + threadIdx.x;
+    if (r < rows && c < cols) tile[k][threadIdx.x] = src[(int64_t)r * lds + c];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int c = bx + k, r = by + threadIdx.x;
+    if (r < rows && c < cols) dst[(int64_t)c * rows + r] = tile[threadIdx.x][k];
+  }
+}
+
+// dst (cols x rows, row-major) = src(rows x cols, pitch lds)^T
+void launch_transpose(const double* src, int64_t lds, int rows, int cols, double* dst,
+                      cudaStream_t s) {
+  dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(rows, 32));
+  count_launch();
+  k_transpose<<<grid, dim3(32, 8), 0, s>>>(src, lds, rows, cols, dst);
+}
+
+__global__ void k_fill(double* p, int64_t n, double v) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    p[e] = v;
+}
+
+void launch_fill(double* p, int64_t n, double v, cudaStream_t s) {
+  if (n <= 0) return;
+  count_launch();
+  k_fill<<<grid_for(n, 256), 256, 0, s>>>(p, n, v);
+}
+
+}  // namespace kp

@@ -1,0 +1,218 @@
+"""GPU parity: the B200 path (through the C ABI) vs the reference's golden vectors and the oracle.
+
+Bars (BASELINE.json north star): 1e-10 relative after one step, 1e-8 after more;
+the line-search alpha must be identical.  "Relative" = max|x - ref| / max|ref|
+per array.
+"""
+
+import numpy as np
+import pytest
+
+from golden_util import NAMES, compare, load, pack_factors
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import kfac_oracle as orc  # noqa: E402
+from paper_2405_15603_b200 import configs as cfgs  # noqa: E402
+from paper_2405_15603_b200.network import Architecture, Parameters, init_params, mats_to_vec  # noqa: E402
+from paper_2405_15603_b200.optim import OptimizerConfig, init_train_state, optimizer_step  # noqa: E402
+from paper_2405_15603_b200.pde import make_problem, sample_batch  # noqa: E402
+
+WL_OF = {"c1": "c1", "c2": "c2", "c3": "c3", "c4": "c4", "c5": "c5", "c1_momentum": "c1"}
+
+
+def _theta_colstack(params):
+    return np.concatenate([np.hstack([w, b[:, None]]).ravel(order="F")
+                           for w, b in zip(params.weights, params.biases)])
+
+
+def _device_mats_to_vec(vec, widths):
+    """Device row-major [W|b] packing -> reference column-stacked vector."""
+    out, off = [], 0
+    for h_in, h_out in zip(widths[:-1], widths[1:]):
+        p, q = h_in + 1, h_out
+        out.append(vec[off:off + p * q].reshape(q, p).ravel(order="F"))
+        off += p * q
+    return np.concatenate(out)
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_kfac_steps_match_reference_golden(name):
+    g = load(name)
+    wl = cfgs.WORKLOADS[WL_OF[name]]
+    prob, params, batch = wl.build(0, int(g["n_interior"]), int(g["n_boundary"]))
+    cfg = OptimizerConfig(kind="kfac", damping=float(g["damping"]), ema=float(g["ema"]),
+                          momentum=float(g["momentum"]))
+    state = init_train_state(params, cfg)
+    t = 1
+    while f"s{t}/alpha" in g:
+        info = optimizer_step(state, batch, prob)
+        p = f"s{t}/"
+        tol = 1e-10 if t == 1 else 1e-8
+        assert info.alpha == float(g[p + "alpha"]), (t, info.alpha, float(g[p + "alpha"]))
+        for key, val in (("loss_interior", info.loss_interior), ("loss_boundary", info.loss_boundary)):
+            ref = float(g[p + key])
+            assert abs(val - ref) <= tol * abs(ref), (key, val, ref)
+        eng = state._engine
+        ls = eng.ls_losses.cpu().numpy().reshape(-1, 2)
+        rel = np.max(np.abs(ls - g[p + "ls_losses"]) / np.abs(g[p + "ls_losses"]))
+        assert rel <= tol, rel
+        widths = eng.widths
+        assert compare(g, p + "grad", _device_mats_to_vec(eng.grad.cpu().numpy(), widths), tol) <= tol
+        assert compare(g, p + "delta", _device_mats_to_vec(eng.delta.cpu().numpy(), widths), tol) <= tol
+        assert compare(g, p + "theta", _theta_colstack(state.params), tol) <= tol
+        assert compare(g, p + "prev_update", mats_to_vec(state.prev_update), tol) <= tol
+        kf = state.kfac
+        for key, mats in (("a_interior", kf.a_interior), ("b_interior", kf.b_interior),
+                          ("a_boundary", kf.a_boundary), ("b_boundary", kf.b_boundary)):
+            assert compare(g, p + key, pack_factors(mats), tol) <= tol, key
+        t += 1
+
+
+def _oracle_vs_device(widths, problem, n_int, n_bnd, steps, momentum=0.0, ema=0.95, damping=1e-3,
+                      seed=3, chunk=None):
+    arch = Architecture(widths)
+    params = init_params(arch, seed)
+    batch = sample_batch(problem, n_int, n_bnd, seed + 100)
+    st = orc.init_state(params.weights, params.biases, ema=ema, damping=damping, momentum=momentum)
+    cfg = OptimizerConfig(kind="kfac", damping=damping, ema=ema, momentum=momentum)
+    state = init_train_state(params, cfg)
+    if chunk is not None:
+        from paper_2405_15603_b200.optim import _engine_for
+        _engine_for(state, batch, tuple(widths))
+        eng = state._engine
+        from paper_2405_15603_b200.engine import KfacEngine
+        new = KfacEngine(widths, n_int, n_bnd, ema=ema, damping=damping, momentum=momentum,
+                         chunk=chunk)
+        kf = state.kfac
+        new.set_factor_lists(kf.a_interior, kf.b_interior, kf.a_boundary, kf.b_boundary)
+        new.set_prev_mats(state.prev_update)
+        new.load_params(state.params)
+        state._engine = new
+        del eng
+    worst = 0.0
+    for t in range(steps):
+        a_ref, _, li_ref, lb_ref = orc.kfac_step(st, batch, problem)
+        info = optimizer_step(state, batch, problem)
+        assert info.alpha == a_ref
+        th_ref = np.concatenate([np.hstack([w, b[:, None]]).ravel() for w, b in zip(st.weights, st.biases)])
+        th = np.concatenate([np.hstack([w, b[:, None]]).ravel()
+                             for w, b in zip(state.params.weights, state.params.biases)])
+        err = max(abs(info.loss_interior - li_ref) / abs(li_ref),
+                  abs(info.loss_boundary - lb_ref) / abs(lb_ref),
+                  np.max(np.abs(th - th_ref)) / np.max(np.abs(th_ref)))
+        worst = max(worst, err)
+        assert err <= (1e-10 if t == 0 else 1e-8), (t, err)
+    return worst
+
+
+@pytest.mark.parametrize("widths,problem", [
+    ((2, 1), "poisson2d_sin"),                      # single linear layer
+    ((2, 7, 1), "poisson2d_sin"),                   # one hidden layer (first act only)
+    ((3, 5, 9, 1), "poisson_norm2"),                # odd widths, K/N tails
+    ((5, 33, 17, 65, 1), "heat4"),                  # partial Laplacian, ragged tiles
+    ((10, 130, 70, 1), "poisson_harmonic_mixed"),   # > 128 wide, 10d
+])
+def test_device_matches_oracle_various_shapes(widths, problem):
+    if problem == "heat4":
+        prob = make_problem("heat", spatial_dim=4)
+    elif problem == "poisson_norm2":
+        prob = make_problem("poisson_norm2", dim=3)
+    else:
+        prob = make_problem(problem)
+    _oracle_vs_device(widths, prob, 37, 11, 3, momentum=0.5)
+
+
+def test_chunked_interior_matches_unchunked():
+    prob = make_problem("poisson_cos_sum")
+    _oracle_vs_device((5, 64, 48, 1), prob, 300, 50, 2, chunk=70)
+
+
+def test_taylor_forward_matches_oracle():
+    from paper_2405_15603_b200.engine import KfacEngine, pack_params
+    prob = make_problem("heat", spatial_dim=4)
+    params = init_params(Architecture((5, 40, 24, 1)), 11)
+    batch = sample_batch(prob, 53, 7, 12)
+    eng = KfacEngine((5, 40, 24, 1), 53, 7, ema=0.9, damping=1e-2, momentum=0.0)
+    eng.load_params(params)
+    from paper_2405_15603_b200.pde import affine_residual_terms
+    r0, seeds = affine_residual_terms(prob, batch.interior)
+    eng.set_batch(batch.interior, r0, seeds, batch.boundary, batch.boundary_targets,
+                  np.diagonal(prob.coeffs.c))
+    u, gu, lu = eng.taylor_forward()
+    cd = np.diagonal(prob.coeffs.c).copy()
+    _, _, (u_r, g_r, l_r) = orc.taylor_forward(params.weights, params.biases, batch.interior, cd)
+    assert np.max(np.abs(u - u_r)) <= 1e-13 * max(1, np.max(np.abs(u_r)))
+    assert np.max(np.abs(gu - g_r)) <= 1e-13 * max(1, np.max(np.abs(g_r)))
+    assert np.max(np.abs(lu - l_r)) <= 1e-12 * max(1, np.max(np.abs(l_r)))
+    li, lb = eng.evaluate_losses()
+    li_r, lb_r = orc.losses_at(params.weights, params.biases, batch, prob, cd)
+    assert abs(li - li_r) <= 1e-12 * abs(li_r) and abs(lb - lb_r) <= 1e-12 * abs(lb_r)
+
+
+def test_kron_sum_solve_matches_dense():
+    from paper_2405_15603_b200.engine import kron_sum_solve_device
+    rng = np.random.default_rng(4)
+    for p, q in ((5, 3), (65, 64), (101, 1), (257, 256)):
+        mk = lambda k: (lambda a: a @ a.T / k + 0.3 * np.eye(k))(rng.standard_normal((k, k)))  # noqa: E731
+        a1, a2, b1, b2 = mk(p), mk(p), mk(q), mk(q)
+        g = rng.standard_normal((q, p))
+        x = kron_sum_solve_device(a1, b1, a2, b2, g)
+        if p * q <= 4000:
+            dense = np.kron(a1, b1) + np.kron(a2, b2)
+            want = np.linalg.solve(dense, g.ravel(order="F")).reshape((q, p), order="F")
+        else:
+            want = orc.kron_sum_solve(a1, b1, a2, b2, g)
+        assert np.max(np.abs(x - want)) <= 1e-10 * np.max(np.abs(want)), (p, q)
+        # residual check of B1 X A1 + B2 X A2 = G
+        res = b1 @ x @ a1 + b2 @ x @ a2 - g
+        assert np.max(np.abs(res)) <= 1e-10 * np.max(np.abs(g))
+
+
+def test_kron_sum_solve_rejects_indefinite():
+    from paper_2405_15603_b200.engine import kron_sum_solve_device
+    from paper_2405_15603_b200.linalg import NotPositiveSemidefiniteError
+    a = np.eye(3)
+    bad = -np.eye(3)
+    with pytest.raises(NotPositiveSemidefiniteError):
+        kron_sum_solve_device(a, np.eye(2), bad, np.eye(2), np.ones((2, 3)))
+
+
+def test_damping_only_gives_half_negative_gradient():
+    # zero factors, damping 1: Delta = -g / 2 (pkg/tests/test_curvature.py:140-146)
+    from paper_2405_15603_b200.engine import kron_sum_solve_device
+    g = np.ones((3, 3))
+    x = kron_sum_solve_device(np.eye(3), np.eye(3), np.eye(3), np.eye(3), g)
+    assert np.allclose(-x, -g / 2.0, atol=1e-12)
+
+
+def test_step_is_bit_deterministic():
+    wl = cfgs.WORKLOADS["c2"]
+    prob, params, batch = wl.build(0, 500, 100)
+    out = []
+    for _ in range(2):
+        state = init_train_state(params.copy(), OptimizerConfig(kind="kfac", damping=1e-3, ema=0.95))
+        for _ in range(2):
+            optimizer_step(state, batch, prob)
+        out.append(np.concatenate([w.ravel() for w in state.params.weights]))
+    assert np.array_equal(out[0], out[1])
+
+
+def test_line_search_error_on_nonfinite_params():
+    from paper_2405_15603_b200.optim import LineSearchError
+    wl = cfgs.WORKLOADS["c1"]
+    prob, params, batch = wl.build(0, 50, 20)
+    params.weights[1][0, 0] = np.nan
+    state = init_train_state(params, OptimizerConfig(kind="kfac", damping=1e-3, ema=0.95))
+    with pytest.raises((LineSearchError, FloatingPointError, ValueError)):
+        optimizer_step(state, batch, prob)
+
+
+def test_nonaffine_residual_rejected():
+    prob = make_problem("log_fokker_planck")
+    params = init_params(Architecture((10, 8, 1)), 0)
+    batch = sample_batch(prob, 10, 5, 0)
+    state = init_train_state(params, OptimizerConfig(kind="kfac", damping=1e-3))
+    with pytest.raises(NotImplementedError):
+        optimizer_step(state, batch, prob)
