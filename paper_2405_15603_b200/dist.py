@@ -1,0 +1,93 @@
+"""Data-parallel KFAC step over several GPUs (one process per GPU, NCCL over NVLink).
+
+Every N-dependent quantity of the step is a sum over collocation points
+(factors src/curvature.py:113-115,133-134; gradient src/optim.py:173-176;
+losses src/pde.py:351,359), so points are sharded contiguously across ranks
+and the parameters / optimizer state are replicated.  A step
+has exactly two exchange points, both sum all-reduces of one contiguous
+device buffer:
+
+1. after the local forward/backward: the UNNORMALISED factor sums, the
+   residual-weighted gradient and sum r^2 (``kp_reduce_buffer``);
+2. after the local line search: the 2 x 31 per-candidate sums of r^2
+   (``kp_linesearch_buffer``).
+
+Normalisation by the global point counts, the EMA, the Kronecker-sum solves
+and the argmin are then computed redundantly — and bit-identically, since the
+all-reduced inputs are identical — on every rank.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .engine import KfacEngine, raise_for_status
+from .pde import affine_residual_terms
+from .taylor import coeff_diagonal
+
+
+def shard_bounds(n: int, rank: int, world: int):
+    """Contiguous, balanced shard [lo, hi) of n points for `rank` of `world`."""
+    base, extra = divmod(n, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+class ShardedKfacStep:
+    """Drives one rank's engine through the phased step with all-reduces in between.
+
+    ``engine`` is anything with ``phase(name)``, ``reduce_buffer()``,
+    ``linesearch_buffer()`` and ``finish_step()`` (the ``KfacEngine`` on GPUs;
+    tests inject a CPU stand-in to check this orchestration under gloo).
+    """
+
+    def __init__(self, engine, all_reduce):
+        self.engine = engine
+        self.all_reduce = all_reduce
+
+    def step(self):
+        e = self.engine
+        e.phase("accumulate")
+        self.all_reduce(e.reduce_buffer())
+        e.phase("precondition")
+        e.phase("linesearch")
+        self.all_reduce(e.linesearch_buffer())
+        e.phase("update")
+        sc, code = e.finish_step()
+        raise_for_status(code, "sharded kfac step")
+        return float(sc[2]), float(sc[3]), float(sc[0]), float(sc[1])
+
+
+def make_rank_engine(widths, batch, problem, rank: int, world: int, *, ema, damping, momentum,
+                     ls_min_exp=-30, ls_max_exp=0, chunk=None):
+    """Engine for this rank's shard of ``batch`` with global normalisers."""
+    n_int, n_bnd = batch.interior.shape[0], batch.boundary.shape[0]
+    if n_int < world or n_bnd < world:
+        raise ValueError("every rank needs at least one interior and one boundary point")
+    i0, i1 = shard_bounds(n_int, rank, world)
+    b0, b1 = shard_bounds(n_bnd, rank, world)
+    eng = KfacEngine(widths, i1 - i0, b1 - b0, ema=ema, damping=damping, momentum=momentum,
+                     ls_min_exp=ls_min_exp, ls_max_exp=ls_max_exp, chunk=chunk,
+                     n_interior_global=n_int, n_boundary_global=n_bnd)
+    upload_shard(eng, batch, problem, rank, world)
+    return eng
+
+
+def upload_shard(eng, batch, problem, rank: int, world: int):
+    n_int, n_bnd = batch.interior.shape[0], batch.boundary.shape[0]
+    i0, i1 = shard_bounds(n_int, rank, world)
+    b0, b1 = shard_bounds(n_bnd, rank, world)
+    x = np.asarray(batch.interior, dtype=np.float64)[i0:i1]
+    r0, seeds = affine_residual_terms(problem, x)
+    eng.set_batch(x, r0, seeds, np.asarray(batch.boundary, dtype=np.float64)[b0:b1],
+                  np.asarray(batch.boundary_targets, dtype=np.float64)[b0:b1],
+                  coeff_diagonal(problem.coeffs))
+
+
+def torch_all_reduce(group=None):
+    import torch.distributed as dist
+
+    def _ar(t):
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+
+    return _ar

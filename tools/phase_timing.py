@@ -1,0 +1,61 @@
+"""Per-phase CUDA-event timing of one KFAC step (diagnostic, not the bench).
+
+    python tools/phase_timing.py --workload c5 --n-interior 3000 [--chunk 0] [--reps 3]
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="c5")
+    ap.add_argument("--n-interior", type=int, default=3000)
+    ap.add_argument("--n-boundary", type=int, default=None)
+    ap.add_argument("--chunk", type=int, default=0)
+    ap.add_argument("--reps", type=int, default=3)
+    a = ap.parse_args()
+    import torch
+
+    from paper_2405_15603_b200 import configs
+    from paper_2405_15603_b200.dist import make_rank_engine
+
+    wl = configs.WORKLOADS[a.workload]
+    nb = a.n_boundary if a.n_boundary is not None else (wl.n_boundary if a.n_interior == wl.n_interior else a.n_interior // 3)
+    prob, params, batch = wl.build(0, a.n_interior, nb)
+    eng = make_rank_engine(wl.widths, batch, prob, 0, 1, ema=wl.ema, damping=wl.damping,
+                           momentum=wl.momentum, chunk=a.chunk or None)
+    eng.load_params(params)
+    eng.init_factors(True)
+    res = {}
+    for rep in range(a.reps):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        evs[0].record()
+        eng.phase("accumulate")
+        evs[1].record()
+        eng.phase("precondition")
+        evs[2].record()
+        eng.phase("linesearch")
+        evs[3].record()
+        eng.phase("update")
+        evs[4].record()
+        sc, code = eng.finish_step()
+        names = ["accumulate", "precondition", "linesearch", "update"]
+        res = {n: evs[i].elapsed_time(evs[i + 1]) for i, n in enumerate(names)}
+        res["total_ms"] = evs[0].elapsed_time(evs[4])
+        res["status"] = code
+        res["alpha"] = float(sc[2])
+    f = configs.flops_per_step(wl.widths, a.n_interior, nb)
+    res["alg_tflops_per_s"] = f / (res["total_ms"] / 1e3) / 1e12
+    res["workload"] = wl.name
+    res["n_interior"] = a.n_interior
+    res["chunk"] = int(eng.prob.chunk)
+    print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()
