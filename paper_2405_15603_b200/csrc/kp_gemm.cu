@@ -137,6 +137,12 @@ static void run_nt(const GemmNT& g, cudaStream_t s) {
 
 void launch_gemm_nt(const GemmNT& g, cudaStream_t s) {
   if (g.M <= 0 || g.N <= 0) return;
+  if (launch_gemm_nt_tma(g, s, 0)) return;
+  launch_gemm_nt_cpasync(g, s);
+}
+
+void launch_gemm_nt_cpasync(const GemmNT& g, cudaStream_t s) {
+  if (g.M <= 0 || g.N <= 0) return;
   if (g.N <= 64)
     run_nt<128, 64, 4, 2, 16, 4>(g, s);
   else

@@ -28,6 +28,11 @@ struct GemmNT {
   int S;
 };
 void launch_gemm_nt(const GemmNT& g, cudaStream_t s);
+// TMA-fed variant (kp_gemm_tma.cu); returns false when the operands do not meet
+// its alignment/shape requirements (the caller then uses the cp.async kernel).
+bool launch_gemm_nt_tma(const GemmNT& g, cudaStream_t s, int variant = 0);
+// cp.async variant only (the fallback).
+void launch_gemm_nt_cpasync(const GemmNT& g, cudaStream_t s);
 
 // Row reduction C[p,q] = sum_r Xh[r,p] * w(r) * Yh[r,q] over rows [0,R), split into
 // `splits` row ranges whose partial tiles go to partial[split][P][Q]; then
@@ -112,8 +117,16 @@ void launch_grad_finalize(const double* gi, const double* gb, double ni, double 
 void launch_axpy_out(const double* x, const double* y, double a, double* out, int64_t n,
                      cudaStream_t s);  // out = x + a*y
 void launch_losses(const double* sums, double ni, double nb, double* scalars, cudaStream_t s);
+// Layer geometry for packing [W|b] rows (pitch h+1) into W rows (pitch h).
+struct WPack {
+  int L;
+  int h[17];
+  int64_t th[16];  // offset of layer l in theta
+  int64_t wo[16];  // offset of layer l in the padded copy
+};
+// out = theta + 2^exp2 dir (dir == nullptr: copy); wpad (optional) = padded W copy of out.
 void launch_candidate(const double* theta, const double* dir, int exp2, double* out, int64_t D,
-                      cudaStream_t s);
+                      const WPack& wp, double* wpad, cudaStream_t s);
 void launch_argmin_update(const double* ls_sums, int ncand, int min_exp, double ni, double nb,
                           double* theta, double* prev, const double* dir, int64_t D,
                           double* scalars, double* ls_losses, int32_t* status, double mu,

@@ -99,6 +99,8 @@ struct Plan {
   int64_t o_partial = 0, o_red = 0, o_grad = 0, o_delta = 0, o_dir = 0, o_thc = 0, o_ls = 0;
   int64_t o_A1 = 0, o_A2 = 0, o_B1 = 0, o_B2 = 0, o_la = 0, o_lb = 0, o_T1 = 0, o_T2 = 0;
   int64_t o_work = 0, o_info = 0;
+  int64_t o_wpad = 0, o_wpadc = 0, wo[MAXL] = {};
+  WPack wp{};
   int64_t lwork = 0;
   int64_t total = 0;  // doubles
   // reduce-buffer sub-offsets (relative to o_red)
@@ -151,6 +153,15 @@ int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
     off += (int64_t)P.p[l] * P.q[l];
   }
   P.D = off;
+  int64_t woff = 0;
+  P.wp.L = P.L;
+  for (int l = 0; l < P.L; ++l) {
+    P.wo[l] = woff;
+    P.wp.h[l] = P.h[l];
+    P.wp.th[l] = P.th[l];
+    P.wp.wo[l] = woff;
+    woff += ((int64_t)P.q[l] * P.h[l] + 1) / 2 * 2;  // keep every layer 16-byte aligned
+  }
   for (int l = 0; l < P.L; ++l) {
     P.fa[l] = P.FA;
     P.FA += (int64_t)P.p[l] * P.p[l];
@@ -211,6 +222,8 @@ int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
   P.o_delta = take(P.D);
   P.o_dir = take(P.D);
   P.o_thc = take(P.D);
+  P.o_wpad = take(woff);
+  P.o_wpadc = take(woff);
   P.o_ls = take(2 * (int64_t)P.ncand);
   P.o_A1 = take((int64_t)P.maxp * P.maxp);
   P.o_A2 = take((int64_t)P.maxp * P.maxp);
@@ -309,7 +322,7 @@ struct ResidualIn {
 
 // Forward pass storing every state needed by the reverse pass (taylor.py:172-203;
 // boundary: network.py:200-213).  Writes residuals r[0..n).
-void forward_store(const Ctx& c, const double* theta, const double* x, int64_t n,
+void forward_store(const Ctx& c, const double* theta, const double* wpad, const double* x, int64_t n,
                    const TaylorDims& td, const double* cdiag, const StateBufs& b,
                    const ResidualIn& ri, double* r, double* u_out) {
   const Plan& P = c.P;
@@ -325,7 +338,7 @@ void forward_store(const Ctx& c, const double* theta, const double* x, int64_t n
   } else {
     launch_first_layer(x, n, P.d, theta + P.th[0], P.h[1], td, cdiag, b.zval0, b.post[1], c.s);
     for (int l = 1; l + 1 < L; ++l) {
-      GemmNT g{b.post[l], P.h[l], theta + P.th[l], P.p[l], b.pre[l], P.h[l + 1],
+      GemmNT g{b.post[l], P.h[l], wpad + P.wo[l], P.h[l], b.pre[l], P.h[l + 1],
                n * td.S, P.h[l + 1], P.h[l], theta + P.th[l] + P.h[l], P.p[l], td.S};
       prof_gemm(c, g);
       launch_act_fwd(b.pre[l], b.post[l + 1], n, P.h[l + 1], td, cdiag, c.s);
@@ -337,7 +350,7 @@ void forward_store(const Ctx& c, const double* theta, const double* x, int64_t n
 }
 
 // Forward pass for losses only (no stored states): ping-pong buffers, in-place activation.
-void forward_loss(const Ctx& c, const double* theta, const double* x, int64_t n,
+void forward_loss(const Ctx& c, const double* theta, const double* wpad, const double* x, int64_t n,
                   const TaylorDims& td, const double* cdiag, double* ping, double* pong,
                   const ResidualIn& ri, double* r, double* u_out) {
   const Plan& P = c.P;
@@ -355,7 +368,7 @@ void forward_loss(const Ctx& c, const double* theta, const double* x, int64_t n,
     double* a = ping;
     double* b = pong;
     for (int l = 1; l + 1 < L; ++l) {
-      GemmNT g{a, P.h[l], theta + P.th[l], P.p[l], b, P.h[l + 1],
+      GemmNT g{a, P.h[l], wpad + P.wo[l], P.h[l], b, P.h[l + 1],
                n * td.S, P.h[l + 1], P.h[l], theta + P.th[l] + P.h[l], P.p[l], td.S};
       prof_gemm(c, g);
       launch_act_fwd(b, b, n, P.h[l + 1], td, cdiag, c.s);
@@ -441,6 +454,7 @@ int phase_accumulate(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, cons
   KP_CUDA_TRY(cudaMemsetAsync(red, 0, sizeof(double) * P.r_count, c.s));
   for (int l = 1; l < P.L; ++l)
     launch_transpose(st->theta + P.th[l], P.p[l], P.q[l], P.h[l], c.at(P.o_wT[l]), c.s);
+  launch_candidate(st->theta, nullptr, 0, nullptr, P.D, P.wp, c.at(P.o_wpad), c.s);
   const TaylorDims tdi{P.S, P.d, true};
   const TaylorDims tdb{1, 0, false};
   const StateBufs bi = interior_bufs(c);
@@ -450,7 +464,7 @@ int phase_accumulate(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, cons
     const double* seeds = bt->seeds + n0 * P.S;
     double* r = c.at(P.o_r) + n0;
     ResidualIn ri{bt->r0 + n0, seeds, nullptr};
-    forward_store(c, st->theta, x, nc, tdi, bt->coeff_diag, bi, ri, r, nullptr);
+    forward_store(c, st->theta, c.at(P.o_wpad), x, nc, tdi, bt->coeff_diag, bi, ri, r, nullptr);
     backward(c, st->theta, nc, tdi, bt->coeff_diag, bi, seeds);
     accumulate(c, x, nc, tdi, bi, seeds, r, red + P.r_aint, red + P.r_bint, red + P.r_gint);
   }
@@ -458,8 +472,8 @@ int phase_accumulate(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, cons
   double* ones = c.at(P.o_ones);
   launch_fill(ones, P.Nb, 1.0, c.s);
   ResidualIn rb{nullptr, nullptr, bt->targets};
-  forward_store(c, st->theta, bt->x_bnd, P.Nb, tdb, bt->coeff_diag, bb, rb, c.at(P.o_rb),
-                nullptr);
+  forward_store(c, st->theta, c.at(P.o_wpad), bt->x_bnd, P.Nb, tdb, bt->coeff_diag, bb, rb,
+                c.at(P.o_rb), nullptr);
   backward(c, st->theta, P.Nb, tdb, bt->coeff_diag, bb, nullptr);
   accumulate(c, bt->x_bnd, P.Nb, tdb, bb, ones, c.at(P.o_rb), red + P.r_abnd, red + P.r_bbnd,
              red + P.r_gbnd);
@@ -554,16 +568,16 @@ int phase_linesearch(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, cons
   double* thc = c.at(P.o_thc);
   double* dir = c.at(P.o_dir);
   for (int k = 0; k < P.ncand; ++k) {
-    launch_candidate(st->theta, dir, cfg->ls_min_exp + k, thc, P.D, c.s);
+    launch_candidate(st->theta, dir, cfg->ls_min_exp + k, thc, P.D, P.wp, c.at(P.o_wpadc), c.s);
     for (int64_t n0 = 0; n0 < P.N; n0 += P.Nc) {
       const int64_t nc = std::min(P.Nc, P.N - n0);
       ResidualIn ri{bt->r0 + n0, bt->seeds + n0 * P.S, nullptr};
-      forward_loss(c, thc, bt->x_int + n0 * P.d, nc, tdi, bt->coeff_diag, c.at(P.o_ping),
+      forward_loss(c, thc, c.at(P.o_wpadc), bt->x_int + n0 * P.d, nc, tdi, bt->coeff_diag, c.at(P.o_ping),
                    c.at(P.o_pong), ri, c.at(P.o_rls) + k * P.N + n0, nullptr);
     }
     ResidualIn rb{nullptr, nullptr, bt->targets};
-    forward_loss(c, thc, bt->x_bnd, P.Nb, tdb, bt->coeff_diag, c.at(P.o_bping), c.at(P.o_bpong),
-                 rb, c.at(P.o_rbls) + k * P.Nb, nullptr);
+    forward_loss(c, thc, c.at(P.o_wpadc), bt->x_bnd, P.Nb, tdb, bt->coeff_diag, c.at(P.o_bping),
+                 c.at(P.o_bpong), rb, c.at(P.o_rbls) + k * P.Nb, nullptr);
   }
   double* ls = c.at(P.o_ls);
   launch_sumsq(c.at(P.o_rls), P.N, P.N, P.ncand, ls, 2, c.s);
@@ -815,11 +829,12 @@ int32_t kp_taylor_forward(kp_context* ctx, const kp_problem* prob, const double*
   if (!theta || !bt || !value || !gradient || !op) return KP_ERR_INVALID;
   Ctx c{ctx, P, static_cast<double*>(ws), (cudaStream_t)stream};
   const TaylorDims tdi{P.S, P.d, true};
+  launch_candidate(theta, nullptr, 0, nullptr, P.D, P.wp, c.at(P.o_wpad), c.s);
   for (int64_t n0 = 0; n0 < P.N; n0 += P.Nc) {
     const int64_t nc = std::min(P.Nc, P.N - n0);
     ResidualIn ri{nullptr, nullptr, nullptr};
     double* u = c.at(P.o_u);
-    forward_loss(c, theta, bt->x_int + n0 * P.d, nc, tdi, bt->coeff_diag, c.at(P.o_ping),
+    forward_loss(c, theta, c.at(P.o_wpad), bt->x_int + n0 * P.d, nc, tdi, bt->coeff_diag, c.at(P.o_ping),
                  c.at(P.o_pong), ri, nullptr, u);
     launch_split_u(u, nc, P.d, value + n0, gradient + n0 * P.d, op + n0, c.s);
   }
@@ -836,14 +851,15 @@ int32_t kp_evaluate_losses(kp_context* ctx, const kp_problem* prob, const double
   Ctx c{ctx, P, static_cast<double*>(ws), (cudaStream_t)stream};
   const TaylorDims tdi{P.S, P.d, true};
   const TaylorDims tdb{1, 0, false};
+  launch_candidate(theta, nullptr, 0, nullptr, P.D, P.wp, c.at(P.o_wpad), c.s);
   for (int64_t n0 = 0; n0 < P.N; n0 += P.Nc) {
     const int64_t nc = std::min(P.Nc, P.N - n0);
     ResidualIn ri{bt->r0 + n0, bt->seeds + n0 * P.S, nullptr};
-    forward_loss(c, theta, bt->x_int + n0 * P.d, nc, tdi, bt->coeff_diag, c.at(P.o_ping),
+    forward_loss(c, theta, c.at(P.o_wpad), bt->x_int + n0 * P.d, nc, tdi, bt->coeff_diag, c.at(P.o_ping),
                  c.at(P.o_pong), ri, c.at(P.o_r) + n0, nullptr);
   }
   ResidualIn rb{nullptr, nullptr, bt->targets};
-  forward_loss(c, theta, bt->x_bnd, P.Nb, tdb, bt->coeff_diag, c.at(P.o_bping), c.at(P.o_bpong),
+  forward_loss(c, theta, c.at(P.o_wpad), bt->x_bnd, P.Nb, tdb, bt->coeff_diag, c.at(P.o_bping), c.at(P.o_bpong),
                rb, c.at(P.o_rb), nullptr);
   double* ss = c.at(P.o_ls);
   launch_sumsq(c.at(P.o_r), P.N, 0, 1, ss, 1, c.s);
