@@ -168,7 +168,9 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-static bool make_map(CUtensorMap* m, const double* base, uint64_t rows, uint64_t cols, uint64_t ld,
+// 2-D FP64 tensor map, 16-column (128 B) boxes of box_rows rows, 128-byte swizzle;
+// cached by geometry (encoding is a host call).
+bool make_tma_map_2d(CUtensorMap* m, const double* base, uint64_t rows, uint64_t cols, uint64_t ld,
                      uint32_t box_rows) {
   using Key = std::tuple<const double*, uint64_t, uint64_t, uint64_t, uint32_t>;
   static std::map<Key, CUtensorMap> cache;
@@ -198,8 +200,8 @@ static bool make_map(CUtensorMap* m, const double* base, uint64_t rows, uint64_t
 template <int BM, int BN, int WM, int WN, int BK, int STAGES>
 static bool run_tma(const GemmNT& g, cudaStream_t s) {
   CUtensorMap ma, mb;
-  if (!make_map(&ma, g.A, (uint64_t)g.M, (uint64_t)g.K, (uint64_t)g.lda, BM)) return false;
-  if (!make_map(&mb, g.B, (uint64_t)g.N, (uint64_t)g.K, (uint64_t)g.ldb, BN)) return false;
+  if (!make_tma_map_2d(&ma, g.A, (uint64_t)g.M, (uint64_t)g.K, (uint64_t)g.lda, BM)) return false;
+  if (!make_tma_map_2d(&mb, g.B, (uint64_t)g.N, (uint64_t)g.K, (uint64_t)g.ldb, BN)) return false;
   const size_t smem = (size_t)STAGES * (BM + BN) * BK * sizeof(double) + 2 * STAGES * 8 + 1024;
   auto kern = k_gemm_nt_tma<BM, BN, WM, WN, BK, STAGES>;
   static bool attr_set = false;

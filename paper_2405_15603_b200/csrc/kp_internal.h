@@ -58,7 +58,22 @@ struct GemmTN {
 size_t gemm_tn_partial_doubles(int64_t R, int P, int Q, bool sym);
 void launch_gemm_tn_accumulate(const GemmTN& g, double* partial, double* acc, cudaStream_t s);
 
+// TMA-fed split-row reduction without bias columns (kp_gemm_tn_tma.cu):
+// acc[p*ldacc + q] += sum_r X[r,p] w(r) Y[r,q], p < nx, q < ny; w(r) = w[r / Sw].
+// Returns false when the operands are not TMA-compatible.
+size_t gemm_tn_tma_partial_doubles(int64_t R, int nx, int ny, bool sym);
+bool gemm_tn_tma_ok(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t R);
+bool launch_gemm_tn_tma_accumulate(const double* X, int64_t ldx, int nx, const double* Y,
+                                   int64_t ldy, int ny, const double* w, int Sw, int64_t R,
+                                   bool sym, double* partial, double* acc, int64_t ldacc,
+                                   cudaStream_t s);
+
 // ---- Taylor-mode elementwise kernels (kp_taylor.cu) ------------------------
+
+// out[j*os] += sum_{n} w_n X[n*rs + j] for j < ncols (w == nullptr: 1);
+// out[ncols*os] += add_count.  scratch: 64 * ncols doubles.
+void launch_colsum(const double* X, int64_t rs, int64_t n, int ncols, const double* w, double* out,
+                   int64_t os, double add_count, double* scratch, cudaStream_t s);
 
 struct TaylorDims {
   int S;       // rows per sample: d + 2 (Taylor) or 1 (plain)

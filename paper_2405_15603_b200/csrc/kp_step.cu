@@ -198,14 +198,19 @@ int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
   size_t part = 1;
   auto upd = [&](int64_t R, int Pp, int Qq, bool sym) {
     part = std::max(part, gemm_tn_partial_doubles(R, Pp, Qq, sym));
+    part = std::max(part, gemm_tn_tma_partial_doubles(R, Pp, Qq, sym));
   };
+  part = std::max(part, (size_t)64 * (P.maxh + P.maxq + 1));  // colsum scratch
   for (int64_t R : {P.Nc, P.Nb}) {
     const bool interior = (R == P.Nc);
     const int64_t rows = interior ? R * P.S : R;
     for (int l = 0; l < P.L; ++l) {
-      upd(l == 0 ? R : rows, P.p[l], P.p[l], true);
+      const int64_t Rz = l == 0 ? R : rows;
+      upd(Rz, P.p[l], P.p[l], true);
       upd(rows, P.q[l], P.q[l], true);
-      upd(l == 0 ? R : rows, P.q[l], P.p[l], false);
+      upd(Rz, P.q[l], P.p[l], false);
+      upd(Rz, P.h[l], P.h[l], true);    // TMA kernel: no bias column
+      upd(Rz, P.q[l], P.h[l], false);
     }
   }
   P.o_partial = take((int64_t)part);
@@ -411,7 +416,11 @@ void backward(const Ctx& c, const double* theta, int64_t n, const TaylorDims& td
   }
 }
 
-// Factor and gradient contractions of one pass into the reduce buffer.
+// Factor and gradient contractions of one pass into the reduce buffer.  The bulk of
+// every contraction runs in the TMA-fed DMMA kernel; the bias-augmentation row /
+// column (the virtual 1 on value rows, curvature.py:88-93) are value-row column
+// sums.  Operands that are not TMA-compatible (odd pitch) use the cp.async kernel,
+// which synthesises the bias column itself.
 void accumulate(const Ctx& c, const double* x, int64_t n, const TaylorDims& td,
                 const StateBufs& b, const double* gl_last, const double* r, double* accA,
                 double* accB, double* accG) {
@@ -420,30 +429,44 @@ void accumulate(const Ctx& c, const double* x, int64_t n, const TaylorDims& td,
   double* part = c.at(P.o_partial);
   const int64_t rows = n * td.S;
   for (int l = 0; l < L; ++l) {
-    const int q = P.q[l];
+    const int q = P.q[l], hz = P.h[l], p = P.p[l];
     const double* G = (l == L - 1) ? gl_last : b.gout[l];
+    const double* Z = (l == 0) ? x : b.post[l];
+    const int64_t ldz = (l == 0) ? P.d : P.h[l];
+    const int64_t Rz = (l == 0) ? n : rows;  // rows of the layer input matrix
+    const int Sz = (l == 0) ? 1 : td.S;      // its value-row period
     // A_l = sum zhat zhat^T over the bias-augmented layer inputs (curvature.py:112-114)
-    if (l == 0) {
-      GemmTN a{x, P.d, P.d, true, x, P.d, P.d, true, nullptr, 1, 1, n, true};
-      launch_gemm_tn_accumulate(a, part, accA + P.fa[0], c.s);
-    } else {
-      GemmTN a{b.post[l], P.h[l], P.h[l], true, b.post[l], P.h[l], P.h[l], true, nullptr, 1,
-               td.S, rows, true};
-      launch_gemm_tn_accumulate(a, part, accA + P.fa[l], c.s);
+    {
+      double* out = accA + P.fa[l];
+      if (launch_gemm_tn_tma_accumulate(Z, ldz, hz, Z, ldz, hz, nullptr, 1, Rz, true, part, out, p,
+                                        c.s)) {
+        launch_colsum(Z, (int64_t)Sz * ldz, n, hz, nullptr, out + (int64_t)hz * p, 1, (double)n,
+                      part, c.s);
+      } else {
+        GemmTN a{Z, ldz, hz, true, Z, ldz, hz, true, nullptr, 1, Sz, Rz, true};
+        launch_gemm_tn_accumulate(a, part, out, c.s);
+      }
     }
     // B_l = sum g g^T over all rows (curvature.py:113,115)
-    {
+    if (!launch_gemm_tn_tma_accumulate(G, q, q, G, q, q, nullptr, 1, rows, true, part,
+                                       accB + P.fb[l], q, c.s)) {
       GemmTN bb{G, q, q, false, G, q, q, false, nullptr, 1, 1, rows, true};
       launch_gemm_tn_accumulate(bb, part, accB + P.fb[l], c.s);
     }
-    // gradient = sum_n r_n sum_s g_{n,s} zhat_{n,s}^T (optim.py:170-176)
-    if (l == 0) {
-      GemmTN gg{G, (int64_t)td.S * q, q, false, x, P.d, P.d, true, r, 1, 1, n, false};
-      launch_gemm_tn_accumulate(gg, part, accG + P.th[0], c.s);
-      if (td.taylor) launch_grad0_deriv(G, r, n, P.d, q, accG + P.th[0], c.s);
-    } else {
-      GemmTN gg{G, q, q, false, b.post[l], P.h[l], P.h[l], true, r, td.S, td.S, rows, false};
-      launch_gemm_tn_accumulate(gg, part, accG + P.th[l], c.s);
+    // gradient = sum_n r_n sum_s g_{n,s} zhat_{n,s}^T (optim.py:170-176); for layer 0 only
+    // the value rows of Z0 = [x; I; 0] are dense (the derivative rows: k_grad0_deriv)
+    {
+      double* out = accG + P.th[l];
+      const int64_t ldg = (l == 0) ? (int64_t)td.S * q : q;
+      const int Sw = (l == 0) ? 1 : td.S;
+      if (launch_gemm_tn_tma_accumulate(G, ldg, q, Z, ldz, hz, r, Sw, Rz, false, part, out, p,
+                                        c.s)) {
+        launch_colsum(G, (int64_t)td.S * q, n, q, r, out + hz, p, 0.0, part, c.s);
+      } else {
+        GemmTN gg{G, ldg, q, false, Z, ldz, hz, true, r, Sw, Sz, Rz, false};
+        launch_gemm_tn_accumulate(gg, part, out, c.s);
+      }
+      if (l == 0 && td.taylor) launch_grad0_deriv(G, r, n, P.d, q, out, c.s);
     }
   }
 }

@@ -272,6 +272,58 @@ void launch_grad0_deriv(const double* gbar0, const double* r, int64_t n, int d, 
 }
 
 // ---------------------------------------------------------------------------
+// weighted value-row column sums: the bias row/column of the factors and of the
+// gradient (the virtual "1" entry of zhat, curvature.py:88-93), two passes with a
+// fixed summation order.
+
+constexpr int COLSUM_GROUPS = 64;
+
+__global__ void k_colsum_partial(const double* __restrict__ X, int64_t rs, int64_t n, int ncols,
+                                 const double* __restrict__ w, double* __restrict__ part) {
+  const int j = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int sub = threadIdx.x >> 5;  // 8 row lanes per block
+  const int g = blockIdx.y;
+  __shared__ double red[8][33];
+  double acc = 0.0;
+  if (j < ncols) {
+    const int64_t per = (n + COLSUM_GROUPS - 1) / COLSUM_GROUPS;
+    const int64_t lo = g * per, hi = min(n, lo + per);
+    for (int64_t r = lo + sub; r < hi; r += 8) {
+      const double v = X[r * rs + j];
+      acc += w ? w[r] * v : v;
+    }
+  }
+  red[sub][threadIdx.x & 31] = acc;
+  __syncthreads();
+  if (sub == 0 && j < ncols) {
+    double v = 0.0;
+    for (int k = 0; k < 8; ++k) v += red[k][threadIdx.x & 31];
+    part[(int64_t)g * ncols + j] = v;
+  }
+}
+
+__global__ void k_colsum_reduce(const double* __restrict__ part, int ncols, double* out,
+                                int64_t os, double add_count) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < ncols) {
+    double v = 0.0;
+    for (int g = 0; g < COLSUM_GROUPS; ++g) v += part[(int64_t)g * ncols + j];
+    out[(int64_t)j * os] += v;
+  }
+  if (j == 0 && add_count != 0.0) out[(int64_t)ncols * os] += add_count;
+}
+
+void launch_colsum(const double* X, int64_t rs, int64_t n, int ncols, const double* w, double* out,
+                   int64_t os, double add_count, double* scratch, cudaStream_t s) {
+  if (n <= 0 || ncols <= 0) return;
+  count_launch();
+  k_colsum_partial<<<dim3((unsigned)ceil_div(ncols, 32), COLSUM_GROUPS), 256, 0, s>>>(X, rs, n, ncols,
+                                                                                    w, scratch);
+  count_launch();
+  k_colsum_reduce<<<(unsigned)ceil_div(ncols, 128), 128, 0, s>>>(scratch, ncols, out, os, add_count);
+}
+
+// ---------------------------------------------------------------------------
 // small utilities
 
 __global__ void k_sumsq(const double* __restrict__ v, int64_t n, int64_t stride,
