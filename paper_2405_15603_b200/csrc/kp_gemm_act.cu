@@ -1,0 +1,280 @@
+// Fused Taylor layer: (N*S, K) x (K, N)^T FP64 DMMA GEMM + bias + tanh Taylor
+// activation (reference src/taylor.py:140-169) in one kernel, sm_100a.
+//
+// The activation of sample n mixes its S = d+2 rows (value, d derivatives,
+// operator row: L z_out = s1 L z + s2 sum_i c_ii g_i^2), so the M tiles are
+// SAMPLE-ALIGNED: a CTA owns nb = floor(128 / S) whole samples (c5: one 102-row
+// sample), loaded by a 2-D TMA box of round_up(nb*S, 8) rows starting at row
+// tile*nb*S, and 128 output units.  8 warps each own 16 units and all m8
+// tiles (up to 16).  After the k loop the pre-activation tile is staged in
+// shared memory (reusing the pipeline buffers) and one thread per
+// (sample, unit) walks the sample's S rows: computes s0, s1, s2 from the value
+// row, the derivative rows and the operator row, and writes them coalesced.
+//
+// Modes: STORE writes the pre-activation (needed by the reverse pass) and the
+// activation output; LOSS writes only the output (line search); LAST does not
+// write the output at all but reduces each row against the last layer's weight
+// vector (h_out = 1), leaving per-tile partial dot products for
+// k_last_from_partials — the line search never materialises the last hidden
+// state.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+
+#include "kp_common.cuh"
+#include "kp_internal.h"
+
+namespace kp {
+
+bool make_tma_map_2d(CUtensorMap* m, const double* base, uint64_t rows, uint64_t cols,
+                     uint64_t ld, uint32_t box_rows);  // kp_gemm_tma.cu
+
+namespace {
+
+constexpr int BN = 128, NWARP = 8, TM_MAX = 16, ROWS_MAX = 128, CPITCH = BN + 4;
+
+__device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* map, int x, int y,
+                                      uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];\n" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_addr(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ int sigma8(int g) { return (g >> 1) + ((g & 1) << 2); }
+
+template <int BK, int STAGES, int MODE, int TM>
+__global__ void __launch_bounds__(NWARP * 32, 1)
+    k_gemm_act(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+               GemmAct g, int tiles_n, int box_rows) {
+  constexpr int SLABS = BK / 16;
+  constexpr int A_STAGE = ROWS_MAX * BK, B_STAGE = BN * BK;
+  extern __shared__ __align__(1024) unsigned char act_raw[];
+  double* sm = reinterpret_cast<double*>(act_raw + ((1024 - (smem_addr(act_raw) & 1023)) & 1023));
+  double* As = sm;
+  double* Bs = sm + STAGES * A_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(Bs + STAGES * B_STAGE);
+  uint64_t* empty = full + STAGES;
+  double* Cs = sm;  // epilogue staging, aliases the (drained) pipeline
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tn = blockIdx.x % tiles_n;
+  const int64_t smp0 = (int64_t)(blockIdx.x / tiles_n) * g.nb;
+  const int S = g.S;
+  const int m0 = (int)(smp0 * S);
+  const int n0 = tn * BN;
+  const int KT = g.K / BK;
+  const uint32_t stage_bytes = (uint32_t)(box_rows + BN) * BK * sizeof(double);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NWARP);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto produce = [&](int kt) {
+    const int s = kt % STAGES;
+    mbar_arrive_expect_tx(&full[s], stage_bytes);
+#pragma unroll
+    for (int sl = 0; sl < SLABS; ++sl) {
+      tma2d(As + s * A_STAGE + sl * ROWS_MAX * 16, &mapA, kt * BK + sl * 16, m0, &full[s]);
+      tma2d(Bs + s * B_STAGE + sl * BN * 16, &mapB, kt * BK + sl * 16, n0, &full[s]);
+    }
+  };
+  if (threadIdx.x == 0)
+    for (int kt = 0; kt < STAGES && kt < KT; ++kt) produce(kt);
+
+  const int g4 = lane >> 2, t4 = lane & 3;
+  const int sg = sigma8(g4);
+  const int ch0 = ((0 + t4) ^ sg) * 2, ch1 = ((4 + t4) ^ sg) * 2;
+
+  double acc[TM][2][2];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  for (int kt = 0; kt < KT; ++kt) {
+    const int s = kt % STAGES;
+    const uint32_t par = (kt / STAGES) & 1;
+    mbar_wait(&full[s], par);
+#pragma unroll
+    for (int sl = 0; sl < SLABS; ++sl) {
+      const double* as = As + s * A_STAGE + sl * ROWS_MAX * 16 + sg * 16;
+      const double* bs = Bs + s * B_STAGE + sl * BN * 16 + (warp * 16 + sg) * 16;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int ch = half ? ch1 : ch0;
+        const double2 b0 = *reinterpret_cast<const double2*>(bs + ch);
+        const double2 b1 = *reinterpret_cast<const double2*>(bs + 8 * 16 + ch);
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+          const double2 a = *reinterpret_cast<const double2*>(as + i * 8 * 16 + ch);
+          dmma_8x8x4(acc[i][0][0], acc[i][0][1], a.x, b0.x);
+          dmma_8x8x4(acc[i][0][0], acc[i][0][1], a.y, b0.y);
+          dmma_8x8x4(acc[i][1][0], acc[i][1][1], a.x, b1.x);
+          dmma_8x8x4(acc[i][1][0], acc[i][1][1], a.y, b1.y);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (threadIdx.x == 0 && kt + STAGES < KT) {
+      mbar_wait(&empty[s], par);
+      produce(kt + STAGES);
+    }
+  }
+  __syncthreads();  // every stage consumed: the pipeline smem becomes the C tile
+
+  // stage pre-activations (+ value-row bias) in smem: row 8i + sigma(g), col 16w + 8j + t (+4)
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int row = i * 8 + sg;
+    const bool vrow = ((row % S) == 0) && g.bias != nullptr;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int c0 = warp * 16 + j * 8 + t4, c1 = c0 + 4;
+      double v0 = acc[i][j][0], v1 = acc[i][j][1];
+      if (vrow) {
+        if (n0 + c0 < g.N) v0 += g.bias[(int64_t)(n0 + c0) * g.bias_stride];
+        if (n0 + c1 < g.N) v1 += g.bias[(int64_t)(n0 + c1) * g.bias_stride];
+      }
+      Cs[row * CPITCH + c0] = v0;
+      Cs[row * CPITCH + c1] = v1;
+    }
+  }
+  __syncthreads();
+
+  const int64_t nsmp = (g.n_samples - smp0) < g.nb ? (g.n_samples - smp0) : (int64_t)g.nb;
+  const int ncol = min(BN, g.N - n0);
+  const int d = g.d;
+  for (int idx = threadIdx.x; idx < nsmp * BN; idx += NWARP * 32) {
+    const int k = idx / BN, j = idx % BN;
+    if (j >= ncol) continue;
+    double* cs = Cs + (k * S) * CPITCH + j;
+    const int64_t grow = (int64_t)m0 + k * S;
+    const TanhD t = tanh_derivs(cs[0], false);
+    if (MODE == ACT_STORE) g.pre[grow * g.ldo + n0 + j] = cs[0];
+    double o0 = t.s0;
+    if (MODE == ACT_LAST) cs[0] = o0;
+    else g.post[grow * g.ldo + n0 + j] = o0;
+    if (!g.taylor) continue;
+    double quad = 0.0;
+    for (int i = 1; i <= d; ++i) {
+      const double gi = cs[i * CPITCH];
+      quad += (gi * g.cdiag[i - 1]) * gi;
+      const double o = t.s1 * gi;
+      if (MODE == ACT_STORE) g.pre[(grow + i) * g.ldo + n0 + j] = gi;
+      if (MODE == ACT_LAST) cs[i * CPITCH] = o;
+      else g.post[(grow + i) * g.ldo + n0 + j] = o;
+    }
+    const double ell = cs[(d + 1) * CPITCH];
+    const double o = t.s1 * ell + t.s2 * quad;
+    if (MODE == ACT_STORE) g.pre[(grow + d + 1) * g.ldo + n0 + j] = ell;
+    if (MODE == ACT_LAST) cs[(d + 1) * CPITCH] = o;
+    else g.post[(grow + d + 1) * g.ldo + n0 + j] = o;
+  }
+  if (MODE == ACT_LAST) {
+    __syncthreads();
+    const int rows = (int)nsmp * S;
+    for (int r = warp; r < rows; r += NWARP) {
+      double a = 0.0;
+      for (int j = lane; j < ncol; j += 32) a = fma(Cs[r * CPITCH + j], g.wlast[n0 + j], a);
+      a = warp_sum(a);
+      if (lane == 0) g.upart[((int64_t)m0 + r) * tiles_n + tn] = a;
+    }
+  }
+}
+
+constexpr int ACT_BK = 32, ACT_STAGES = 3;
+
+template <int MODE, int TM>
+bool run_act(const GemmAct& g, int box_rows, cudaStream_t s) {
+  CUtensorMap ma, mb;
+  const int64_t M = g.n_samples * g.S;
+  if (!make_tma_map_2d(&ma, g.A, (uint64_t)M, (uint64_t)g.K, (uint64_t)g.lda, box_rows)) return false;
+  if (!make_tma_map_2d(&mb, g.B, (uint64_t)g.N, (uint64_t)g.K, (uint64_t)g.ldb, BN)) return false;
+  const size_t pipe = (size_t)ACT_STAGES * (ROWS_MAX + BN) * ACT_BK * sizeof(double);
+  const size_t cst = (size_t)ROWS_MAX * CPITCH * sizeof(double);
+  const size_t smem = std::max(pipe + 2 * ACT_STAGES * 8, cst) + 1024;
+  auto kern = k_gemm_act<ACT_BK, ACT_STAGES, MODE, TM>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = true;
+  }
+  const int tiles_n = (int)ceil_div(g.N, BN);
+  const int64_t tiles = ceil_div(g.n_samples, g.nb) * tiles_n;
+  count_launch();
+  kern<<<(unsigned)tiles, NWARP * 32, smem, s>>>(ma, mb, g, tiles_n, box_rows);
+  return true;
+}
+
+}  // namespace
+
+int gemm_act_samples_per_tile(int S) { return S <= ROWS_MAX ? ROWS_MAX / S : 0; }
+
+bool launch_gemm_act(GemmAct g, int mode, cudaStream_t s) {
+  if (g.n_samples <= 0) return true;
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (g.S > ROWS_MAX || g.K % ACT_BK != 0 || g.lda % 2 || g.ldb % 2 || !al16(g.A) || !al16(g.B) ||
+      g.n_samples * g.S >= (int64_t(1) << 31))
+    return false;
+  g.nb = gemm_act_samples_per_tile(g.S);
+  const int box_rows = (g.nb * g.S + 7) / 8 * 8;
+  // the m8-tile count is a template parameter: predicated-off DMMAs still occupy the
+  // tensor pipe, so a runtime guard over a 16-tile array wastes up to 16/tm of it
+  switch (box_rows / 8) {
+#define KP_ACT_CASE(T)                                                   \
+  case T:                                                                \
+    if (mode == ACT_STORE) return run_act<ACT_STORE, T>(g, box_rows, s); \
+    if (mode == ACT_LOSS) return run_act<ACT_LOSS, T>(g, box_rows, s);   \
+    return run_act<ACT_LAST, T>(g, box_rows, s);
+    KP_ACT_CASE(9)
+    KP_ACT_CASE(10)
+    KP_ACT_CASE(11)
+    KP_ACT_CASE(12)
+    KP_ACT_CASE(13)
+    KP_ACT_CASE(14)
+    KP_ACT_CASE(15)
+    KP_ACT_CASE(16)
+#undef KP_ACT_CASE
+    default:
+      return false;
+  }
+}
+
+// u_{n,s} = sum_t upart[(n*S+s)*ntn + t] + (s == 0) b;  residual as in k_last_layer.
+__global__ void k_last_from_partials(const double* __restrict__ upart, int ntn, int64_t n,
+                                     TaylorDims td, const double* __restrict__ bias,
+                                     const double* __restrict__ r0, const double* __restrict__ seeds,
+                                     const double* __restrict__ targets, double* __restrict__ r) {
+  for (int64_t smp = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; smp < n;
+       smp += (int64_t)gridDim.x * blockDim.x) {
+    double v = td.taylor ? r0[smp] : 0.0;
+    for (int s = 0; s < td.S; ++s) {
+      const double* up = upart + (smp * td.S + s) * ntn;
+      double u = 0.0;
+      for (int t = 0; t < ntn; ++t) u += up[t];
+      if (s == 0) u += bias[0];
+      if (td.taylor) v += seeds[smp * td.S + s] * u;
+      else v = u - targets[smp];
+    }
+    r[smp] = v;
+  }
+}
+
+void launch_last_from_partials(const double* upart, int ntn, int64_t n, TaylorDims td,
+                               const double* bias, const double* r0, const double* seeds,
+                               const double* targets, double* r, cudaStream_t s) {
+  if (n <= 0) return;
+  count_launch();
+  const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(n, 128), 148 * 16);
+  k_last_from_partials<<<blocks, 128, 0, s>>>(upart, ntn, n, td, bias, r0, seeds, targets, r);
+}
+
+}  // namespace kp

@@ -68,6 +68,31 @@ bool launch_gemm_tn_tma_accumulate(const double* X, int64_t ldx, int nx, const d
                                    bool sym, double* partial, double* acc, int64_t ldacc,
                                    cudaStream_t s);
 
+// ---- fused Taylor layer: GEMM + bias + activation (kp_gemm_act.cu) ----------
+struct TaylorDims;
+enum ActMode { ACT_STORE = 0, ACT_LOSS = 1, ACT_LAST = 2 };
+struct GemmAct {
+  const double* A;  // (n_samples*S) x K layer input
+  int64_t lda;
+  const double* B;  // N x K weights (pitch ldb)
+  int64_t ldb;
+  const double* bias;
+  int64_t bias_stride;
+  int64_t n_samples;
+  int S, d;
+  bool taylor;
+  int N, K;
+  const double* cdiag;
+  double* pre;    // ACT_STORE: pre-activation out
+  double* post;   // ACT_STORE / ACT_LOSS: activation out
+  int64_t ldo;
+  const double* wlast;  // ACT_LAST: last-layer weight row (length N)
+  double* upart;        // ACT_LAST: (n_samples*S) x ceil(N/128) partial dots
+  int nb;               // set by the launcher
+};
+int gemm_act_samples_per_tile(int S);
+bool launch_gemm_act(GemmAct g, int mode, cudaStream_t s);
+
 // ---- Taylor-mode elementwise kernels (kp_taylor.cu) ------------------------
 
 // out[j*os] += sum_{n} w_n X[n*rs + j] for j < ncols (w == nullptr: 1);
@@ -109,6 +134,10 @@ struct ActBwd {
 };
 void launch_act_bwd(const ActBwd& a, int64_t n, int h, TaylorDims td, const double* cdiag,
                     cudaStream_t s);
+// Scalar output from ACT_LAST partials + residual (same semantics as launch_last_layer).
+void launch_last_from_partials(const double* upart, int ntn, int64_t n, TaylorDims td,
+                               const double* bias, const double* r0, const double* seeds,
+                               const double* targets, double* r, cudaStream_t s);
 // Layer-0 gradient, derivative-row part: acc[j*(d+1)+i] += sum_n r_n gbar0[n, 1+i, j].
 void launch_grad0_deriv(const double* gbar0, const double* r, int64_t n, int d, int h1,
                         double* acc, cudaStream_t s);

@@ -95,7 +95,7 @@ struct Plan {
   int64_t o_ping = 0, o_pong = 0;
   int64_t o_bzval0 = 0, o_bpost[MAXL] = {}, o_bpre[MAXL] = {}, o_bg[MAXL] = {};
   int64_t o_bping = 0, o_bpong = 0, o_ones = 0;
-  int64_t o_r = 0, o_rb = 0, o_rls = 0, o_rbls = 0, o_u = 0;
+  int64_t o_r = 0, o_rb = 0, o_rls = 0, o_rbls = 0, o_u = 0, o_upart = 0;
   int64_t o_partial = 0, o_red = 0, o_grad = 0, o_delta = 0, o_dir = 0, o_thc = 0, o_ls = 0;
   int64_t o_A1 = 0, o_A2 = 0, o_B1 = 0, o_B2 = 0, o_la = 0, o_lb = 0, o_T1 = 0, o_T2 = 0;
   int64_t o_work = 0, o_info = 0;
@@ -183,6 +183,7 @@ int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
   P.o_ping = take(Mc * P.maxh);
   P.o_pong = take(Mc * P.maxh);
   P.o_u = take(Mc);
+  P.o_upart = take(std::max(Mc, P.Nb) * ceil_div(std::max(P.maxh, 1), 128));
   P.o_bzval0 = take(P.Nb * P.h[1]);
   for (int l = 1; l < P.L; ++l) P.o_bpost[l] = take(P.Nb * P.h[l]);
   for (int l = 1; l + 1 < P.L; ++l) P.o_bpre[l] = take(P.Nb * P.h[l + 1]);
@@ -263,11 +264,12 @@ struct Ctx {
   double* at(int64_t off) const { return W + off; }
 };
 
-// Optional CUDA-event timing of the hidden-layer forward GEMMs.
-void prof_gemm(const Ctx& c, const GemmNT& g) {
+// Optional CUDA-event timing of the hidden-layer forward GEMMs (fused or not).
+template <typename F>
+void prof_launch(const Ctx& c, double flops, F&& launch) {
   kp_context* ctx = c.ctx;
   if (!ctx->profile) {
-    launch_gemm_nt(g, c.s);
+    launch();
     return;
   }
   if (ctx->ev_used + 2 > ctx->ev.size()) {
@@ -278,11 +280,49 @@ void prof_gemm(const Ctx& c, const GemmNT& g) {
     }
   }
   cudaEventRecord(ctx->ev[ctx->ev_used], c.s);
-  launch_gemm_nt(g, c.s);
+  launch();
   cudaEventRecord(ctx->ev[ctx->ev_used + 1], c.s);
   ctx->ev_used += 2;
-  ctx->prof_flops += 2.0 * (double)g.M * g.N * g.K;
+  ctx->prof_flops += flops;
   ctx->prof_launches += 1;
+}
+
+void prof_gemm(const Ctx& c, const GemmNT& g) {
+  prof_launch(c, 2.0 * (double)g.M * g.N * g.K, [&] { launch_gemm_nt(g, c.s); });
+}
+
+// Hidden layer l forward: fused GEMM + bias + activation when possible, else GEMM then
+// the elementwise activation kernel.  mode: ACT_STORE (pre + post), ACT_LOSS (post).
+void hidden_layer(const Ctx& c, const double* theta, const double* wpad, int l, const double* in,
+                  int64_t n, const TaylorDims& td, const double* cdiag, double* pre, double* post,
+                  int mode) {
+  const Plan& P = c.P;
+  GemmAct ga{};
+  ga.A = in;
+  ga.lda = P.h[l];
+  ga.B = wpad + P.wo[l];
+  ga.ldb = P.h[l];
+  ga.bias = theta + P.th[l] + P.h[l];
+  ga.bias_stride = P.p[l];
+  ga.n_samples = n;
+  ga.S = td.S;
+  ga.d = td.d;
+  ga.taylor = td.taylor;
+  ga.N = P.h[l + 1];
+  ga.K = P.h[l];
+  ga.cdiag = cdiag;
+  ga.pre = pre;
+  ga.post = post;
+  ga.ldo = P.h[l + 1];
+  bool done = false;
+  prof_launch(c, 2.0 * (double)n * td.S * P.h[l] * P.h[l + 1],
+              [&] { done = launch_gemm_act(ga, mode, c.s); });
+  if (done) return;
+  double* out = mode == ACT_STORE ? pre : post;
+  GemmNT g{in, P.h[l], wpad + P.wo[l], P.h[l], out, P.h[l + 1], n * td.S, P.h[l + 1], P.h[l],
+           theta + P.th[l] + P.h[l], P.p[l], td.S};
+  prof_gemm(c, g);
+  launch_act_fwd(out, post, n, P.h[l + 1], td, cdiag, c.s);
 }
 
 struct StateBufs {
@@ -342,12 +382,8 @@ void forward_store(const Ctx& c, const double* theta, const double* wpad, const 
     }
   } else {
     launch_first_layer(x, n, P.d, theta + P.th[0], P.h[1], td, cdiag, b.zval0, b.post[1], c.s);
-    for (int l = 1; l + 1 < L; ++l) {
-      GemmNT g{b.post[l], P.h[l], wpad + P.wo[l], P.h[l], b.pre[l], P.h[l + 1],
-               n * td.S, P.h[l + 1], P.h[l], theta + P.th[l] + P.h[l], P.p[l], td.S};
-      prof_gemm(c, g);
-      launch_act_fwd(b.pre[l], b.post[l + 1], n, P.h[l + 1], td, cdiag, c.s);
-    }
+    for (int l = 1; l + 1 < L; ++l)
+      hidden_layer(c, theta, wpad, l, b.post[l], n, td, cdiag, b.pre[l], b.post[l + 1], ACT_STORE);
     last_in = b.post[L - 1];
   }
   launch_last_layer(last_in, n, P.h[L - 1], theta + P.th[L - 1], td, ri.r0, ri.seeds, ri.targets,
@@ -373,10 +409,35 @@ void forward_loss(const Ctx& c, const double* theta, const double* wpad, const d
     double* a = ping;
     double* b = pong;
     for (int l = 1; l + 1 < L; ++l) {
-      GemmNT g{a, P.h[l], wpad + P.wo[l], P.h[l], b, P.h[l + 1],
-               n * td.S, P.h[l + 1], P.h[l], theta + P.th[l] + P.h[l], P.p[l], td.S};
-      prof_gemm(c, g);
-      launch_act_fwd(b, b, n, P.h[l + 1], td, cdiag, c.s);
+      if (l == L - 2 && u_out == nullptr) {
+        // last hidden layer: fuse the h_out = 1 output layer, never store this state
+        GemmAct ga{};
+        ga.A = a;
+        ga.lda = P.h[l];
+        ga.B = wpad + P.wo[l];
+        ga.ldb = P.h[l];
+        ga.bias = theta + P.th[l] + P.h[l];
+        ga.bias_stride = P.p[l];
+        ga.n_samples = n;
+        ga.S = td.S;
+        ga.d = td.d;
+        ga.taylor = td.taylor;
+        ga.N = P.h[l + 1];
+        ga.K = P.h[l];
+        ga.cdiag = cdiag;
+        ga.wlast = theta + P.th[L - 1];
+        ga.upart = c.at(P.o_upart);
+        bool done = false;
+        prof_launch(c, 2.0 * (double)n * td.S * P.h[l] * P.h[l + 1],
+                    [&] { done = launch_gemm_act(ga, ACT_LAST, c.s); });
+        if (done) {
+          launch_last_from_partials(c.at(P.o_upart), (int)ceil_div(P.h[l + 1], 128), n, td,
+                                    theta + P.th[L - 1] + P.h[L - 1], ri.r0, ri.seeds, ri.targets,
+                                    r, c.s);
+          return;
+        }
+      }
+      hidden_layer(c, theta, wpad, l, a, n, td, cdiag, b, b, ACT_LOSS);
       std::swap(a, b);
     }
     cur = a;
