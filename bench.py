@@ -235,6 +235,7 @@ def run_ours(args):
     eng.profile(False)
     clk = clocks.stop()
     launches = (k1 - k0) // max(args.steps, 1)
+    chunk = int(eng.prob.chunk)
 
     t = torch.tensor([ms_total, gemm_ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -249,7 +250,11 @@ def run_ours(args):
     # end to end through the public API (host numpy in, host numpy out), 1 GPU
     e2e = None
     if not args.no_e2e and world == 1:
+        eng.close()  # release the device-timed engine's workspace first
+        del eng, do_step
+        torch.cuda.empty_cache()
         e2e = run_e2e(args, wl, prob, params, batch)
+        eng = None
     elif not args.no_e2e and world > 1:
         e2e = run_e2e_sharded(args, wl, prob, params, batch, rank, world, eng, stepper)
 
@@ -280,7 +285,7 @@ def run_ours(args):
             "data": "synthetic (reference seeding recipe, SURVEY.md §8d)",
             "config": {"workload": wl.name, "widths": list(wl.widths), "n_interior_per_gpu": n_loc,
                        "n_boundary_per_gpu": nb_loc, "n_interior_total": n_glob,
-                       "n_boundary_total": nb_glob, "chunk": int(eng.prob.chunk),
+                       "n_boundary_total": nb_glob, "chunk": chunk,
                        "parallelism": f"dp{world}",
                        "l2": "working set (Taylor states, GBs) far larger than the 126 MB L2"},
             "kfac_steps_per_s": steps_per_s,

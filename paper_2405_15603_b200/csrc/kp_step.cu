@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <thread>
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -52,7 +53,32 @@ struct kp_context {
   double prof_flops = 0.0;
   int64_t prof_launches = 0;
   double prof_ms_done = 0.0;
+  // side streams for the per-layer Kronecker-sum solves (2 per layer: A and B factor pairs)
+  std::vector<cudaStream_t> side;
+  std::vector<cusolverDnHandle_t> side_solver;
+  std::vector<cublasHandle_t> side_blas;
+  std::vector<cudaEvent_t> side_ev;
 };
+
+static int ensure_side_streams(kp_context* c, int n) {
+  while ((int)c->side.size() < n) {
+    cudaStream_t s;
+    KP_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    cusolverDnHandle_t h;
+    if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) return KP_ERR_CUDA;
+    cusolverDnSetStream(h, s);
+    cublasHandle_t b;
+    if (cublasCreate(&b) != CUBLAS_STATUS_SUCCESS) return KP_ERR_CUDA;
+    cublasSetStream(b, s);
+    cudaEvent_t e;
+    KP_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->side.push_back(s);
+    c->side_solver.push_back(h);
+    c->side_blas.push_back(b);
+    c->side_ev.push_back(e);
+  }
+  return KP_OK;
+}
 
 #define KP_SOLVER_TRY(expr)                                                          \
   do {                                                                               \
@@ -99,6 +125,11 @@ struct Plan {
   int64_t o_partial = 0, o_red = 0, o_grad = 0, o_delta = 0, o_dir = 0, o_thc = 0, o_ls = 0;
   int64_t o_A1 = 0, o_A2 = 0, o_B1 = 0, o_B2 = 0, o_la = 0, o_lb = 0, o_T1 = 0, o_T2 = 0;
   int64_t o_work = 0, o_info = 0;
+  // per-layer Kronecker-solve scratch (layers solve concurrently on side streams)
+  int64_t k_A1[MAXL] = {}, k_A2[MAXL] = {}, k_B1[MAXL] = {}, k_B2[MAXL] = {}, k_la[MAXL] = {},
+          k_lb[MAXL] = {}, k_T1[MAXL] = {}, k_T2[MAXL] = {}, k_wa[MAXL] = {}, k_wb[MAXL] = {},
+          k_info[MAXL] = {};
+  int lw[MAXL][2] = {};
   int64_t o_wpad = 0, o_wpadc = 0, wo[MAXL] = {};
   WPack wp{};
   int64_t lwork = 0;
@@ -241,17 +272,33 @@ int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
   P.o_T2 = take((int64_t)P.maxp * P.maxq);
   int lwork = 1;
   for (int l = 0; l < P.L; ++l) {
-    for (int n : {P.p[l], P.q[l]}) {
+    for (int k = 0; k < 2; ++k) {
+      const int n = k == 0 ? P.p[l] : P.q[l];
       int lw = 0;
       KP_SOLVER_TRY(cusolverDnDsygvd_bufferSize(ctx->solver, CUSOLVER_EIG_TYPE_1,
                                                 CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
                                                 n, nullptr, n, nullptr, n, nullptr, &lw));
+      P.lw[l][k] = std::max(lw, 1);
       lwork = std::max(lwork, lw);
     }
   }
   P.lwork = lwork;
   P.o_work = take(lwork);
   P.o_info = take(8);
+  for (int l = 0; l < P.L; ++l) {
+    const int64_t p = P.p[l], q = P.q[l];
+    P.k_A1[l] = take(p * p);
+    P.k_A2[l] = take(p * p);
+    P.k_B1[l] = take(q * q);
+    P.k_B2[l] = take(q * q);
+    P.k_la[l] = take(p);
+    P.k_lb[l] = take(q);
+    P.k_T1[l] = take(p * q);
+    P.k_T2[l] = take(p * q);
+    P.k_wa[l] = take(P.lw[l][0]);
+    P.k_wb[l] = take(P.lw[l][1]);
+    P.k_info[l] = take(4);
+  }
   P.total = o;
   return KP_OK;
 }
@@ -572,36 +619,48 @@ int phase_accumulate(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, cons
 // T_A^T A1 T_A = diag(la) (likewise B), X = T_B [(T_B^T G T_A) / (lb la^T + 1)] T_A^T
 // solves B1 X A1 + B2 X A2 = G — the same unique solution as the reference's
 // inverse-square-root route.  Writes out = sign * X (q x p row-major).
+// Generalised symmetric-definite eigenproblem M1 x = lam M2 x (cuSOLVER sygvd, type 1):
+// Cholesky of M2 + eigh; on return M1 holds T with T^T M2 T = I, T^T M1 T = diag(lam).
+int gen_eig(cusolverDnHandle_t h, int n, double* M1, double* M2, double* lam, double* work,
+            int lwork, int* info) {
+  KP_SOLVER_TRY(cusolverDnDsygvd(h, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
+                                 CUBLAS_FILL_MODE_LOWER, n, M1, n, M2, n, lam, work, lwork, info));
+  return KP_OK;
+}
+
+// out (q x p row-major) = sign * T_B [(T_B^T G T_A) / (lb la^T + 1)] T_A^T.  Column-major
+// views: G^T is p x q (ld p), T_A = A1 (p x p), T_B = B1 (q x q).
+int kron_combine(cublasHandle_t h, cudaStream_t s, int p, int q, const double* TA,
+                 const double* la, const double* TB, const double* lb, const double* G,
+                 double* out, double sign, double* T1, double* T2) {
+  const double one = 1.0, zero = 0.0;
+  KP_BLAS_TRY(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, p, q, q, &one, G, p, TB, q, &zero, T1, p));
+  KP_BLAS_TRY(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, p, q, p, &one, TA, p, T1, p, &zero, T2, p));
+  launch_kron_scale(T2, la, p, lb, q, s);
+  KP_BLAS_TRY(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, p, q, q, &one, T2, p, TB, q, &zero, T1, p));
+  KP_BLAS_TRY(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, p, q, p, &sign, TA, p, T1, p, &zero, out, p));
+  return KP_OK;
+}
+
+// Damped two-term Kronecker-sum solve for one layer (linalg.py:136-174) by the
+// generalised symmetric-definite eigenproblems A1 x = l A2 x, B1 y = m B2 y:
+// with T_A^T A2 T_A = I, T_A^T A1 T_A = diag(la) (likewise B),
+// X = T_B [(T_B^T G T_A) / (lb la^T + 1)] T_A^T solves B1 X A1 + B2 X A2 = G — the
+// same unique solution as the reference's inverse-square-root route.  Single stream.
 int kron_solve(kp_context* ctx, const Ctx& c, int p, int q, double* A1, double* A2, double* B1,
                double* B2, const double* G, double* out, double sign, int* info,
                int32_t* status) {
   const Plan& P = c.P;
   double* la = c.at(P.o_la);
   double* lb = c.at(P.o_lb);
-  double* T1 = c.at(P.o_T1);
-  double* T2 = c.at(P.o_T2);
   double* work = c.at(P.o_work);
   KP_SOLVER_TRY(cusolverDnSetStream(ctx->solver, c.s));
   KP_BLAS_TRY(cublasSetStream(ctx->blas, c.s));
-  KP_SOLVER_TRY(cusolverDnDsygvd(ctx->solver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
-                                 CUBLAS_FILL_MODE_LOWER, p, A1, p, A2, p, la, work,
-                                 (int)P.lwork, info));
-  KP_SOLVER_TRY(cusolverDnDsygvd(ctx->solver, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
-                                 CUBLAS_FILL_MODE_LOWER, q, B1, q, B2, q, lb, work,
-                                 (int)P.lwork, info + 1));
+  KP_TRY(gen_eig(ctx->solver, p, A1, A2, la, work, (int)P.lwork, info));
+  KP_TRY(gen_eig(ctx->solver, q, B1, B2, lb, work, (int)P.lwork, info + 1));
   launch_eig_status(la, p, lb, q, info, status, c.s);
-  // column-major views: G^T is p x q (ld p); T_A = A1 (p x p), T_B = B1 (q x q)
-  const double one = 1.0, zero = 0.0;
-  KP_BLAS_TRY(cublasDgemm(ctx->blas, CUBLAS_OP_N, CUBLAS_OP_N, p, q, q, &one, G, p, B1, q, &zero,
-                          T1, p));  // G^T T_B
-  KP_BLAS_TRY(cublasDgemm(ctx->blas, CUBLAS_OP_T, CUBLAS_OP_N, p, q, p, &one, A1, p, T1, p, &zero,
-                          T2, p));  // (T_B^T G T_A)^T
-  launch_kron_scale(T2, la, p, lb, q, c.s);
-  KP_BLAS_TRY(cublasDgemm(ctx->blas, CUBLAS_OP_N, CUBLAS_OP_T, p, q, q, &one, T2, p, B1, q, &zero,
-                          T1, p));  // Y^T T_B^T
-  KP_BLAS_TRY(cublasDgemm(ctx->blas, CUBLAS_OP_N, CUBLAS_OP_N, p, q, p, &sign, A1, p, T1, p,
-                          &zero, out, p));  // sign * (T_B Y T_A^T)^T
-  return KP_OK;
+  return kron_combine(ctx->blas, c.s, p, q, A1, la, B1, lb, G, out, sign, c.at(P.o_T1),
+                      c.at(P.o_T2));
 }
 
 int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp_step_out* out) {
@@ -623,20 +682,55 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
   launch_grad_finalize(red + P.r_gint, red + P.r_gbnd, Ng, Nbg, grad, P.D, c.s);
   launch_losses(red + P.r_ss, Ng, Nbg, out->scalars, c.s);
   double* delta = c.at(P.o_delta);
-  int* info = reinterpret_cast<int*>(c.at(P.o_info));
   const double lam = cfg->damping;
-  for (int l = 0; l < P.L; ++l) {
-    double* A1 = c.at(P.o_A1);
-    double* A2 = c.at(P.o_A2);
-    double* B1 = c.at(P.o_B1);
-    double* B2 = c.at(P.o_B2);
-    launch_damped_copy(st->a_int + P.fa[l], lam, P.p[l], A1, c.s);
-    launch_damped_copy(st->a_bnd + P.fa[l], lam, P.p[l], A2, c.s);
-    launch_damped_copy(st->b_int + P.fb[l], lam, P.q[l], B1, c.s);
-    launch_damped_copy(st->b_bnd + P.fb[l], lam, P.q[l], B2, c.s);
-    KP_TRY(kron_solve(c.ctx, c, P.p[l], P.q[l], A1, A2, B1, B2, grad + P.th[l], delta + P.th[l],
-                      -1.0, info, out->status));
+  // The 2L generalised eigenproblems are independent: fan out over side streams (A and B
+  // factor pair of layer l on streams 2l and 2l+1), combine on 2l, join back.
+  kp_context* ctx = c.ctx;
+  KP_TRY(ensure_side_streams(ctx, 2 * P.L + 1));
+  cudaEvent_t ready = ctx->side_ev[2 * P.L];
+  KP_CUDA_TRY(cudaEventRecord(ready, c.s));
+  // cuSOLVER's sygvd blocks the calling host thread, so each factor-pair solve is issued
+  // from its own host thread (own handle + stream) to let the 2L solves overlap on the GPU.
+  std::vector<int> rc(2 * P.L, KP_OK);
+  auto solve_pair = [&](int l, int k) {
+    cudaSetDevice(ctx->device);
+    cudaStream_t s = ctx->side[2 * l + k];
+    if (cudaStreamWaitEvent(s, ready, 0) != cudaSuccess) {
+      rc[2 * l + k] = KP_ERR_CUDA;
+      return;
+    }
+    int* info = reinterpret_cast<int*>(c.at(P.k_info[l])) + k;
+    if (k == 0) {
+      launch_damped_copy(st->a_int + P.fa[l], lam, P.p[l], c.at(P.k_A1[l]), s);
+      launch_damped_copy(st->a_bnd + P.fa[l], lam, P.p[l], c.at(P.k_A2[l]), s);
+      rc[2 * l] = gen_eig(ctx->side_solver[2 * l], P.p[l], c.at(P.k_A1[l]), c.at(P.k_A2[l]),
+                          c.at(P.k_la[l]), c.at(P.k_wa[l]), P.lw[l][0], info);
+    } else {
+      launch_damped_copy(st->b_int + P.fb[l], lam, P.q[l], c.at(P.k_B1[l]), s);
+      launch_damped_copy(st->b_bnd + P.fb[l], lam, P.q[l], c.at(P.k_B2[l]), s);
+      rc[2 * l + 1] = gen_eig(ctx->side_solver[2 * l + 1], P.q[l], c.at(P.k_B1[l]),
+                              c.at(P.k_B2[l]), c.at(P.k_lb[l]), c.at(P.k_wb[l]), P.lw[l][1], info);
+    }
+    cudaEventRecord(ctx->side_ev[2 * l + k], s);
+  };
+  {
+    std::vector<std::thread> pool;
+    for (int l = 0; l < P.L; ++l)
+      for (int k = 0; k < 2; ++k) pool.emplace_back(solve_pair, l, k);
+    for (auto& t : pool) t.join();
   }
+  for (int v : rc) KP_TRY(v);
+  for (int l = 0; l < P.L; ++l) {
+    cudaStream_t s = ctx->side[2 * l];
+    KP_CUDA_TRY(cudaStreamWaitEvent(s, ctx->side_ev[2 * l + 1], 0));
+    launch_eig_status(c.at(P.k_la[l]), P.p[l], c.at(P.k_lb[l]), P.q[l],
+                      reinterpret_cast<int*>(c.at(P.k_info[l])), out->status, s);
+    KP_TRY(kron_combine(ctx->side_blas[2 * l], s, P.p[l], P.q[l], c.at(P.k_A1[l]), c.at(P.k_la[l]),
+                        c.at(P.k_B1[l]), c.at(P.k_lb[l]), grad + P.th[l], delta + P.th[l], -1.0,
+                        c.at(P.k_T1[l]), c.at(P.k_T2[l])));
+    KP_CUDA_TRY(cudaEventRecord(ctx->side_ev[2 * l], s));
+  }
+  for (int l = 0; l < P.L; ++l) KP_CUDA_TRY(cudaStreamWaitEvent(c.s, ctx->side_ev[2 * l], 0));
   launch_axpy_out(delta, st->prev_update, cfg->momentum, c.at(P.o_dir), P.D, c.s);
   if (out->grad) KP_CUDA_TRY(cudaMemcpyAsync(out->grad, grad, sizeof(double) * P.D,
                                              cudaMemcpyDeviceToDevice, c.s));
@@ -737,6 +831,13 @@ int32_t kp_context_create(int32_t device, kp_context** out) {
 
 int32_t kp_context_destroy(kp_context* c) {
   if (!c) return KP_OK;
+  for (size_t k = 0; k < c->side.size(); ++k) {
+    cudaStreamSynchronize(c->side[k]);
+    cusolverDnDestroy(c->side_solver[k]);
+    cublasDestroy(c->side_blas[k]);
+    cudaEventDestroy(c->side_ev[k]);
+    cudaStreamDestroy(c->side[k]);
+  }
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   if (c->blas) cublasDestroy(c->blas);
   if (c->solver) cusolverDnDestroy(c->solver);
