@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--force-dist", action="store_true",
+                    help="use the sharded NCCL step even at world size 1 (plumbing check)")
     return ap.parse_args()
 
 
@@ -184,7 +186,8 @@ def run_ours(args):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    sharded = world > 1 or args.force_dist
+    if sharded:
         dist.init_process_group("nccl", device_id=dev)
     wl = configs.WORKLOADS[args.workload]
     n_loc = args.n_interior
@@ -193,11 +196,11 @@ def run_ours(args):
     prob, params, batch = wl.build(0, n_glob, nb_glob)
 
     def barrier():
-        if world > 1:
+        if sharded:
             dist.barrier()
         torch.cuda.synchronize()
 
-    if world > 1:
+    if sharded:
         eng = make_rank_engine(wl.widths, batch, prob, rank, world, ema=wl.ema, damping=wl.damping,
                                momentum=wl.momentum, chunk=args.chunk or None)
         stepper = ShardedKfacStep(eng, torch_all_reduce())
@@ -238,7 +241,7 @@ def run_ours(args):
     chunk = int(eng.prob.chunk)
 
     t = torch.tensor([ms_total, gemm_ms], dtype=torch.float64, device=dev)
-    if world > 1:
+    if sharded:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total, gemm_ms_max = float(t[0]), float(t[1])
     ms_step = ms_total / args.steps
@@ -249,13 +252,13 @@ def run_ours(args):
 
     # end to end through the public API (host numpy in, host numpy out), 1 GPU
     e2e = None
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e and not sharded:
         eng.close()  # release the device-timed engine's workspace first
         del eng, do_step
         torch.cuda.empty_cache()
         e2e = run_e2e(args, wl, prob, params, batch)
         eng = None
-    elif not args.no_e2e and world > 1:
+    elif not args.no_e2e and sharded:
         e2e = run_e2e_sharded(args, wl, prob, params, batch, rank, world, eng, stepper)
 
     cpu = None
@@ -306,7 +309,7 @@ def run_ours(args):
             "losses_last_step": infos[-1][2:] if infos else None,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded:
         dist.barrier()
         dist.destroy_process_group()
 

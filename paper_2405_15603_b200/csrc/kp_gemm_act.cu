@@ -32,7 +32,7 @@ bool make_tma_map_2d(CUtensorMap* m, const double* base, uint64_t rows, uint64_t
 
 namespace {
 
-constexpr int BN = 128, NWARP = 8, TM_MAX = 16, ROWS_MAX = 128, CPITCH = BN + 4;
+constexpr int BN = 128, ROWS_MAX = 128, CPITCH = BN + 4;
 
 __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* map, int x, int y,
                                       uint64_t* bar) {
@@ -45,12 +45,18 @@ __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* map, int x, 
 
 __device__ __forceinline__ int sigma8(int g) { return (g >> 1) + ((g & 1) << 2); }
 
-template <int BK, int STAGES, int MODE, int TM>
-__global__ void __launch_bounds__(NWARP * 32, 1)
+// NW warps, each owning BN / NW output units and all TM m8 tiles.  NW = 4 keeps the
+// per-CTA footprint small enough for two co-resident CTAs per SM (one's epilogue
+// overlaps the other's DMMA loop); NW = 8 serves the 15-16 tile shapes.
+template <int BK, int STAGES, int MODE, int TM, int NW>
+__global__ void __launch_bounds__(NW * 32, 8 / NW)
     k_gemm_act(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                GemmAct g, int tiles_n, int box_rows) {
+  constexpr int NWARP = NW;
+  constexpr int WCOLS = BN / NW, TNW = WCOLS / 8;  // units and n8 tiles per warp
   constexpr int SLABS = BK / 16;
-  constexpr int A_STAGE = ROWS_MAX * BK, B_STAGE = BN * BK;
+  constexpr int AROWS = TM * 8;
+  constexpr int A_STAGE = AROWS * BK, B_STAGE = BN * BK;
   extern __shared__ __align__(1024) unsigned char act_raw[];
   double* sm = reinterpret_cast<double*>(act_raw + ((1024 - (smem_addr(act_raw) & 1023)) & 1023));
   double* As = sm;
@@ -81,7 +87,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
     mbar_arrive_expect_tx(&full[s], stage_bytes);
 #pragma unroll
     for (int sl = 0; sl < SLABS; ++sl) {
-      tma2d(As + s * A_STAGE + sl * ROWS_MAX * 16, &mapA, kt * BK + sl * 16, m0, &full[s]);
+      tma2d(As + s * A_STAGE + sl * AROWS * 16, &mapA, kt * BK + sl * 16, m0, &full[s]);
       tma2d(Bs + s * B_STAGE + sl * BN * 16, &mapB, kt * BK + sl * 16, n0, &full[s]);
     }
   };
@@ -92,11 +98,11 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
   const int sg = sigma8(g4);
   const int ch0 = ((0 + t4) ^ sg) * 2, ch1 = ((4 + t4) ^ sg) * 2;
 
-  double acc[TM][2][2];
+  double acc[TM][TNW][2];
 #pragma unroll
   for (int i = 0; i < TM; ++i)
 #pragma unroll
-    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < TNW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   for (int kt = 0; kt < KT; ++kt) {
     const int s = kt % STAGES;
@@ -104,20 +110,22 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
     mbar_wait(&full[s], par);
 #pragma unroll
     for (int sl = 0; sl < SLABS; ++sl) {
-      const double* as = As + s * A_STAGE + sl * ROWS_MAX * 16 + sg * 16;
-      const double* bs = Bs + s * B_STAGE + sl * BN * 16 + (warp * 16 + sg) * 16;
+      const double* as = As + s * A_STAGE + sl * AROWS * 16 + sg * 16;
+      const double* bs = Bs + s * B_STAGE + sl * BN * 16 + (warp * WCOLS + sg) * 16;
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
         const int ch = half ? ch1 : ch0;
-        const double2 b0 = *reinterpret_cast<const double2*>(bs + ch);
-        const double2 b1 = *reinterpret_cast<const double2*>(bs + 8 * 16 + ch);
+        double2 b[TNW];
+#pragma unroll
+        for (int j = 0; j < TNW; ++j) b[j] = *reinterpret_cast<const double2*>(bs + j * 8 * 16 + ch);
 #pragma unroll
         for (int i = 0; i < TM; ++i) {
           const double2 a = *reinterpret_cast<const double2*>(as + i * 8 * 16 + ch);
-          dmma_8x8x4(acc[i][0][0], acc[i][0][1], a.x, b0.x);
-          dmma_8x8x4(acc[i][0][0], acc[i][0][1], a.y, b0.y);
-          dmma_8x8x4(acc[i][1][0], acc[i][1][1], a.x, b1.x);
-          dmma_8x8x4(acc[i][1][0], acc[i][1][1], a.y, b1.y);
+#pragma unroll
+          for (int j = 0; j < TNW; ++j) {
+            dmma_8x8x4(acc[i][j][0], acc[i][j][1], a.x, b[j].x);
+            dmma_8x8x4(acc[i][j][0], acc[i][j][1], a.y, b[j].y);
+          }
         }
       }
     }
@@ -136,8 +144,8 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
     const int row = i * 8 + sg;
     const bool vrow = ((row % S) == 0) && g.bias != nullptr;
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int c0 = warp * 16 + j * 8 + t4, c1 = c0 + 4;
+    for (int j = 0; j < TNW; ++j) {
+      const int c0 = warp * WCOLS + j * 8 + t4, c1 = c0 + 4;
       double v0 = acc[i][j][0], v1 = acc[i][j][1];
       if (vrow) {
         if (n0 + c0 < g.N) v0 += g.bias[(int64_t)(n0 + c0) * g.bias_stride];
@@ -190,18 +198,17 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
   }
 }
 
-constexpr int ACT_BK = 32, ACT_STAGES = 3;
-
-template <int MODE, int TM>
+template <int MODE, int TM, int NW, int BK, int STAGES>
 bool run_act(const GemmAct& g, int box_rows, cudaStream_t s) {
   CUtensorMap ma, mb;
   const int64_t M = g.n_samples * g.S;
+  if (g.K % BK) return false;
   if (!make_tma_map_2d(&ma, g.A, (uint64_t)M, (uint64_t)g.K, (uint64_t)g.lda, box_rows)) return false;
   if (!make_tma_map_2d(&mb, g.B, (uint64_t)g.N, (uint64_t)g.K, (uint64_t)g.ldb, BN)) return false;
-  const size_t pipe = (size_t)ACT_STAGES * (ROWS_MAX + BN) * ACT_BK * sizeof(double);
-  const size_t cst = (size_t)ROWS_MAX * CPITCH * sizeof(double);
-  const size_t smem = std::max(pipe + 2 * ACT_STAGES * 8, cst) + 1024;
-  auto kern = k_gemm_act<ACT_BK, ACT_STAGES, MODE, TM>;
+  const size_t pipe = (size_t)STAGES * (TM * 8 + BN) * BK * sizeof(double) + 2 * STAGES * 8;
+  const size_t cst = (size_t)TM * 8 * CPITCH * sizeof(double);
+  const size_t smem = std::max(pipe, cst) + 1024;
+  auto kern = k_gemm_act<BK, STAGES, MODE, TM, NW>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -210,8 +217,16 @@ bool run_act(const GemmAct& g, int box_rows, cudaStream_t s) {
   const int tiles_n = (int)ceil_div(g.N, BN);
   const int64_t tiles = ceil_div(g.n_samples, g.nb) * tiles_n;
   count_launch();
-  kern<<<(unsigned)tiles, NWARP * 32, smem, s>>>(ma, mb, g, tiles_n, box_rows);
+  kern<<<(unsigned)tiles, NW * 32, smem, s>>>(ma, mb, g, tiles_n, box_rows);
   return true;
+}
+
+// tile shapes up to 13 m8 tiles: 4 warps, BK 16, 3 stages -> ~111 KB, two CTAs per SM;
+// 14-16 tiles: 8 warps, BK 32, 3 stages (one CTA per SM).
+template <int MODE, int TM>
+bool run_act_tm(const GemmAct& g, int box_rows, cudaStream_t s) {
+  if constexpr (TM <= 13) return run_act<MODE, TM, 4, 16, 3>(g, box_rows, s);
+  else return run_act<MODE, TM, 8, 32, 3>(g, box_rows, s);
 }
 
 }  // namespace
@@ -221,7 +236,7 @@ int gemm_act_samples_per_tile(int S) { return S <= ROWS_MAX ? ROWS_MAX / S : 0; 
 bool launch_gemm_act(GemmAct g, int mode, cudaStream_t s) {
   if (g.n_samples <= 0) return true;
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  if (g.S > ROWS_MAX || g.K % ACT_BK != 0 || g.lda % 2 || g.ldb % 2 || !al16(g.A) || !al16(g.B) ||
+  if (g.S > ROWS_MAX || g.K % 16 != 0 || g.lda % 2 || g.ldb % 2 || !al16(g.A) || !al16(g.B) ||
       g.n_samples * g.S >= (int64_t(1) << 31))
     return false;
   g.nb = gemm_act_samples_per_tile(g.S);
@@ -231,9 +246,9 @@ bool launch_gemm_act(GemmAct g, int mode, cudaStream_t s) {
   switch (box_rows / 8) {
 #define KP_ACT_CASE(T)                                                   \
   case T:                                                                \
-    if (mode == ACT_STORE) return run_act<ACT_STORE, T>(g, box_rows, s); \
-    if (mode == ACT_LOSS) return run_act<ACT_LOSS, T>(g, box_rows, s);   \
-    return run_act<ACT_LAST, T>(g, box_rows, s);
+    if (mode == ACT_STORE) return run_act_tm<ACT_STORE, T>(g, box_rows, s); \
+    if (mode == ACT_LOSS) return run_act_tm<ACT_LOSS, T>(g, box_rows, s);   \
+    return run_act_tm<ACT_LAST, T>(g, box_rows, s);
     KP_ACT_CASE(9)
     KP_ACT_CASE(10)
     KP_ACT_CASE(11)
