@@ -110,8 +110,11 @@ struct TaylorDims {
 // post-activation state (n*S x h1) -> post.  Derivative rows of the pre-activation
 // are W0[:, i] and its operator row is 0 (reference taylor.py:124-131).
 void launch_first_layer(const double* x, int64_t n, int d, const double* theta0, int h1,
-                        TaylorDims td, const double* cdiag, double* zval, double* post,
-                        cudaStream_t s);
+                        TaylorDims td, const double* w0t, const double* q0, double* zval,
+                        double* post, cudaStream_t s);
+// Per parameter set: w0t = W0^T (d x h1), q0[j] = sum_i (W0[j,i] c_i) W0[j,i].
+void launch_prep_layer0(const double* theta0, int d, int h1, const double* cdiag, double* w0t,
+                        double* q0, cudaStream_t s);
 // Taylor activation (taylor.py:151-169): pre (n*S x h) -> post.
 void launch_act_fwd(const double* pre, double* post, int64_t n, int h, TaylorDims td,
                     const double* cdiag, cudaStream_t s);
@@ -125,8 +128,8 @@ void launch_last_layer(const double* post, int64_t n, int h, const double* theta
 // rank-1 seeds (x) w_last (first reverse step, taylor.py:262,271).
 struct ActBwd {
   const double* pre;      // n*S x h (nullptr -> use zval/theta0)
-  const double* zval;     // n x h
-  const double* theta0;   // [W0 | b0] rows of length d + 1
+  const double* zval;     // n x h   (layer-0 pre-activation value rows)
+  const double* w0t;      // d x h   (layer-0 derivative rows, W0^T)
   const double* gin;      // n*S x h (nullptr -> rank-1)
   const double* seeds;    // n*S (rank-1; nullptr -> ones)
   const double* wlast;    // h (rank-1)

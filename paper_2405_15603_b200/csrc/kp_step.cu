@@ -131,6 +131,7 @@ struct Plan {
           k_info[MAXL] = {};
   int lw[MAXL][2] = {};
   int64_t o_wpad = 0, o_wpadc = 0, wo[MAXL] = {};
+  int64_t o_w0t = 0, o_q0 = 0, o_w0tc = 0, o_q0c = 0;
   WPack wp{};
   int64_t lwork = 0;
   int64_t total = 0;  // doubles
@@ -261,6 +262,10 @@ int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
   P.o_thc = take(P.D);
   P.o_wpad = take(woff);
   P.o_wpadc = take(woff);
+  P.o_w0t = take((int64_t)P.d * P.h[1]);
+  P.o_q0 = take(P.h[1]);
+  P.o_w0tc = take((int64_t)P.d * P.h[1]);
+  P.o_q0c = take(P.h[1]);
   P.o_ls = take(2 * (int64_t)P.ncand);
   P.o_A1 = take((int64_t)P.maxp * P.maxp);
   P.o_A2 = take((int64_t)P.maxp * P.maxp);
@@ -414,6 +419,8 @@ struct ResidualIn {
 
 // Forward pass storing every state needed by the reverse pass (taylor.py:172-203;
 // boundary: network.py:200-213).  Writes residuals r[0..n).
+// `cand` selects the prepared copies of this parameter set: false = theta (o_wpad, o_w0t,
+// o_q0), true = the line-search candidate (o_wpadc, o_w0tc, o_q0c).
 void forward_store(const Ctx& c, const double* theta, const double* wpad, const double* x, int64_t n,
                    const TaylorDims& td, const double* cdiag, const StateBufs& b,
                    const ResidualIn& ri, double* r, double* u_out) {
@@ -428,7 +435,8 @@ void forward_store(const Ctx& c, const double* theta, const double* wpad, const 
       last_in = x;
     }
   } else {
-    launch_first_layer(x, n, P.d, theta + P.th[0], P.h[1], td, cdiag, b.zval0, b.post[1], c.s);
+    launch_first_layer(x, n, P.d, theta + P.th[0], P.h[1], td, c.at(P.o_w0t), c.at(P.o_q0),
+                       b.zval0, b.post[1], c.s);
     for (int l = 1; l + 1 < L; ++l)
       hidden_layer(c, theta, wpad, l, b.post[l], n, td, cdiag, b.pre[l], b.post[l + 1], ACT_STORE);
     last_in = b.post[L - 1];
@@ -440,7 +448,7 @@ void forward_store(const Ctx& c, const double* theta, const double* wpad, const 
 // Forward pass for losses only (no stored states): ping-pong buffers, in-place activation.
 void forward_loss(const Ctx& c, const double* theta, const double* wpad, const double* x, int64_t n,
                   const TaylorDims& td, const double* cdiag, double* ping, double* pong,
-                  const ResidualIn& ri, double* r, double* u_out) {
+                  const ResidualIn& ri, double* r, double* u_out, bool cand = false) {
   const Plan& P = c.P;
   const int L = P.L;
   const double* cur;
@@ -452,7 +460,9 @@ void forward_loss(const Ctx& c, const double* theta, const double* wpad, const d
       cur = x;
     }
   } else {
-    launch_first_layer(x, n, P.d, theta + P.th[0], P.h[1], td, cdiag, nullptr, ping, c.s);
+    double* zs = td.taylor ? c.at(P.o_zval0) : c.at(P.o_bzval0);
+    launch_first_layer(x, n, P.d, theta + P.th[0], P.h[1], td, c.at(cand ? P.o_w0tc : P.o_w0t),
+                       c.at(cand ? P.o_q0c : P.o_q0), zs, ping, c.s);
     double* a = ping;
     double* b = pong;
     for (int l = 1; l + 1 < L; ++l) {
@@ -503,7 +513,7 @@ void backward(const Ctx& c, const double* theta, int64_t n, const TaylorDims& td
     ActBwd a{};
     a.pre = (L - 2 == 0) ? nullptr : b.pre[L - 2];
     a.zval = b.zval0;
-    a.theta0 = theta + P.th[0];
+    a.w0t = c.at(P.o_w0t);
     a.gin = nullptr;
     a.seeds = seeds;
     a.wlast = theta + P.th[L - 1];
@@ -517,7 +527,7 @@ void backward(const Ctx& c, const double* theta, int64_t n, const TaylorDims& td
     ActBwd a{};
     a.pre = (l - 1 == 0) ? nullptr : b.pre[l - 1];
     a.zval = b.zval0;
-    a.theta0 = theta + P.th[0];
+    a.w0t = c.at(P.o_w0t);
     a.gin = b.ping;
     a.gout = b.gout[l - 1];
     launch_act_bwd(a, n, P.h[l], td, cdiag, c.s);
@@ -586,6 +596,8 @@ int phase_accumulate(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, cons
   for (int l = 1; l < P.L; ++l)
     launch_transpose(st->theta + P.th[l], P.p[l], P.q[l], P.h[l], c.at(P.o_wT[l]), c.s);
   launch_candidate(st->theta, nullptr, 0, nullptr, P.D, P.wp, c.at(P.o_wpad), c.s);
+  if (P.L >= 2)
+    launch_prep_layer0(st->theta, P.d, P.h[1], bt->coeff_diag, c.at(P.o_w0t), c.at(P.o_q0), c.s);
   const TaylorDims tdi{P.S, P.d, true};
   const TaylorDims tdb{1, 0, false};
   const StateBufs bi = interior_bufs(c);
@@ -747,15 +759,17 @@ int phase_linesearch(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, cons
   double* dir = c.at(P.o_dir);
   for (int k = 0; k < P.ncand; ++k) {
     launch_candidate(st->theta, dir, cfg->ls_min_exp + k, thc, P.D, P.wp, c.at(P.o_wpadc), c.s);
+    if (P.L >= 2)
+      launch_prep_layer0(thc, P.d, P.h[1], bt->coeff_diag, c.at(P.o_w0tc), c.at(P.o_q0c), c.s);
     for (int64_t n0 = 0; n0 < P.N; n0 += P.Nc) {
       const int64_t nc = std::min(P.Nc, P.N - n0);
       ResidualIn ri{bt->r0 + n0, bt->seeds + n0 * P.S, nullptr};
       forward_loss(c, thc, c.at(P.o_wpadc), bt->x_int + n0 * P.d, nc, tdi, bt->coeff_diag, c.at(P.o_ping),
-                   c.at(P.o_pong), ri, c.at(P.o_rls) + k * P.N + n0, nullptr);
+                   c.at(P.o_pong), ri, c.at(P.o_rls) + k * P.N + n0, nullptr, true);
     }
     ResidualIn rb{nullptr, nullptr, bt->targets};
     forward_loss(c, thc, c.at(P.o_wpadc), bt->x_bnd, P.Nb, tdb, bt->coeff_diag, c.at(P.o_bping),
-                 c.at(P.o_bpong), rb, c.at(P.o_rbls) + k * P.Nb, nullptr);
+                 c.at(P.o_bpong), rb, c.at(P.o_rbls) + k * P.Nb, nullptr, true);
   }
   double* ls = c.at(P.o_ls);
   launch_sumsq(c.at(P.o_rls), P.N, P.N, P.ncand, ls, 2, c.s);
@@ -1015,6 +1029,8 @@ int32_t kp_taylor_forward(kp_context* ctx, const kp_problem* prob, const double*
   Ctx c{ctx, P, static_cast<double*>(ws), (cudaStream_t)stream};
   const TaylorDims tdi{P.S, P.d, true};
   launch_candidate(theta, nullptr, 0, nullptr, P.D, P.wp, c.at(P.o_wpad), c.s);
+  if (P.L >= 2)
+    launch_prep_layer0(theta, P.d, P.h[1], bt->coeff_diag, c.at(P.o_w0t), c.at(P.o_q0), c.s);
   for (int64_t n0 = 0; n0 < P.N; n0 += P.Nc) {
     const int64_t nc = std::min(P.Nc, P.N - n0);
     ResidualIn ri{nullptr, nullptr, nullptr};
@@ -1037,6 +1053,8 @@ int32_t kp_evaluate_losses(kp_context* ctx, const kp_problem* prob, const double
   const TaylorDims tdi{P.S, P.d, true};
   const TaylorDims tdb{1, 0, false};
   launch_candidate(theta, nullptr, 0, nullptr, P.D, P.wp, c.at(P.o_wpad), c.s);
+  if (P.L >= 2)
+    launch_prep_layer0(theta, P.d, P.h[1], bt->coeff_diag, c.at(P.o_w0t), c.at(P.o_q0), c.s);
   for (int64_t n0 = 0; n0 < P.N; n0 += P.Nc) {
     const int64_t nc = std::min(P.Nc, P.N - n0);
     ResidualIn ri{bt->r0 + n0, bt->seeds + n0 * P.S, nullptr};

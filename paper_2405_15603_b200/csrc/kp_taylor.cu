@@ -18,46 +18,62 @@ static inline unsigned grid_for(int64_t n, int threads) {
 }
 
 // ---------------------------------------------------------------------------
-// layer 0 + first activation (taylor.py:124-169 specialised: Z0 = [x; I; 0])
+// layer 0 + first activation (taylor.py:124-169 specialised: Z0 = [x; I; 0], so the
+// pre-activation of sample n is (z_n = x_n W0^T + b0, derivative rows W0[:, i], operator
+// row 0)).  z comes from a small GEMM; this kernel only expands the S output rows, with
+// W0^T (coalesced across units) and q_j = sum_i (W0[j,i] c_i) W0[j,i] prepared once per
+// parameter set (k_prep_layer0).
 
-__global__ void k_first_layer(const double* __restrict__ x, int64_t n, int d,
-                              const double* __restrict__ th0, int h1, TaylorDims td,
-                              const double* __restrict__ cdiag, double* __restrict__ zval,
-                              double* __restrict__ post) {
-  const int p0 = d + 1;
+__global__ void k_prep_layer0(const double* __restrict__ th0, int d, int h1,
+                              const double* __restrict__ cdiag, double* __restrict__ w0t,
+                              double* __restrict__ q0) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < h1; j += gridDim.x * blockDim.x) {
+    const double* w = th0 + (int64_t)j * (d + 1);
+    double q = 0.0;
+    for (int i = 0; i < d; ++i) {
+      const double g = w[i];
+      w0t[(int64_t)i * h1 + j] = g;
+      q += (g * cdiag[i]) * g;
+    }
+    q0[j] = q;
+  }
+}
+
+void launch_prep_layer0(const double* theta0, int d, int h1, const double* cdiag, double* w0t,
+                        double* q0, cudaStream_t s) {
+  count_launch();
+  k_prep_layer0<<<(unsigned)ceil_div(h1, 128), 128, 0, s>>>(theta0, d, h1, cdiag, w0t, q0);
+}
+
+__global__ void k_first_expand(const double* __restrict__ zval, int64_t n, int h1, TaylorDims td,
+                               const double* __restrict__ w0t, const double* __restrict__ q0,
+                               double* __restrict__ post) {
   const int64_t total = n * h1;
+  const int d = td.d;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t smp = e / h1;
     const int j = (int)(e % h1);
-    const double* w = th0 + (int64_t)j * p0;
-    const double* xr = x + smp * d;
-    double z = 0.0;
-    for (int k = 0; k < d; ++k) z = fma(xr[k], w[k], z);
-    z += w[d];  // bias on the value row (taylor.py:147)
-    if (zval) zval[e] = z;
-    const TanhD t = tanh_derivs(z, false);
+    const TanhD t = tanh_derivs(zval[e], false);
     double* out = post + smp * td.S * h1 + j;
     out[0] = t.s0;
     if (!td.taylor) continue;
-    double quad = 0.0;
-    for (int i = 0; i < d; ++i) {
-      const double g = w[i];  // derivative row i of the pre-activation is W0[:, i]
-      out[(int64_t)(i + 1) * h1] = t.s1 * g;
-      quad += (g * cdiag[i]) * g;
-    }
+#pragma unroll 4
+    for (int i = 0; i < d; ++i) out[(int64_t)(i + 1) * h1] = t.s1 * w0t[(int64_t)i * h1 + j];
     // operator row: s1 * 0 + s2 * quad (taylor.py:168 with L z_in = 0)
-    out[(int64_t)(d + 1) * h1] = t.s2 * quad;
+    out[(int64_t)(d + 1) * h1] = t.s2 * q0[j];
   }
 }
 
 void launch_first_layer(const double* x, int64_t n, int d, const double* theta0, int h1,
-                        TaylorDims td, const double* cdiag, double* zval, double* post,
-                        cudaStream_t s) {
-  const int64_t total = n * h1;
-  if (total <= 0) return;
+                        TaylorDims td, const double* w0t, const double* q0, double* zval,
+                        double* post, cudaStream_t s) {
+  if (n <= 0) return;
+  // z = x W0^T + b0 (value rows only; bias on every row of this n x h1 product)
+  GemmNT g{x, d, theta0, d + 1, zval, h1, n, h1, d, theta0 + d, d + 1, 1};
+  launch_gemm_nt(g, s);
   count_launch();
-  k_first_layer<<<grid_for(total, 256), 256, 0, s>>>(x, n, d, theta0, h1, td, cdiag, zval, post);
+  k_first_expand<<<grid_for(n * h1, 256), 256, 0, s>>>(zval, n, h1, td, w0t, q0, post);
 }
 
 // ---------------------------------------------------------------------------
@@ -154,7 +170,6 @@ void launch_split_u(const double* u, int64_t n, int d, double* value, double* gr
                     cudaStream_t s) {
   if (n <= 0) return;
   count_launch();
-  count_launch();
   k_split_u<<<grid_for(n * (d + 2), 256), 256, 0, s>>>(u, n, d, value, grad, op);
 }
 
@@ -172,7 +187,6 @@ __global__ void k_initial_state(const double* __restrict__ x, int64_t n, int d,
 
 void launch_initial_state(const double* x, int64_t n, int d, double* z, cudaStream_t s) {
   if (n <= 0) return;
-  count_launch();
   count_launch();
   k_initial_state<<<grid_for(n * (d + 2) * d, 256), 256, 0, s>>>(x, n, d, z);
 }
@@ -200,7 +214,6 @@ __global__ void k_act_bwd(ActBwd a, int64_t n, int h, TaylorDims td,
     const int64_t smp = e / h;
     const int j = (int)(e % h);
     const int64_t base = smp * td.S * h + j;
-    const double* w0 = a.pre ? nullptr : a.theta0 + (int64_t)j * (d + 1);
     const double z = a.pre ? a.pre[base] : a.zval[e];
     const TanhD t = tanh_derivs(z, td.taylor);
     const double wl = a.gin ? 0.0 : a.wlast[j];
@@ -218,8 +231,9 @@ __global__ void k_act_bwd(ActBwd a, int64_t n, int h, TaylorDims td,
     const double ell = a.pre ? a.pre[base + (int64_t)(d + 1) * h] : 0.0;
     double quad = 0.0, ggb = 0.0;
     const double two_s2 = 2.0 * t.s2;
+#pragma unroll 4
     for (int i = 1; i <= d; ++i) {
-      const double g = a.pre ? a.pre[base + (int64_t)i * h] : w0[i - 1];
+      const double g = a.pre ? a.pre[base + (int64_t)i * h] : a.w0t[(int64_t)(i - 1) * h + j];
       const double gb = gin_at(i);
       const double cg = g * cdiag[i - 1];
       quad += cg * g;
