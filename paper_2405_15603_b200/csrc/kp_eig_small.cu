@@ -1,0 +1,296 @@
+// On-device generalised symmetric-definite eigensolver for small factors (n <= 96)
+// and the Kronecker-sum combine, FP64, sm_100a.  Used for the layers whose factors
+// fit in one CTA's shared memory (every layer of BASELINE configs c1-c3); larger
+// layers go through cuSOLVER sygvd.  Everything stays on the device: no host sync,
+// one launch for all small factor pairs, one for all small combines.
+//
+// For a pair (F1, F2) with damping lam (reference src/curvature.py:150-161):
+//   M1 = F1 + lam I, M2 = F2 + lam I
+//   M2 = L L^T (Cholesky; failure -> not positive definite, src/linalg.py:128-132)
+//   C  = L^-1 M1 L^-T (two forward substitutions, C symmetric)
+//   C  = V diag(lam) V^T  (parallel cyclic Jacobi, round-robin pairing)
+//   T  = L^-T V           (so T^T M2 T = I, T^T M1 T = diag(lam))
+// Combine (src/linalg.py:168-173 restated on the generalised basis):
+//   out = -T_B [(T_B^T G T_A) / (lb la^T + 1)] T_A^T.
+// Jacobi is accurate to a few ulps relative to each eigenpair; the solution of the
+// Kronecker-sum system is unique, so it matches the reference's LAPACK route to
+// roundoff (tests/test_gpu_parity.py).
+#include <algorithm>
+
+#include "../../include/kfac_pinn_b200.h"
+#include "kp_common.cuh"
+#include "kp_internal.h"
+
+namespace kp {
+
+namespace {
+
+constexpr int EIG_THREADS = 1024;
+constexpr int EIG_MAXN = 96;
+constexpr int EIG_MAX_SWEEPS = 30;
+// Rotate only when |a_pq| > tol * sqrt(|a_pp a_qq|): relative accuracy ~1e-14 per eigenpair
+// (the KFAC parity bar is 1e-10); tighter values let roundoff re-trigger rotations forever.
+constexpr double kJacobiTol = 1e-14;
+
+__host__ __device__ inline int eig_pitch(int n) { return ((n - 1 + 15) / 16) * 16 + 1; }
+
+__device__ int g_eig_sweeps_max = 0;  // diagnostic: most Jacobi sweeps used by any job
+
+__device__ __forceinline__ void set_status_dev(int32_t* status, int32_t code) {
+  atomicCAS(status, 0, code);
+}
+
+// One CTA (32 warps) per factor pair.  smem: L, C, V (n x n each, row-major).
+__global__ void __launch_bounds__(EIG_THREADS) k_gen_eig_small(const SmallEigJobs jobs,
+                                                              int32_t* status) {
+  extern __shared__ double esm[];
+  const SmallEigJob jb = jobs.job[blockIdx.x];
+  const int n = jb.n;
+  const int ld = eig_pitch(n);  // 16k+1 doubles: column walks hit 32 distinct banks
+  double* L = esm;
+  double* C = L + n * ld;
+  double* V = C + n * ld;
+  __shared__ int flag;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  constexpr int NWARPS = EIG_THREADS / 32;
+  const double lam = jb.damping;
+
+  // load M2 = F2 + lam I into L and M1 = F1 + lam I into C
+  for (int e = tid; e < n * n; e += EIG_THREADS) {
+    const int i = e / n, j = e % n;
+    L[i * ld + j] = jb.f2[e] + (i == j ? lam : 0.0);
+    C[i * ld + j] = jb.f1[e] + (i == j ? lam : 0.0);
+  }
+  if (tid == 0) flag = 0;
+  __syncthreads();
+
+  // right-looking Cholesky of M2 (lower triangle of L); warp w owns rows w, w+32, ...
+  for (int k = 0; k < n; ++k) {
+    const double a = L[k * ld + k];
+    if (!(a > 0.0)) {
+      if (tid == 0) flag = n + k + 1;  // LAPACK convention: info > n -> second matrix not PD
+      break;
+    }
+    const double dk = sqrt(a);
+    const double inv = 1.0 / dk;
+    __syncthreads();  // everyone has read L[k][k]
+    if (tid == 0) L[k * ld + k] = dk;
+    for (int i = k + 1 + tid; i < n; i += EIG_THREADS) L[i * ld + k] *= inv;
+    __syncthreads();
+    for (int i = k + 1 + warp; i < n; i += NWARPS) {
+      const double lik = L[i * ld + k];
+      for (int j = k + 1 + lane; j <= i; j += 32) L[i * ld + j] -= lik * L[j * ld + k];
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (flag != 0) {
+    if (tid == 0) {
+      if (jb.info) *jb.info = flag;
+      set_status_dev(status, KP_ERR_NOT_PSD);
+    }
+    return;
+  }
+
+  // C <- L^-1 C then C <- L^-1 C^T (C symmetric).  Warp per column, lanes split the dot
+  // product of each forward-substitution row.
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int j = warp; j < n; j += NWARPS) {
+      for (int i = 0; i < n; ++i) {
+        double acc = 0.0;
+        for (int k = lane; k < i; k += 32) acc += L[i * ld + k] * V[k * ld + j];
+        acc = warp_sum(acc);
+        const double rhs = pass == 0 ? C[i * ld + j] : C[j * ld + i];
+        if (lane == 0) V[i * ld + j] = (rhs - acc) / L[i * ld + i];
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < n * ld; e += EIG_THREADS) C[e] = V[e];
+    __syncthreads();
+  }
+  // symmetrise (roundoff) and V = I
+  for (int e = tid; e < n * n; e += EIG_THREADS) {
+    const int i = e / n, j = e % n;
+    if (i < j) {
+      const double a = 0.5 * (C[i * ld + j] + C[j * ld + i]);
+      C[i * ld + j] = a;
+      C[j * ld + i] = a;
+    }
+    V[i * ld + j] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+
+  // parallel cyclic Jacobi, round-robin ordering over m = n rounded up to even; warp w owns
+  // pairs w and w + 32 of every round and keeps their rotations in registers.
+  const int m = (n + 1) & ~1;
+  const int npair = m / 2;
+  for (int sweep = 0; sweep < EIG_MAX_SWEEPS; ++sweep) {
+    if (tid == 0) flag = 0;
+    __syncthreads();
+    for (int round = 0; round < m - 1; ++round) {
+      int pr[2], qr[2];
+      double cr[2], sr[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int k = warp + u * NWARPS;
+        pr[u] = 0;
+        qr[u] = n;
+        cr[u] = 1.0;
+        sr[u] = 0.0;
+        if (k >= npair) continue;
+        const int a = (k == 0) ? 0 : 1 + (k - 1 + round) % (m - 1);
+        const int b = 1 + (m - 2 - k + round) % (m - 1);
+        const int p = min(a, b), q = max(a, b);
+        pr[u] = p;
+        qr[u] = q;
+        if (q >= n) continue;
+        const double apq = C[p * ld + q];
+        const double app = C[p * ld + p], aqq = C[q * ld + q];
+        if (apq * apq > kJacobiTol * kJacobiTol * fabs(app * aqq) && fabs(apq) > 1e-300) {
+          // t = sign(theta) / (|theta| + sqrt(theta^2 + 1)), theta = (aqq - app) / (2 apq)
+          const double dd = aqq - app;
+          const double two_apq = 2.0 * apq;
+          const double den = fabs(dd) + sqrt(fma(dd, dd, two_apq * two_apq));
+          const double t = ((dd >= 0.0) == (apq >= 0.0) ? 1.0 : -1.0) * fabs(two_apq) / den;
+          cr[u] = rsqrt(fma(t, t, 1.0));
+          sr[u] = t * cr[u];
+          if (lane == 0) flag = 1;
+        }
+      }
+      __syncthreads();  // all rotation parameters read C before any row update
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int p = pr[u], q = qr[u];
+        const double c = cr[u], s = sr[u];
+        if (q >= n || s == 0.0) continue;
+        for (int col = lane; col < n; col += 32) {
+          const double x = C[p * ld + col], y = C[q * ld + col];
+          C[p * ld + col] = c * x - s * y;
+          C[q * ld + col] = s * x + c * y;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int p = pr[u], q = qr[u];
+        const double c = cr[u], s = sr[u];
+        if (q >= n || s == 0.0) continue;
+        for (int row = lane; row < n; row += 32) {
+          const double x = C[row * ld + p], y = C[row * ld + q];
+          C[row * ld + p] = c * x - s * y;
+          C[row * ld + q] = s * x + c * y;
+          const double vx = V[row * ld + p], vy = V[row * ld + q];
+          V[row * ld + p] = c * vx - s * vy;
+          V[row * ld + q] = s * vx + c * vy;
+        }
+      }
+      __syncthreads();
+    }
+    if (flag == 0) {
+      if (tid == 0) atomicMax(&g_eig_sweeps_max, sweep + 1);
+      break;
+    }
+    if (sweep == EIG_MAX_SWEEPS - 1 && tid == 0) atomicMax(&g_eig_sweeps_max, 1000 + sweep);
+  }
+
+  // eigenvalues; T = L^-T V (back substitution, warp per column) written to global
+  for (int i = tid; i < n; i += EIG_THREADS) jb.lam[i] = C[i * ld + i];
+  __syncthreads();
+  for (int j = warp; j < n; j += NWARPS) {
+    for (int i = n - 1; i >= 0; --i) {
+      double acc = 0.0;
+      for (int k = i + 1 + lane; k < n; k += 32) acc += L[k * ld + i] * C[k * ld + j];
+      acc = warp_sum(acc);
+      if (lane == 0) C[i * ld + j] = (V[i * ld + j] - acc) / L[i * ld + i];  // C reused as T
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < n * n; e += EIG_THREADS) jb.t[e] = C[(e / n) * ld + e % n];
+  if (tid == 0 && jb.info) *jb.info = 0;
+  // PSD check on the generalised eigenvalues (src/linalg.py:79-83, 165-166)
+  if (tid == 0) {
+    double hi = 0.0, mn = INFINITY;
+    for (int i = 0; i < n; ++i) {
+      const double v = jb.lam[i];
+      mn = fmin(mn, v);
+      hi = fmax(hi, fabs(v));
+    }
+    if (mn < -1e-6 * fmax(hi, 1e-300)) set_status_dev(status, KP_ERR_NOT_PSD);
+  }
+}
+
+// One CTA per layer: out (q x p, row-major) = sign * T_B [(T_B^T G T_A) / (lb la^T + 1)] T_A^T
+// with T_A (p x p) and T_B (q x q) row-major (column k = eigenvector k).
+__global__ void __launch_bounds__(1024) k_kron_combine_small(const SmallCombineJobs jobs) {
+  const SmallCombineJob jb = jobs.job[blockIdx.x];
+  const int p = jb.p, q = jb.q;
+  const int tid = threadIdx.x;
+  // T1 = G T_A (q x p)
+  for (int e = tid; e < q * p; e += blockDim.x) {
+    const int i = e / p, j = e % p;
+    double v = 0.0;
+    for (int k = 0; k < p; ++k) v += jb.g[i * p + k] * jb.ta[k * p + j];
+    jb.t1[e] = v;
+  }
+  __syncthreads();
+  // W = (T_B^T T1) / (lb_i la_j + 1)
+  for (int e = tid; e < q * p; e += blockDim.x) {
+    const int i = e / p, j = e % p;
+    double v = 0.0;
+    for (int k = 0; k < q; ++k) v += jb.tb[k * q + i] * jb.t1[k * p + j];
+    jb.t2[e] = v / (jb.lb[i] * jb.la[j] + 1.0);
+  }
+  __syncthreads();
+  // T1 = W T_A^T
+  for (int e = tid; e < q * p; e += blockDim.x) {
+    const int i = e / p, j = e % p;
+    double v = 0.0;
+    for (int k = 0; k < p; ++k) v += jb.t2[i * p + k] * jb.ta[j * p + k];
+    jb.t1[e] = v;
+  }
+  __syncthreads();
+  // out = sign * T_B T1
+  for (int e = tid; e < q * p; e += blockDim.x) {
+    const int i = e / p, j = e % p;
+    double v = 0.0;
+    for (int k = 0; k < q; ++k) v += jb.tb[i * q + k] * jb.t1[k * p + j];
+    jb.out[e] = jb.sign * v;
+  }
+}
+
+}  // namespace
+
+int small_eig_max_n() { return EIG_MAXN; }
+
+int small_eig_sweeps_used() {
+  int v = 0;
+  cudaMemcpyFromSymbol(&v, g_eig_sweeps_max, sizeof(int));
+  return v;
+}
+
+size_t small_eig_smem_bytes(int n) { return sizeof(double) * 3 * (size_t)n * eig_pitch(n); }
+
+void launch_gen_eig_small(const SmallEigJobs& jobs, int njobs, int max_n, int32_t* status,
+                          cudaStream_t s) {
+  if (njobs <= 0) return;
+  const size_t smem = small_eig_smem_bytes(max_n);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_gen_eig_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)small_eig_smem_bytes(EIG_MAXN));
+    attr_set = true;
+  }
+  count_launch();
+  k_gen_eig_small<<<njobs, EIG_THREADS, smem, s>>>(jobs, status);
+}
+
+void launch_kron_combine_small(const SmallCombineJobs& jobs, int njobs, cudaStream_t s) {
+  if (njobs <= 0) return;
+  count_launch();
+  k_kron_combine_small<<<njobs, 1024, 0, s>>>(jobs);
+}
+
+}  // namespace kp

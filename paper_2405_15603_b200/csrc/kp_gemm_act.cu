@@ -225,8 +225,12 @@ bool run_act(const GemmAct& g, int box_rows, cudaStream_t s) {
 // 14-16 tiles: 8 warps, BK 32, 3 stages (one CTA per SM).
 template <int MODE, int TM>
 bool run_act_tm(const GemmAct& g, int box_rows, cudaStream_t s) {
-  if constexpr (TM <= 13) return run_act<MODE, TM, 4, 16, 3>(g, box_rows, s);
-  else return run_act<MODE, TM, 8, 32, 3>(g, box_rows, s);
+  if constexpr (TM <= 13) {
+    return run_act<MODE, TM, 4, 16, 3>(g, box_rows, s);
+  } else {
+    if (g.K % 32 == 0) return run_act<MODE, TM, 8, 32, 3>(g, box_rows, s);
+    return run_act<MODE, TM, 8, 16, 6>(g, box_rows, s);
+  }
 }
 
 }  // namespace

@@ -98,7 +98,7 @@ bool launch_gemm_act(GemmAct g, int mode, cudaStream_t s);
 // out[j*os] += sum_{n} w_n X[n*rs + j] for j < ncols (w == nullptr: 1);
 // out[ncols*os] += add_count.  scratch: 64 * ncols doubles.
 void launch_colsum(const double* X, int64_t rs, int64_t n, int ncols, const double* w, double* out,
-                   int64_t os, double add_count, double* scratch, cudaStream_t s);
+                   int64_t os, double add_count, double* scratch, cudaStream_t s, int tr_h = 0);
 
 struct TaylorDims {
   int S;       // rows per sample: d + 2 (Taylor) or 1 (plain)
@@ -185,5 +185,39 @@ void launch_kron_scale(double* W, const double* la, int p, const double* lb, int
                        cudaStream_t s);
 void launch_set_status(int32_t* status, int32_t code, cudaStream_t s);
 void launch_identity(double* F, int n, double v, cudaStream_t s);
+
+// ---- small on-device generalised eigensolver + combine (kp_eig_small.cu) ---------
+struct SmallEigJob {
+  int n;
+  const double* f1;  // first factor (M1 = f1 + damping I)
+  const double* f2;  // second factor (M2 = f2 + damping I, Cholesky'd)
+  double damping;
+  double* t;         // n x n row-major, column k = generalised eigenvector k
+  double* lam;       // n eigenvalues
+  int* info;
+};
+struct SmallEigJobs {
+  SmallEigJob job[32];
+};
+struct SmallCombineJob {
+  int p, q;
+  const double* g;   // q x p gradient
+  const double* ta;  // p x p
+  const double* tb;  // q x q
+  const double* la;
+  const double* lb;
+  double* t1;        // q x p scratch
+  double* t2;        // q x p scratch
+  double* out;       // q x p
+  double sign;
+};
+struct SmallCombineJobs {
+  SmallCombineJob job[16];
+};
+int small_eig_max_n();
+size_t small_eig_smem_bytes(int n);
+void launch_gen_eig_small(const SmallEigJobs& jobs, int njobs, int max_n, int32_t* status,
+                          cudaStream_t s);
+void launch_kron_combine_small(const SmallCombineJobs& jobs, int njobs, cudaStream_t s);
 
 }  // namespace kp

@@ -58,6 +58,10 @@ struct kp_context {
   std::vector<cusolverDnHandle_t> side_solver;
   std::vector<cublasHandle_t> side_blas;
   std::vector<cudaEvent_t> side_ev;
+  // cache of the last workspace plan (make_plan queries cuSOLVER workspace sizes: host cost)
+  kp_problem plan_key{};
+  bool plan_valid = false;
+  std::vector<unsigned char> plan_blob;
 };
 
 static int ensure_side_streams(kp_context* c, int n) {
@@ -234,6 +238,7 @@ int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
     part = std::max(part, gemm_tn_tma_partial_doubles(R, Pp, Qq, sym));
   };
   part = std::max(part, (size_t)64 * (P.maxh + P.maxq + 1));  // colsum scratch
+  part = std::max(part, (size_t)64 * P.d * P.h[1]);             // layer-0 derivative colsum
   for (int64_t R : {P.Nc, P.Nb}) {
     const bool interior = (R == P.Nc);
     const int64_t rows = interior ? R * P.S : R;
@@ -584,7 +589,10 @@ void accumulate(const Ctx& c, const double* x, int64_t n, const TaylorDims& td,
         GemmTN gg{G, ldg, q, false, Z, ldz, hz, true, r, Sw, Sz, Rz, false};
         launch_gemm_tn_accumulate(gg, part, out, c.s);
       }
-      if (l == 0 && td.taylor) launch_grad0_deriv(G, r, n, P.d, q, out, c.s);
+      // layer 0, derivative rows e_i: out[j][i] += sum_n r_n Gbar0[n, 1+i, j] — a weighted sum
+      // over samples of the contiguous d x q block after each value row
+      if (l == 0 && td.taylor)
+        launch_colsum(G + q, (int64_t)td.S * q, n, P.d * q, r, out, p, 0.0, part, c.s, q);
     }
   }
 }
@@ -701,8 +709,33 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
   KP_TRY(ensure_side_streams(ctx, 2 * P.L + 1));
   cudaEvent_t ready = ctx->side_ev[2 * P.L];
   KP_CUDA_TRY(cudaEventRecord(ready, c.s));
-  // cuSOLVER's sygvd blocks the calling host thread, so each factor-pair solve is issued
-  // from its own host thread (own handle + stream) to let the 2L solves overlap on the GPU.
+  // Small layers (both factors <= small_eig_max_n()): on-device Jacobi solver, all of them in
+  // two launches on the main stream.  Larger layers: cuSOLVER sygvd, which blocks the calling
+  // host thread, so each factor-pair solve is issued from its own host thread (own handle +
+  // stream) to let the solves overlap on the GPU.
+  std::vector<int> big;
+  {
+    SmallEigJobs ej{};
+    SmallCombineJobs cj{};
+    int ne = 0, nc = 0, maxn = 1;
+    for (int l = 0; l < P.L; ++l) {
+      if (std::max(P.p[l], P.q[l]) > small_eig_max_n()) {
+        big.push_back(l);
+        continue;
+      }
+      int* info = reinterpret_cast<int*>(c.at(P.k_info[l]));
+      ej.job[ne++] = SmallEigJob{P.p[l], st->a_int + P.fa[l], st->a_bnd + P.fa[l], lam,
+                                 c.at(P.k_A1[l]), c.at(P.k_la[l]), info};
+      ej.job[ne++] = SmallEigJob{P.q[l], st->b_int + P.fb[l], st->b_bnd + P.fb[l], lam,
+                                 c.at(P.k_B1[l]), c.at(P.k_lb[l]), info + 1};
+      cj.job[nc++] = SmallCombineJob{P.p[l], P.q[l], grad + P.th[l], c.at(P.k_A1[l]),
+                                     c.at(P.k_B1[l]), c.at(P.k_la[l]), c.at(P.k_lb[l]),
+                                     c.at(P.k_T1[l]), c.at(P.k_T2[l]), delta + P.th[l], -1.0};
+      maxn = std::max(maxn, std::max(P.p[l], P.q[l]));
+    }
+    launch_gen_eig_small(ej, ne, maxn, out->status, c.s);
+    launch_kron_combine_small(cj, nc, c.s);
+  }
   std::vector<int> rc(2 * P.L, KP_OK);
   auto solve_pair = [&](int l, int k) {
     cudaSetDevice(ctx->device);
@@ -725,14 +758,14 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
     }
     cudaEventRecord(ctx->side_ev[2 * l + k], s);
   };
-  {
+  if (!big.empty()) {
     std::vector<std::thread> pool;
-    for (int l = 0; l < P.L; ++l)
+    for (int l : big)
       for (int k = 0; k < 2; ++k) pool.emplace_back(solve_pair, l, k);
     for (auto& t : pool) t.join();
   }
   for (int v : rc) KP_TRY(v);
-  for (int l = 0; l < P.L; ++l) {
+  for (int l : big) {
     cudaStream_t s = ctx->side[2 * l];
     KP_CUDA_TRY(cudaStreamWaitEvent(s, ctx->side_ev[2 * l + 1], 0));
     launch_eig_status(c.at(P.k_la[l]), P.p[l], c.at(P.k_lb[l]), P.q[l],
@@ -742,7 +775,7 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
                         c.at(P.k_T1[l]), c.at(P.k_T2[l])));
     KP_CUDA_TRY(cudaEventRecord(ctx->side_ev[2 * l], s));
   }
-  for (int l = 0; l < P.L; ++l) KP_CUDA_TRY(cudaStreamWaitEvent(c.s, ctx->side_ev[2 * l], 0));
+  for (int l : big) KP_CUDA_TRY(cudaStreamWaitEvent(c.s, ctx->side_ev[2 * l], 0));
   launch_axpy_out(delta, st->prev_update, cfg->momentum, c.at(P.o_dir), P.D, c.s);
   if (out->grad) KP_CUDA_TRY(cudaMemcpyAsync(out->grad, grad, sizeof(double) * P.D,
                                              cudaMemcpyDeviceToDevice, c.s));
@@ -795,9 +828,23 @@ int validate_cfg(const kp_problem* pr, const kp_kfac_config* cfg) {
   return KP_OK;
 }
 
+int cached_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
+  if (ctx->plan_valid && std::memcmp(&ctx->plan_key, pr, sizeof(kp_problem)) == 0 &&
+      ctx->plan_blob.size() == sizeof(Plan)) {
+    std::memcpy(&P, ctx->plan_blob.data(), sizeof(Plan));
+    return KP_OK;
+  }
+  KP_TRY(make_plan(ctx, pr, P));
+  ctx->plan_key = *pr;
+  ctx->plan_blob.resize(sizeof(Plan));
+  std::memcpy(ctx->plan_blob.data(), &P, sizeof(Plan));
+  ctx->plan_valid = true;
+  return KP_OK;
+}
+
 int prepare(kp_context* ctx, const kp_problem* pr, Plan& P, size_t ws_bytes) {
   if (!ctx || !pr) return KP_ERR_INVALID;
-  KP_TRY(make_plan(ctx, pr, P));
+  KP_TRY(cached_plan(ctx, pr, P));
   if ((size_t)P.total * sizeof(double) > ws_bytes) return KP_ERR_WORKSPACE;
   return KP_OK;
 }
@@ -908,7 +955,7 @@ int64_t kp_factor_count(const kp_net* net, int32_t which) {
 int32_t kp_workspace_bytes(kp_context* ctx, const kp_problem* pr, size_t* bytes) {
   if (!ctx || !pr || !bytes) return KP_ERR_INVALID;
   Plan P;
-  KP_TRY(make_plan(ctx, pr, P));
+  KP_TRY(cached_plan(ctx, pr, P));
   *bytes = (size_t)P.total * sizeof(double);
   return KP_OK;
 }
@@ -945,7 +992,7 @@ int32_t kp_init_state(kp_context* ctx, const kp_net* net, kp_state* st, int32_t 
 int32_t kp_reduce_buffer(kp_context* ctx, const kp_problem* pr, void* ws, double** ptr,
                          int64_t* count) {
   Plan P;
-  KP_TRY(make_plan(ctx, pr, P));
+  KP_TRY(cached_plan(ctx, pr, P));
   *ptr = static_cast<double*>(ws) + P.o_red;
   *count = P.r_count;
   return KP_OK;
@@ -954,7 +1001,7 @@ int32_t kp_reduce_buffer(kp_context* ctx, const kp_problem* pr, void* ws, double
 int32_t kp_linesearch_buffer(kp_context* ctx, const kp_problem* pr, void* ws, double** ptr,
                              int64_t* count) {
   Plan P;
-  KP_TRY(make_plan(ctx, pr, P));
+  KP_TRY(cached_plan(ctx, pr, P));
   *ptr = static_cast<double*>(ws) + P.o_ls;
   *count = 2LL * P.ncand;
   return KP_OK;
@@ -1120,6 +1167,19 @@ int32_t kp_kron_sum_solve(kp_context* ctx, int32_t p, int32_t q, const double* a
   P.lwork = (int64_t)(ws_bytes / sizeof(double)) - o;
   Ctx c{ctx, P, static_cast<double*>(ws), s};
   KP_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int32_t), s));
+  if (std::max(p, q) <= small_eig_max_n()) {
+    SmallEigJobs ej{};
+    SmallCombineJobs cj{};
+    int* info = reinterpret_cast<int*>(c.at(P.o_info));
+    ej.job[0] = SmallEigJob{p, a1, a2, 0.0, c.at(P.o_A1), c.at(P.o_la), info};
+    ej.job[1] = SmallEigJob{q, b1, b2, 0.0, c.at(P.o_B1), c.at(P.o_lb), info + 1};
+    cj.job[0] = SmallCombineJob{p, q, g, c.at(P.o_A1), c.at(P.o_B1), c.at(P.o_la), c.at(P.o_lb),
+                                c.at(P.o_T1), c.at(P.o_T2), x, 1.0};
+    launch_gen_eig_small(ej, 2, std::max(p, q), status, s);
+    launch_kron_combine_small(cj, 1, s);
+    KP_CUDA_TRY(cudaGetLastError());
+    return KP_OK;
+  }
   KP_CUDA_TRY(cudaMemcpyAsync(c.at(P.o_A1), a1, sizeof(double) * p * p, cudaMemcpyDeviceToDevice, s));
   KP_CUDA_TRY(cudaMemcpyAsync(c.at(P.o_A2), a2, sizeof(double) * p * p, cudaMemcpyDeviceToDevice, s));
   KP_CUDA_TRY(cudaMemcpyAsync(c.at(P.o_B1), b1, sizeof(double) * q * q, cudaMemcpyDeviceToDevice, s));

@@ -45,23 +45,41 @@ void launch_prep_layer0(const double* theta0, int d, int h1, const double* cdiag
   k_prep_layer0<<<(unsigned)ceil_div(h1, 128), 128, 0, s>>>(theta0, d, h1, cdiag, w0t, q0);
 }
 
-__global__ void k_first_expand(const double* __restrict__ zval, int64_t n, int h1, TaylorDims td,
-                               const double* __restrict__ w0t, const double* __restrict__ q0,
-                               double* __restrict__ post) {
-  const int64_t total = n * h1;
+// One warp per (sample, 32-unit tile): lane j writes unit j of every one of the sample's
+// S rows (256-byte coalesced stores); the W0^T tile and q live in shared memory.
+constexpr int EXP_WARPS = 8;
+
+__global__ void __launch_bounds__(EXP_WARPS * 32)
+    k_first_expand(const double* __restrict__ zval, int64_t n, int h1, TaylorDims td,
+                   const double* __restrict__ w0t, const double* __restrict__ q0,
+                   double* __restrict__ post, int64_t samples_per_block) {
+  extern __shared__ double wsm[];  // [d][32] W0^T tile, then q[32]
   const int d = td.d;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t smp = e / h1;
-    const int j = (int)(e % h1);
-    const TanhD t = tanh_derivs(zval[e], false);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int j0 = blockIdx.x * 32;
+  const int j = j0 + lane;
+  const bool valid = j < h1;
+  if (td.taylor) {
+    for (int e = threadIdx.x; e < d * 32; e += blockDim.x) {
+      const int i = e / 32, jj = j0 + e % 32;
+      wsm[e] = jj < h1 ? w0t[(int64_t)i * h1 + jj] : 0.0;
+    }
+    if (threadIdx.x < 32) wsm[d * 32 + threadIdx.x] = valid ? q0[j] : 0.0;
+    __syncthreads();
+  }
+  const double qj = td.taylor ? wsm[d * 32 + lane] : 0.0;
+  const int64_t s_begin = (int64_t)blockIdx.y * samples_per_block;
+  const int64_t s_end = min(n, s_begin + samples_per_block);
+  for (int64_t smp = s_begin + warp; smp < s_end; smp += EXP_WARPS) {
+    if (!valid) continue;
+    const TanhD t = tanh_derivs(zval[smp * h1 + j], false);
     double* out = post + smp * td.S * h1 + j;
     out[0] = t.s0;
     if (!td.taylor) continue;
-#pragma unroll 4
-    for (int i = 0; i < d; ++i) out[(int64_t)(i + 1) * h1] = t.s1 * w0t[(int64_t)i * h1 + j];
+#pragma unroll 8
+    for (int i = 0; i < d; ++i) out[(int64_t)(i + 1) * h1] = t.s1 * wsm[i * 32 + lane];
     // operator row: s1 * 0 + s2 * quad (taylor.py:168 with L z_in = 0)
-    out[(int64_t)(d + 1) * h1] = t.s2 * q0[j];
+    out[(int64_t)(d + 1) * h1] = t.s2 * qj;
   }
 }
 
@@ -72,8 +90,13 @@ void launch_first_layer(const double* x, int64_t n, int d, const double* theta0,
   // z = x W0^T + b0 (value rows only; bias on every row of this n x h1 product)
   GemmNT g{x, d, theta0, d + 1, zval, h1, n, h1, d, theta0 + d, d + 1, 1};
   launch_gemm_nt(g, s);
+  const unsigned tiles = (unsigned)ceil_div(h1, 32);
+  const int64_t groups = std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, EXP_WARPS), 148LL * 8 / tiles + 1));
+  const int64_t spb = ceil_div(n, groups);
+  const size_t smem = td.taylor ? sizeof(double) * (size_t)(td.d * 32 + 32) : 0;
   count_launch();
-  k_first_expand<<<grid_for(n * h1, 256), 256, 0, s>>>(zval, n, h1, td, w0t, q0, post);
+  k_first_expand<<<dim3(tiles, (unsigned)ceil_div(n, spb)), EXP_WARPS * 32, smem, s>>>(
+      zval, n, h1, td, w0t, q0, post, spb);
 }
 
 // ---------------------------------------------------------------------------
@@ -231,14 +254,27 @@ __global__ void k_act_bwd(ActBwd a, int64_t n, int h, TaylorDims td,
     const double ell = a.pre ? a.pre[base + (int64_t)(d + 1) * h] : 0.0;
     double quad = 0.0, ggb = 0.0;
     const double two_s2 = 2.0 * t.s2;
-#pragma unroll 4
-    for (int i = 1; i <= d; ++i) {
-      const double g = a.pre ? a.pre[base + (int64_t)i * h] : a.w0t[(int64_t)(i - 1) * h + j];
-      const double gb = gin_at(i);
-      const double cg = g * cdiag[i - 1];
-      quad += cg * g;
-      ggb += g * gb;
-      a.gout[base + (int64_t)i * h] = t.s1 * gb + two_s2 * cg * lb;
+    // derivative rows in batches of 4: issue the loads first (memory-level parallelism)
+    for (int i0 = 1; i0 <= d; i0 += 4) {
+      double gv[4], gbv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u;
+        if (i <= d) {
+          gv[u] = a.pre ? a.pre[base + (int64_t)i * h] : a.w0t[(int64_t)(i - 1) * h + j];
+          gbv[u] = gin_at(i);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u;
+        if (i <= d) {
+          const double cg = gv[u] * cdiag[i - 1];
+          quad += cg * gv[u];
+          ggb += gv[u] * gbv[u];
+          a.gout[base + (int64_t)i * h] = t.s1 * gbv[u] + two_s2 * cg * lb;
+        }
+      }
     }
     a.gout[base + (int64_t)(d + 1) * h] = t.s1 * lb;
     a.gout[base] = t.s1 * vb + t.s2 * ggb + t.s2 * ell * lb + t.s3 * quad * lb;
@@ -317,24 +353,27 @@ __global__ void k_colsum_partial(const double* __restrict__ X, int64_t rs, int64
 }
 
 __global__ void k_colsum_reduce(const double* __restrict__ part, int ncols, double* out,
-                                int64_t os, double add_count) {
+                                int64_t os, double add_count, int tr_h) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j < ncols) {
     double v = 0.0;
     for (int g = 0; g < COLSUM_GROUPS; ++g) v += part[(int64_t)g * ncols + j];
-    out[(int64_t)j * os] += v;
+    // tr_h > 0: column jj = i * tr_h + u lands at out[u * os + i] (transposed block)
+    const int64_t o = tr_h > 0 ? (int64_t)(j % tr_h) * os + j / tr_h : (int64_t)j * os;
+    out[o] += v;
   }
   if (j == 0 && add_count != 0.0) out[(int64_t)ncols * os] += add_count;
 }
 
 void launch_colsum(const double* X, int64_t rs, int64_t n, int ncols, const double* w, double* out,
-                   int64_t os, double add_count, double* scratch, cudaStream_t s) {
+                   int64_t os, double add_count, double* scratch, cudaStream_t s, int tr_h) {
   if (n <= 0 || ncols <= 0) return;
   count_launch();
   k_colsum_partial<<<dim3((unsigned)ceil_div(ncols, 32), COLSUM_GROUPS), 256, 0, s>>>(X, rs, n, ncols,
                                                                                     w, scratch);
   count_launch();
-  k_colsum_reduce<<<(unsigned)ceil_div(ncols, 128), 128, 0, s>>>(scratch, ncols, out, os, add_count);
+  k_colsum_reduce<<<(unsigned)ceil_div(ncols, 128), 128, 0, s>>>(scratch, ncols, out, os, add_count,
+                                                                  tr_h);
 }
 
 // ---------------------------------------------------------------------------
