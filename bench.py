@@ -294,7 +294,7 @@ def run_ours(args):
             "kfac_steps_per_s": steps_per_s,
             "alg_tflops_per_s": f_step * steps_per_s / 1e12,
             "alg_frac_fp64_peak": f_step * steps_per_s / 1e12 / (FP64_DMMA_PEAK_TFLOPS * world),
-            "roofline": {"bound": "tensor", "kernel": "k_gemm_nt (FP64 DMMA forward GEMM)",
+            "roofline": {"bound": "tensor", "kernel": "k_gemm_act (TMA-fed FP64 DMMA forward GEMM fused with the Taylor activation; hidden-layer forwards)",
                          "achieved": achieved_tflops, "peak": FP64_DMMA_PEAK_TFLOPS,
                          "unit": "TFLOP/s",
                          "frac": (achieved_tflops / FP64_DMMA_PEAK_TFLOPS) if achieved_tflops else None,

@@ -184,6 +184,8 @@ void launch_eig_status(const double* la, int p, const double* lb, int q, const i
 void launch_kron_scale(double* W, const double* la, int p, const double* lb, int q,
                        cudaStream_t s);
 void launch_set_status(int32_t* status, int32_t code, cudaStream_t s);
+void launch_gen_eig_1x1(const double* f1, const double* f2, double lam, double* t, double* eig,
+                        int* info, cudaStream_t s);
 void launch_identity(double* F, int n, double v, cudaStream_t s);
 
 // ---- small on-device generalised eigensolver + combine (kp_eig_small.cu) ---------

@@ -223,6 +223,27 @@ void launch_kron_scale(double* W, const double* la, int p, const double* lb, int
   k_kron_scale<<<grid1((int64_t)p * q), 256, 0, s>>>(W, la, p, lb, q);
 }
 
+// 1 x 1 generalised eigenproblem: M1 = f1 + lam, M2 = f2 + lam; T = 1/sqrt(M2), eig = M1/M2.
+__global__ void k_gen_eig_1x1(const double* f1, const double* f2, double lam, double* t,
+                              double* eig, int* info) {
+  const double m1 = f1[0] + lam, m2 = f2[0] + lam;
+  if (!(m2 > 0.0)) {
+    *info = 2;  // LAPACK convention: info > n -> second matrix not PD
+    t[0] = 0.0;
+    eig[0] = 0.0;
+    return;
+  }
+  t[0] = 1.0 / sqrt(m2);
+  eig[0] = m1 / m2;
+  *info = 0;
+}
+
+void launch_gen_eig_1x1(const double* f1, const double* f2, double lam, double* t, double* eig,
+                        int* info, cudaStream_t s) {
+  count_launch();
+  k_gen_eig_1x1<<<1, 1, 0, s>>>(f1, f2, lam, t, eig, info);
+}
+
 __global__ void k_set_status(int32_t* status, int32_t code) { set_status(status, code); }
 
 void launch_set_status(int32_t* status, int32_t code, cudaStream_t s) {

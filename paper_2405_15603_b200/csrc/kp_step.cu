@@ -20,6 +20,7 @@
 #include <atomic>
 #include <thread>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -676,8 +677,12 @@ int kron_solve(kp_context* ctx, const Ctx& c, int p, int q, double* A1, double* 
   double* work = c.at(P.o_work);
   KP_SOLVER_TRY(cusolverDnSetStream(ctx->solver, c.s));
   KP_BLAS_TRY(cublasSetStream(ctx->blas, c.s));
-  KP_TRY(gen_eig(ctx->solver, p, A1, A2, la, work, (int)P.lwork, info));
-  KP_TRY(gen_eig(ctx->solver, q, B1, B2, lb, work, (int)P.lwork, info + 1));
+  KP_CUDA_TRY(cudaMemsetAsync(info, 0, 2 * sizeof(int), c.s));
+  // 1 x 1 factors (e.g. the h_out = 1 layer's B) are solved in closed form
+  if (p == 1) launch_gen_eig_1x1(A1, A2, 0.0, A1, la, info, c.s);
+  else KP_TRY(gen_eig(ctx->solver, p, A1, A2, la, work, (int)P.lwork, info));
+  if (q == 1) launch_gen_eig_1x1(B1, B2, 0.0, B1, lb, info + 1, c.s);
+  else KP_TRY(gen_eig(ctx->solver, q, B1, B2, lb, work, (int)P.lwork, info + 1));
   launch_eig_status(la, p, lb, q, info, status, c.s);
   return kron_combine(ctx->blas, c.s, p, q, A1, la, B1, lb, G, out, sign, c.at(P.o_T1),
                       c.at(P.o_T2));
@@ -745,24 +750,37 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
       return;
     }
     int* info = reinterpret_cast<int*>(c.at(P.k_info[l])) + k;
-    if (k == 0) {
-      launch_damped_copy(st->a_int + P.fa[l], lam, P.p[l], c.at(P.k_A1[l]), s);
-      launch_damped_copy(st->a_bnd + P.fa[l], lam, P.p[l], c.at(P.k_A2[l]), s);
-      rc[2 * l] = gen_eig(ctx->side_solver[2 * l], P.p[l], c.at(P.k_A1[l]), c.at(P.k_A2[l]),
-                          c.at(P.k_la[l]), c.at(P.k_wa[l]), P.lw[l][0], info);
+    // zero the info word first: it must not depend on what the workspace held before
+    if (cudaMemsetAsync(info, 0, sizeof(int), s) != cudaSuccess) {
+      rc[2 * l + k] = KP_ERR_CUDA;
+      return;
+    }
+    const int n = k == 0 ? P.p[l] : P.q[l];
+    const double* f1 = k == 0 ? st->a_int + P.fa[l] : st->b_int + P.fb[l];
+    const double* f2 = k == 0 ? st->a_bnd + P.fa[l] : st->b_bnd + P.fb[l];
+    double* m1 = c.at(k == 0 ? P.k_A1[l] : P.k_B1[l]);
+    double* m2 = c.at(k == 0 ? P.k_A2[l] : P.k_B2[l]);
+    double* ev = c.at(k == 0 ? P.k_la[l] : P.k_lb[l]);
+    if (n == 1) {
+      launch_gen_eig_1x1(f1, f2, lam, m1, ev, info, s);
     } else {
-      launch_damped_copy(st->b_int + P.fb[l], lam, P.q[l], c.at(P.k_B1[l]), s);
-      launch_damped_copy(st->b_bnd + P.fb[l], lam, P.q[l], c.at(P.k_B2[l]), s);
-      rc[2 * l + 1] = gen_eig(ctx->side_solver[2 * l + 1], P.q[l], c.at(P.k_B1[l]),
-                              c.at(P.k_B2[l]), c.at(P.k_lb[l]), c.at(P.k_wb[l]), P.lw[l][1], info);
+      launch_damped_copy(f1, lam, n, m1, s);
+      launch_damped_copy(f2, lam, n, m2, s);
+      rc[2 * l + k] = gen_eig(ctx->side_solver[2 * l + k], n, m1, m2, ev,
+                              c.at(k == 0 ? P.k_wa[l] : P.k_wb[l]), P.lw[l][k], info);
     }
     cudaEventRecord(ctx->side_ev[2 * l + k], s);
   };
   if (!big.empty()) {
-    std::vector<std::thread> pool;
-    for (int l : big)
-      for (int k = 0; k < 2; ++k) pool.emplace_back(solve_pair, l, k);
-    for (auto& t : pool) t.join();
+    if (getenv("KP_SERIAL_EIG")) {  // diagnostic: issue the solves from this thread
+      for (int l : big)
+        for (int k = 0; k < 2; ++k) solve_pair(l, k);
+    } else {
+      std::vector<std::thread> pool;
+      for (int l : big)
+        for (int k = 0; k < 2; ++k) pool.emplace_back(solve_pair, l, k);
+      for (auto& t : pool) t.join();
+    }
   }
   for (int v : rc) KP_TRY(v);
   for (int l : big) {
@@ -776,6 +794,15 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
     KP_CUDA_TRY(cudaEventRecord(ctx->side_ev[2 * l], s));
   }
   for (int l : big) KP_CUDA_TRY(cudaStreamWaitEvent(c.s, ctx->side_ev[2 * l], 0));
+  if (getenv("KP_DEBUG_EIG")) {  // diagnostic: print the per-layer eigensolver info words
+    cudaStreamSynchronize(c.s);
+    for (int l = 0; l < P.L; ++l) {
+      int inf[2] = {0, 0};
+      cudaMemcpy(inf, c.at(P.k_info[l]), sizeof(inf), cudaMemcpyDeviceToHost);
+      fprintf(stderr, "[kp] layer %d p=%d q=%d info=(%d,%d) lw=(%d,%d)\n", l, P.p[l], P.q[l],
+              inf[0], inf[1], P.lw[l][0], P.lw[l][1]);
+    }
+  }
   launch_axpy_out(delta, st->prev_update, cfg->momentum, c.at(P.o_dir), P.D, c.s);
   if (out->grad) KP_CUDA_TRY(cudaMemcpyAsync(out->grad, grad, sizeof(double) * P.D,
                                              cudaMemcpyDeviceToDevice, c.s));
