@@ -40,6 +40,12 @@ __global__ void __launch_bounds__(WM* WN * 32, 1) k_gemm_nt(GemmNT g, int tiles_
   const int64_t m0 = (int64_t)(blockIdx.x / tiles_n) * BM;
   const int n0 = tn * BN;
   const int KT = (g.K + BK - 1) / BK;
+  if (blockIdx.y > 0) {  // batch entry
+    g.A += blockIdx.y * g.sA;
+    g.B += blockIdx.y * g.sB;
+    g.C += blockIdx.y * g.sC;
+    if (g.bias) g.bias += blockIdx.y * g.sBias;
+  }
 
   auto load = [&](int stage, int kt) {
     const int k0 = kt * BK;
@@ -132,12 +138,12 @@ static void run_nt(const GemmNT& g, cudaStream_t s) {
   const int tiles_n = (int)ceil_div(g.N, BN);
   const int64_t tiles = ceil_div(g.M, BM) * tiles_n;
   count_launch();
-  kern<<<(unsigned)tiles, WM * WN * 32, smem, s>>>(g, tiles_n);
+  kern<<<dim3((unsigned)tiles, (unsigned)g.batch), WM * WN * 32, smem, s>>>(g, tiles_n);
 }
 
 void launch_gemm_nt(const GemmNT& g, cudaStream_t s) {
   if (g.M <= 0 || g.N <= 0) return;
-  if (launch_gemm_nt_tma(g, s, 0)) return;
+  if (g.batch == 1 && launch_gemm_nt_tma(g, s, 0)) return;
   launch_gemm_nt_cpasync(g, s);
 }
 

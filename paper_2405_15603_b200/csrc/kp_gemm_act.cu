@@ -69,8 +69,18 @@ __global__ void __launch_bounds__(NW * 32, 8 / NW)
   const int tn = blockIdx.x % tiles_n;
   const int64_t smp0 = (int64_t)(blockIdx.x / tiles_n) * g.nb;
   const int S = g.S;
-  const int m0 = (int)(smp0 * S);
+  const int kk = blockIdx.y;  // candidate batch entry
+  const int m0 = (int)(smp0 * S);                             // row inside this entry
+  const int ma = (int)(kk * g.n_samples * S + m0);            // row in the stacked A map
   const int n0 = tn * BN;
+  const int nb0 = kk * g.N + n0;                              // row in the stacked B map
+  if (kk > 0) {
+    if (g.bias) g.bias += kk * g.bias_bstride;
+    if (g.pre) g.pre += kk * g.out_bstride;
+    if (g.post) g.post += kk * g.out_bstride;
+    if (g.upart) g.upart += kk * g.upart_bstride;
+    if (g.wlast) g.wlast += kk * g.wlast_bstride;
+  }
   const int KT = g.K / BK;
   const uint32_t stage_bytes = (uint32_t)(box_rows + BN) * BK * sizeof(double);
 
@@ -87,8 +97,8 @@ __global__ void __launch_bounds__(NW * 32, 8 / NW)
     mbar_arrive_expect_tx(&full[s], stage_bytes);
 #pragma unroll
     for (int sl = 0; sl < SLABS; ++sl) {
-      tma2d(As + s * A_STAGE + sl * AROWS * 16, &mapA, kt * BK + sl * 16, m0, &full[s]);
-      tma2d(Bs + s * B_STAGE + sl * BN * 16, &mapB, kt * BK + sl * 16, n0, &full[s]);
+      tma2d(As + s * A_STAGE + sl * AROWS * 16, &mapA, kt * BK + sl * 16, ma, &full[s]);
+      tma2d(Bs + s * B_STAGE + sl * BN * 16, &mapB, kt * BK + sl * 16, nb0, &full[s]);
     }
   };
   if (threadIdx.x == 0)
@@ -201,10 +211,11 @@ __global__ void __launch_bounds__(NW * 32, 8 / NW)
 template <int MODE, int TM, int NW, int BK, int STAGES>
 bool run_act(const GemmAct& g, int box_rows, cudaStream_t s) {
   CUtensorMap ma, mb;
-  const int64_t M = g.n_samples * g.S;
+  const int64_t M = g.n_samples * g.S * g.batch;
   if (g.K % BK) return false;
   if (!make_tma_map_2d(&ma, g.A, (uint64_t)M, (uint64_t)g.K, (uint64_t)g.lda, box_rows)) return false;
-  if (!make_tma_map_2d(&mb, g.B, (uint64_t)g.N, (uint64_t)g.K, (uint64_t)g.ldb, BN)) return false;
+  if (!make_tma_map_2d(&mb, g.B, (uint64_t)g.N * g.batch, (uint64_t)g.K, (uint64_t)g.ldb, BN))
+    return false;
   const size_t pipe = (size_t)STAGES * (TM * 8 + BN) * BK * sizeof(double) + 2 * STAGES * 8;
   const size_t cst = (size_t)TM * 8 * CPITCH * sizeof(double);
   const size_t smem = std::max(pipe, cst) + 1024;
@@ -217,7 +228,7 @@ bool run_act(const GemmAct& g, int box_rows, cudaStream_t s) {
   const int tiles_n = (int)ceil_div(g.N, BN);
   const int64_t tiles = ceil_div(g.n_samples, g.nb) * tiles_n;
   count_launch();
-  kern<<<(unsigned)tiles, NW * 32, smem, s>>>(ma, mb, g, tiles_n, box_rows);
+  kern<<<dim3((unsigned)tiles, (unsigned)g.batch), NW * 32, smem, s>>>(ma, mb, g, tiles_n, box_rows);
   return true;
 }
 
@@ -237,11 +248,15 @@ bool run_act_tm(const GemmAct& g, int box_rows, cudaStream_t s) {
 
 int gemm_act_samples_per_tile(int S) { return S <= ROWS_MAX ? ROWS_MAX / S : 0; }
 
+bool gemm_act_ok(int S, int K, int64_t lda, int64_t ldb) {
+  return S <= ROWS_MAX && K % 16 == 0 && lda % 2 == 0 && ldb % 2 == 0;
+}
+
 bool launch_gemm_act(GemmAct g, int mode, cudaStream_t s) {
   if (g.n_samples <= 0) return true;
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (g.S > ROWS_MAX || g.K % 16 != 0 || g.lda % 2 || g.ldb % 2 || !al16(g.A) || !al16(g.B) ||
-      g.n_samples * g.S >= (int64_t(1) << 31))
+      g.n_samples * g.S * g.batch >= (int64_t(1) << 31) || g.N * (int64_t)g.batch >= (int64_t(1) << 31))
     return false;
   g.nb = gemm_act_samples_per_tile(g.S);
   const int box_rows = (g.nb * g.S + 7) / 8 * 8;
@@ -271,7 +286,11 @@ bool launch_gemm_act(GemmAct g, int mode, cudaStream_t s) {
 __global__ void k_last_from_partials(const double* __restrict__ upart, int ntn, int64_t n,
                                      TaylorDims td, const double* __restrict__ bias,
                                      const double* __restrict__ r0, const double* __restrict__ seeds,
-                                     const double* __restrict__ targets, double* __restrict__ r) {
+                                     const double* __restrict__ targets, double* __restrict__ r,
+                                     int64_t bias_bstride, int64_t r_bstride) {
+  upart += (int64_t)blockIdx.y * n * td.S * ntn;
+  bias += (int64_t)blockIdx.y * bias_bstride;
+  r += (int64_t)blockIdx.y * r_bstride;
   for (int64_t smp = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; smp < n;
        smp += (int64_t)gridDim.x * blockDim.x) {
     double v = td.taylor ? r0[smp] : 0.0;
@@ -289,11 +308,13 @@ __global__ void k_last_from_partials(const double* __restrict__ upart, int ntn, 
 
 void launch_last_from_partials(const double* upart, int ntn, int64_t n, TaylorDims td,
                                const double* bias, const double* r0, const double* seeds,
-                               const double* targets, double* r, cudaStream_t s) {
+                               const double* targets, double* r, cudaStream_t s, int batch,
+                               int64_t bias_bstride, int64_t r_bstride) {
   if (n <= 0) return;
   count_launch();
   const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(n, 128), 148 * 16);
-  k_last_from_partials<<<blocks, 128, 0, s>>>(upart, ntn, n, td, bias, r0, seeds, targets, r);
+  k_last_from_partials<<<dim3(blocks, (unsigned)batch), 128, 0, s>>>(
+      upart, ntn, n, td, bias, r0, seeds, targets, r, bias_bstride, r_bstride);
 }
 
 }  // namespace kp

@@ -26,6 +26,9 @@ struct GemmNT {
   const double* bias;
   int64_t bias_stride;
   int S;
+  // optional batch (grid.y): operand / output / bias offsets per batch entry
+  int batch = 1;
+  int64_t sA = 0, sB = 0, sC = 0, sBias = 0;
 };
 void launch_gemm_nt(const GemmNT& g, cudaStream_t s);
 // TMA-fed variant (kp_gemm_tma.cu); returns false when the operands do not meet
@@ -89,7 +92,13 @@ struct GemmAct {
   const double* wlast;  // ACT_LAST: last-layer weight row (length N)
   double* upart;        // ACT_LAST: (n_samples*S) x ceil(N/128) partial dots
   int nb;               // set by the launcher
+  // candidate batch (grid.y): A is the stack of `batch` (n_samples*S) x K states, B the
+  // stack of `batch` N x K weight blocks (row-contiguous), outputs/bias offset per entry
+  int batch = 1;
+  int64_t bias_bstride = 0, out_bstride = 0, upart_bstride = 0, wlast_bstride = 0;
 };
+// Whether launch_gemm_act can run this layer shape (fused path available).
+bool gemm_act_ok(int S, int K, int64_t lda, int64_t ldb);
 int gemm_act_samples_per_tile(int S);
 bool launch_gemm_act(GemmAct g, int mode, cudaStream_t s);
 
@@ -109,12 +118,13 @@ struct TaylorDims {
 // Layer 0 fused with its activation: pre-activation value z = x W0^T + b0 -> zval,
 // post-activation state (n*S x h1) -> post.  Derivative rows of the pre-activation
 // are W0[:, i] and its operator row is 0 (reference taylor.py:124-131).
+// batch > 1: parameter sets theta0 + kk*D; zval/post/w0t/q0 stacked per entry.
 void launch_first_layer(const double* x, int64_t n, int d, const double* theta0, int h1,
                         TaylorDims td, const double* w0t, const double* q0, double* zval,
-                        double* post, cudaStream_t s);
+                        double* post, cudaStream_t s, int batch = 1, int64_t D = 0);
 // Per parameter set: w0t = W0^T (d x h1), q0[j] = sum_i (W0[j,i] c_i) W0[j,i].
 void launch_prep_layer0(const double* theta0, int d, int h1, const double* cdiag, double* w0t,
-                        double* q0, cudaStream_t s);
+                        double* q0, cudaStream_t s, int batch = 1, int64_t D = 0);
 // Taylor activation (taylor.py:151-169): pre (n*S x h) -> post.
 void launch_act_fwd(const double* pre, double* post, int64_t n, int h, TaylorDims td,
                     const double* cdiag, cudaStream_t s);
@@ -140,7 +150,8 @@ void launch_act_bwd(const ActBwd& a, int64_t n, int h, TaylorDims td, const doub
 // Scalar output from ACT_LAST partials + residual (same semantics as launch_last_layer).
 void launch_last_from_partials(const double* upart, int ntn, int64_t n, TaylorDims td,
                                const double* bias, const double* r0, const double* seeds,
-                               const double* targets, double* r, cudaStream_t s);
+                               const double* targets, double* r, cudaStream_t s, int batch = 1,
+                               int64_t bias_bstride = 0, int64_t r_bstride = 0);
 // Layer-0 gradient, derivative-row part: acc[j*(d+1)+i] += sum_n r_n gbar0[n, 1+i, j].
 void launch_grad0_deriv(const double* gbar0, const double* r, int64_t n, int d, int h1,
                         double* acc, cudaStream_t s);
@@ -169,11 +180,13 @@ struct WPack {
   int L;
   int h[17];
   int64_t th[16];  // offset of layer l in theta
-  int64_t wo[16];  // offset of layer l in the padded copy
+  int64_t wo[16];  // offset of layer l's block in the padded copy
+  int64_t ws[16];  // stride between batch entries inside layer l's block (q_l * h_l)
 };
-// out = theta + 2^exp2 dir (dir == nullptr: copy); wpad (optional) = padded W copy of out.
+// For kk < batch: out[kk] = theta + 2^(exp2 + kk) dir (dir == nullptr: copy theta);
+// wpad (optional): padded W copies, entry kk of layer l at wo[l] + kk * ws[l].
 void launch_candidate(const double* theta, const double* dir, int exp2, double* out, int64_t D,
-                      const WPack& wp, double* wpad, cudaStream_t s);
+                      const WPack& wp, double* wpad, cudaStream_t s, int batch = 1);
 void launch_argmin_update(const double* ls_sums, int ncand, int min_exp, double ni, double nb,
                           double* theta, double* prev, const double* dir, int64_t D,
                           double* scalars, double* ls_losses, int32_t* status, double mu,

@@ -85,12 +85,14 @@ void launch_losses(const double* sums, double ni, double nb, double* scalars, cu
 // theta_c = theta + 2^e * dir  (add_scaled, network.py:299-305); optionally also the
 // padded weight copy (per layer W_l as q x h_l, pitch h_l) that the TMA GEMM reads.
 __global__ void k_candidate(const double* __restrict__ th, const double* __restrict__ dir,
-                            double alpha, double* __restrict__ out, int64_t D, WPack wp,
+                            int exp2, double* __restrict__ out, int64_t D, WPack wp,
                             double* __restrict__ wpad) {
+  const int kk = blockIdx.y;
+  const double alpha = ldexp(1.0, exp2 + kk);
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < D;
        e += (int64_t)gridDim.x * blockDim.x) {
     const double v = dir ? th[e] + alpha * dir[e] : th[e];
-    if (out) out[e] = v;
+    if (out) out[kk * D + e] = v;
     if (wpad) {
       int l = 0;
       while (l + 1 < wp.L && e >= wp.th[l + 1]) ++l;
@@ -98,15 +100,15 @@ __global__ void k_candidate(const double* __restrict__ th, const double* __restr
       const int p = wp.h[l] + 1;
       const int64_t row = r / p;
       const int col = (int)(r % p);
-      if (col < wp.h[l]) wpad[wp.wo[l] + row * wp.h[l] + col] = v;
+      if (col < wp.h[l]) wpad[wp.wo[l] + kk * wp.ws[l] + row * wp.h[l] + col] = v;
     }
   }
 }
 
 void launch_candidate(const double* theta, const double* dir, int exp2, double* out, int64_t D,
-                      const WPack& wp, double* wpad, cudaStream_t s) {
+                      const WPack& wp, double* wpad, cudaStream_t s, int batch) {
   count_launch();
-  k_candidate<<<grid1(D), 256, 0, s>>>(theta, dir, ldexp(1.0, exp2), out, D, wp, wpad);
+  k_candidate<<<dim3(grid1(D), (unsigned)batch), 256, 0, s>>>(theta, dir, exp2, out, D, wp, wpad);
 }
 
 // Grid argmin (optim.py:195-211) then theta += alpha dir, prev = alpha dir.

@@ -137,7 +137,9 @@ struct Plan {
   int lw[MAXL][2] = {};
   int64_t o_wpad = 0, o_wpadc = 0, wo[MAXL] = {};
   int64_t o_w0t = 0, o_q0 = 0, o_w0tc = 0, o_q0c = 0;
-  WPack wp{};
+  WPack wp{};   // layout of the padded copy of theta
+  WPack wpc{};  // layout of the Bc line-search candidates' padded copies (layer-major)
+  int Bc = 1;   // line-search candidates evaluated per batched launch
   int64_t lwork = 0;
   int64_t total = 0;  // doubles
   // reduce-buffer sub-offsets (relative to o_red)
@@ -199,6 +201,21 @@ int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
     P.wp.wo[l] = woff;
     woff += ((int64_t)P.q[l] * P.h[l] + 1) / 2 * 2;  // keep every layer 16-byte aligned
   }
+  // candidate batching: small problems evaluate all grid points per launch
+  {
+    bool fused_ok = P.L >= 3;
+    for (int l = 1; l + 1 < P.L; ++l) fused_ok = fused_ok && gemm_act_ok(P.S, P.h[l], P.h[l], P.h[l]);
+    const int64_t per = std::max<int64_t>(P.Nc * P.S, P.Nb) * P.maxh;
+    const int64_t cap = 300000000;  // doubles per stacked state buffer
+    P.Bc = fused_ok ? (int)std::max<int64_t>(1, std::min<int64_t>(P.ncand, cap / std::max<int64_t>(per, 1))) : 1;
+  }
+  int64_t wcoff = 0;
+  P.wpc = P.wp;
+  for (int l = 0; l < P.L; ++l) {
+    P.wpc.wo[l] = wcoff;
+    P.wpc.ws[l] = (int64_t)P.q[l] * P.h[l];
+    wcoff += ((int64_t)P.Bc * P.q[l] * P.h[l] + 1) / 2 * 2;
+  }
   for (int l = 0; l < P.L; ++l) {
     P.fa[l] = P.FA;
     P.FA += (int64_t)P.p[l] * P.p[l];
@@ -213,20 +230,20 @@ int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
     return at;
   };
   for (int l = 1; l < P.L; ++l) P.o_wT[l] = take((int64_t)P.h[l] * P.q[l]);
-  P.o_zval0 = take(P.Nc * P.h[1]);
+  P.o_zval0 = take(P.Bc * P.Nc * P.h[1]);
   for (int l = 1; l < P.L; ++l) P.o_post[l] = take(Mc * P.h[l]);
   for (int l = 1; l + 1 < P.L; ++l) P.o_pre[l] = take(Mc * P.h[l + 1]);
   for (int l = 0; l + 1 < P.L; ++l) P.o_gout[l] = take(Mc * P.h[l + 1]);
-  P.o_ping = take(Mc * P.maxh);
-  P.o_pong = take(Mc * P.maxh);
+  P.o_ping = take(P.Bc * Mc * P.maxh);
+  P.o_pong = take(P.Bc * Mc * P.maxh);
   P.o_u = take(Mc);
-  P.o_upart = take(std::max(Mc, P.Nb) * ceil_div(std::max(P.maxh, 1), 128));
-  P.o_bzval0 = take(P.Nb * P.h[1]);
+  P.o_upart = take(P.Bc * std::max(Mc, P.Nb) * ceil_div(std::max(P.maxh, 1), 128));
+  P.o_bzval0 = take(P.Bc * P.Nb * P.h[1]);
   for (int l = 1; l < P.L; ++l) P.o_bpost[l] = take(P.Nb * P.h[l]);
   for (int l = 1; l + 1 < P.L; ++l) P.o_bpre[l] = take(P.Nb * P.h[l + 1]);
   for (int l = 0; l + 1 < P.L; ++l) P.o_bg[l] = take(P.Nb * P.h[l + 1]);
-  P.o_bping = take(P.Nb * P.maxh);
-  P.o_bpong = take(P.Nb * P.maxh);
+  P.o_bping = take(P.Bc * P.Nb * P.maxh);
+  P.o_bpong = take(P.Bc * P.Nb * P.maxh);
   P.o_ones = take(P.Nb);
   P.o_r = take(P.N);
   P.o_rb = take(P.Nb);
@@ -265,13 +282,13 @@ int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
   P.o_grad = take(P.D);
   P.o_delta = take(P.D);
   P.o_dir = take(P.D);
-  P.o_thc = take(P.D);
+  P.o_thc = take(P.Bc * P.D);
   P.o_wpad = take(woff);
-  P.o_wpadc = take(woff);
+  P.o_wpadc = take(wcoff);
   P.o_w0t = take((int64_t)P.d * P.h[1]);
   P.o_q0 = take(P.h[1]);
-  P.o_w0tc = take((int64_t)P.d * P.h[1]);
-  P.o_q0c = take(P.h[1]);
+  P.o_w0tc = take((int64_t)P.Bc * P.d * P.h[1]);
+  P.o_q0c = take((int64_t)P.Bc * P.h[1]);
   P.o_ls = take(2 * (int64_t)P.ncand);
   P.o_A1 = take((int64_t)P.maxp * P.maxp);
   P.o_A2 = take((int64_t)P.maxp * P.maxp);
@@ -351,14 +368,15 @@ void prof_gemm(const Ctx& c, const GemmNT& g) {
 
 // Hidden layer l forward: fused GEMM + bias + activation when possible, else GEMM then
 // the elementwise activation kernel.  mode: ACT_STORE (pre + post), ACT_LOSS (post).
-void hidden_layer(const Ctx& c, const double* theta, const double* wpad, int l, const double* in,
+// wl = padded W_l (h_{l+1} x h_l, pitch h_l).
+void hidden_layer(const Ctx& c, const double* theta, const double* wl, int l, const double* in,
                   int64_t n, const TaylorDims& td, const double* cdiag, double* pre, double* post,
                   int mode) {
   const Plan& P = c.P;
   GemmAct ga{};
   ga.A = in;
   ga.lda = P.h[l];
-  ga.B = wpad + P.wo[l];
+  ga.B = wl;
   ga.ldb = P.h[l];
   ga.bias = theta + P.th[l] + P.h[l];
   ga.bias_stride = P.p[l];
@@ -377,7 +395,7 @@ void hidden_layer(const Ctx& c, const double* theta, const double* wpad, int l, 
               [&] { done = launch_gemm_act(ga, mode, c.s); });
   if (done) return;
   double* out = mode == ACT_STORE ? pre : post;
-  GemmNT g{in, P.h[l], wpad + P.wo[l], P.h[l], out, P.h[l + 1], n * td.S, P.h[l + 1], P.h[l],
+  GemmNT g{in, P.h[l], wl, P.h[l], out, P.h[l + 1], n * td.S, P.h[l + 1], P.h[l],
            theta + P.th[l] + P.h[l], P.p[l], td.S};
   prof_gemm(c, g);
   launch_act_fwd(out, post, n, P.h[l + 1], td, cdiag, c.s);
@@ -444,19 +462,24 @@ void forward_store(const Ctx& c, const double* theta, const double* wpad, const 
     launch_first_layer(x, n, P.d, theta + P.th[0], P.h[1], td, c.at(P.o_w0t), c.at(P.o_q0),
                        b.zval0, b.post[1], c.s);
     for (int l = 1; l + 1 < L; ++l)
-      hidden_layer(c, theta, wpad, l, b.post[l], n, td, cdiag, b.pre[l], b.post[l + 1], ACT_STORE);
+      hidden_layer(c, theta, wpad + P.wo[l], l, b.post[l], n, td, cdiag, b.pre[l], b.post[l + 1],
+                   ACT_STORE);
     last_in = b.post[L - 1];
   }
   launch_last_layer(last_in, n, P.h[L - 1], theta + P.th[L - 1], td, ri.r0, ri.seeds, ri.targets,
                     r, u_out, c.s);
 }
 
-// Forward pass for losses only (no stored states): ping-pong buffers, in-place activation.
+// Forward pass for losses only (no stored states): ping-pong buffers.  `batch` parameter
+// sets are evaluated per launch (theta + kk*D, padded weights per `wp`, states stacked in
+// ping/pong, residuals r + kk*r_bstride); batch > 1 requires the fused layer path.
 void forward_loss(const Ctx& c, const double* theta, const double* wpad, const double* x, int64_t n,
                   const TaylorDims& td, const double* cdiag, double* ping, double* pong,
-                  const ResidualIn& ri, double* r, double* u_out, bool cand = false) {
+                  const ResidualIn& ri, double* r, double* u_out, bool cand = false,
+                  int batch = 1, int64_t r_bstride = 0) {
   const Plan& P = c.P;
   const int L = P.L;
+  const WPack& wp = cand ? P.wpc : P.wp;
   const double* cur;
   if (L == 1) {
     if (td.taylor) {
@@ -468,45 +491,63 @@ void forward_loss(const Ctx& c, const double* theta, const double* wpad, const d
   } else {
     double* zs = td.taylor ? c.at(P.o_zval0) : c.at(P.o_bzval0);
     launch_first_layer(x, n, P.d, theta + P.th[0], P.h[1], td, c.at(cand ? P.o_w0tc : P.o_w0t),
-                       c.at(cand ? P.o_q0c : P.o_q0), zs, ping, c.s);
+                       c.at(cand ? P.o_q0c : P.o_q0), zs, ping, c.s, batch, P.D);
     double* a = ping;
     double* b = pong;
     for (int l = 1; l + 1 < L; ++l) {
+      GemmAct ga{};
+      ga.A = a;
+      ga.lda = P.h[l];
+      ga.B = wpad + wp.wo[l];
+      ga.ldb = P.h[l];
+      ga.bias = theta + P.th[l] + P.h[l];
+      ga.bias_stride = P.p[l];
+      ga.n_samples = n;
+      ga.S = td.S;
+      ga.d = td.d;
+      ga.taylor = td.taylor;
+      ga.N = P.h[l + 1];
+      ga.K = P.h[l];
+      ga.cdiag = cdiag;
+      ga.batch = batch;
+      ga.bias_bstride = P.D;
       if (l == L - 2 && u_out == nullptr) {
         // last hidden layer: fuse the h_out = 1 output layer, never store this state
-        GemmAct ga{};
-        ga.A = a;
-        ga.lda = P.h[l];
-        ga.B = wpad + P.wo[l];
-        ga.ldb = P.h[l];
-        ga.bias = theta + P.th[l] + P.h[l];
-        ga.bias_stride = P.p[l];
-        ga.n_samples = n;
-        ga.S = td.S;
-        ga.d = td.d;
-        ga.taylor = td.taylor;
-        ga.N = P.h[l + 1];
-        ga.K = P.h[l];
-        ga.cdiag = cdiag;
+        const int ntn = (int)ceil_div(P.h[l + 1], 128);
         ga.wlast = theta + P.th[L - 1];
+        ga.wlast_bstride = P.D;
         ga.upart = c.at(P.o_upart);
+        ga.upart_bstride = n * td.S * ntn;
         bool done = false;
-        prof_launch(c, 2.0 * (double)n * td.S * P.h[l] * P.h[l + 1],
+        prof_launch(c, 2.0 * (double)batch * n * td.S * P.h[l] * P.h[l + 1],
                     [&] { done = launch_gemm_act(ga, ACT_LAST, c.s); });
         if (done) {
-          launch_last_from_partials(c.at(P.o_upart), (int)ceil_div(P.h[l + 1], 128), n, td,
-                                    theta + P.th[L - 1] + P.h[L - 1], ri.r0, ri.seeds, ri.targets,
-                                    r, c.s);
+          launch_last_from_partials(c.at(P.o_upart), ntn, n, td, theta + P.th[L - 1] + P.h[L - 1],
+                                    ri.r0, ri.seeds, ri.targets, r, c.s, batch, P.D, r_bstride);
           return;
         }
+      } else {
+        ga.post = b;
+        ga.ldo = P.h[l + 1];
+        ga.out_bstride = n * td.S * P.h[l + 1];
+        bool done = false;
+        prof_launch(c, 2.0 * (double)batch * n * td.S * P.h[l] * P.h[l + 1],
+                    [&] { done = launch_gemm_act(ga, ACT_LOSS, c.s); });
+        if (done) {
+          std::swap(a, b);
+          continue;
+        }
       }
-      hidden_layer(c, theta, wpad, l, a, n, td, cdiag, b, b, ACT_LOSS);
+      // unfused fallback (only reachable with batch == 1, see make_plan)
+      hidden_layer(c, theta, wpad + wp.wo[l], l, a, n, td, cdiag, b, b, ACT_LOSS);
       std::swap(a, b);
     }
     cur = a;
   }
-  launch_last_layer(cur, n, P.h[L - 1], theta + P.th[L - 1], td, ri.r0, ri.seeds, ri.targets, r,
-                    u_out, c.s);
+  for (int kk = 0; kk < batch; ++kk)
+    launch_last_layer(cur + (int64_t)kk * n * td.S * P.h[L - 1], n, P.h[L - 1],
+                      theta + kk * P.D + P.th[L - 1], td, ri.r0, ri.seeds, ri.targets,
+                      r ? r + kk * r_bstride : nullptr, u_out, c.s);
 }
 
 // Reverse pass (taylor.py:242-276 / network.py:216-232): gout[l] for l < L-1.
@@ -817,19 +858,23 @@ int phase_linesearch(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, cons
   const TaylorDims tdb{1, 0, false};
   double* thc = c.at(P.o_thc);
   double* dir = c.at(P.o_dir);
-  for (int k = 0; k < P.ncand; ++k) {
-    launch_candidate(st->theta, dir, cfg->ls_min_exp + k, thc, P.D, P.wp, c.at(P.o_wpadc), c.s);
+  for (int k0 = 0; k0 < P.ncand; k0 += P.Bc) {
+    const int nb = std::min(P.Bc, P.ncand - k0);
+    launch_candidate(st->theta, dir, cfg->ls_min_exp + k0, thc, P.D, P.wpc, c.at(P.o_wpadc), c.s,
+                     nb);
     if (P.L >= 2)
-      launch_prep_layer0(thc, P.d, P.h[1], bt->coeff_diag, c.at(P.o_w0tc), c.at(P.o_q0c), c.s);
+      launch_prep_layer0(thc, P.d, P.h[1], bt->coeff_diag, c.at(P.o_w0tc), c.at(P.o_q0c), c.s, nb,
+                         P.D);
     for (int64_t n0 = 0; n0 < P.N; n0 += P.Nc) {
       const int64_t nc = std::min(P.Nc, P.N - n0);
       ResidualIn ri{bt->r0 + n0, bt->seeds + n0 * P.S, nullptr};
-      forward_loss(c, thc, c.at(P.o_wpadc), bt->x_int + n0 * P.d, nc, tdi, bt->coeff_diag, c.at(P.o_ping),
-                   c.at(P.o_pong), ri, c.at(P.o_rls) + k * P.N + n0, nullptr, true);
+      forward_loss(c, thc, c.at(P.o_wpadc), bt->x_int + n0 * P.d, nc, tdi, bt->coeff_diag,
+                   c.at(P.o_ping), c.at(P.o_pong), ri, c.at(P.o_rls) + k0 * P.N + n0, nullptr, true,
+                   nb, P.N);
     }
     ResidualIn rb{nullptr, nullptr, bt->targets};
     forward_loss(c, thc, c.at(P.o_wpadc), bt->x_bnd, P.Nb, tdb, bt->coeff_diag, c.at(P.o_bping),
-                 c.at(P.o_bpong), rb, c.at(P.o_rbls) + k * P.Nb, nullptr, true);
+                 c.at(P.o_bpong), rb, c.at(P.o_rbls) + k0 * P.Nb, nullptr, true, nb, P.Nb);
   }
   double* ls = c.at(P.o_ls);
   launch_sumsq(c.at(P.o_rls), P.N, P.N, P.ncand, ls, 2, c.s);

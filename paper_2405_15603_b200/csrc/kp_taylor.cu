@@ -26,7 +26,10 @@ static inline unsigned grid_for(int64_t n, int threads) {
 
 __global__ void k_prep_layer0(const double* __restrict__ th0, int d, int h1,
                               const double* __restrict__ cdiag, double* __restrict__ w0t,
-                              double* __restrict__ q0) {
+                              double* __restrict__ q0, int64_t D) {
+  th0 += (int64_t)blockIdx.y * D;
+  w0t += (int64_t)blockIdx.y * d * h1;
+  q0 += (int64_t)blockIdx.y * h1;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < h1; j += gridDim.x * blockDim.x) {
     const double* w = th0 + (int64_t)j * (d + 1);
     double q = 0.0;
@@ -40,9 +43,10 @@ __global__ void k_prep_layer0(const double* __restrict__ th0, int d, int h1,
 }
 
 void launch_prep_layer0(const double* theta0, int d, int h1, const double* cdiag, double* w0t,
-                        double* q0, cudaStream_t s) {
+                        double* q0, cudaStream_t s, int batch, int64_t D) {
   count_launch();
-  k_prep_layer0<<<(unsigned)ceil_div(h1, 128), 128, 0, s>>>(theta0, d, h1, cdiag, w0t, q0);
+  k_prep_layer0<<<dim3((unsigned)ceil_div(h1, 128), (unsigned)batch), 128, 0, s>>>(
+      theta0, d, h1, cdiag, w0t, q0, D);
 }
 
 // One warp per (sample, 32-unit tile): lane j writes unit j of every one of the sample's
@@ -55,6 +59,13 @@ __global__ void __launch_bounds__(EXP_WARPS * 32)
                    double* __restrict__ post, int64_t samples_per_block) {
   extern __shared__ double wsm[];  // [d][32] W0^T tile, then q[32]
   const int d = td.d;
+  {  // candidate batch entry (grid.z)
+    const int64_t kk = blockIdx.z;
+    zval += kk * n * h1;
+    post += kk * n * td.S * h1;
+    w0t += kk * (int64_t)d * h1;
+    q0 += kk * h1;
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int j0 = blockIdx.x * 32;
   const int j = j0 + lane;
@@ -85,18 +96,22 @@ __global__ void __launch_bounds__(EXP_WARPS * 32)
 
 void launch_first_layer(const double* x, int64_t n, int d, const double* theta0, int h1,
                         TaylorDims td, const double* w0t, const double* q0, double* zval,
-                        double* post, cudaStream_t s) {
+                        double* post, cudaStream_t s, int batch, int64_t D) {
   if (n <= 0) return;
   // z = x W0^T + b0 (value rows only; bias on every row of this n x h1 product)
   GemmNT g{x, d, theta0, d + 1, zval, h1, n, h1, d, theta0 + d, d + 1, 1};
+  g.batch = batch;
+  g.sB = D;
+  g.sBias = D;
+  g.sC = n * h1;
   launch_gemm_nt(g, s);
   const unsigned tiles = (unsigned)ceil_div(h1, 32);
   const int64_t groups = std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, EXP_WARPS), 148LL * 8 / tiles + 1));
   const int64_t spb = ceil_div(n, groups);
   const size_t smem = td.taylor ? sizeof(double) * (size_t)(td.d * 32 + 32) : 0;
   count_launch();
-  k_first_expand<<<dim3(tiles, (unsigned)ceil_div(n, spb)), EXP_WARPS * 32, smem, s>>>(
-      zval, n, h1, td, w0t, q0, post, spb);
+  k_first_expand<<<dim3(tiles, (unsigned)ceil_div(n, spb), (unsigned)batch), EXP_WARPS * 32, smem,
+                   s>>>(zval, n, h1, td, w0t, q0, post, spb);
 }
 
 // ---------------------------------------------------------------------------
