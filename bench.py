@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--workload", default="c5")
+    ap.add_argument("--optimizer", choices=("kfac", "kfac_star"), default="kfac",
+                    help="kfac (the BASELINE metric) or kfac_star (src/optim.py:266-320)")
     ap.add_argument("--n-interior", type=int, default=16384, help="interior points per GPU")
     ap.add_argument("--n-boundary", type=int, default=None, help="boundary points per GPU")
     ap.add_argument("--chunk", type=int, default=0)
@@ -180,7 +182,8 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2405_15603_b200 import configs
-    from paper_2405_15603_b200.dist import ShardedKfacStep, make_rank_engine, shard_bounds, torch_all_reduce
+    from paper_2405_15603_b200.dist import (ShardedKfacStarStep, ShardedKfacStep, make_rank_engine,
+                                            torch_all_reduce)
     from paper_2405_15603_b200.engine import KfacEngine
 
     rank, world, local = dist_env()
@@ -203,12 +206,13 @@ def run_ours(args):
     if sharded:
         eng = make_rank_engine(wl.widths, batch, prob, rank, world, ema=wl.ema, damping=wl.damping,
                                momentum=wl.momentum, chunk=args.chunk or None)
-        stepper = ShardedKfacStep(eng, torch_all_reduce())
+        cls = ShardedKfacStarStep if args.optimizer == "kfac_star" else ShardedKfacStep
+        stepper = cls(eng, torch_all_reduce())
         do_step = stepper.step
     else:
         eng = make_rank_engine(wl.widths, batch, prob, 0, 1, ema=wl.ema, damping=wl.damping,
                                momentum=wl.momentum, chunk=args.chunk or None)
-        do_step = eng.step
+        do_step = eng.star_step if args.optimizer == "kfac_star" else eng.step
 
     def reset_state():
         eng.load_params(params)
@@ -286,7 +290,8 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference seeding recipe, SURVEY.md §8d)",
-            "config": {"workload": wl.name, "widths": list(wl.widths), "n_interior_per_gpu": n_loc,
+            "config": {"workload": wl.name, "optimizer": args.optimizer,
+                       "widths": list(wl.widths), "n_interior_per_gpu": n_loc,
                        "n_boundary_per_gpu": nb_loc, "n_interior_total": n_glob,
                        "n_boundary_total": nb_glob, "chunk": chunk,
                        "parallelism": f"dp{world}",

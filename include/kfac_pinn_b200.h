@@ -167,6 +167,26 @@ int32_t kp_kfac_phase_update(kp_context* ctx, const kp_problem* prob, const kp_k
                              kp_state* st, kp_step_out* out, void* workspace,
                              size_t workspace_bytes, void* stream);
 
+/* KFAC* step (src/optim.py:266-320): the same factors and preconditioned direction
+ * Delta as kp_kfac_step, then the exact Gramian-vector products G Delta and G prev
+ * (computed as Jacobian-vector products + a weighted reverse contraction — the N x D
+ * residual-Jacobian rows of src/curvature.py:169-194 are never formed), the 2 x 2
+ * quadratic model for (alpha, mu) (src/optim.py:266-286) and the update
+ * theta += alpha Delta + mu prev.  out->scalars = {loss_int, loss_bnd, alpha, mu}.
+ * Sharded use: phases accumulate, precondition, star_gvp, [all-reduce kp_gvp_buffer],
+ * star_update. */
+int32_t kp_kfac_star_step(kp_context* ctx, const kp_problem* prob, const kp_kfac_config* cfg,
+                          kp_state* st, const kp_batch* batch, kp_step_out* out, void* workspace,
+                          size_t workspace_bytes, void* stream);
+int32_t kp_gvp_buffer(kp_context* ctx, const kp_problem* prob, void* workspace, double** ptr,
+                      int64_t* count);
+int32_t kp_kfac_star_phase_gvp(kp_context* ctx, const kp_problem* prob, const kp_kfac_config* cfg,
+                               kp_state* st, const kp_batch* batch, kp_step_out* out,
+                               void* workspace, size_t workspace_bytes, void* stream);
+int32_t kp_kfac_star_phase_update(kp_context* ctx, const kp_problem* prob,
+                                  const kp_kfac_config* cfg, kp_state* st, kp_step_out* out,
+                                  void* workspace, size_t workspace_bytes, void* stream);
+
 /* Forward-Laplacian forward (src/taylor.py:172-203) of the parameters `theta`
  * at the interior points of `batch`: writes u (N), grad u (N x d), L u (N).
  * Uses prob->n_interior / chunk; boundary fields of prob/batch are ignored. */

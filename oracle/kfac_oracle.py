@@ -26,6 +26,9 @@ oracle function                       reference it follows
 ``precondition``                      src/curvature.py:140-163
 ``line_search``                       src/optim.py:195-211
 ``kfac_step`` / ``optimizer_step``     src/optim.py:237-263, 396-402
+``kfac_star_step``                    src/optim.py:266-320 (exact Gramian-vector
+                                      products from the per-sample residual
+                                      Jacobian rows, src/curvature.py:169-194,253-260)
 ====================================  ======================================
 
 Pinning: ``tests/test_oracle_golden.py`` checks this module against golden
@@ -391,3 +394,85 @@ def kfac_step(st: OracleState, batch, problem, record=None):
         record.update(grad_mats=ev.grad_mats, delta=delta, direction=direction,
                       ls_losses=np.array(ls), r_int=ev.r_int, r_bnd=ev.r_bnd)
     return alpha, st.momentum, ev.loss_interior, ev.loss_boundary
+
+
+# ---------------------------------------------------------------------------
+# KFAC* (optim.py:266-320)
+
+
+def jacobian_rows(ev):
+    """Per-sample residual Jacobian rows, interior and boundary (curvature.py:169-194).
+
+    Row layout: per layer the (q x p) matrix sum_s g_{n,s} zhat_{n,s}^T flattened
+    column-stacked, layers concatenated (the package-wide convention)."""
+    segs_i, segs_b = [], []
+    for l in range(len(ev.gbar)):
+        zh = _augment_rows(ev.lin_in[l])                  # (N, S, p)
+        blk = np.matmul(zh.transpose(0, 2, 1), ev.gbar[l])  # (N, p, q)
+        segs_i.append(blk.reshape(blk.shape[0], -1))
+        zb = np.hstack([ev.bnd_lin_in[l], np.ones((ev.bnd_lin_in[l].shape[0], 1))])
+        bb = zb[:, :, None] * ev.bnd_grads[l][:, None, :]
+        segs_b.append(bb.reshape(bb.shape[0], -1))
+    return np.concatenate(segs_i, axis=1), np.concatenate(segs_b, axis=1)
+
+
+def _vec(mats):
+    return np.concatenate([np.asarray(m).ravel(order="F") for m in mats])
+
+
+def solve_quadratic_model(have_prev, m11, m12, m22, rhs1, rhs2):
+    """Minimise the (alpha, mu) quadratic model (optim.py:266-286)."""
+    tiny = 1e-300
+    det = m11 * m22 - m12 * m12
+    scale = max(abs(m11 * m22), m12 * m12, tiny)
+    if have_prev and det > 1e-12 * scale:
+        return (-rhs1 * m22 + rhs2 * m12) / det, (rhs1 * m12 - rhs2 * m11) / det
+    if m11 <= tiny:
+        return 0.0, 0.0
+    return -rhs1 / m11, 0.0
+
+
+def kfac_star_step(st: OracleState, batch, problem, record=None):
+    """One KFAC* step (optim.py:296-320) + non-finite check (optim.py:398-401)."""
+    cdiag = np.diagonal(np.asarray(problem.coeffs.c, dtype=np.float64)).copy()
+    ev = evaluate_batch(st.weights, st.biases, batch, problem, cdiag)
+    kf = st.kfac
+    beta = kf.ema
+    a_new, b_new = interior_factors(ev.lin_in, ev.gbar)
+    kf.a_int = [beta * o + (1.0 - beta) * n for o, n in zip(kf.a_int, a_new)]
+    kf.b_int = [beta * o + (1.0 - beta) * n for o, n in zip(kf.b_int, b_new)]
+    a_new, b_new = boundary_factors(ev.bnd_lin_in, ev.bnd_grads)
+    kf.a_bnd = [beta * o + (1.0 - beta) * n for o, n in zip(kf.a_bnd, a_new)]
+    kf.b_bnd = [beta * o + (1.0 - beta) * n for o, n in zip(kf.b_bnd, b_new)]
+    delta = precondition(kf, ev.grad_mats)
+    ri, rb = jacobian_rows(ev)
+
+    def gvp(v):
+        out = ri.T @ (ri @ v) / ri.shape[0]
+        return out + rb.T @ (rb @ v) / rb.shape[0]
+
+    dv, pv, gv = _vec(delta), _vec(st.prev_update), _vec(ev.grad_mats)
+    lam = kf.damping
+    g_dv = gvp(dv)
+    m11 = float(dv @ g_dv + lam * dv @ dv)
+    rhs1 = float(dv @ gv)
+    have_prev = bool(pv @ pv > 0.0)
+    if have_prev:
+        g_pv = gvp(pv)
+        m12 = float(dv @ g_pv + lam * dv @ pv)
+        m22 = float(pv @ g_pv + lam * pv @ pv)
+        rhs2 = float(pv @ gv)
+    else:
+        m12 = m22 = rhs2 = 0.0
+    alpha, mu = solve_quadratic_model(have_prev, m11, m12, m22, rhs1, rhs2)
+    update = [alpha * dl + mu * pu for dl, pu in zip(delta, st.prev_update)]
+    st.weights = [w + 1.0 * m[:, :-1] for w, m in zip(st.weights, update)]
+    st.biases = [b + 1.0 * m[:, -1] for b, m in zip(st.biases, update)]
+    st.prev_update = update
+    st.step += 1
+    for w, b in zip(st.weights, st.biases):
+        if not (np.all(np.isfinite(w)) and np.all(np.isfinite(b))):
+            raise FloatingPointError("parameters became non-finite during the step")
+    if record is not None:
+        record.update(grad_mats=ev.grad_mats, delta=delta, m=(m11, m12, m22, rhs1, rhs2))
+    return alpha, mu, ev.loss_interior, ev.loss_boundary

@@ -84,6 +84,17 @@ _SIGS = {
     "kp_kfac_phase_update": (C.c_int32, [C.c_void_p, P(kp_problem), P(kp_kfac_config),
                                          P(kp_state), P(kp_step_out), C.c_void_p, C.c_size_t,
                                          C.c_void_p]),
+    "kp_kfac_star_step": (C.c_int32, [C.c_void_p, P(kp_problem), P(kp_kfac_config), P(kp_state),
+                                      P(kp_batch), P(kp_step_out), C.c_void_p, C.c_size_t,
+                                      C.c_void_p]),
+    "kp_gvp_buffer": (C.c_int32, [C.c_void_p, P(kp_problem), C.c_void_p, P(C.c_void_p),
+                                  P(C.c_int64)]),
+    "kp_kfac_star_phase_gvp": (C.c_int32, [C.c_void_p, P(kp_problem), P(kp_kfac_config),
+                                           P(kp_state), P(kp_batch), P(kp_step_out), C.c_void_p,
+                                           C.c_size_t, C.c_void_p]),
+    "kp_kfac_star_phase_update": (C.c_int32, [C.c_void_p, P(kp_problem), P(kp_kfac_config),
+                                              P(kp_state), P(kp_step_out), C.c_void_p,
+                                              C.c_size_t, C.c_void_p]),
     "kp_taylor_forward": (C.c_int32, [C.c_void_p, P(kp_problem), C.c_void_p, P(kp_batch),
                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
                                       C.c_void_p]),

@@ -197,6 +197,21 @@ void launch_eig_status(const double* la, int p, const double* lb, int q, const i
 void launch_kron_scale(double* W, const double* la, int p, const double* lb, int q,
                        cudaStream_t s);
 void launch_set_status(int32_t* status, int32_t code, cudaStream_t s);
+// KFAC*: batched deterministic dot products, quadratic-model solve and update
+struct DotJobs {
+  const double* a[8];
+  const double* b[8];
+};
+void launch_dots(const DotJobs& jobs, int n, int64_t D, double* out, cudaStream_t s);
+void launch_star_solve_update(const double* dots, double lam, double* theta, double* prev,
+                              const double* delta, int64_t D, double* scalars, int32_t* status,
+                              cudaStream_t s);
+// jv[n] += sum over the sample's S rows of <G_row, Y_row> (both pitch q)
+void launch_rowdot_accum(const double* G, const double* Y, int q, int64_t n, int S, double* jv,
+                         cudaStream_t s);
+// layer-0 Jacobian-vector product (value rows from y0val, derivative rows from V0^T)
+void launch_jvp_layer0(const double* G, const double* y0val, const double* v0t, int64_t n, int d,
+                       int h1, double* jv, cudaStream_t s);
 void launch_gen_eig_1x1(const double* f1, const double* f2, double lam, double* t, double* eig,
                         int* info, cudaStream_t s);
 void launch_identity(double* F, int n, double v, cudaStream_t s);

@@ -246,6 +246,86 @@ void launch_gen_eig_1x1(const double* f1, const double* f2, double lam, double* 
   k_gen_eig_1x1<<<1, 1, 0, s>>>(f1, f2, lam, t, eig, info);
 }
 
+// ---- KFAC* (reference src/optim.py:266-320) --------------------------------------
+
+// out[k] = sum_e a_k[e] b_k[e] (one block per dot, fixed-order tree: deterministic)
+__global__ void k_dots(DotJobs jobs, int64_t D, double* out) {
+  __shared__ double red[512];
+  const double* a = jobs.a[blockIdx.x];
+  const double* b = jobs.b[blockIdx.x];
+  double acc = 0.0;
+  for (int64_t e = threadIdx.x; e < D; e += blockDim.x) acc = fma(a[e], b[e], acc);
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = red[0];
+}
+
+void launch_dots(const DotJobs& jobs, int n, int64_t D, double* out, cudaStream_t s) {
+  count_launch();
+  k_dots<<<n, 512, 0, s>>>(jobs, D, out);
+}
+
+// solve_quadratic_model (optim.py:266-286) on the 8 dots
+//   [0] d.Gd [1] d.d [2] d.g [3] p.p [4] d.Gp [5] d.p [6] p.Gp [7] p.g
+__global__ void k_star_solve(const double* dt, double lam, double* scalars) {
+  const double m11 = dt[0] + lam * dt[1];
+  const double rhs1 = dt[2];
+  const bool have_prev = dt[3] > 0.0;
+  double m12 = 0.0, m22 = 0.0, rhs2 = 0.0;
+  if (have_prev) {
+    m12 = dt[4] + lam * dt[5];
+    m22 = dt[6] + lam * dt[3];
+    rhs2 = dt[7];
+  }
+  const double tiny = 1e-300;
+  const double det = m11 * m22 - m12 * m12;
+  const double scale = fmax(fmax(fabs(m11 * m22), m12 * m12), tiny);
+  double alpha, mu;
+  if (have_prev && det > 1e-12 * scale) {
+    alpha = (-rhs1 * m22 + rhs2 * m12) / det;
+    mu = (rhs1 * m12 - rhs2 * m11) / det;
+  } else if (m11 <= tiny) {
+    alpha = 0.0;
+    mu = 0.0;
+  } else {
+    alpha = -rhs1 / m11;
+    mu = 0.0;
+  }
+  scalars[2] = alpha;
+  scalars[3] = mu;
+}
+
+// update = alpha Delta + mu prev; theta += update; prev = update (optim.py:315-318)
+__global__ void k_star_update(double* __restrict__ th, double* __restrict__ prev,
+                              const double* __restrict__ delta, int64_t D,
+                              const double* __restrict__ scalars, int32_t* status) {
+  if (*status != 0) return;
+  const double alpha = scalars[2], mu = scalars[3];
+  bool bad = false;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < D;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double u = alpha * delta[e] + mu * prev[e];
+    const double v = th[e] + u;
+    th[e] = v;
+    prev[e] = u;
+    bad |= !isfinite(v);
+  }
+  if (bad) set_status(status, KP_ERR_NONFINITE);
+}
+
+void launch_star_solve_update(const double* dots, double lam, double* theta, double* prev,
+                              const double* delta, int64_t D, double* scalars, int32_t* status,
+                              cudaStream_t s) {
+  count_launch();
+  k_star_solve<<<1, 1, 0, s>>>(dots, lam, scalars);
+  count_launch();
+  k_star_update<<<grid1(D), 256, 0, s>>>(theta, prev, delta, D, scalars, status);
+}
+
 __global__ void k_set_status(int32_t* status, int32_t code) { set_status(status, code); }
 
 void launch_set_status(int32_t* status, int32_t code, cudaStream_t s) {

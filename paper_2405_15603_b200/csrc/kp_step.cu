@@ -139,6 +139,9 @@ struct Plan {
   int64_t o_w0t = 0, o_q0 = 0, o_w0tc = 0, o_q0c = 0;
   WPack wp{};   // layout of the padded copy of theta
   WPack wpc{};  // layout of the Bc line-search candidates' padded copies (layer-major)
+  // KFAC*: Gramian-vector products
+  int64_t o_gv = 0, o_gvd = 0, o_gvp = 0, o_jv = 0, o_jvb = 0, o_wpadv = 0, o_v0t = 0, o_vq0 = 0,
+          o_dots = 0;
   int Bc = 1;   // line-search candidates evaluated per batched launch
   int64_t lwork = 0;
   int64_t total = 0;  // doubles
@@ -289,6 +292,15 @@ int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
   P.o_q0 = take(P.h[1]);
   P.o_w0tc = take((int64_t)P.Bc * P.d * P.h[1]);
   P.o_q0c = take((int64_t)P.Bc * P.h[1]);
+  P.o_gv = take(4 * P.D);  // reduce buffer #3: G.Delta (int, bnd), G.prev (int, bnd), raw sums
+  P.o_gvd = take(P.D);
+  P.o_gvp = take(P.D);
+  P.o_jv = take(P.Nc);
+  P.o_jvb = take(P.Nb);
+  P.o_wpadv = take(woff);
+  P.o_v0t = take((int64_t)P.d * P.h[1]);
+  P.o_vq0 = take(P.h[1]);
+  P.o_dots = take(8);
   P.o_ls = take(2 * (int64_t)P.ncand);
   P.o_A1 = take((int64_t)P.maxp * P.maxp);
   P.o_A2 = take((int64_t)P.maxp * P.maxp);
@@ -581,6 +593,36 @@ void backward(const Ctx& c, const double* theta, int64_t n, const TaylorDims& td
   }
 }
 
+// One layer of  acc += sum_n w_n sum_s g_{n,s} zhat_{n,s}^T  — the residual-weighted gradient
+// (optim.py:170-176, w = r) and, with w = J v, the exact Gramian-vector product of KFAC*
+// (curvature.py:253-260).  For layer 0 only the value rows of Z0 = [x; I; 0] are dense; the
+// derivative rows e_i contribute a weighted column sum.
+void contract_grad_layer(const Ctx& c, const double* x, int64_t n, const TaylorDims& td,
+                         const StateBufs& b, const double* gl_last, const double* w,
+                         double* accG, int l) {
+  const Plan& P = c.P;
+  double* part = c.at(P.o_partial);
+  const int64_t rows = n * td.S;
+  const int q = P.q[l], hz = P.h[l], p = P.p[l];
+  const double* G = (l == P.L - 1) ? gl_last : b.gout[l];
+  const double* Z = (l == 0) ? x : b.post[l];
+  const int64_t ldz = (l == 0) ? P.d : P.h[l];
+  const int64_t Rz = (l == 0) ? n : rows;
+  const int Sz = (l == 0) ? 1 : td.S;
+  double* out = accG + P.th[l];
+  const int64_t ldg = (l == 0) ? (int64_t)td.S * q : q;
+  const int Sw = (l == 0) ? 1 : td.S;
+  if (launch_gemm_tn_tma_accumulate(G, ldg, q, Z, ldz, hz, w, Sw, Rz, false, part, out, p, c.s)) {
+    launch_colsum(G, (int64_t)td.S * q, n, q, w, out + hz, p, 0.0, part, c.s);
+  } else {
+    GemmTN gg{G, ldg, q, false, Z, ldz, hz, true, w, Sw, Sz, Rz, false};
+    launch_gemm_tn_accumulate(gg, part, out, c.s);
+  }
+  // derivative rows e_i: out[j][i] += sum_n w_n Gbar0[n, 1+i, j] (contiguous d x q block)
+  if (l == 0 && td.taylor)
+    launch_colsum(G + q, (int64_t)td.S * q, n, P.d * q, w, out, p, 0.0, part, c.s, q);
+}
+
 // Factor and gradient contractions of one pass into the reduce buffer.  The bulk of
 // every contraction runs in the TMA-fed DMMA kernel; the bias-augmentation row /
 // column (the virtual 1 on value rows, curvature.py:88-93) are value-row column
@@ -618,24 +660,7 @@ void accumulate(const Ctx& c, const double* x, int64_t n, const TaylorDims& td,
       GemmTN bb{G, q, q, false, G, q, q, false, nullptr, 1, 1, rows, true};
       launch_gemm_tn_accumulate(bb, part, accB + P.fb[l], c.s);
     }
-    // gradient = sum_n r_n sum_s g_{n,s} zhat_{n,s}^T (optim.py:170-176); for layer 0 only
-    // the value rows of Z0 = [x; I; 0] are dense (the derivative rows: k_grad0_deriv)
-    {
-      double* out = accG + P.th[l];
-      const int64_t ldg = (l == 0) ? (int64_t)td.S * q : q;
-      const int Sw = (l == 0) ? 1 : td.S;
-      if (launch_gemm_tn_tma_accumulate(G, ldg, q, Z, ldz, hz, r, Sw, Rz, false, part, out, p,
-                                        c.s)) {
-        launch_colsum(G, (int64_t)td.S * q, n, q, r, out + hz, p, 0.0, part, c.s);
-      } else {
-        GemmTN gg{G, ldg, q, false, Z, ldz, hz, true, r, Sw, Sz, Rz, false};
-        launch_gemm_tn_accumulate(gg, part, out, c.s);
-      }
-      // layer 0, derivative rows e_i: out[j][i] += sum_n r_n Gbar0[n, 1+i, j] — a weighted sum
-      // over samples of the contiguous d x q block after each value row
-      if (l == 0 && td.taylor)
-        launch_colsum(G + q, (int64_t)td.S * q, n, P.d * q, r, out, p, 0.0, part, c.s, q);
-    }
+    contract_grad_layer(c, x, n, td, b, gl_last, r, accG, l);
   }
 }
 
@@ -890,6 +915,104 @@ int phase_update(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp_step_
   return KP_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// KFAC* (reference src/optim.py:266-320): Gramian-vector products G v for v in {Delta,
+// prev} without the per-sample Jacobian rows.  With J_n the residual Jacobian of point n,
+// (J v)_n = sum_l sum_s <gbar_{n,s,l}, V_l zhat_{n,s,l}> and G v = sum_n (J v)_n J_n^T / N
+// (+ the boundary term), i.e. the gradient contraction with weights (J v)_n.
+
+// jv[n] = (J v)_n for the points of one pass (states in b, seeds/ones in gl_last); V's padded
+// weights and V0^T must be prepared in o_wpadv / o_v0t.
+void jvp_pass(const Ctx& c, const double* x, int64_t n, const TaylorDims& td, const StateBufs& b,
+              const double* gl_last, const double* V, double* jv) {
+  const Plan& P = c.P;
+  const int L = P.L;
+  cudaMemsetAsync(jv, 0, sizeof(double) * n, c.s);
+  const double* wv = c.at(P.o_wpadv);
+  for (int l = 0; l < L; ++l) {
+    const int q = P.q[l];
+    const double* G = (l == L - 1) ? gl_last : b.gout[l];
+    if (l == 0) {
+      // value rows: y = V0[:, :d] x + V0[:, d]   (n x q)
+      double* y0 = c.at(P.o_pong);
+      GemmNT g{x, P.d, V + P.th[0], P.p[0], y0, q, n, q, P.d, V + P.th[0] + P.d, P.p[0], 1};
+      launch_gemm_nt(g, c.s);
+      if (td.taylor) launch_jvp_layer0(G, y0, c.at(P.o_v0t), n, P.d, q, jv, c.s);
+      else launch_rowdot_accum(G, y0, q, n, 1, jv, c.s);
+    } else {
+      double* y = c.at(P.o_ping);
+      GemmNT g{b.post[l], P.h[l], wv + P.wo[l], P.h[l], y, q, n * td.S, q, P.h[l],
+               V + P.th[l] + P.h[l], P.p[l], td.S};
+      launch_gemm_nt(g, c.s);
+      launch_rowdot_accum(G, y, q, n, td.S, jv, c.s);
+    }
+  }
+}
+
+int phase_star_gvp(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, const kp_batch* bt) {
+  const Plan& P = c.P;
+  double* gv = c.at(P.o_gv);
+  KP_CUDA_TRY(cudaMemsetAsync(gv, 0, sizeof(double) * 4 * P.D, c.s));
+  const TaylorDims tdi{P.S, P.d, true};
+  const TaylorDims tdb{1, 0, false};
+  const bool single = P.Nc >= P.N;  // else the interior states are recomputed per chunk
+  const double* vecs[2] = {c.at(P.o_delta), st->prev_update};
+  const StateBufs bi = interior_bufs(c);
+  auto prep = [&](const double* v) {
+    launch_candidate(v, nullptr, 0, nullptr, P.D, P.wp, c.at(P.o_wpadv), c.s);
+    if (P.L >= 2)
+      launch_prep_layer0(v, P.d, P.h[1], bt->coeff_diag, c.at(P.o_v0t), c.at(P.o_vq0), c.s);
+  };
+  for (int64_t n0 = 0; n0 < P.N; n0 += P.Nc) {
+    const int64_t nc = std::min(P.Nc, P.N - n0);
+    const double* x = bt->x_int + n0 * P.d;
+    const double* seeds = bt->seeds + n0 * P.S;
+    if (!single) {
+      launch_candidate(st->theta, nullptr, 0, nullptr, P.D, P.wp, c.at(P.o_wpad), c.s);
+      if (P.L >= 2)
+        launch_prep_layer0(st->theta, P.d, P.h[1], bt->coeff_diag, c.at(P.o_w0t), c.at(P.o_q0),
+                           c.s);
+      ResidualIn ri{bt->r0 + n0, seeds, nullptr};
+      forward_store(c, st->theta, c.at(P.o_wpad), x, nc, tdi, bt->coeff_diag, bi, ri,
+                    c.at(P.o_r) + n0, nullptr);
+      backward(c, st->theta, nc, tdi, bt->coeff_diag, bi, seeds);
+    }
+    for (int v = 0; v < 2; ++v) {
+      prep(vecs[v]);
+      jvp_pass(c, x, nc, tdi, bi, seeds, vecs[v], c.at(P.o_jv));
+      for (int l = 0; l < P.L; ++l)
+        contract_grad_layer(c, x, nc, tdi, bi, seeds, c.at(P.o_jv), gv + (2 * v) * P.D, l);
+    }
+  }
+  const StateBufs bb = boundary_bufs(c);
+  for (int v = 0; v < 2; ++v) {
+    prep(vecs[v]);
+    jvp_pass(c, bt->x_bnd, P.Nb, tdb, bb, c.at(P.o_ones), vecs[v], c.at(P.o_jvb));
+    for (int l = 0; l < P.L; ++l)
+      contract_grad_layer(c, bt->x_bnd, P.Nb, tdb, bb, c.at(P.o_ones), c.at(P.o_jvb),
+                          gv + (2 * v + 1) * P.D, l);
+  }
+  return KP_OK;
+}
+
+int phase_star_update(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp_step_out* out) {
+  const Plan& P = c.P;
+  const double Ng = cfg->n_interior_global, Nbg = cfg->n_boundary_global;
+  double* gv = c.at(P.o_gv);
+  // G v = J_int^T J_int v / N + J_bnd^T J_bnd v / Nb   (curvature.py:253-260)
+  launch_grad_finalize(gv, gv + P.D, Ng, Nbg, c.at(P.o_gvd), P.D, c.s);
+  launch_grad_finalize(gv + 2 * P.D, gv + 3 * P.D, Ng, Nbg, c.at(P.o_gvp), P.D, c.s);
+  const double* d = c.at(P.o_delta);
+  const double* p = st->prev_update;
+  const double* g = c.at(P.o_grad);
+  DotJobs dj{{d, d, d, p, d, d, p, p}, {c.at(P.o_gvd), d, g, p, c.at(P.o_gvp), p, c.at(P.o_gvp), g}};
+  launch_dots(dj, 8, P.D, c.at(P.o_dots), c.s);
+  launch_star_solve_update(c.at(P.o_dots), cfg->damping, st->theta, st->prev_update, d, P.D,
+                           out->scalars, out->status, c.s);
+  return KP_OK;
+}
+
 int validate_cfg(const kp_problem* pr, const kp_kfac_config* cfg) {
   if (!cfg) return KP_ERR_INVALID;
   if (!(cfg->ema >= 0.0 && cfg->ema < 1.0)) return KP_ERR_INVALID;
@@ -1135,6 +1258,49 @@ int32_t kp_kfac_step(kp_context* ctx, const kp_problem* prob, const kp_kfac_conf
   KP_TRY(phase_precondition(c, cfg, st, out));
   KP_TRY(phase_linesearch(c, cfg, st, bt));
   KP_TRY(phase_update(c, cfg, st, out));
+  KP_CUDA_TRY(cudaGetLastError());
+  return KP_OK;
+}
+
+
+int32_t kp_gvp_buffer(kp_context* ctx, const kp_problem* pr, void* ws, double** ptr,
+                      int64_t* count) {
+  Plan P;
+  KP_TRY(cached_plan(ctx, pr, P));
+  *ptr = static_cast<double*>(ws) + P.o_gv;
+  *count = 4 * P.D;
+  return KP_OK;
+}
+
+int32_t kp_kfac_star_phase_gvp(kp_context* ctx, const kp_problem* prob, const kp_kfac_config* cfg,
+                               kp_state* st, const kp_batch* bt, kp_step_out* out, void* ws,
+                               size_t ws_bytes, void* stream) {
+  KP_PHASE_PROLOGUE
+  if (!bt) return KP_ERR_INVALID;
+  KP_TRY(phase_star_gvp(c, cfg, st, bt));
+  KP_CUDA_TRY(cudaGetLastError());
+  return KP_OK;
+}
+
+int32_t kp_kfac_star_phase_update(kp_context* ctx, const kp_problem* prob,
+                                  const kp_kfac_config* cfg, kp_state* st, kp_step_out* out,
+                                  void* ws, size_t ws_bytes, void* stream) {
+  KP_PHASE_PROLOGUE
+  KP_TRY(phase_star_update(c, cfg, st, out));
+  KP_CUDA_TRY(cudaGetLastError());
+  return KP_OK;
+}
+
+int32_t kp_kfac_star_step(kp_context* ctx, const kp_problem* prob, const kp_kfac_config* cfg,
+                          kp_state* st, const kp_batch* bt, kp_step_out* out, void* ws,
+                          size_t ws_bytes, void* stream) {
+  KP_PHASE_PROLOGUE
+  if (!bt) return KP_ERR_INVALID;
+  KP_CUDA_TRY(cudaMemsetAsync(out->status, 0, sizeof(int32_t), c.s));
+  KP_TRY(phase_accumulate(c, cfg, st, bt));
+  KP_TRY(phase_precondition(c, cfg, st, out));
+  KP_TRY(phase_star_gvp(c, cfg, st, bt));
+  KP_TRY(phase_star_update(c, cfg, st, out));
   KP_CUDA_TRY(cudaGetLastError());
   return KP_OK;
 }

@@ -392,6 +392,56 @@ void launch_colsum(const double* X, int64_t rs, int64_t n, int ncols, const doub
 }
 
 // ---------------------------------------------------------------------------
+// Jacobian-vector products for the exact Gramian-vector product of KFAC*
+// (reference src/curvature.py:169-194,253-260 without materialising the rows):
+// jv_n += sum_{s} <gbar_{n,s}, y_{n,s}> with y = V zhat (one warp per sample).
+
+__global__ void k_rowdot_accum(const double* __restrict__ G, const double* __restrict__ Y, int q,
+                               int64_t n, int S, double* __restrict__ jv) {
+  const int lane = threadIdx.x & 31;
+  const int64_t smp = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (smp >= n) return;
+  const int64_t len = (int64_t)S * q;
+  const double* g = G + smp * len;
+  const double* y = Y + smp * len;
+  double acc = 0.0;
+  for (int64_t e = lane; e < len; e += 32) acc = fma(g[e], y[e], acc);
+  acc = warp_sum(acc);
+  if (lane == 0) jv[smp] += acc;
+}
+
+void launch_rowdot_accum(const double* G, const double* Y, int q, int64_t n, int S, double* jv,
+                         cudaStream_t s) {
+  if (n <= 0) return;
+  count_launch();
+  k_rowdot_accum<<<(unsigned)ceil_div(n, 8), 256, 0, s>>>(G, Y, q, n, S, jv);
+}
+
+// Layer 0: zhat rows are [x; 1] (value), [e_i; 0] (derivatives), 0 (operator), so
+// y_value = V0[:, :d] x + V0[:, d] (y0val, from a GEMM) and y_i = V0[:, i].
+__global__ void k_jvp_layer0(const double* __restrict__ G, const double* __restrict__ y0val,
+                             const double* __restrict__ v0t, int64_t n, int d, int h1,
+                             double* __restrict__ jv) {
+  const int lane = threadIdx.x & 31;
+  const int64_t smp = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (smp >= n) return;
+  const int S = d + 2;
+  const double* g = G + smp * S * h1;
+  double acc = 0.0;
+  for (int j = lane; j < h1; j += 32) acc = fma(g[j], y0val[smp * h1 + j], acc);
+  for (int64_t e = lane; e < (int64_t)d * h1; e += 32) acc = fma(g[h1 + e], v0t[e], acc);
+  acc = warp_sum(acc);
+  if (lane == 0) jv[smp] += acc;
+}
+
+void launch_jvp_layer0(const double* G, const double* y0val, const double* v0t, int64_t n, int d,
+                       int h1, double* jv, cudaStream_t s) {
+  if (n <= 0) return;
+  count_launch();
+  k_jvp_layer0<<<(unsigned)ceil_div(n, 8), 256, 0, s>>>(G, y0val, v0t, n, d, h1, jv);
+}
+
+// ---------------------------------------------------------------------------
 // small utilities
 
 __global__ void k_sumsq(const double* __restrict__ v, int64_t n, int64_t stride,

@@ -58,6 +58,23 @@ class ShardedKfacStep:
         return float(sc[2]), float(sc[3]), float(sc[0]), float(sc[1])
 
 
+class ShardedKfacStarStep(ShardedKfacStep):
+    """KFAC* over P ranks: the factor/gradient all-reduce, then one all-reduce of the
+    partial Gramian-vector products (kp_gvp_buffer) before the 2 x 2 model solve."""
+
+    def step(self):
+        e = self.engine
+        e.phase("accumulate")
+        self.all_reduce(e.reduce_buffer())
+        e.phase("precondition")
+        e.phase("star_gvp")
+        self.all_reduce(e.gvp_buffer())
+        e.phase("star_update")
+        sc, code = e.finish_step()
+        raise_for_status(code, "sharded kfac_star step")
+        return float(sc[2]), float(sc[3]), float(sc[0]), float(sc[1])
+
+
 def make_rank_engine(widths, batch, problem, rank: int, world: int, *, ema, damping, momentum,
                      ls_min_exp=-30, ls_max_exp=0, chunk=None):
     """Engine for this rank's shard of ``batch`` with global normalisers."""

@@ -243,6 +243,16 @@ class KfacEngine:
         raise_for_status(code, "kfac step")
         return float(sc[2]), float(sc[3]), float(sc[0]), float(sc[1])
 
+    def launch_star_step(self):
+        """Enqueue one KFAC* step (src/optim.py:266-320) on the current stream."""
+        raise_for_status(self.lib.kp_kfac_star_step(*self._args()), "kp_kfac_star_step")
+
+    def star_step(self):
+        self.launch_star_step()
+        sc, code = self.finish_step()
+        raise_for_status(code, "kfac_star step")
+        return float(sc[2]), float(sc[3]), float(sc[0]), float(sc[1])
+
     # phased step for sharded multi-GPU runs (SURVEY.md §8e)
     def reduce_buffer(self):
         ptr, cnt = C.c_void_p(), C.c_int64()
@@ -254,6 +264,12 @@ class KfacEngine:
         ptr, cnt = C.c_void_p(), C.c_int64()
         raise_for_status(self.lib.kp_linesearch_buffer(self.ctx, C.byref(self.prob),
                                                        C.c_void_p(_ptr(self.ws)), C.byref(ptr), C.byref(cnt)))
+        return self._view(ptr.value, cnt.value)
+
+    def gvp_buffer(self):
+        ptr, cnt = C.c_void_p(), C.c_int64()
+        raise_for_status(self.lib.kp_gvp_buffer(self.ctx, C.byref(self.prob), C.c_void_p(_ptr(self.ws)),
+                                                C.byref(ptr), C.byref(cnt)))
         return self._view(ptr.value, cnt.value)
 
     def _view(self, ptr: int, count: int):
@@ -272,6 +288,10 @@ class KfacEngine:
             rc = self.lib.kp_kfac_phase_precondition(*a[:4], *a[5:])
         elif name == "update":
             rc = self.lib.kp_kfac_phase_update(*a[:4], *a[5:])
+        elif name == "star_gvp":
+            rc = self.lib.kp_kfac_star_phase_gvp(*a)
+        elif name == "star_update":
+            rc = self.lib.kp_kfac_star_phase_update(*a[:4], *a[5:])
         else:
             raise ValueError(name)
         raise_for_status(rc, f"phase {name}")

@@ -12,6 +12,8 @@ reference (/root/reference/pkg/src/pinnopt/optim.py):
 * ``init_train_state`` ↔ optim.py:102-117;
 * ``optimizer_step``   ↔ optim.py:396-402 — one KFAC step (optim.py:251-263) as
   one C-ABI call (``kp_kfac_step``) on the GPU; it mutates ``state`` in place.
+  ``kind="kfac_star"`` (optim.py:266-320) runs ``kp_kfac_star_step``: the same
+  factors and direction plus exact Gramian-vector products and the 2 x 2 model.
 
 The reference's objects (its ``Parameters``, ``Batch``, ``PdeProblem``) are
 accepted as they are (duck typing), so the reference harness's
@@ -209,7 +211,10 @@ def _kfac_device_step(state: TrainState, batch, problem) -> StepInfo:
             raise ValueError("damping must be positive for Kronecker preconditioning")
     eng.set_batch(x, r0, seeds, np.asarray(batch.boundary, dtype=np.float64),
                   np.asarray(batch.boundary_targets, dtype=np.float64), cdiag)
-    eng.launch_step()
+    if state.config.kind == "kfac_star":
+        eng.launch_star_step()
+    else:
+        eng.launch_step()
     sc, code = eng.finish_step()
     # mirror the device state back to the reference-visible fields
     mats = eng.param_mats()
@@ -231,8 +236,8 @@ def _kfac_device_step(state: TrainState, batch, problem) -> StepInfo:
 
 
 def optimizer_step(state: TrainState, batch, problem) -> StepInfo:
-    """One optimisation step (optim.py:396-402); kind="kfac" runs on the B200."""
-    if state.config.kind != "kfac":
+    """One optimisation step (optim.py:396-402); kinds "kfac" and "kfac_star" run on the B200."""
+    if state.config.kind not in ("kfac", "kfac_star"):
         raise NotImplementedError(
             f"optimizer kind {state.config.kind!r} is outside the accelerated KFAC path")
     return _kfac_device_step(state, batch, problem)

@@ -49,6 +49,10 @@ PLAN = {
     "c4": ("c4", 150, 50, 2),
     "c5": ("c5", 24, 8, 2),
     "c1_momentum": ("c1", 200, 60, 3),
+    # KFAC* (src/optim.py:266-320): same inputs, exact Gramian-vector products + 2x2 model
+    "c1_star": ("c1", 300, 80, 3),
+    "c3_star": ("c3", 200, 100, 3),
+    "c5_star": ("c5", 24, 8, 2),
 }
 
 
@@ -86,14 +90,18 @@ def put(out, key, arr):
 
 
 def main():
+    only = set(sys.argv[1:])
     for name, (wkey, n_int, n_bnd, steps) in PLAN.items():
+        if only and name not in only:
+            continue
         wl = cfgs.WORKLOADS[wkey]
         prob = ref_problem(wl)
         arch = network.Architecture(wl.widths)
         params = network.init_params(arch, _stream_seed(0, 0))
         batch = pde.sample_batch(prob, n_int, n_bnd, _stream_seed(0, 1, 0))
         momentum = 0.9 if name.endswith("momentum") else wl.momentum
-        cfg = optim.OptimizerConfig(kind="kfac", damping=wl.damping, ema=wl.ema,
+        kind = "kfac_star" if name.endswith("_star") else "kfac"
+        cfg = optim.OptimizerConfig(kind=kind, damping=wl.damping, ema=wl.ema,
                                     momentum=momentum, init_mode="identity")
         state = optim.init_train_state(params, cfg)
         out = {"widths": np.array(wl.widths), "n_interior": np.array(n_int),
@@ -114,15 +122,17 @@ def main():
             curvature.boundary_factor_update(kf, ev.boundary_trace.linear_inputs, ev.boundary_grads)
             delta = curvature.precondition_gradient(kf, ev.grad_mats)
             direction = [d + momentum * p for d, p in zip(delta, state.prev_update)]
-            grid = cfg.line_search_grid()
-            ls = np.array([optim.evaluate_losses(network.add_scaled(state.params, direction, a),
-                                                 batch, prob) for a in grid])
-            info = optim.optimizer_step(state, batch, prob)
             pre = f"s{t}/"
+            if kind == "kfac":
+                grid = cfg.line_search_grid()
+                ls = np.array([optim.evaluate_losses(network.add_scaled(state.params, direction, a),
+                                                     batch, prob) for a in grid])
+                out[pre + "ls_losses"] = ls
+            info = optim.optimizer_step(state, batch, prob)
             out[pre + "loss_interior"] = np.array(info.loss_interior)
             out[pre + "loss_boundary"] = np.array(info.loss_boundary)
             out[pre + "alpha"] = np.array(info.alpha)
-            out[pre + "ls_losses"] = ls
+            out[pre + "mu"] = np.array(info.mu)
             put(out, pre + "grad", network.mats_to_vec(ev.grad_mats))
             put(out, pre + "delta", network.mats_to_vec(delta))
             put(out, pre + "theta", network.params_to_vec(state.params))
@@ -130,7 +140,8 @@ def main():
             for fname in ("a_interior", "b_interior", "a_boundary", "b_boundary"):
                 mats = getattr(state.kfac, fname)
                 put(out, pre + fname, np.concatenate([m.ravel() for m in mats]))
-            print(f"{name} step {t}: loss={info.loss_total:.6e} alpha={info.alpha:g}", flush=True)
+            print(f"{name} step {t}: loss={info.loss_total:.6e} alpha={info.alpha:.10g} "
+                  f"mu={info.mu:.10g}", flush=True)
         out["numpy_version"] = np.array(np.__version__)
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
 

@@ -8,7 +8,7 @@ per array.
 import numpy as np
 import pytest
 
-from golden_util import NAMES, compare, load, pack_factors
+from golden_util import NAMES, STAR_NAMES, compare, load, pack_factors
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -19,7 +19,8 @@ from paper_2405_15603_b200.network import Architecture, Parameters, init_params,
 from paper_2405_15603_b200.optim import OptimizerConfig, init_train_state, optimizer_step  # noqa: E402
 from paper_2405_15603_b200.pde import make_problem, sample_batch  # noqa: E402
 
-WL_OF = {"c1": "c1", "c2": "c2", "c3": "c3", "c4": "c4", "c5": "c5", "c1_momentum": "c1"}
+WL_OF = {"c1": "c1", "c2": "c2", "c3": "c3", "c4": "c4", "c5": "c5", "c1_momentum": "c1",
+         "c1_star": "c1", "c3_star": "c3", "c5_star": "c5"}
 
 
 def _theta_colstack(params):
@@ -216,3 +217,54 @@ def test_nonaffine_residual_rejected():
     state = init_train_state(params, OptimizerConfig(kind="kfac", damping=1e-3))
     with pytest.raises(NotImplementedError):
         optimizer_step(state, batch, prob)
+
+
+@pytest.mark.parametrize("name", STAR_NAMES)
+def test_kfac_star_steps_match_reference_golden(name):
+    """KFAC* on the device (kp_kfac_star_step): exact Gramian-vector products via JVP +
+    weighted reverse contraction vs the reference's Jacobian-row route."""
+    g = load(name)
+    wl = cfgs.WORKLOADS[WL_OF[name]]
+    prob, params, batch = wl.build(0, int(g["n_interior"]), int(g["n_boundary"]))
+    cfg = OptimizerConfig(kind="kfac_star", damping=float(g["damping"]), ema=float(g["ema"]),
+                          momentum=float(g["momentum"]))
+    state = init_train_state(params, cfg)
+    t = 1
+    while f"s{t}/alpha" in g:
+        info = optimizer_step(state, batch, prob)
+        p = f"s{t}/"
+        tol = 1e-10 if t == 1 else 1e-8
+        a_ref, m_ref = float(g[p + "alpha"]), float(g[p + "mu"])
+        assert abs(info.alpha - a_ref) <= tol * abs(a_ref), (info.alpha, a_ref)
+        assert abs(info.mu - m_ref) <= tol * max(abs(m_ref), 1.0), (info.mu, m_ref)
+        for key, val in (("loss_interior", info.loss_interior), ("loss_boundary", info.loss_boundary)):
+            ref = float(g[p + key])
+            assert abs(val - ref) <= tol * abs(ref), (key, val, ref)
+        eng = state._engine
+        widths = eng.widths
+        assert compare(g, p + "delta", _device_mats_to_vec(eng.delta.cpu().numpy(), widths), tol) <= tol
+        assert compare(g, p + "theta", _theta_colstack(state.params), tol) <= tol
+        assert compare(g, p + "prev_update", mats_to_vec(state.prev_update), tol) <= tol
+        t += 1
+
+
+def test_kfac_star_chunked_matches_single_chunk():
+    """Multi-chunk KFAC* recomputes the interior states for the Gramian products."""
+    from paper_2405_15603_b200.engine import KfacEngine
+    from paper_2405_15603_b200.pde import affine_residual_terms
+    wl = cfgs.WORKLOADS["c2"]
+    prob, params, batch = wl.build(0, 240, 60)
+    r0, seeds = affine_residual_terms(prob, batch.interior)
+    out = []
+    for chunk in (None, 70):
+        eng = KfacEngine(wl.widths, 240, 60, ema=0.95, damping=1e-3, momentum=0.0, chunk=chunk)
+        eng.set_batch(batch.interior, r0, seeds, batch.boundary, batch.boundary_targets,
+                      np.diagonal(prob.coeffs.c))
+        eng.load_params(params)
+        eng.init_factors(True)
+        res = [eng.star_step() for _ in range(2)]
+        out.append((res, eng.theta_numpy()))
+    (r1, t1), (r2, t2) = out
+    for a, b in zip(r1, r2):
+        assert abs(a[0] - b[0]) <= 1e-10 * abs(b[0]) and abs(a[1] - b[1]) <= 1e-10 * max(abs(b[1]), 1)
+    assert np.max(np.abs(t1 - t2)) <= 1e-10 * np.max(np.abs(t2))

@@ -9,12 +9,13 @@ reference's seeded parameters and batches bit-for-bit.
 import numpy as np
 import pytest
 
-from golden_util import NAMES, compare, load, pack_factors
+from golden_util import NAMES, STAR_NAMES, compare, load, pack_factors
 from oracle import kfac_oracle as orc
 from paper_2405_15603_b200 import configs as cfgs
 from paper_2405_15603_b200.network import params_to_vec
 
-WL_OF = {"c1": "c1", "c2": "c2", "c3": "c3", "c4": "c4", "c5": "c5", "c1_momentum": "c1"}
+WL_OF = {"c1": "c1", "c2": "c2", "c3": "c3", "c4": "c4", "c5": "c5", "c1_momentum": "c1",
+         "c1_star": "c1", "c3_star": "c3", "c5_star": "c5"}
 
 
 def build(name):
@@ -24,7 +25,7 @@ def build(name):
     return g, wl, prob, params, batch
 
 
-@pytest.mark.parametrize("name", NAMES)
+@pytest.mark.parametrize("name", NAMES + STAR_NAMES)
 def test_inputs_bit_identical_to_reference(name):
     g, wl, prob, params, batch = build(name)
     assert compare(g, "in/interior", batch.interior, 0) == 0.0
@@ -60,5 +61,35 @@ def test_oracle_matches_reference_steps(name):
         for key, mats in (("a_interior", kf.a_int), ("b_interior", kf.b_int),
                           ("a_boundary", kf.a_bnd), ("b_boundary", kf.b_bnd)):
             assert compare(g, p + key, pack_factors(mats), tol) <= tol, key
+        t += 1
+    assert t > 1
+
+
+def rel(a, b):
+    return abs(a - b) / max(abs(b), 1e-300)
+
+
+@pytest.mark.parametrize("name", STAR_NAMES)
+def test_oracle_matches_reference_kfac_star(name):
+    """KFAC* (src/optim.py:266-320): alpha/mu from the exact-Gramian quadratic model."""
+    from paper_2405_15603_b200.network import mats_to_vec
+    g, wl, prob, params, batch = build(name)
+    st = orc.init_state(params.weights, params.biases, ema=float(g["ema"]),
+                        damping=float(g["damping"]), momentum=float(g["momentum"]))
+    t = 1
+    while f"s{t}/alpha" in g:
+        rec = {}
+        alpha, mu, li, lb = orc.kfac_star_step(st, batch, prob, record=rec)
+        p = f"s{t}/"
+        tol = 1e-10 if t == 1 else 1e-8
+        assert rel(alpha, float(g[p + "alpha"])) <= tol
+        assert abs(mu - float(g[p + "mu"])) <= tol * max(abs(float(g[p + "mu"])), 1.0)
+        assert rel(li, float(g[p + "loss_interior"])) <= tol
+        assert rel(lb, float(g[p + "loss_boundary"])) <= tol
+        assert compare(g, p + "delta", mats_to_vec(rec["delta"]), tol) <= tol
+        theta = np.concatenate([np.hstack([w, b[:, None]]).ravel(order="F")
+                                for w, b in zip(st.weights, st.biases)])
+        assert compare(g, p + "theta", theta, tol) <= tol
+        assert compare(g, p + "prev_update", mats_to_vec(st.prev_update), tol) <= tol
         t += 1
     assert t > 1

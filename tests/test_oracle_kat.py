@@ -166,3 +166,34 @@ def test_momentum_recurrence():
     for l in range(2):
         expect = alpha * (rec["delta"][l] + first[l])
         assert np.max(np.abs((st.weights[l] - before[l]) - expect[:, :-1])) <= 1e-12
+
+
+def test_kfac_star_quadratic_model_rules():
+    # pkg/tests/test_optim.py:184-207: identity-Gramian Rayleigh solution; parallel
+    # directions fall back to the alpha-only solve
+    rng = np.random.default_rng(5)
+    dv, gv = rng.standard_normal(4), rng.standard_normal(4)
+    a, m = orc.solve_quadratic_model(False, float(dv @ dv), 0.0, 0.0, float(dv @ gv), 0.0)
+    assert abs(a + float(dv @ gv) / float(dv @ dv)) <= 1e-14 and m == 0.0
+    d = np.array([1.0, 2.0])
+    m11 = float(d @ d)
+    k = 2.5
+    a, m = orc.solve_quadratic_model(True, m11, k * m11, k * k * m11, 3.0, 3.0 * k)
+    assert m == 0.0 and abs(a + 3.0 / m11) <= 1e-14
+
+
+def test_kfac_star_first_step_is_alpha_only_and_stationary():
+    # pkg/tests/test_optim.py:159-183, 209-237: mu = 0 without a previous update, and the
+    # solved (alpha, mu) zero the gradient of the quadratic model on the next step
+    prob = make_problem("poisson2d_sin")
+    p = init_params(Architecture((2, 6, 1)), 3)
+    batch = sample_batch(prob, 12, 6, 6)
+    st = orc.init_state(p.weights, p.biases, ema=0.5, damping=1e-3)
+    _, mu, _, _ = orc.kfac_star_step(st, batch, prob)
+    assert mu == 0.0
+    rec = {}
+    alpha, mu, _, _ = orc.kfac_star_step(st, batch, prob, record=rec)
+    m11, m12, m22, rhs1, rhs2 = rec["m"]
+    res = np.array([m11 * alpha + m12 * mu + rhs1, m12 * alpha + m22 * mu + rhs2])
+    gnorm = np.linalg.norm(np.concatenate([g.ravel() for g in rec["grad_mats"]]))
+    assert np.linalg.norm(res) <= 1e-8 * gnorm
