@@ -35,6 +35,8 @@ class CpuShardEngine:
         n_red = sum(2 * a + 2 * b + 2 * g for a, b, g in self.sizes) + 2
         self.red = torch.zeros(n_red, dtype=torch.float64)
         self.ls = torch.zeros(2 * len(self.grid), dtype=torch.float64)
+        D = sum(g for _, _, g in self.sizes)
+        self.gvb = torch.zeros(4 * D, dtype=torch.float64)
         self.L = L
         self.scalars = np.zeros(4)
 
@@ -43,6 +45,9 @@ class CpuShardEngine:
 
     def linesearch_buffer(self):
         return self.ls
+
+    def gvp_buffer(self):
+        return self.gvb
 
     def _pack(self, parts):
         flat = np.concatenate([np.asarray(p).ravel() for p in parts])
@@ -101,6 +106,8 @@ class CpuShardEngine:
         self.scalars[0] = ssi / (2 * self.ng)
         self.scalars[1] = ssb / (2 * self.nbg)
         delta = orc.precondition(kf, grads)
+        self.delta = delta
+        self.grads = grads
         self.dir = [d + self.mu * p for d, p in zip(delta, self.prev)]
 
     def _linesearch(self):
@@ -127,6 +134,43 @@ class CpuShardEngine:
         self.w = [w + best_a * m[:, :-1] for w, m in zip(self.w, self.dir)]
         self.b = [b + best_a * m[:, -1] for b, m in zip(self.b, self.dir)]
         self.prev = [best_a * m for m in self.dir]
+
+    # KFAC*: local (unnormalised) Gramian-vector products from this shard's Jacobian rows
+    def _star_gvp(self):
+        cd = self.cd
+        x = self.x
+
+        class B:  # minimal batch view for the oracle
+            pass
+
+        b = B()
+        b.interior, b.boundary, b.boundary_targets = self.x, self.xb, self.tg
+        ev = orc.evaluate_batch(self.w, self.b, b, self.prob, cd)
+        ri, rb = orc.jacobian_rows(ev)
+        dv, pv = orc._vec(self.delta), orc._vec(self.prev)
+        parts = [ri.T @ (ri @ dv), rb.T @ (rb @ dv), ri.T @ (ri @ pv), rb.T @ (rb @ pv)]
+        self.gvb.copy_(torch.from_numpy(np.concatenate(parts)))
+        del x
+
+    def _star_update(self):
+        D = self.gvb.numel() // 4
+        v = self.gvb.numpy()
+        g_dv = v[:D] / self.ng + v[D:2 * D] / self.nbg
+        g_pv = v[2 * D:3 * D] / self.ng + v[3 * D:] / self.nbg
+        dv, pv, gv = orc._vec(self.delta), orc._vec(self.prev), orc._vec(self.grads)
+        lam = self.lam
+        m11, rhs1 = float(dv @ g_dv + lam * dv @ dv), float(dv @ gv)
+        have_prev = bool(pv @ pv > 0.0)
+        if have_prev:
+            m12, m22, rhs2 = float(dv @ g_pv + lam * dv @ pv), float(pv @ g_pv + lam * pv @ pv), float(pv @ gv)
+        else:
+            m12 = m22 = rhs2 = 0.0
+        alpha, mu = orc.solve_quadratic_model(have_prev, m11, m12, m22, rhs1, rhs2)
+        upd = [alpha * d + mu * p for d, p in zip(self.delta, self.prev)]
+        self.w = [w + u[:, :-1] for w, u in zip(self.w, upd)]
+        self.b = [b + u[:, -1] for b, u in zip(self.b, upd)]
+        self.prev = upd
+        self.scalars[2], self.scalars[3] = alpha, mu
 
     def finish_step(self):
         return self.scalars.copy(), 0

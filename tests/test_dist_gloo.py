@@ -24,7 +24,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, star=False):
     import sys
 
     here = os.path.dirname(os.path.abspath(__file__))
@@ -36,7 +36,8 @@ def _worker(rank, world, port, q):
     try:
         from cpu_shard_engine import CpuShardEngine
         from paper_2405_15603_b200 import configs
-        from paper_2405_15603_b200.dist import ShardedKfacStep, shard_bounds, torch_all_reduce
+        from paper_2405_15603_b200.dist import (ShardedKfacStarStep, ShardedKfacStep, shard_bounds,
+                                                torch_all_reduce)
 
         wl = configs.WORKLOADS["c3"]
         prob, params, batch = wl.build(0, 90, 31)
@@ -45,14 +46,15 @@ def _worker(rank, world, port, q):
         eng = CpuShardEngine(params.weights, params.biases, batch.interior[i0:i1],
                              batch.boundary[b0:b1], batch.boundary_targets[b0:b1], prob, 90, 31,
                              ema=wl.ema, damping=wl.damping, momentum=0.3)
-        stepper = ShardedKfacStep(eng, torch_all_reduce())
+        stepper = (ShardedKfacStarStep if star else ShardedKfacStep)(eng, torch_all_reduce())
         infos = [stepper.step() for _ in range(3)]
         q.put((rank, infos, [w.copy() for w in eng.w]))
     finally:
         dist.destroy_process_group()
 
 
-def test_sharded_step_matches_single_process_oracle():
+@pytest.mark.parametrize("star", [False, True], ids=["kfac", "kfac_star"])
+def test_sharded_step_matches_single_process_oracle(star):
     from oracle import kfac_oracle as orc
     from paper_2405_15603_b200 import configs
 
@@ -60,7 +62,7 @@ def test_sharded_step_matches_single_process_oracle():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, star)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
@@ -72,10 +74,14 @@ def test_sharded_step_matches_single_process_oracle():
     wl = configs.WORKLOADS["c3"]
     prob, params, batch = wl.build(0, 90, 31)
     st = orc.init_state(params.weights, params.biases, ema=wl.ema, damping=wl.damping, momentum=0.3)
-    ref = [orc.kfac_step(st, batch, prob) for _ in range(3)]
+    step = orc.kfac_star_step if star else orc.kfac_step
+    ref = [step(st, batch, prob) for _ in range(3)]
     for rank, infos, ws in res:
-        for t, ((a, mu, li, lb), (ar, _, lir, lbr)) in enumerate(zip(infos, ref)):
-            assert a == ar
+        for t, ((a, mu, li, lb), (ar, mur, lir, lbr)) in enumerate(zip(infos, ref)):
+            if star:
+                assert abs(a - ar) <= 1e-9 * abs(ar) and abs(mu - mur) <= 1e-9 * max(abs(mur), 1.0)
+            else:
+                assert a == ar
             tol = 1e-10 if t == 0 else 1e-8
             assert abs(li - lir) <= tol * abs(lir) and abs(lb - lbr) <= tol * abs(lbr)
         for w, wr in zip(ws, st.weights):
