@@ -38,7 +38,7 @@ extern "C" {
 #endif
 
 #define KP_MAX_LAYERS 16
-#define KP_ABI_VERSION 1
+#define KP_ABI_VERSION 2
 
 typedef enum kp_status {
   KP_OK = 0,
@@ -94,7 +94,11 @@ typedef struct kp_state {
   double* b_bnd;
 } kp_state;
 
-/* One collocation batch (src/pde.py:54-60) plus the affine residual terms. */
+/* One collocation batch (src/pde.py:54-60) plus the residual terms.  The interior
+ * residual is r = r0 + seeds . [u, grad u, Lu] + sum_i quad_i (d u/d x_i)^2 per point
+ * (quad = NULL: affine).  Its reverse-pass seeds [dr/du, dr/dgrad, dr/dLu]
+ * (src/optim.py:157-158) are seeds + [0, 2 quad_i grad_i u, 0] at the current outputs —
+ * this covers every catalog residual including log-Fokker-Planck (src/pde.py:253-263). */
 typedef struct kp_batch {
   const double* x_int;
   const double* r0;
@@ -102,6 +106,7 @@ typedef struct kp_batch {
   const double* x_bnd;
   const double* targets;
   const double* coeff_diag;  /* d: diagonal operator coefficients (src/taylor.py:43-87) */
+  const double* quad;        /* N x d quadratic gradient coefficients, or NULL */
 } kp_batch;
 
 /* Step outputs (device).  scalars[4] = {loss_interior, loss_boundary, alpha, mu}

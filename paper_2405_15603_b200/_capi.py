@@ -13,7 +13,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libkfac_pinn_b200.so")
 MAX_LAYERS = 16
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 KP_OK = 0
 KP_ERR_INVALID = 1
@@ -45,7 +45,8 @@ class kp_state(C.Structure):
 
 
 class kp_batch(C.Structure):
-    _fields_ = [(n, C.c_void_p) for n in ("x_int", "r0", "seeds", "x_bnd", "targets", "coeff_diag")]
+    _fields_ = [(n, C.c_void_p) for n in ("x_int", "r0", "seeds", "x_bnd", "targets", "coeff_diag",
+                                          "quad")]
 
 
 class kp_step_out(C.Structure):

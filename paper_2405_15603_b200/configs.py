@@ -66,6 +66,11 @@ WORKLOADS = {
                    (100, 768, 768, 512, 512, 1), 3000, 1000),
 }
 
+# Not a BASELINE config: the reference catalog's log-Fokker-Planck problem (pde.py:234-276),
+# whose residual is quadratic in grad u — exercises the non-affine seed path.
+WORKLOADS["lfp"] = Workload("lfp_logfokkerplanck9p1d", "log_fokker_planck", (),
+                            (10, 48, 48, 32, 1), 500, 200)
+
 C5_SWEEP = (3000, 16384, 65536)
 
 

@@ -283,25 +283,31 @@ bool launch_gemm_act(GemmAct g, int mode, cudaStream_t s) {
 }
 
 // u_{n,s} = sum_t upart[(n*S+s)*ntn + t] + (s == 0) b;  residual as in k_last_layer.
+constexpr int KP_LAST_MAX_S = 130;  // S <= 128 on the fused path
 __global__ void k_last_from_partials(const double* __restrict__ upart, int ntn, int64_t n,
                                      TaylorDims td, const double* __restrict__ bias,
                                      const double* __restrict__ r0, const double* __restrict__ seeds,
                                      const double* __restrict__ targets, double* __restrict__ r,
-                                     int64_t bias_bstride, int64_t r_bstride) {
+                                     int64_t bias_bstride, int64_t r_bstride,
+                                     const double* __restrict__ quad) {
   upart += (int64_t)blockIdx.y * n * td.S * ntn;
   bias += (int64_t)blockIdx.y * bias_bstride;
   r += (int64_t)blockIdx.y * r_bstride;
   for (int64_t smp = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; smp < n;
        smp += (int64_t)gridDim.x * blockDim.x) {
-    double v = td.taylor ? r0[smp] : 0.0;
+    double uu[KP_LAST_MAX_S];
+    double v = 0.0;
     for (int s = 0; s < td.S; ++s) {
       const double* up = upart + (smp * td.S + s) * ntn;
       double u = 0.0;
       for (int t = 0; t < ntn; ++t) u += up[t];
       if (s == 0) u += bias[0];
-      if (td.taylor) v += seeds[smp * td.S + s] * u;
+      if (td.taylor) uu[s] = u;
       else v = u - targets[smp];
     }
+    if (td.taylor)
+      v = point_residual(uu, td.S, r0[smp], seeds + smp * td.S, quad ? quad + smp * td.d : nullptr,
+                         nullptr);
     r[smp] = v;
   }
 }
@@ -309,12 +315,12 @@ __global__ void k_last_from_partials(const double* __restrict__ upart, int ntn, 
 void launch_last_from_partials(const double* upart, int ntn, int64_t n, TaylorDims td,
                                const double* bias, const double* r0, const double* seeds,
                                const double* targets, double* r, cudaStream_t s, int batch,
-                               int64_t bias_bstride, int64_t r_bstride) {
+                               int64_t bias_bstride, int64_t r_bstride, const double* quad) {
   if (n <= 0) return;
   count_launch();
   const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(n, 128), 148 * 16);
   k_last_from_partials<<<dim3(blocks, (unsigned)batch), 128, 0, s>>>(
-      upart, ntn, n, td, bias, r0, seeds, targets, r, bias_bstride, r_bstride);
+      upart, ntn, n, td, bias, r0, seeds, targets, r, bias_bstride, r_bstride, quad);
 }
 
 }  // namespace kp

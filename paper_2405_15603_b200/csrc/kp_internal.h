@@ -6,6 +6,23 @@
 
 namespace kp {
 
+// Interior residual of one point from its output triple u[0..S) (S = d + 2):
+// r = r0 + seeds . u + sum_i quad_i u_{1+i}^2; optional effective seeds (reverse pass).
+__host__ __device__ inline double point_residual(const double* u, int S, double r0,
+                                                  const double* seeds, const double* quad,
+                                                  double* seeds_out) {
+  double v = r0;
+  for (int s = 0; s < S; ++s) v += seeds[s] * u[s];
+  if (quad) {
+    for (int i = 0; i < S - 2; ++i) v += quad[i] * u[1 + i] * u[1 + i];
+  }
+  if (seeds_out) {
+    for (int s = 0; s < S; ++s)
+      seeds_out[s] = seeds[s] + ((quad && s >= 1 && s <= S - 2) ? 2.0 * quad[s - 1] * u[s] : 0.0);
+  }
+  return v;
+}
+
 // Host-side count of this library's kernel launches (reported as gpu_launches).
 void count_launch();
 int64_t launch_count();
@@ -130,9 +147,12 @@ void launch_act_fwd(const double* pre, double* post, int64_t n, int h, TaylorDim
                     const double* cdiag, cudaStream_t s);
 // Scalar output + residual: u_{n,s} = post[n*S+s,:] . w + (s==0) b;
 // taylor: r_n = r0_n + sum_s seeds[n,s] u_{n,s};  plain: r_n = u_n - target_n.
+// quad (n x d, optional): residual += sum_i quad_i u_i^2; seeds_out (n x S, optional): the
+// reverse-pass seeds at these outputs, seeds + [0, 2 quad_i u_i, 0].
 void launch_last_layer(const double* post, int64_t n, int h, const double* theta_last,
                        TaylorDims td, const double* r0, const double* seeds,
-                       const double* targets, double* r, double* u_out, cudaStream_t s);
+                       const double* targets, double* r, double* u_out, cudaStream_t s,
+                       const double* quad = nullptr, double* seeds_out = nullptr);
 // Adjoint of the Taylor activation (taylor.py:206-239).  Pre-activation either a
 // stored state `pre` or (layer 0) zval + W0.  gin either a stored adjoint or the
 // rank-1 seeds (x) w_last (first reverse step, taylor.py:262,271).
@@ -151,7 +171,8 @@ void launch_act_bwd(const ActBwd& a, int64_t n, int h, TaylorDims td, const doub
 void launch_last_from_partials(const double* upart, int ntn, int64_t n, TaylorDims td,
                                const double* bias, const double* r0, const double* seeds,
                                const double* targets, double* r, cudaStream_t s, int batch = 1,
-                               int64_t bias_bstride = 0, int64_t r_bstride = 0);
+                               int64_t bias_bstride = 0, int64_t r_bstride = 0,
+                               const double* quad = nullptr);
 // Layer-0 gradient, derivative-row part: acc[j*(d+1)+i] += sum_n r_n gbar0[n, 1+i, j].
 void launch_grad0_deriv(const double* gbar0, const double* r, int64_t n, int d, int h1,
                         double* acc, cudaStream_t s);

@@ -142,6 +142,7 @@ struct Plan {
   // KFAC*: Gramian-vector products
   int64_t o_gv = 0, o_gvd = 0, o_gvp = 0, o_jv = 0, o_jvb = 0, o_wpadv = 0, o_v0t = 0, o_vq0 = 0,
           o_dots = 0;
+  int64_t o_seeds_eff = 0;  // per-point reverse-pass seeds of a non-affine residual
   int Bc = 1;   // line-search candidates evaluated per batched launch
   int64_t lwork = 0;
   int64_t total = 0;  // doubles
@@ -301,6 +302,7 @@ int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
   P.o_v0t = take((int64_t)P.d * P.h[1]);
   P.o_vq0 = take(P.h[1]);
   P.o_dots = take(8);
+  P.o_seeds_eff = take(P.N * P.S);
   P.o_ls = take(2 * (int64_t)P.ncand);
   P.o_A1 = take((int64_t)P.maxp * P.maxp);
   P.o_A2 = take((int64_t)P.maxp * P.maxp);
@@ -451,6 +453,8 @@ struct ResidualIn {
   const double* r0;
   const double* seeds;
   const double* targets;
+  const double* quad = nullptr;  // interior: quadratic gradient coefficients (n x d)
+  double* seeds_out = nullptr;   // interior: effective reverse-pass seeds (n x S)
 };
 
 // Forward pass storing every state needed by the reverse pass (taylor.py:172-203;
@@ -479,7 +483,7 @@ void forward_store(const Ctx& c, const double* theta, const double* wpad, const 
     last_in = b.post[L - 1];
   }
   launch_last_layer(last_in, n, P.h[L - 1], theta + P.th[L - 1], td, ri.r0, ri.seeds, ri.targets,
-                    r, u_out, c.s);
+                    r, u_out, c.s, ri.quad, ri.seeds_out);
 }
 
 // Forward pass for losses only (no stored states): ping-pong buffers.  `batch` parameter
@@ -535,7 +539,8 @@ void forward_loss(const Ctx& c, const double* theta, const double* wpad, const d
                     [&] { done = launch_gemm_act(ga, ACT_LAST, c.s); });
         if (done) {
           launch_last_from_partials(c.at(P.o_upart), ntn, n, td, theta + P.th[L - 1] + P.h[L - 1],
-                                    ri.r0, ri.seeds, ri.targets, r, c.s, batch, P.D, r_bstride);
+                                    ri.r0, ri.seeds, ri.targets, r, c.s, batch, P.D, r_bstride,
+                                    ri.quad);
           return;
         }
       } else {
@@ -559,7 +564,7 @@ void forward_loss(const Ctx& c, const double* theta, const double* wpad, const d
   for (int kk = 0; kk < batch; ++kk)
     launch_last_layer(cur + (int64_t)kk * n * td.S * P.h[L - 1], n, P.h[L - 1],
                       theta + kk * P.D + P.th[L - 1], td, ri.r0, ri.seeds, ri.targets,
-                      r ? r + kk * r_bstride : nullptr, u_out, c.s);
+                      r ? r + kk * r_bstride : nullptr, u_out, c.s, ri.quad);
 }
 
 // Reverse pass (taylor.py:242-276 / network.py:216-232): gout[l] for l < L-1.
@@ -682,6 +687,11 @@ int phase_accumulate(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, cons
     const double* seeds = bt->seeds + n0 * P.S;
     double* r = c.at(P.o_r) + n0;
     ResidualIn ri{bt->r0 + n0, seeds, nullptr};
+    if (bt->quad) {  // seeds depend on the outputs (optim.py:157-158): computed by the forward
+      ri.quad = bt->quad + n0 * P.d;
+      ri.seeds_out = c.at(P.o_seeds_eff) + n0 * P.S;
+      seeds = ri.seeds_out;
+    }
     forward_store(c, st->theta, c.at(P.o_wpad), x, nc, tdi, bt->coeff_diag, bi, ri, r, nullptr);
     backward(c, st->theta, nc, tdi, bt->coeff_diag, bi, seeds);
     accumulate(c, x, nc, tdi, bi, seeds, r, red + P.r_aint, red + P.r_bint, red + P.r_gint);
@@ -893,6 +903,7 @@ int phase_linesearch(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, cons
     for (int64_t n0 = 0; n0 < P.N; n0 += P.Nc) {
       const int64_t nc = std::min(P.Nc, P.N - n0);
       ResidualIn ri{bt->r0 + n0, bt->seeds + n0 * P.S, nullptr};
+      if (bt->quad) ri.quad = bt->quad + n0 * P.d;
       forward_loss(c, thc, c.at(P.o_wpadc), bt->x_int + n0 * P.d, nc, tdi, bt->coeff_diag,
                    c.at(P.o_ping), c.at(P.o_pong), ri, c.at(P.o_rls) + k0 * P.N + n0, nullptr, true,
                    nb, P.N);
@@ -967,13 +978,17 @@ int phase_star_gvp(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, const 
   for (int64_t n0 = 0; n0 < P.N; n0 += P.Nc) {
     const int64_t nc = std::min(P.Nc, P.N - n0);
     const double* x = bt->x_int + n0 * P.d;
-    const double* seeds = bt->seeds + n0 * P.S;
+    const double* seeds = bt->quad ? c.at(P.o_seeds_eff) + n0 * P.S : bt->seeds + n0 * P.S;
     if (!single) {
       launch_candidate(st->theta, nullptr, 0, nullptr, P.D, P.wp, c.at(P.o_wpad), c.s);
       if (P.L >= 2)
         launch_prep_layer0(st->theta, P.d, P.h[1], bt->coeff_diag, c.at(P.o_w0t), c.at(P.o_q0),
                            c.s);
-      ResidualIn ri{bt->r0 + n0, seeds, nullptr};
+      ResidualIn ri{bt->r0 + n0, bt->seeds + n0 * P.S, nullptr};
+      if (bt->quad) {
+        ri.quad = bt->quad + n0 * P.d;
+        ri.seeds_out = c.at(P.o_seeds_eff) + n0 * P.S;
+      }
       forward_store(c, st->theta, c.at(P.o_wpad), x, nc, tdi, bt->coeff_diag, bi, ri,
                     c.at(P.o_r) + n0, nullptr);
       backward(c, st->theta, nc, tdi, bt->coeff_diag, bi, seeds);
@@ -1343,6 +1358,7 @@ int32_t kp_evaluate_losses(kp_context* ctx, const kp_problem* prob, const double
   for (int64_t n0 = 0; n0 < P.N; n0 += P.Nc) {
     const int64_t nc = std::min(P.Nc, P.N - n0);
     ResidualIn ri{bt->r0 + n0, bt->seeds + n0 * P.S, nullptr};
+    if (bt->quad) ri.quad = bt->quad + n0 * P.d;
     forward_loss(c, theta, c.at(P.o_wpad), bt->x_int + n0 * P.d, nc, tdi, bt->coeff_diag, c.at(P.o_ping),
                  c.at(P.o_pong), ri, c.at(P.o_r) + n0, nullptr);
   }

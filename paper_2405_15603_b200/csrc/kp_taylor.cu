@@ -157,7 +157,8 @@ constexpr int LAST_MAX_ROWS = 1024;
 __global__ void __launch_bounds__(LAST_THREADS) k_last_layer(
     const double* __restrict__ post, int64_t n, int h, const double* __restrict__ th,
     TaylorDims td, int spb, const double* __restrict__ r0, const double* __restrict__ seeds,
-    const double* __restrict__ targets, double* __restrict__ r, double* __restrict__ u_out) {
+    const double* __restrict__ targets, double* __restrict__ r, double* __restrict__ u_out,
+    const double* __restrict__ quad, double* __restrict__ seeds_out) {
   __shared__ double u[LAST_MAX_ROWS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t s0 = (int64_t)blockIdx.x * spb;
@@ -181,9 +182,9 @@ __global__ void __launch_bounds__(LAST_THREADS) k_last_layer(
     const int64_t smp = s0 + k;
     double v;
     if (td.taylor) {
-      v = r0[smp];
-      const double* sd = seeds + smp * td.S;
-      for (int s = 0; s < td.S; ++s) v += sd[s] * u[k * td.S + s];
+      v = point_residual(u + k * td.S, td.S, r0[smp], seeds + smp * td.S,
+                         quad ? quad + smp * td.d : nullptr,
+                         seeds_out ? seeds_out + smp * td.S : nullptr);
     } else {
       v = u[k] - targets[smp];
     }
@@ -231,13 +232,15 @@ void launch_initial_state(const double* x, int64_t n, int d, double* z, cudaStre
 
 void launch_last_layer(const double* post, int64_t n, int h, const double* theta_last,
                        TaylorDims td, const double* r0, const double* seeds,
-                       const double* targets, double* r, double* u_out, cudaStream_t s) {
+                       const double* targets, double* r, double* u_out, cudaStream_t s,
+                       const double* quad, double* seeds_out) {
   if (n <= 0) return;
   const int spb = std::max(1, std::min(LAST_MAX_ROWS / td.S, 64));
   const int64_t blocks = ceil_div(n, spb);
   count_launch();
   k_last_layer<<<(unsigned)blocks, LAST_THREADS, 0, s>>>(post, n, h, theta_last, td, spb, r0,
-                                                         seeds, targets, r, u_out);
+                                                         seeds, targets, r, u_out, quad,
+                                                         seeds_out);
 }
 
 // ---------------------------------------------------------------------------

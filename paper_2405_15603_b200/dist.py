@@ -22,7 +22,7 @@ from __future__ import annotations
 import numpy as np
 
 from .engine import KfacEngine, raise_for_status
-from .pde import affine_residual_terms
+from .pde import residual_terms
 from .taylor import coeff_diagonal
 
 
@@ -95,10 +95,10 @@ def upload_shard(eng, batch, problem, rank: int, world: int):
     i0, i1 = shard_bounds(n_int, rank, world)
     b0, b1 = shard_bounds(n_bnd, rank, world)
     x = np.asarray(batch.interior, dtype=np.float64)[i0:i1]
-    r0, seeds = affine_residual_terms(problem, x)
+    r0, seeds, quad = residual_terms(problem, x)
     eng.set_batch(x, r0, seeds, np.asarray(batch.boundary, dtype=np.float64)[b0:b1],
                   np.asarray(batch.boundary_targets, dtype=np.float64)[b0:b1],
-                  coeff_diagonal(problem.coeffs))
+                  coeff_diagonal(problem.coeffs), quad)
 
 
 def torch_all_reduce(group=None):

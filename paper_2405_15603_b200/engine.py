@@ -130,8 +130,9 @@ class KfacEngine:
         self.x_bnd = z(self.n_boundary * self.d)
         self.targets = z(self.n_boundary)
         self.cdiag = z(self.d)
+        self.quad = None  # allocated on first non-affine batch
         self.batch = _capi.kp_batch(_ptr(self.x_int), _ptr(self.r0), _ptr(self.seeds),
-                                    _ptr(self.x_bnd), _ptr(self.targets), _ptr(self.cdiag))
+                                    _ptr(self.x_bnd), _ptr(self.targets), _ptr(self.cdiag), 0)
         self.prob = _capi.kp_problem()
         self.prob.net = self.net
         self.prob.n_interior, self.prob.n_boundary = self.n_interior, self.n_boundary
@@ -183,9 +184,19 @@ class KfacEngine:
         raise_for_status(self.lib.kp_init_state(self.ctx, C.byref(self.net), C.byref(self.st),
                                                 int(bool(identity)), C.c_void_p(self.stream.cuda_stream)))
 
-    def set_batch(self, x_int, r0, seeds, x_bnd, targets, cdiag):
+    def set_batch(self, x_int, r0, seeds, x_bnd, targets, cdiag, quad=None):
+        """Upload one batch; ``quad`` (N x d) makes the residual quadratic in grad u
+        (pde.residual_terms), None keeps it affine."""
         if x_int.shape != (self.n_interior, self.d) or x_bnd.shape != (self.n_boundary, self.d):
             raise ValueError("batch shape does not match the engine")
+        if quad is None:
+            self.batch.quad = 0
+        else:
+            if self.quad is None:
+                self.quad = self.torch.zeros(self.n_interior * self.d, dtype=self.torch.float64,
+                                             device=self.device)
+            self._h2d(self.quad, quad)
+            self.batch.quad = _ptr(self.quad)
         self._h2d(self.x_int, x_int)
         self._h2d(self.r0, r0)
         self._h2d(self.seeds, seeds)

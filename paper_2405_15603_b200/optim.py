@@ -29,7 +29,7 @@ import numpy as np
 from . import network
 from .curvature import KfacState
 from .engine import KfacEngine, LineSearchError, pack_mats
-from .pde import affine_residual_terms
+from .pde import residual_terms
 from .taylor import coeff_diagonal
 
 __all__ = [
@@ -201,7 +201,7 @@ def _kfac_device_step(state: TrainState, batch, problem) -> StepInfo:
     widths = (params.weights[0].shape[1],) + tuple(w.shape[0] for w in params.weights)
     cdiag = coeff_diagonal(problem.coeffs)
     x = np.asarray(batch.interior, dtype=np.float64)
-    r0, seeds = affine_residual_terms(problem, x)
+    r0, seeds, quad = residual_terms(problem, x)
     eng = _engine_for(state, batch, widths)
     _sync_host_edits(state, eng)
     if state._kfac_host is not None:
@@ -210,7 +210,7 @@ def _kfac_device_step(state: TrainState, batch, problem) -> StepInfo:
         if eng.cfg.damping <= 0:
             raise ValueError("damping must be positive for Kronecker preconditioning")
     eng.set_batch(x, r0, seeds, np.asarray(batch.boundary, dtype=np.float64),
-                  np.asarray(batch.boundary_targets, dtype=np.float64), cdiag)
+                  np.asarray(batch.boundary_targets, dtype=np.float64), cdiag, quad)
     if state.config.kind == "kfac_star":
         eng.launch_star_step()
     else:

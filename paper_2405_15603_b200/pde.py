@@ -34,6 +34,7 @@ __all__ = [
     "make_problem",
     "sample_batch",
     "affine_residual_terms",
+    "residual_terms",
 ]
 
 
@@ -312,3 +313,51 @@ def affine_residual_terms(problem, x, rtol: float = 1e-12):
     seeds[:, 1:d + 1] = dg
     seeds[:, d + 1] = dop
     return np.ascontiguousarray(r0), seeds
+
+
+def residual_terms(problem, x, rtol: float = 1e-12):
+    """Split an interior residual that is quadratic in the output gradient.
+
+    Returns ``(r0, seeds, quad)`` such that, per point,
+    ``r = r0 + seeds . [u, grad u, Lu] + sum_i quad_i (grad_i u)^2`` and the reverse-pass
+    seeds of optim.py:157-158 are ``seeds + [0, 2 quad * grad u, 0]``.  ``quad`` is None
+    for affine residuals (every BASELINE config).  The family covers every catalog
+    residual, including log-Fokker-Planck (pde.py:253-263: quad_i = -1 on the spatial
+    directions, seeds_i = -x_i / 2).  The problem's own callables are probed at two
+    random output triples; anything outside the family raises ``NotImplementedError``
+    (the device path has no CPU fallback).
+    """
+    x = np.asarray(x, dtype=np.float64)
+    n, d = x.shape
+    zu, zg = np.zeros(n), np.zeros((n, d))
+    r0 = np.asarray(problem.residual(x, zu, zg, zu), dtype=np.float64)
+    bc = lambda a, shape: np.broadcast_to(np.asarray(a, np.float64), shape).copy()  # noqa: E731
+    du0, dg0, dop0 = problem.residual_grads(x, zu, zg, zu)
+    du0, dg0, dop0 = bc(du0, (n,)), bc(dg0, (n, d)), bc(dop0, (n,))
+    gen = np.random.default_rng(12345)
+    pts = [(gen.standard_normal(n), gen.uniform(0.5, 1.5, (n, d)) * gen.choice([-1, 1], (n, d)),
+            gen.standard_normal(n)) for _ in range(2)]
+    u1, g1, o1 = pts[0]
+    du1, dg1, dop1 = problem.residual_grads(x, u1, g1, o1)
+    du1, dg1, dop1 = bc(du1, (n,)), bc(dg1, (n, d)), bc(dop1, (n,))
+    quad = (dg1 - dg0) / (2.0 * g1)
+    ok = np.array_equal(du1, du0) and np.array_equal(dop1, dop0) and np.all(np.isfinite(quad))
+    for (u, g, o) in pts:
+        if not ok:
+            break
+        _, dg, _ = problem.residual_grads(x, u, g, o)
+        ok = np.allclose(bc(dg, (n, d)), dg0 + 2.0 * quad * g, rtol=1e-10, atol=1e-12)
+        r = np.asarray(problem.residual(x, u, g, o), dtype=np.float64)
+        pred = r0 + du0 * u + np.einsum("ni,ni->n", dg0, g) + np.einsum("ni,ni->n", quad, g * g) + dop0 * o
+        ok = ok and np.all(np.abs(r - pred) <= rtol * 1e3 * np.maximum(np.abs(r), 1.0))
+    if not ok:
+        raise NotImplementedError(
+            f"problem {getattr(problem, 'name', '?')!r}: residual is not of the form "
+            "r0 + a u + b.grad u + c.(grad u)^2 + e Lu; the device KFAC path does not support it")
+    seeds = np.empty((n, d + 2))
+    seeds[:, 0] = du0
+    seeds[:, 1:d + 1] = dg0
+    seeds[:, d + 1] = dop0
+    if not np.any(quad):
+        quad = None
+    return np.ascontiguousarray(r0), seeds, (None if quad is None else np.ascontiguousarray(quad))

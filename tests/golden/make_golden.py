@@ -53,13 +53,16 @@ PLAN = {
     "c1_star": ("c1", 300, 80, 3),
     "c3_star": ("c3", 200, 100, 3),
     "c5_star": ("c5", 24, 8, 2),
+    # reference catalog log-Fokker-Planck (non-affine residual, per-point seeds)
+    "lfp": ("lfp", 300, 100, 3),
+    "lfp_star": ("lfp", 300, 100, 3),
 }
 
 
 def ref_problem(wl):
     """Reference PdeProblem for a workload (catalog where it exists, else rigged)."""
-    if wl.problem == "poisson2d_sin":
-        return pde.make_problem("poisson2d_sin")
+    if wl.problem in ("poisson2d_sin", "log_fokker_planck"):
+        return pde.make_problem(wl.problem)
     if wl.problem == "poisson_cos_sum" and dict(wl.problem_params).get("dim", 5) == 5:
         return pde.make_problem("poisson_cos_sum")
     mine = wl.make_problem()

@@ -20,7 +20,7 @@ from paper_2405_15603_b200.optim import OptimizerConfig, init_train_state, optim
 from paper_2405_15603_b200.pde import make_problem, sample_batch  # noqa: E402
 
 WL_OF = {"c1": "c1", "c2": "c2", "c3": "c3", "c4": "c4", "c5": "c5", "c1_momentum": "c1",
-         "c1_star": "c1", "c3_star": "c3", "c5_star": "c5"}
+         "c1_star": "c1", "c3_star": "c3", "c5_star": "c5", "lfp": "lfp", "lfp_star": "lfp"}
 
 
 def _theta_colstack(params):
@@ -210,9 +210,14 @@ def test_line_search_error_on_nonfinite_params():
         optimizer_step(state, batch, prob)
 
 
-def test_nonaffine_residual_rejected():
-    prob = make_problem("log_fokker_planck")
-    params = init_params(Architecture((10, 8, 1)), 0)
+def test_unsupported_residual_rejected():
+    # a residual quadratic in u (seed dr/du depends on u) is outside the device family
+    from paper_2405_15603_b200.pde import PdeProblem
+    base = make_problem("poisson2d_sin")
+    prob = PdeProblem(**{**base.__dict__,
+                         "residual": lambda x, u, g, op: u * u - op,
+                         "residual_grads": lambda x, u, g, op: (2 * u, np.zeros_like(g), -np.ones_like(u))})
+    params = init_params(Architecture((2, 8, 1)), 0)
     batch = sample_batch(prob, 10, 5, 0)
     state = init_train_state(params, OptimizerConfig(kind="kfac", damping=1e-3))
     with pytest.raises(NotImplementedError):

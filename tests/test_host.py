@@ -96,6 +96,20 @@ def test_nonaffine_residual_is_rejected():
         affine_residual_terms(prob, b.interior)
 
 
+def test_log_fokker_planck_is_quadratic_in_grad():
+    # pde.py:253-263: r = u_t - s/2 - x.grad_x u / 2 - |grad_x u|^2 - Lu
+    from paper_2405_15603_b200.pde import residual_terms
+    prob = make_problem("log_fokker_planck")
+    b = sample_batch(prob, 32, 8, 2)
+    r0, seeds, quad = residual_terms(prob, b.interior)
+    assert np.allclose(r0, -4.5)
+    assert np.allclose(quad[:, 0], 0.0) and np.allclose(quad[:, 1:], -1.0)
+    assert np.allclose(seeds[:, 1], 1.0) and np.allclose(seeds[:, 2:11], -0.5 * b.interior[:, 1:])
+    assert np.allclose(seeds[:, 11], -1.0)
+    # affine problems keep quad = None
+    assert residual_terms(make_problem("poisson2d_sin"), b.interior[:, :2])[2] is None
+
+
 def test_heat_sine_product_solution_solves_pde():
     # u = exp(-pi^2 t) prod sin(pi x_i): u_t = -pi^2 u, 1/4 Lap_x u = 1/4 * (-4 pi^2) u
     prob = make_problem("heat", spatial_dim=4, solution="sine_product")

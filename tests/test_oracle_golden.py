@@ -15,7 +15,7 @@ from paper_2405_15603_b200 import configs as cfgs
 from paper_2405_15603_b200.network import params_to_vec
 
 WL_OF = {"c1": "c1", "c2": "c2", "c3": "c3", "c4": "c4", "c5": "c5", "c1_momentum": "c1",
-         "c1_star": "c1", "c3_star": "c3", "c5_star": "c5"}
+         "c1_star": "c1", "c3_star": "c3", "c5_star": "c5", "lfp": "lfp", "lfp_star": "lfp"}
 
 
 def build(name):
