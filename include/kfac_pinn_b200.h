@@ -199,6 +199,12 @@ int32_t kp_taylor_forward(kp_context* ctx, const kp_problem* prob, const double*
                           const kp_batch* batch, double* value, double* gradient,
                           double* op, void* workspace, size_t workspace_bytes, void* stream);
 
+/* Plain MLP forward u(x) (src/network.py:200-213) at prob->n_boundary points x
+ * (n x d) — the evaluation pass of eval_l2 (src/harness.py:155-166). */
+int32_t kp_mlp_forward(kp_context* ctx, const kp_problem* prob, const double* theta,
+                       const double* x, double* u, void* workspace, size_t workspace_bytes,
+                       void* stream);
+
 /* evaluate_losses (src/optim.py:148-152) at `theta`: losses[0..1]. */
 int32_t kp_evaluate_losses(kp_context* ctx, const kp_problem* prob, const double* theta,
                            const kp_batch* batch, double* losses, void* workspace,

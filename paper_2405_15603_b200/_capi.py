@@ -99,6 +99,8 @@ _SIGS = {
     "kp_taylor_forward": (C.c_int32, [C.c_void_p, P(kp_problem), C.c_void_p, P(kp_batch),
                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
                                       C.c_void_p]),
+    "kp_mlp_forward": (C.c_int32, [C.c_void_p, P(kp_problem), C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.c_void_p, C.c_size_t, C.c_void_p]),
     "kp_evaluate_losses": (C.c_int32, [C.c_void_p, P(kp_problem), C.c_void_p, P(kp_batch),
                                        C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "kp_kron_solve_workspace_bytes": (C.c_int32, [C.c_void_p, C.c_int32, C.c_int32,

@@ -1343,6 +1343,22 @@ int32_t kp_taylor_forward(kp_context* ctx, const kp_problem* prob, const double*
   return KP_OK;
 }
 
+
+int32_t kp_mlp_forward(kp_context* ctx, const kp_problem* prob, const double* theta,
+                       const double* x, double* u, void* ws, size_t ws_bytes, void* stream) {
+  Plan P;
+  KP_TRY(prepare(ctx, prob, P, ws_bytes));
+  if (!theta || !x || !u) return KP_ERR_INVALID;
+  Ctx c{ctx, P, static_cast<double*>(ws), (cudaStream_t)stream};
+  const TaylorDims tdb{1, 0, false};
+  launch_candidate(theta, nullptr, 0, nullptr, P.D, P.wp, c.at(P.o_wpad), c.s);
+  ResidualIn rb{nullptr, nullptr, nullptr};
+  forward_loss(c, theta, c.at(P.o_wpad), x, P.Nb, tdb, nullptr, c.at(P.o_bping), c.at(P.o_bpong),
+               rb, nullptr, u);
+  KP_CUDA_TRY(cudaGetLastError());
+  return KP_OK;
+}
+
 int32_t kp_evaluate_losses(kp_context* ctx, const kp_problem* prob, const double* theta,
                            const kp_batch* bt, double* losses, void* ws, size_t ws_bytes,
                            void* stream) {

@@ -139,3 +139,24 @@ def test_shard_bounds_cover_exactly(n, world):
         assert b == c
     sizes = [b - a for a, b in spans]
     assert max(sizes) - min(sizes) <= 1
+
+
+def test_run_config_mirrors_reference_validation():
+    from paper_2405_15603_b200.harness import RunConfig
+    cfg = RunConfig(problem="heat", widths=[2, 8, 1], optimizer="kfac")
+    assert cfg.resample_every == 100 and cfg.to_dict()["optimizer"] == "kfac"
+    for bad in ({"n_interior": 0}, {"eval_every": 0}, {"resample_every": -1}, {"optimizer": "lbfgs"}):
+        with pytest.raises(ValueError):
+            RunConfig(**{**dict(problem="heat", widths=[2, 8, 1], optimizer="kfac"), **bad})
+    with pytest.raises(ValueError):
+        RunConfig.from_dict({"problem": "heat", "widths": [2, 1], "optimizer": "kfac", "bogus": 1})
+
+
+def test_checkpoint_roundtrip(tmp_path):
+    from paper_2405_15603_b200.harness import load_checkpoint, save_checkpoint
+    p = init_params(Architecture((3, 4, 1)), 2)
+    save_checkpoint(str(tmp_path / "c.json"), p)
+    q, conf = load_checkpoint(str(tmp_path / "c.json"))
+    assert conf is None
+    for a, b in zip(p.weights + p.biases, q.weights + q.biases):
+        assert np.array_equal(a, b)
