@@ -38,7 +38,7 @@ extern "C" {
 #endif
 
 #define KP_MAX_LAYERS 16
-#define KP_ABI_VERSION 2
+#define KP_ABI_VERSION 3
 
 typedef enum kp_status {
   KP_OK = 0,
@@ -105,8 +105,13 @@ typedef struct kp_batch {
   const double* seeds;
   const double* x_bnd;
   const double* targets;
-  const double* coeff_diag;  /* d: diagonal operator coefficients (src/taylor.py:43-87) */
+  const double* coeff_diag;  /* d: diagonal operator coefficients (src/taylor.py:43-87), or
+                                the eigenvalues lambda of a dense c (see coeff_rot) */
   const double* quad;        /* N x d quadratic gradient coefficients, or NULL */
+  const double* coeff_rot;   /* NULL (c diagonal), or the d x d row-major orthogonal Q of
+                                c = Q diag(lambda) Q^T (src/taylor.py:72-75).  The engine then
+                                propagates derivatives along the columns of Q; seeds stay in
+                                the coordinate basis.  Not combinable with quad. */
 } kp_batch;
 
 /* Step outputs (device).  scalars[4] = {loss_interior, loss_boundary, alpha, mu}
@@ -191,6 +196,14 @@ int32_t kp_kfac_star_phase_gvp(kp_context* ctx, const kp_problem* prob, const kp
 int32_t kp_kfac_star_phase_update(kp_context* ctx, const kp_problem* prob,
                                   const kp_kfac_config* cfg, kp_state* st, kp_step_out* out,
                                   void* workspace, size_t workspace_bytes, void* stream);
+
+/* kp_kfac_step (star = 0) or kp_kfac_star_step (star = 1) replayed from a CUDA graph
+ * captured on first use, when every layer's Kronecker solve runs on the device (factor
+ * sizes <= 96, no host-blocking library call) and profiling is off; otherwise the same
+ * as the plain call.  Intended for launch-bound small problems (BASELINE c1-c3). */
+int32_t kp_kfac_step_graphed(kp_context* ctx, const kp_problem* prob, const kp_kfac_config* cfg,
+                             kp_state* st, const kp_batch* batch, kp_step_out* out,
+                             void* workspace, size_t workspace_bytes, void* stream, int32_t star);
 
 /* Forward-Laplacian forward (src/taylor.py:172-203) of the parameters `theta`
  * at the interior points of `batch`: writes u (N), grad u (N x d), L u (N).

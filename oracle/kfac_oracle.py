@@ -72,6 +72,21 @@ def tanh_derivs(z, order=3):
 # forward-Laplacian engine
 
 
+def _apply_c(cdiag, g):
+    """Contract the coefficients over the derivative axis of an (N, d, h) stack
+    (taylor.py:66-75): ``cdiag`` is the diagonal (d,) or the dense matrix (d, d)."""
+    if cdiag.ndim == 1:
+        return g * cdiag[None, :, None]
+    return np.einsum("ij,njh->nih", cdiag, g)
+
+
+def coeffs_of(problem):
+    """Diagonal of the problem's c when it is diagonal (taylor.py:56-57), else c itself."""
+    c = np.asarray(problem.coeffs.c, dtype=np.float64)
+    diag = np.diagonal(c).copy()
+    return diag if np.array_equal(c, np.diag(diag)) else c
+
+
 def taylor_forward(weights, biases, x, cdiag):
     """Propagate [value | d/dx_1..d | Lz] rows through the MLP (taylor.py:172-203).
 
@@ -96,7 +111,7 @@ def taylor_forward(weights, biases, x, cdiag):
             break
         s0, s1, s2, _ = tanh_derivs(y[:, 0, :], order=2)
         g = y[:, 1:d + 1, :]
-        quad = np.sum((g * cdiag[None, :, None]) * g, axis=1)
+        quad = np.sum(_apply_c(cdiag, g) * g, axis=1)
         z = np.empty_like(y)              # taylor_forward_activation, taylor.py:151-169
         z[:, 0, :] = s0
         z[:, 1:d + 1, :] = s1[:, None, :] * g
@@ -108,12 +123,12 @@ def taylor_forward(weights, biases, x, cdiag):
 
 def activation_backward(y, gout, cdiag):
     """Adjoint of the Taylor activation (taylor.py:206-239); ``y`` is the pre-activation state."""
-    d = cdiag.size
+    d = cdiag.shape[0]
     s0, s1, s2, s3 = tanh_derivs(y[:, 0, :], order=3)
     g = y[:, 1:d + 1, :]
     ell = y[:, d + 1, :]
     vb, gb, lb = gout[:, 0, :], gout[:, 1:d + 1, :], gout[:, d + 1, :]
-    cg = g * cdiag[None, :, None]
+    cg = _apply_c(cdiag, g)
     quad = np.sum(cg * g, axis=1)
     gin = np.empty_like(gout)
     gin[:, d + 1, :] = s1 * lb
@@ -366,7 +381,7 @@ def kfac_step(st: OracleState, batch, problem, record=None):
     ``record`` (a dict, optional) receives the intermediates the parity tests
     compare: grad_mats, delta, direction, line-search losses.
     """
-    cdiag = np.diagonal(np.asarray(problem.coeffs.c, dtype=np.float64)).copy()
+    cdiag = coeffs_of(problem)
     ev = evaluate_batch(st.weights, st.biases, batch, problem, cdiag)
     kf = st.kfac
     a_new, b_new = interior_factors(ev.lin_in, ev.gbar)
@@ -434,7 +449,7 @@ def solve_quadratic_model(have_prev, m11, m12, m22, rhs1, rhs2):
 
 def kfac_star_step(st: OracleState, batch, problem, record=None):
     """One KFAC* step (optim.py:296-320) + non-finite check (optim.py:398-401)."""
-    cdiag = np.diagonal(np.asarray(problem.coeffs.c, dtype=np.float64)).copy()
+    cdiag = coeffs_of(problem)
     ev = evaluate_batch(st.weights, st.biases, batch, problem, cdiag)
     kf = st.kfac
     beta = kf.ema

@@ -13,7 +13,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libkfac_pinn_b200.so")
 MAX_LAYERS = 16
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 KP_OK = 0
 KP_ERR_INVALID = 1
@@ -46,7 +46,7 @@ class kp_state(C.Structure):
 
 class kp_batch(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("x_int", "r0", "seeds", "x_bnd", "targets", "coeff_diag",
-                                          "quad")]
+                                          "quad", "coeff_rot")]
 
 
 class kp_step_out(C.Structure):
@@ -88,6 +88,9 @@ _SIGS = {
     "kp_kfac_star_step": (C.c_int32, [C.c_void_p, P(kp_problem), P(kp_kfac_config), P(kp_state),
                                       P(kp_batch), P(kp_step_out), C.c_void_p, C.c_size_t,
                                       C.c_void_p]),
+    "kp_kfac_step_graphed": (C.c_int32, [C.c_void_p, P(kp_problem), P(kp_kfac_config), P(kp_state),
+                                         P(kp_batch), P(kp_step_out), C.c_void_p, C.c_size_t,
+                                         C.c_void_p, C.c_int32]),
     "kp_gvp_buffer": (C.c_int32, [C.c_void_p, P(kp_problem), C.c_void_p, P(C.c_void_p),
                                   P(C.c_int64)]),
     "kp_kfac_star_phase_gvp": (C.c_int32, [C.c_void_p, P(kp_problem), P(kp_kfac_config),

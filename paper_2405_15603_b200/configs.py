@@ -9,12 +9,14 @@ EMA 0.95, momentum 0 and identity init.  All data are synthetic.
 
 from __future__ import annotations
 
+import dataclasses
 from dataclasses import dataclass
 
 import numpy as np
 
 from .network import Architecture, init_params
 from .pde import make_problem, sample_batch
+from .taylor import OperatorCoeffs
 
 STREAM_INIT, STREAM_BATCH = 0, 1
 
@@ -36,9 +38,16 @@ class Workload:
     ema: float = 0.95
     momentum: float = 0.0
     steps: int = 10
+    dense_coeffs_seed: int | None = None  # replace c by a random dense symmetric matrix
 
     def make_problem(self):
-        return make_problem(self.problem, **dict(self.problem_params))
+        prob = make_problem(self.problem, **dict(self.problem_params))
+        if self.dense_coeffs_seed is not None:
+            # the reference's own dense-coefficient test matrices (pkg/tests/test_taylor.py:22-24,
+            # test_acceptance.py:34-35): c = (R + R^T) / 2, R standard normal
+            r = np.random.default_rng(self.dense_coeffs_seed).standard_normal((prob.dim, prob.dim))
+            prob = dataclasses.replace(prob, coeffs=OperatorCoeffs(0.5 * (r + r.T)))
+        return prob
 
     def build(self, seed: int = 0, n_interior: int | None = None, n_boundary: int | None = None):
         """(problem, params, batch) with the reference seeding recipe."""
@@ -70,6 +79,11 @@ WORKLOADS = {
 # whose residual is quadratic in grad u — exercises the non-affine seed path.
 WORKLOADS["lfp"] = Workload("lfp_logfokkerplanck9p1d", "log_fokker_planck", (),
                             (10, 48, 48, 32, 1), 500, 200)
+
+# Not a BASELINE config: c2's network and residual with a dense, indefinite operator
+# coefficient matrix (reference taylor.py:72-75, the non-diagonal branch of OperatorCoeffs.apply).
+WORKLOADS["dense"] = Workload("dense_poisson5d", "poisson_cos_sum", (("dim", 5),),
+                              (5, 64, 64, 48, 48, 1), 400, 100, dense_coeffs_seed=5)
 
 C5_SWEEP = (3000, 16384, 65536)
 

@@ -140,7 +140,9 @@ void launch_first_layer(const double* x, int64_t n, int d, const double* theta0,
                         TaylorDims td, const double* w0t, const double* q0, double* zval,
                         double* post, cudaStream_t s, int batch = 1, int64_t D = 0);
 // Per parameter set: w0t = W0^T (d x h1), q0[j] = sum_i (W0[j,i] c_i) W0[j,i].
-void launch_prep_layer0(const double* theta0, int d, int h1, const double* cdiag, double* w0t,
+// rot (d x d, or NULL): derivative directions Q[:, k] instead of e_k (dense coefficients).
+void launch_prep_layer0(const double* theta0, int d, int h1, const double* cdiag, const double* rot,
+                        double* w0t,
                         double* q0, cudaStream_t s, int batch = 1, int64_t D = 0);
 // Taylor activation (taylor.py:151-169): pre (n*S x h) -> post.
 void launch_act_fwd(const double* pre, double* post, int64_t n, int h, TaylorDims td,
@@ -183,6 +185,13 @@ void launch_transpose(const double* src, int64_t lds, int rows, int cols, double
                       cudaStream_t s);
 void launch_fill(double* p, int64_t n, double v, cudaStream_t s);
 // u (n x S) -> value (n), grad (n x d), op (n)
+// Rows of X (n rows of pitch `stride`, d entries each) replaced in place by Q^T x
+// (transpose = 1) or Q x (transpose = 0).
+void launch_rotate_rows(double* X, int64_t stride, int64_t n, int d, const double* Q, int transpose,
+                        cudaStream_t s);
+// out[j * ldo + i] += sum_k T[j * d + k] Q[i * d + k]   (q x d times Q^T)
+void launch_rot_accum(const double* T, int q, int d, const double* Q, double* out, int64_t ldo,
+                      cudaStream_t s);
 void launch_split_u(const double* u, int64_t n, int d, double* value, double* grad, double* op,
                     cudaStream_t s);
 // initial_state (taylor.py:124-131): z (n*S x d) = [x; I; 0]

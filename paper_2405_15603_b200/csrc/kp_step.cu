@@ -59,6 +59,11 @@ struct kp_context {
   std::vector<cusolverDnHandle_t> side_solver;
   std::vector<cublasHandle_t> side_blas;
   std::vector<cudaEvent_t> side_ev;
+  // CUDA-graph replay of whole steps (only when every layer uses the on-device solver)
+  cudaStream_t cap_stream = nullptr;
+  cudaEvent_t cap_in = nullptr, cap_out = nullptr;
+  std::vector<unsigned char> graph_key;
+  cudaGraphExec_t graph_exec = nullptr;
   // cache of the last workspace plan (make_plan queries cuSOLVER workspace sizes: host cost)
   kp_problem plan_key{};
   bool plan_valid = false;
@@ -143,6 +148,8 @@ struct Plan {
   int64_t o_gv = 0, o_gvd = 0, o_gvp = 0, o_jv = 0, o_jvb = 0, o_wpadv = 0, o_v0t = 0, o_vq0 = 0,
           o_dots = 0;
   int64_t o_seeds_eff = 0;  // per-point reverse-pass seeds of a non-affine residual
+                            // (or the rotated seeds of dense coefficients)
+  int64_t o_rotg = 0;       // layer-0 derivative-row gradient in the rotated basis (h1 x d)
   int Bc = 1;   // line-search candidates evaluated per batched launch
   int64_t lwork = 0;
   int64_t total = 0;  // doubles
@@ -303,6 +310,7 @@ int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
   P.o_vq0 = take(P.h[1]);
   P.o_dots = take(8);
   P.o_seeds_eff = take(P.N * P.S);
+  P.o_rotg = take((int64_t)P.h[1] * P.d);
   P.o_ls = take(2 * (int64_t)P.ncand);
   P.o_A1 = take((int64_t)P.maxp * P.maxp);
   P.o_A2 = take((int64_t)P.maxp * P.maxp);
@@ -350,6 +358,7 @@ struct Ctx {
   const Plan& P;
   double* W;  // workspace base
   cudaStream_t s;
+  const double* rot = nullptr;  // Q of dense operator coefficients (kp_batch.coeff_rot)
   double* at(int64_t off) const { return W + off; }
 };
 
@@ -624,8 +633,16 @@ void contract_grad_layer(const Ctx& c, const double* x, int64_t n, const TaylorD
     launch_gemm_tn_accumulate(gg, part, out, c.s);
   }
   // derivative rows e_i: out[j][i] += sum_n w_n Gbar0[n, 1+i, j] (contiguous d x q block)
-  if (l == 0 && td.taylor)
-    launch_colsum(G + q, (int64_t)td.S * q, n, P.d * q, w, out, p, 0.0, part, c.s, q);
+  if (l == 0 && td.taylor) {
+    if (!c.rot) {
+      launch_colsum(G + q, (int64_t)td.S * q, n, P.d * q, w, out, p, 0.0, part, c.s, q);
+    } else {  // rows along Q[:, k]: out[j][i] += sum_k (sum_n w_n Gbar0[n, 1+k, j]) Q[i][k]
+      double* t = c.at(P.o_rotg);
+      cudaMemsetAsync(t, 0, sizeof(double) * q * P.d, c.s);
+      launch_colsum(G + q, (int64_t)td.S * q, n, P.d * q, w, t, P.d, 0.0, part, c.s, q);
+      launch_rot_accum(t, q, P.d, c.rot, out, p, c.s);
+    }
+  }
 }
 
 // Factor and gradient contractions of one pass into the reduce buffer.  The bulk of
@@ -677,7 +694,7 @@ int phase_accumulate(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, cons
     launch_transpose(st->theta + P.th[l], P.p[l], P.q[l], P.h[l], c.at(P.o_wT[l]), c.s);
   launch_candidate(st->theta, nullptr, 0, nullptr, P.D, P.wp, c.at(P.o_wpad), c.s);
   if (P.L >= 2)
-    launch_prep_layer0(st->theta, P.d, P.h[1], bt->coeff_diag, c.at(P.o_w0t), c.at(P.o_q0), c.s);
+    launch_prep_layer0(st->theta, P.d, P.h[1], bt->coeff_diag, bt->coeff_rot, c.at(P.o_w0t), c.at(P.o_q0), c.s);
   const TaylorDims tdi{P.S, P.d, true};
   const TaylorDims tdb{1, 0, false};
   const StateBufs bi = interior_bufs(c);
@@ -787,9 +804,14 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
   // The 2L generalised eigenproblems are independent: fan out over side streams (A and B
   // factor pair of layer l on streams 2l and 2l+1), combine on 2l, join back.
   kp_context* ctx = c.ctx;
-  KP_TRY(ensure_side_streams(ctx, 2 * P.L + 1));
-  cudaEvent_t ready = ctx->side_ev[2 * P.L];
-  KP_CUDA_TRY(cudaEventRecord(ready, c.s));
+  bool any_big = false;
+  for (int l = 0; l < P.L; ++l) any_big |= std::max(P.p[l], P.q[l]) > small_eig_max_n();
+  cudaEvent_t ready = nullptr;
+  if (any_big) {
+    KP_TRY(ensure_side_streams(ctx, 2 * P.L + 1));
+    ready = ctx->side_ev[2 * P.L];
+    KP_CUDA_TRY(cudaEventRecord(ready, c.s));
+  }
   // Small layers (both factors <= small_eig_max_n()): on-device Jacobi solver, all of them in
   // two launches on the main stream.  Larger layers: cuSOLVER sygvd, which blocks the calling
   // host thread, so each factor-pair solve is issued from its own host thread (own handle +
@@ -898,7 +920,7 @@ int phase_linesearch(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, cons
     launch_candidate(st->theta, dir, cfg->ls_min_exp + k0, thc, P.D, P.wpc, c.at(P.o_wpadc), c.s,
                      nb);
     if (P.L >= 2)
-      launch_prep_layer0(thc, P.d, P.h[1], bt->coeff_diag, c.at(P.o_w0tc), c.at(P.o_q0c), c.s, nb,
+      launch_prep_layer0(thc, P.d, P.h[1], bt->coeff_diag, bt->coeff_rot, c.at(P.o_w0tc), c.at(P.o_q0c), c.s, nb,
                          P.D);
     for (int64_t n0 = 0; n0 < P.N; n0 += P.Nc) {
       const int64_t nc = std::min(P.Nc, P.N - n0);
@@ -973,7 +995,7 @@ int phase_star_gvp(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, const 
   auto prep = [&](const double* v) {
     launch_candidate(v, nullptr, 0, nullptr, P.D, P.wp, c.at(P.o_wpadv), c.s);
     if (P.L >= 2)
-      launch_prep_layer0(v, P.d, P.h[1], bt->coeff_diag, c.at(P.o_v0t), c.at(P.o_vq0), c.s);
+      launch_prep_layer0(v, P.d, P.h[1], bt->coeff_diag, bt->coeff_rot, c.at(P.o_v0t), c.at(P.o_vq0), c.s);
   };
   for (int64_t n0 = 0; n0 < P.N; n0 += P.Nc) {
     const int64_t nc = std::min(P.Nc, P.N - n0);
@@ -982,7 +1004,7 @@ int phase_star_gvp(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, const 
     if (!single) {
       launch_candidate(st->theta, nullptr, 0, nullptr, P.D, P.wp, c.at(P.o_wpad), c.s);
       if (P.L >= 2)
-        launch_prep_layer0(st->theta, P.d, P.h[1], bt->coeff_diag, c.at(P.o_w0t), c.at(P.o_q0),
+        launch_prep_layer0(st->theta, P.d, P.h[1], bt->coeff_diag, bt->coeff_rot, c.at(P.o_w0t), c.at(P.o_q0),
                            c.s);
       ResidualIn ri{bt->r0 + n0, bt->seeds + n0 * P.S, nullptr};
       if (bt->quad) {
@@ -1102,6 +1124,13 @@ int32_t kp_context_create(int32_t device, kp_context** out) {
 
 int32_t kp_context_destroy(kp_context* c) {
   if (!c) return KP_OK;
+  if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+  if (c->cap_stream) {
+    cudaStreamSynchronize(c->cap_stream);
+    cudaStreamDestroy(c->cap_stream);
+  }
+  if (c->cap_in) cudaEventDestroy(c->cap_in);
+  if (c->cap_out) cudaEventDestroy(c->cap_out);
   for (size_t k = 0; k < c->side.size(); ++k) {
     cudaStreamSynchronize(c->side[k]);
     cusolverDnDestroy(c->side_solver[k]);
@@ -1217,6 +1246,28 @@ int32_t kp_linesearch_buffer(kp_context* ctx, const kp_problem* pr, void* ws, do
   return KP_OK;
 }
 
+
+// Dense operator coefficients (kp_batch.coeff_rot != NULL): the engine works in the
+// eigenbasis of c, so the gradient part of the seeds is rotated in once per call,
+// seeds'[1..d] = Q^T seeds[1..d] (into the workspace), and the rotated batch is used.
+int rotated_batch(Ctx& c, const kp_batch* bt, kp_batch& tmp, const kp_batch*& use) {
+  use = bt;
+  if (!bt || !bt->coeff_rot) return KP_OK;
+  if (bt->quad) return KP_ERR_INVALID;  // quadratic-in-grad residuals need coordinate rows
+  const Plan& P = c.P;
+  c.rot = bt->coeff_rot;
+  tmp = *bt;
+  if (P.N > 0 && bt->seeds) {
+    double* s = c.at(P.o_seeds_eff);
+    KP_CUDA_TRY(cudaMemcpyAsync(s, bt->seeds, sizeof(double) * P.N * P.S, cudaMemcpyDeviceToDevice,
+                                c.s));
+    launch_rotate_rows(s + 1, P.S, P.N, P.d, bt->coeff_rot, 1, c.s);
+    tmp.seeds = s;
+  }
+  use = &tmp;
+  return KP_OK;
+}
+
 #define KP_PHASE_PROLOGUE                                            \
   Plan P;                                                            \
   KP_TRY(prepare(ctx, prob, P, ws_bytes));                           \
@@ -1229,6 +1280,9 @@ int32_t kp_kfac_phase_accumulate(kp_context* ctx, const kp_problem* prob,
                                  kp_step_out* out, void* ws, size_t ws_bytes, void* stream) {
   KP_PHASE_PROLOGUE
   if (!bt) return KP_ERR_INVALID;
+  kp_batch bt_rot;
+  const kp_batch* bt_in = bt;
+  KP_TRY(rotated_batch(c, bt_in, bt_rot, bt));
   KP_CUDA_TRY(cudaMemsetAsync(out->status, 0, sizeof(int32_t), c.s));
   KP_TRY(phase_accumulate(c, cfg, st, bt));
   KP_CUDA_TRY(cudaGetLastError());
@@ -1249,6 +1303,9 @@ int32_t kp_kfac_phase_linesearch(kp_context* ctx, const kp_problem* prob,
                                  kp_step_out* out, void* ws, size_t ws_bytes, void* stream) {
   KP_PHASE_PROLOGUE
   if (!bt) return KP_ERR_INVALID;
+  kp_batch bt_rot;
+  const kp_batch* bt_in = bt;
+  KP_TRY(rotated_batch(c, bt_in, bt_rot, bt));
   KP_TRY(phase_linesearch(c, cfg, st, bt));
   KP_CUDA_TRY(cudaGetLastError());
   return KP_OK;
@@ -1268,6 +1325,9 @@ int32_t kp_kfac_step(kp_context* ctx, const kp_problem* prob, const kp_kfac_conf
                      size_t ws_bytes, void* stream) {
   KP_PHASE_PROLOGUE
   if (!bt) return KP_ERR_INVALID;
+  kp_batch bt_rot;
+  const kp_batch* bt_in = bt;
+  KP_TRY(rotated_batch(c, bt_in, bt_rot, bt));
   KP_CUDA_TRY(cudaMemsetAsync(out->status, 0, sizeof(int32_t), c.s));
   KP_TRY(phase_accumulate(c, cfg, st, bt));
   KP_TRY(phase_precondition(c, cfg, st, out));
@@ -1292,6 +1352,9 @@ int32_t kp_kfac_star_phase_gvp(kp_context* ctx, const kp_problem* prob, const kp
                                size_t ws_bytes, void* stream) {
   KP_PHASE_PROLOGUE
   if (!bt) return KP_ERR_INVALID;
+  kp_batch bt_rot;
+  const kp_batch* bt_in = bt;
+  KP_TRY(rotated_batch(c, bt_in, bt_rot, bt));
   KP_TRY(phase_star_gvp(c, cfg, st, bt));
   KP_CUDA_TRY(cudaGetLastError());
   return KP_OK;
@@ -1311,12 +1374,91 @@ int32_t kp_kfac_star_step(kp_context* ctx, const kp_problem* prob, const kp_kfac
                           size_t ws_bytes, void* stream) {
   KP_PHASE_PROLOGUE
   if (!bt) return KP_ERR_INVALID;
+  kp_batch bt_rot;
+  const kp_batch* bt_in = bt;
+  KP_TRY(rotated_batch(c, bt_in, bt_rot, bt));
   KP_CUDA_TRY(cudaMemsetAsync(out->status, 0, sizeof(int32_t), c.s));
   KP_TRY(phase_accumulate(c, cfg, st, bt));
   KP_TRY(phase_precondition(c, cfg, st, out));
   KP_TRY(phase_star_gvp(c, cfg, st, bt));
   KP_TRY(phase_star_update(c, cfg, st, out));
   KP_CUDA_TRY(cudaGetLastError());
+  return KP_OK;
+}
+
+
+// Whole step (KFAC or KFAC*) replayed from a CUDA graph captured on first use.  Only when
+// every layer's Kronecker solve runs on the device (no host-blocking cuSOLVER call) and
+// profiling is off; otherwise identical to kp_kfac_step / kp_kfac_star_step.  The graph is
+// keyed on every argument (pointers and configuration values are baked into the nodes).
+int32_t kp_kfac_step_graphed(kp_context* ctx, const kp_problem* prob, const kp_kfac_config* cfg,
+                             kp_state* st, const kp_batch* bt, kp_step_out* out, void* ws,
+                             size_t ws_bytes, void* stream, int32_t star) {
+  auto plain = [&]() {
+    return star ? kp_kfac_star_step(ctx, prob, cfg, st, bt, out, ws, ws_bytes, stream)
+                : kp_kfac_step(ctx, prob, cfg, st, bt, out, ws, ws_bytes, stream);
+  };
+  if (!ctx || !prob || !cfg || !st || !bt || !out) return KP_ERR_INVALID;
+  Plan P;
+  KP_TRY(prepare(ctx, prob, P, ws_bytes));
+  bool capturable = !ctx->profile;
+  for (int l = 0; l < P.L; ++l) capturable &= std::max(P.p[l], P.q[l]) <= small_eig_max_n();
+  if (!capturable) return plain();
+  std::vector<unsigned char> key;
+  auto put = [&](const void* p, size_t n) {
+    const unsigned char* b = static_cast<const unsigned char*>(p);
+    key.insert(key.end(), b, b + n);
+  };
+  put(prob, sizeof(*prob));
+  put(cfg, sizeof(*cfg));
+  put(st, sizeof(*st));
+  put(bt, sizeof(*bt));
+  put(out, sizeof(*out));
+  put(&ws, sizeof(ws));
+  put(&ws_bytes, sizeof(ws_bytes));
+  put(&star, sizeof(star));
+  cudaStream_t caller = (cudaStream_t)stream;
+  if (!ctx->cap_stream) {
+    KP_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+    KP_CUDA_TRY(cudaEventCreateWithFlags(&ctx->cap_in, cudaEventDisableTiming));
+    KP_CUDA_TRY(cudaEventCreateWithFlags(&ctx->cap_out, cudaEventDisableTiming));
+  }
+  if (!ctx->graph_exec || key != ctx->graph_key) {
+    if (ctx->graph_exec) {
+      cudaGraphExecDestroy(ctx->graph_exec);
+      ctx->graph_exec = nullptr;
+    }
+    // one uncaptured step first: lazy one-time setup (function attributes, tensor maps)
+    // must not happen inside the capture
+    KP_TRY(plain());
+    KP_CUDA_TRY(cudaEventRecord(ctx->cap_in, caller));
+    KP_CUDA_TRY(cudaStreamWaitEvent(ctx->cap_stream, ctx->cap_in, 0));
+    KP_CUDA_TRY(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeThreadLocal));
+    const int rc = star ? kp_kfac_star_step(ctx, prob, cfg, st, bt, out, ws, ws_bytes, ctx->cap_stream)
+                        : kp_kfac_step(ctx, prob, cfg, st, bt, out, ws, ws_bytes, ctx->cap_stream);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(ctx->cap_stream, &graph);
+    if (rc != KP_OK || ce != cudaSuccess || !graph) {
+      if (graph) cudaGraphDestroy(graph);
+      cudaGetLastError();
+      return rc != KP_OK ? rc : KP_ERR_CUDA;
+    }
+    const cudaError_t ie = cudaGraphInstantiate(&ctx->graph_exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) {
+      ctx->graph_exec = nullptr;
+      return KP_ERR_CUDA;
+    }
+    ctx->graph_key = key;
+    KP_CUDA_TRY(cudaEventRecord(ctx->cap_out, ctx->cap_stream));
+    KP_CUDA_TRY(cudaStreamWaitEvent(caller, ctx->cap_out, 0));
+    return KP_OK;  // the uncaptured step above was this call's step
+  }
+  KP_CUDA_TRY(cudaEventRecord(ctx->cap_in, caller));
+  KP_CUDA_TRY(cudaStreamWaitEvent(ctx->cap_stream, ctx->cap_in, 0));
+  KP_CUDA_TRY(cudaGraphLaunch(ctx->graph_exec, ctx->cap_stream));
+  KP_CUDA_TRY(cudaEventRecord(ctx->cap_out, ctx->cap_stream));
+  KP_CUDA_TRY(cudaStreamWaitEvent(caller, ctx->cap_out, 0));
   return KP_OK;
 }
 
@@ -1330,7 +1472,7 @@ int32_t kp_taylor_forward(kp_context* ctx, const kp_problem* prob, const double*
   const TaylorDims tdi{P.S, P.d, true};
   launch_candidate(theta, nullptr, 0, nullptr, P.D, P.wp, c.at(P.o_wpad), c.s);
   if (P.L >= 2)
-    launch_prep_layer0(theta, P.d, P.h[1], bt->coeff_diag, c.at(P.o_w0t), c.at(P.o_q0), c.s);
+    launch_prep_layer0(theta, P.d, P.h[1], bt->coeff_diag, bt->coeff_rot, c.at(P.o_w0t), c.at(P.o_q0), c.s);
   for (int64_t n0 = 0; n0 < P.N; n0 += P.Nc) {
     const int64_t nc = std::min(P.Nc, P.N - n0);
     ResidualIn ri{nullptr, nullptr, nullptr};
@@ -1338,6 +1480,8 @@ int32_t kp_taylor_forward(kp_context* ctx, const kp_problem* prob, const double*
     forward_loss(c, theta, c.at(P.o_wpad), bt->x_int + n0 * P.d, nc, tdi, bt->coeff_diag, c.at(P.o_ping),
                  c.at(P.o_pong), ri, nullptr, u);
     launch_split_u(u, nc, P.d, value + n0, gradient + n0 * P.d, op + n0, c.s);
+    // dense coefficients: the derivative rows are along Q[:, k]; grad u = Q g'
+    if (bt->coeff_rot) launch_rotate_rows(gradient + n0 * P.d, P.d, nc, P.d, bt->coeff_rot, 0, c.s);
   }
   KP_CUDA_TRY(cudaGetLastError());
   return KP_OK;
@@ -1366,11 +1510,14 @@ int32_t kp_evaluate_losses(kp_context* ctx, const kp_problem* prob, const double
   KP_TRY(prepare(ctx, prob, P, ws_bytes));
   if (!theta || !bt || !losses) return KP_ERR_INVALID;
   Ctx c{ctx, P, static_cast<double*>(ws), (cudaStream_t)stream};
+  kp_batch bt_rot;
+  const kp_batch* bt_in = bt;
+  KP_TRY(rotated_batch(c, bt_in, bt_rot, bt));
   const TaylorDims tdi{P.S, P.d, true};
   const TaylorDims tdb{1, 0, false};
   launch_candidate(theta, nullptr, 0, nullptr, P.D, P.wp, c.at(P.o_wpad), c.s);
   if (P.L >= 2)
-    launch_prep_layer0(theta, P.d, P.h[1], bt->coeff_diag, c.at(P.o_w0t), c.at(P.o_q0), c.s);
+    launch_prep_layer0(theta, P.d, P.h[1], bt->coeff_diag, bt->coeff_rot, c.at(P.o_w0t), c.at(P.o_q0), c.s);
   for (int64_t n0 = 0; n0 < P.N; n0 += P.Nc) {
     const int64_t nc = std::min(P.Nc, P.N - n0);
     ResidualIn ri{bt->r0 + n0, bt->seeds + n0 * P.S, nullptr};

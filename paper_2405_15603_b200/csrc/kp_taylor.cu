@@ -24,29 +24,84 @@ static inline unsigned grid_for(int64_t n, int threads) {
 // W0^T (coalesced across units) and q_j = sum_i (W0[j,i] c_i) W0[j,i] prepared once per
 // parameter set (k_prep_layer0).
 
+// Dense coefficients c = Q diag(lambda) Q^T: the derivative rows are taken along the
+// eigenvectors, Z0 = [x; Q^T; 0], so the layer-0 derivative rows become (W0 Q)[:, k] and
+// every quadratic form sum_ij c_ij g_i g_j is the diagonal sum_k lambda_k g'_k^2.  The
+// factors, gradient and Gramian contractions sum over rows and are invariant under this
+// orthogonal change of rows; only the seeds (rotated in) and the layer-0 weight gradient
+// and output gradient (rotated back) see Q.
 __global__ void k_prep_layer0(const double* __restrict__ th0, int d, int h1,
-                              const double* __restrict__ cdiag, double* __restrict__ w0t,
-                              double* __restrict__ q0, int64_t D) {
+                              const double* __restrict__ cdiag, const double* __restrict__ rot,
+                              double* __restrict__ w0t, double* __restrict__ q0, int64_t D) {
   th0 += (int64_t)blockIdx.y * D;
   w0t += (int64_t)blockIdx.y * d * h1;
   q0 += (int64_t)blockIdx.y * h1;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < h1; j += gridDim.x * blockDim.x) {
     const double* w = th0 + (int64_t)j * (d + 1);
     double q = 0.0;
-    for (int i = 0; i < d; ++i) {
-      const double g = w[i];
-      w0t[(int64_t)i * h1 + j] = g;
-      q += (g * cdiag[i]) * g;
+    for (int k = 0; k < d; ++k) {
+      double g;
+      if (rot) {
+        g = 0.0;
+        for (int i = 0; i < d; ++i) g = fma(w[i], rot[(int64_t)i * d + k], g);
+      } else {
+        g = w[k];
+      }
+      w0t[(int64_t)k * h1 + j] = g;
+      q += (g * cdiag[k]) * g;
     }
     q0[j] = q;
   }
 }
 
-void launch_prep_layer0(const double* theta0, int d, int h1, const double* cdiag, double* w0t,
-                        double* q0, cudaStream_t s, int batch, int64_t D) {
+void launch_prep_layer0(const double* theta0, int d, int h1, const double* cdiag, const double* rot,
+                        double* w0t, double* q0, cudaStream_t s, int batch, int64_t D) {
   count_launch();
   k_prep_layer0<<<dim3((unsigned)ceil_div(h1, 128), (unsigned)batch), 128, 0, s>>>(
-      theta0, d, h1, cdiag, w0t, q0, D);
+      theta0, d, h1, cdiag, rot, w0t, q0, D);
+}
+
+__global__ void k_rotate_rows(double* __restrict__ X, int64_t stride, int64_t n, int d,
+                              const double* __restrict__ Q, int transpose) {
+  extern __shared__ double row[];
+  for (int64_t r = blockIdx.x; r < n; r += gridDim.x) {
+    double* x = X + r * stride;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) row[i] = x[i];
+    __syncthreads();
+    for (int k = threadIdx.x; k < d; k += blockDim.x) {
+      double acc = 0.0;
+      if (transpose)
+        for (int i = 0; i < d; ++i) acc = fma(Q[(int64_t)i * d + k], row[i], acc);
+      else
+        for (int i = 0; i < d; ++i) acc = fma(Q[(int64_t)k * d + i], row[i], acc);
+      x[k] = acc;
+    }
+    __syncthreads();
+  }
+}
+
+void launch_rotate_rows(double* X, int64_t stride, int64_t n, int d, const double* Q, int transpose,
+                        cudaStream_t s) {
+  if (n <= 0 || d <= 0) return;
+  count_launch();
+  const unsigned blocks = (unsigned)std::min<int64_t>(n, 148 * 16);
+  k_rotate_rows<<<blocks, 128, sizeof(double) * d, s>>>(X, stride, n, d, Q, transpose);
+}
+
+__global__ void k_rot_accum(const double* __restrict__ T, int q, int d, const double* __restrict__ Q,
+                            double* __restrict__ out, int64_t ldo) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)q * d) return;
+  const int j = (int)(e / d), i = (int)(e % d);
+  double acc = 0.0;
+  for (int k = 0; k < d; ++k) acc = fma(T[(int64_t)j * d + k], Q[(int64_t)i * d + k], acc);
+  out[(int64_t)j * ldo + i] += acc;
+}
+
+void launch_rot_accum(const double* T, int q, int d, const double* Q, double* out, int64_t ldo,
+                      cudaStream_t s) {
+  count_launch();
+  k_rot_accum<<<(unsigned)ceil_div((int64_t)q * d, 256), 256, 0, s>>>(T, q, d, Q, out, ldo);
 }
 
 // One warp per (sample, 32-unit tile): lane j writes unit j of every one of the sample's

@@ -23,7 +23,7 @@ import numpy as np
 
 from .engine import KfacEngine, raise_for_status
 from .pde import residual_terms
-from .taylor import coeff_diagonal
+from .taylor import coeff_matrix
 
 
 def shard_bounds(n: int, rank: int, world: int):
@@ -98,7 +98,7 @@ def upload_shard(eng, batch, problem, rank: int, world: int):
     r0, seeds, quad = residual_terms(problem, x)
     eng.set_batch(x, r0, seeds, np.asarray(batch.boundary, dtype=np.float64)[b0:b1],
                   np.asarray(batch.boundary_targets, dtype=np.float64)[b0:b1],
-                  coeff_diagonal(problem.coeffs), quad)
+                  coeff_matrix(problem.coeffs), quad)
 
 
 def torch_all_reduce(group=None):

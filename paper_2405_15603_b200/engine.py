@@ -21,6 +21,7 @@ import numpy as np
 
 from . import _capi
 from .linalg import NotPositiveSemidefiniteError
+from .taylor import coeff_spectrum
 
 
 class LineSearchError(RuntimeError):
@@ -131,6 +132,8 @@ class KfacEngine:
         self.targets = z(self.n_boundary)
         self.cdiag = z(self.d)
         self.quad = None  # allocated on first non-affine batch
+        self.rot = None   # eigenvectors of a dense coefficient matrix (first use)
+        self._coeff_key = self._lam = self._rot_host = None
         self.batch = _capi.kp_batch(_ptr(self.x_int), _ptr(self.r0), _ptr(self.seeds),
                                     _ptr(self.x_bnd), _ptr(self.targets), _ptr(self.cdiag), 0)
         self.prob = _capi.kp_problem()
@@ -186,9 +189,31 @@ class KfacEngine:
 
     def set_batch(self, x_int, r0, seeds, x_bnd, targets, cdiag, quad=None):
         """Upload one batch; ``quad`` (N x d) makes the residual quadratic in grad u
-        (pde.residual_terms), None keeps it affine."""
+        (pde.residual_terms), None keeps it affine.  ``cdiag`` is the operator's
+        coefficient diagonal (d,) or its full symmetric matrix (d, d); a non-diagonal
+        matrix switches the engine to its eigenbasis (taylor.coeff_spectrum)."""
         if x_int.shape != (self.n_interior, self.d) or x_bnd.shape != (self.n_boundary, self.d):
             raise ValueError("batch shape does not match the engine")
+        cmat = np.asarray(cdiag, dtype=np.float64)
+        key = (cmat.shape, cmat.tobytes())
+        if key != self._coeff_key:
+            lam, rot = coeff_spectrum(cmat)
+            if lam.shape != (self.d,):
+                raise ValueError(f"operator dim {lam.size} does not match input dim {self.d}")
+            self._coeff_key, self._lam, self._rot_host = key, lam, rot
+            if rot is not None:
+                if self.rot is None:
+                    self.rot = self.torch.zeros(self.d * self.d, dtype=self.torch.float64,
+                                                device=self.device)
+                self._h2d(self.rot, rot)
+        cdiag = self._lam
+        if self._rot_host is not None:
+            if quad is not None:
+                raise NotImplementedError(
+                    "a residual quadratic in grad u with non-diagonal operator coefficients")
+            self.batch.coeff_rot = _ptr(self.rot)
+        else:
+            self.batch.coeff_rot = 0
         if quad is None:
             self.batch.quad = 0
         else:
@@ -237,9 +262,14 @@ class KfacEngine:
                 C.byref(self.batch), C.byref(self.out), C.c_void_p(_ptr(self.ws)),
                 C.c_size_t(self.ws_bytes), C.c_void_p(self.stream.cuda_stream))
 
+    use_graph = True  # replay small (device-solver-only) steps from a captured CUDA graph
+
     def launch_step(self):
         """Enqueue one whole KFAC step on the current stream (no host sync)."""
-        raise_for_status(self.lib.kp_kfac_step(*self._args()), "kp_kfac_step")
+        if self.use_graph:
+            raise_for_status(self.lib.kp_kfac_step_graphed(*self._args(), 0), "kp_kfac_step")
+        else:
+            raise_for_status(self.lib.kp_kfac_step(*self._args()), "kp_kfac_step")
 
     def finish_step(self):
         """Synchronise, read StepInfo scalars and raise on a device-side failure."""
@@ -256,7 +286,10 @@ class KfacEngine:
 
     def launch_star_step(self):
         """Enqueue one KFAC* step (src/optim.py:266-320) on the current stream."""
-        raise_for_status(self.lib.kp_kfac_star_step(*self._args()), "kp_kfac_star_step")
+        if self.use_graph:
+            raise_for_status(self.lib.kp_kfac_step_graphed(*self._args(), 1), "kp_kfac_star_step")
+        else:
+            raise_for_status(self.lib.kp_kfac_star_step(*self._args()), "kp_kfac_star_step")
 
     def star_step(self):
         self.launch_star_step()

@@ -290,7 +290,7 @@ def _initial_losses(state, batch, problem):
     builds the engine the first optimizer_step reuses)."""
     from .optim import _engine_for
     from .pde import residual_terms
-    from .taylor import coeff_diagonal
+    from .taylor import coeff_matrix
 
     params = state.params
     widths = (params.weights[0].shape[1],) + tuple(w.shape[0] for w in params.weights)
@@ -298,5 +298,5 @@ def _initial_losses(state, batch, problem):
     r0, seeds, quad = residual_terms(problem, x)
     eng = _engine_for(state, batch, widths)
     eng.set_batch(x, r0, seeds, np.asarray(batch.boundary, np.float64),
-                  np.asarray(batch.boundary_targets, np.float64), coeff_diagonal(problem.coeffs), quad)
+                  np.asarray(batch.boundary_targets, np.float64), coeff_matrix(problem.coeffs), quad)
     return eng.evaluate_losses()

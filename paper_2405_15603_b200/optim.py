@@ -30,7 +30,7 @@ from . import network
 from .curvature import KfacState
 from .engine import KfacEngine, LineSearchError, pack_mats
 from .pde import residual_terms
-from .taylor import coeff_diagonal
+from .taylor import coeff_matrix
 
 __all__ = [
     "OptimizerConfig",
@@ -199,7 +199,7 @@ def _sync_host_edits(state: TrainState, eng: KfacEngine):
 def _kfac_device_step(state: TrainState, batch, problem) -> StepInfo:
     params = state.params
     widths = (params.weights[0].shape[1],) + tuple(w.shape[0] for w in params.weights)
-    cdiag = coeff_diagonal(problem.coeffs)
+    cdiag = coeff_matrix(problem.coeffs)
     x = np.asarray(batch.interior, dtype=np.float64)
     r0, seeds, quad = residual_terms(problem, x)
     eng = _engine_for(state, batch, widths)

@@ -67,12 +67,36 @@ class OperatorCoeffs:
         return cls(c)
 
 
+def coeff_matrix(coeffs) -> np.ndarray:
+    """The symmetric d x d coefficient matrix of any coefficient object with a ``c``."""
+    return np.asarray(coeffs.c, dtype=np.float64)
+
+
+def coeff_spectrum(c):
+    """``(lam, rot)`` with c = rot diag(lam) rot^T for the device engine.
+
+    Diagonal c (every catalog operator, reference pde.py:84-268; the test at
+    taylor.py:56-57) gives ``(diag(c), None)`` and the coordinate derivative rows of
+    the reference.  A dense c (taylor.py:72-75) gives its eigendecomposition: the
+    engine then propagates derivatives along the eigenvectors, where the operator's
+    quadratic form is diagonal.  A 1-D ``c`` is taken as the diagonal.
+    """
+    c = np.asarray(c, dtype=np.float64)
+    if c.ndim == 1:
+        return c.copy(), None
+    if c.ndim != 2 or c.shape[0] != c.shape[1]:
+        raise ValueError(f"coefficients must be square, got shape {c.shape}")
+    diag = np.diagonal(c).copy()
+    if np.array_equal(c, np.diag(diag)):
+        return diag, None
+    lam, rot = np.linalg.eigh(0.5 * (c + c.T))
+    return lam, np.ascontiguousarray(rot)
+
+
 def coeff_diagonal(coeffs) -> np.ndarray:
     """Diagonal of any coefficient object with a ``c`` matrix; raises if not diagonal."""
-    c = np.asarray(coeffs.c, dtype=np.float64)
+    c = coeff_matrix(coeffs)
     diag = np.diagonal(c).copy()
     if not np.array_equal(c, np.diag(diag)):
-        raise NotImplementedError(
-            "device path supports diagonal operator coefficients only "
-            "(every catalog operator is diagonal, reference pde.py:84-199)")
+        raise NotImplementedError("coefficients are not diagonal; use coeff_spectrum")
     return diag

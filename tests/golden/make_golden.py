@@ -56,6 +56,9 @@ PLAN = {
     # reference catalog log-Fokker-Planck (non-affine residual, per-point seeds)
     "lfp": ("lfp", 300, 100, 3),
     "lfp_star": ("lfp", 300, 100, 3),
+    # dense (non-diagonal) operator coefficients (src/taylor.py:72-75)
+    "dense": ("dense", 400, 100, 3),
+    "dense_star": ("dense", 300, 100, 3),
 }
 
 
@@ -63,7 +66,8 @@ def ref_problem(wl):
     """Reference PdeProblem for a workload (catalog where it exists, else rigged)."""
     if wl.problem in ("poisson2d_sin", "log_fokker_planck"):
         return pde.make_problem(wl.problem)
-    if wl.problem == "poisson_cos_sum" and dict(wl.problem_params).get("dim", 5) == 5:
+    if (wl.problem == "poisson_cos_sum" and dict(wl.problem_params).get("dim", 5) == 5
+            and wl.dense_coeffs_seed is None):
         return pde.make_problem("poisson_cos_sum")
     mine = wl.make_problem()
     coeffs = pde.OperatorCoeffs(np.asarray(mine.coeffs.c))
@@ -114,6 +118,13 @@ def main():
         put(out, "in/boundary", batch.boundary)
         put(out, "in/targets", batch.boundary_targets)
         put(out, "in/theta", network.params_to_vec(params))
+        if wl.dense_coeffs_seed is not None:
+            from pinnopt import taylor as ref_taylor
+            out["in/coeffs"] = np.asarray(prob.coeffs.c)
+            _, tout = ref_taylor.taylor_forward(params, batch.interior, prob.coeffs)
+            put(out, "taylor/value", tout.value)
+            put(out, "taylor/gradient", tout.gradient)
+            put(out, "taylor/operator", tout.operator)
         for t in range(1, steps + 1):
             # intermediates of this step, recomputed exactly as kfac_step does (optim.py:237-263)
             ev = optim.evaluate_batch(state.params, batch, prob)

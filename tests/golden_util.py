@@ -5,8 +5,8 @@ import os
 import numpy as np
 
 GOLDEN_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
-NAMES = ("c1", "c2", "c3", "c4", "c5", "c1_momentum", "lfp")
-STAR_NAMES = ("c1_star", "c3_star", "c5_star", "lfp_star")
+NAMES = ("c1", "c2", "c3", "c4", "c5", "c1_momentum", "lfp", "dense")
+STAR_NAMES = ("c1_star", "c3_star", "c5_star", "lfp_star", "dense_star")
 
 
 def load(name):

@@ -20,7 +20,8 @@ from paper_2405_15603_b200.optim import OptimizerConfig, init_train_state, optim
 from paper_2405_15603_b200.pde import make_problem, sample_batch  # noqa: E402
 
 WL_OF = {"c1": "c1", "c2": "c2", "c3": "c3", "c4": "c4", "c5": "c5", "c1_momentum": "c1",
-         "c1_star": "c1", "c3_star": "c3", "c5_star": "c5", "lfp": "lfp", "lfp_star": "lfp"}
+         "c1_star": "c1", "c3_star": "c3", "c5_star": "c5", "lfp": "lfp", "lfp_star": "lfp",
+         "dense": "dense", "dense_star": "dense"}
 
 
 def _theta_colstack(params):
@@ -123,6 +124,55 @@ def test_device_matches_oracle_various_shapes(widths, problem):
     else:
         prob = make_problem(problem)
     _oracle_vs_device(widths, prob, 37, 11, 3, momentum=0.5)
+
+
+def _with_dense_coeffs(prob, seed):
+    """The problem with c replaced by a random dense symmetric matrix (the reference's
+    own dense-coefficient tests: pkg/tests/test_taylor.py:22-24)."""
+    import dataclasses
+    from paper_2405_15603_b200.taylor import OperatorCoeffs
+    r = np.random.default_rng(seed).standard_normal((prob.dim, prob.dim))
+    return dataclasses.replace(prob, coeffs=OperatorCoeffs(0.5 * (r + r.T)))
+
+
+@pytest.mark.parametrize("widths,problem,chunk", [
+    ((2, 1), "poisson2d_sin", None),
+    ((2, 7, 1), "poisson2d_sin", None),
+    ((5, 33, 17, 65, 1), "heat4", None),             # u_t seed: the rotated seed path
+    ((10, 130, 70, 1), "poisson_harmonic_mixed", None),
+    ((5, 40, 24, 1), "heat4", 13),                  # chunked interior
+])
+def test_dense_coefficients_match_oracle(widths, problem, chunk):
+    """Non-diagonal operator coefficients (reference taylor.py:72-75): the device works in
+    the eigenbasis of c; results must match the oracle's dense contraction."""
+    prob = make_problem("heat", spatial_dim=4) if problem == "heat4" else make_problem(problem)
+    _oracle_vs_device(widths, _with_dense_coeffs(prob, 7), 37, 11, 3, momentum=0.5, chunk=chunk)
+
+
+def test_dense_coefficients_taylor_forward_matches_reference():
+    from paper_2405_15603_b200.engine import KfacEngine
+    from paper_2405_15603_b200.pde import residual_terms
+    g = load("dense")
+    wl = cfgs.WORKLOADS["dense"]
+    prob, params, batch = wl.build(0, int(g["n_interior"]), int(g["n_boundary"]))
+    eng = KfacEngine(wl.widths, batch.interior.shape[0], batch.boundary.shape[0], ema=0.95,
+                     damping=1e-3, momentum=0.0)
+    eng.load_params(params)
+    r0, seeds, _ = residual_terms(prob, batch.interior)
+    eng.set_batch(batch.interior, r0, seeds, batch.boundary, batch.boundary_targets, prob.coeffs.c)
+    u, gu, lu = eng.taylor_forward()
+    for key, arr in (("value", u), ("gradient", gu), ("operator", lu)):
+        assert compare(g, "taylor/" + key, arr, 1e-12) <= 1e-12, key
+    eng.close()
+
+
+def test_dense_coefficients_with_quadratic_residual_rejected():
+    prob = _with_dense_coeffs(make_problem("log_fokker_planck"), 1)
+    params = init_params(Architecture((10, 8, 1)), 0)
+    batch = sample_batch(prob, 10, 5, 0)
+    state = init_train_state(params, OptimizerConfig(kind="kfac", damping=1e-3))
+    with pytest.raises(NotImplementedError):
+        optimizer_step(state, batch, prob)
 
 
 def test_chunked_interior_matches_unchunked():

@@ -15,7 +15,8 @@ from paper_2405_15603_b200 import configs as cfgs
 from paper_2405_15603_b200.network import params_to_vec
 
 WL_OF = {"c1": "c1", "c2": "c2", "c3": "c3", "c4": "c4", "c5": "c5", "c1_momentum": "c1",
-         "c1_star": "c1", "c3_star": "c3", "c5_star": "c5", "lfp": "lfp", "lfp_star": "lfp"}
+         "c1_star": "c1", "c3_star": "c3", "c5_star": "c5", "lfp": "lfp", "lfp_star": "lfp",
+         "dense": "dense", "dense_star": "dense"}
 
 
 def build(name):
@@ -32,6 +33,18 @@ def test_inputs_bit_identical_to_reference(name):
     assert compare(g, "in/boundary", batch.boundary, 0) == 0.0
     assert compare(g, "in/targets", batch.boundary_targets, 0) == 0.0
     assert compare(g, "in/theta", params_to_vec(params), 0) == 0.0
+    if "in/coeffs" in g:
+        assert np.array_equal(np.asarray(prob.coeffs.c), g["in/coeffs"])
+
+
+def test_oracle_dense_coefficient_taylor_forward():
+    # the non-diagonal branch of OperatorCoeffs.apply (reference taylor.py:72-75)
+    g, wl, prob, params, batch = build("dense")
+    _, _, (u, gu, lu) = orc.taylor_forward(params.weights, params.biases, batch.interior,
+                                           orc.coeffs_of(prob))
+    assert orc.coeffs_of(prob).ndim == 2
+    for key, arr in (("value", u), ("gradient", gu), ("operator", lu)):
+        assert compare(g, "taylor/" + key, arr, 1e-12) <= 1e-12
 
 
 @pytest.mark.parametrize("name", NAMES)
