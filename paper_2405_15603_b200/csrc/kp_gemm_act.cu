@@ -32,7 +32,7 @@ bool make_tma_map_2d(CUtensorMap* m, const double* base, uint64_t rows, uint64_t
 
 namespace {
 
-constexpr int BN = 128, ROWS_MAX = 128, CPITCH = BN + 4;
+constexpr int BN_MAX = 128, ROWS_MAX = 128;
 
 __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* map, int x, int y,
                                       uint64_t* bar) {
@@ -48,11 +48,12 @@ __device__ __forceinline__ int sigma8(int g) { return (g >> 1) + ((g & 1) << 2);
 // NW warps, each owning BN / NW output units and all TM m8 tiles.  NW = 4 keeps the
 // per-CTA footprint small enough for two co-resident CTAs per SM (one's epilogue
 // overlaps the other's DMMA loop); NW = 8 serves the 15-16 tile shapes.
-template <int BK, int STAGES, int MODE, int TM, int NW>
+template <int BK, int STAGES, int MODE, int TM, int NW, int BN>
 __global__ void __launch_bounds__(NW * 32, 8 / NW)
     k_gemm_act(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                GemmAct g, int tiles_n, int box_rows) {
   constexpr int NWARP = NW;
+  constexpr int CPITCH = BN + 4;
   constexpr int WCOLS = BN / NW, TNW = WCOLS / 8;  // units and n8 tiles per warp
   constexpr int SLABS = BK / 16;
   constexpr int AROWS = TM * 8;
@@ -208,8 +209,9 @@ __global__ void __launch_bounds__(NW * 32, 8 / NW)
   }
 }
 
-template <int MODE, int TM, int NW, int BK, int STAGES>
+template <int MODE, int TM, int NW, int BK, int STAGES, int BN = BN_MAX>
 bool run_act(const GemmAct& g, int box_rows, cudaStream_t s) {
+  constexpr int CPITCH = BN + 4;
   CUtensorMap ma, mb;
   const int64_t M = g.n_samples * g.S * g.batch;
   if (g.K % BK) return false;
@@ -219,7 +221,7 @@ bool run_act(const GemmAct& g, int box_rows, cudaStream_t s) {
   const size_t pipe = (size_t)STAGES * (TM * 8 + BN) * BK * sizeof(double) + 2 * STAGES * 8;
   const size_t cst = (size_t)TM * 8 * CPITCH * sizeof(double);
   const size_t smem = std::max(pipe, cst) + 1024;
-  auto kern = k_gemm_act<BK, STAGES, MODE, TM, NW>;
+  auto kern = k_gemm_act<BK, STAGES, MODE, TM, NW, BN>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -233,12 +235,18 @@ bool run_act(const GemmAct& g, int box_rows, cudaStream_t s) {
 }
 
 // tile shapes up to 13 m8 tiles: 4 warps, BK 16, 3 stages -> ~111 KB, two CTAs per SM;
-// 14-16 tiles: 8 warps, BK 32, 3 stages (one CTA per SM).
+// 14-16 tiles: 8 warps, BK 32, 3 stages (one CTA per SM).  Narrow layers (N <= 64, the
+// small-d configs: many samples per tile, short K) use 64-unit tiles with 4 warps so two
+// or more CTAs share an SM and no tensor work is spent on padding columns.
 template <int MODE, int TM>
 bool run_act_tm(const GemmAct& g, int box_rows, cudaStream_t s) {
   if constexpr (TM <= 13) {
     return run_act<MODE, TM, 4, 16, 3>(g, box_rows, s);
   } else {
+    if (g.N <= 64) {
+      if (g.K % 32 == 0 && g.K <= 64) return run_act<MODE, TM, 4, 32, 2, 64>(g, box_rows, s);
+      return run_act<MODE, TM, 4, 16, 3, 64>(g, box_rows, s);
+    }
     if (g.K % 32 == 0) return run_act<MODE, TM, 8, 32, 3>(g, box_rows, s);
     return run_act<MODE, TM, 8, 16, 6>(g, box_rows, s);
   }
