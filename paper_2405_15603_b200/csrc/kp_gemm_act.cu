@@ -243,11 +243,14 @@ bool run_act_tm(const GemmAct& g, int box_rows, cudaStream_t s) {
   if constexpr (TM <= 13) {
     return run_act<MODE, TM, 4, 16, 3>(g, box_rows, s);
   } else {
+    // (15 m8 tiles with BK 32 exceed the register file: BK 16 only)
     if (g.N <= 64) {
-      if (g.K % 32 == 0 && g.K <= 64) return run_act<MODE, TM, 4, 32, 2, 64>(g, box_rows, s);
+      if constexpr (TM != 15)
+        if (g.K % 32 == 0 && g.K <= 64) return run_act<MODE, TM, 4, 32, 2, 64>(g, box_rows, s);
       return run_act<MODE, TM, 4, 16, 3, 64>(g, box_rows, s);
     }
-    if (g.K % 32 == 0) return run_act<MODE, TM, 8, 32, 3>(g, box_rows, s);
+    if constexpr (TM != 15)
+      if (g.K % 32 == 0) return run_act<MODE, TM, 8, 32, 3>(g, box_rows, s);
     return run_act<MODE, TM, 8, 16, 6>(g, box_rows, s);
   }
 }

@@ -323,3 +323,28 @@ def test_kfac_star_chunked_matches_single_chunk():
     for a, b in zip(r1, r2):
         assert abs(a[0] - b[0]) <= 1e-10 * abs(b[0]) and abs(a[1] - b[1]) <= 1e-10 * max(abs(b[1]), 1)
     assert np.max(np.abs(t1 - t2)) <= 1e-10 * np.max(np.abs(t2))
+
+
+@pytest.mark.parametrize("star", [False, True], ids=["kfac", "kfac_star"])
+def test_graph_replay_is_bit_identical(star):
+    """kp_kfac_step_graphed (whole step replayed from a captured CUDA graph) == the plain
+    call, bit for bit, over several steps (the graph is captured on the second step)."""
+    from paper_2405_15603_b200.dist import make_rank_engine
+    wl = cfgs.WORKLOADS["c3"]
+    prob, params, batch = wl.build(0, 300, 80)
+    runs = []
+    for graph in (False, True):
+        eng = make_rank_engine(wl.widths, batch, prob, 0, 1, ema=wl.ema, damping=wl.damping,
+                               momentum=0.3)
+        eng.use_graph = graph
+        eng.load_params(params)
+        eng.init_factors(True)
+        fn = eng.star_step if star else eng.step
+        infos = [fn() for _ in range(4)]
+        runs.append((infos, eng.theta_numpy(), eng.factor_lists()))
+        eng.close()
+    assert runs[0][0] == runs[1][0]
+    assert np.array_equal(runs[0][1], runs[1][1])
+    for fa, fb in zip(runs[0][2], runs[1][2]):
+        for a, b in zip(fa, fb):
+            assert np.array_equal(a, b)
