@@ -208,7 +208,10 @@ __global__ void __launch_bounds__(EIG_THREADS) k_gen_eig_small(const SmallEigJob
     }
   }
   __syncthreads();
-  for (int e = tid; e < n * n; e += EIG_THREADS) jb.t[e] = C[(e / n) * ld + e % n];
+  for (int e = tid; e < n * n; e += EIG_THREADS) {
+    const int i = e / n, j = e % n;
+    jb.t[jb.col_major ? j * n + i : e] = C[i * ld + j];
+  }
   if (tid == 0 && jb.info) *jb.info = 0;
   // PSD check on the generalised eigenvalues (src/linalg.py:79-83, 165-166)
   if (tid == 0) {

@@ -255,6 +255,7 @@ struct SmallEigJob {
   double* t;         // n x n row-major, column k = generalised eigenvector k
   double* lam;       // n eigenvalues
   int* info;
+  int col_major = 0;  // 1: write t column-major (the cuSOLVER layout, for a cuBLAS combine)
 };
 struct SmallEigJobs {
   SmallEigJob job[32];

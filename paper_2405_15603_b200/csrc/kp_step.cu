@@ -804,39 +804,48 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
   // The 2L generalised eigenproblems are independent: fan out over side streams (A and B
   // factor pair of layer l on streams 2l and 2l+1), combine on 2l, join back.
   kp_context* ctx = c.ctx;
+  // Factor pairs up to small_eig_max_n(): on-device Cholesky + Jacobi solver, all of them in
+  // one launch on the main stream (plus one combine launch for the layers whose two pairs are
+  // both small).  Larger pairs: cuSOLVER sygvd, which blocks the calling host thread, so each
+  // is issued from its own host thread (own handle + stream); a layer with a large pair is
+  // combined with cuBLAS on its side stream.
+  auto pair_small = [&](int l, int k) { return (k == 0 ? P.p[l] : P.q[l]) <= small_eig_max_n(); };
   bool any_big = false;
-  for (int l = 0; l < P.L; ++l) any_big |= std::max(P.p[l], P.q[l]) > small_eig_max_n();
-  cudaEvent_t ready = nullptr;
+  for (int l = 0; l < P.L; ++l) any_big |= !pair_small(l, 0) || !pair_small(l, 1);
+  cudaEvent_t ready = nullptr, small_done = nullptr;
   if (any_big) {
-    KP_TRY(ensure_side_streams(ctx, 2 * P.L + 1));
+    KP_TRY(ensure_side_streams(ctx, 2 * P.L + 2));
     ready = ctx->side_ev[2 * P.L];
+    small_done = ctx->side_ev[2 * P.L + 1];
     KP_CUDA_TRY(cudaEventRecord(ready, c.s));
   }
-  // Small layers (both factors <= small_eig_max_n()): on-device Jacobi solver, all of them in
-  // two launches on the main stream.  Larger layers: cuSOLVER sygvd, which blocks the calling
-  // host thread, so each factor-pair solve is issued from its own host thread (own handle +
-  // stream) to let the solves overlap on the GPU.
-  std::vector<int> big;
+  std::vector<int> big;  // layers with at least one cuSOLVER pair
   {
     SmallEigJobs ej{};
     SmallCombineJobs cj{};
     int ne = 0, nc = 0, maxn = 1;
     for (int l = 0; l < P.L; ++l) {
-      if (std::max(P.p[l], P.q[l]) > small_eig_max_n()) {
-        big.push_back(l);
-        continue;
-      }
       int* info = reinterpret_cast<int*>(c.at(P.k_info[l]));
-      ej.job[ne++] = SmallEigJob{P.p[l], st->a_int + P.fa[l], st->a_bnd + P.fa[l], lam,
-                                 c.at(P.k_A1[l]), c.at(P.k_la[l]), info};
-      ej.job[ne++] = SmallEigJob{P.q[l], st->b_int + P.fb[l], st->b_bnd + P.fb[l], lam,
-                                 c.at(P.k_B1[l]), c.at(P.k_lb[l]), info + 1};
-      cj.job[nc++] = SmallCombineJob{P.p[l], P.q[l], grad + P.th[l], c.at(P.k_A1[l]),
-                                     c.at(P.k_B1[l]), c.at(P.k_la[l]), c.at(P.k_lb[l]),
-                                     c.at(P.k_T1[l]), c.at(P.k_T2[l]), delta + P.th[l], -1.0};
-      maxn = std::max(maxn, std::max(P.p[l], P.q[l]));
+      const bool sa = pair_small(l, 0), sb = pair_small(l, 1);
+      if (sa) {
+        ej.job[ne++] = SmallEigJob{P.p[l], st->a_int + P.fa[l], st->a_bnd + P.fa[l], lam,
+                                   c.at(P.k_A1[l]), c.at(P.k_la[l]), info, sb ? 0 : 1};
+        maxn = std::max(maxn, P.p[l]);
+      }
+      if (sb) {
+        ej.job[ne++] = SmallEigJob{P.q[l], st->b_int + P.fb[l], st->b_bnd + P.fb[l], lam,
+                                   c.at(P.k_B1[l]), c.at(P.k_lb[l]), info + 1, sa ? 0 : 1};
+        maxn = std::max(maxn, P.q[l]);
+      }
+      if (sa && sb)
+        cj.job[nc++] = SmallCombineJob{P.p[l], P.q[l], grad + P.th[l], c.at(P.k_A1[l]),
+                                       c.at(P.k_B1[l]), c.at(P.k_la[l]), c.at(P.k_lb[l]),
+                                       c.at(P.k_T1[l]), c.at(P.k_T2[l]), delta + P.th[l], -1.0};
+      else
+        big.push_back(l);
     }
     launch_gen_eig_small(ej, ne, maxn, out->status, c.s);
+    if (any_big) KP_CUDA_TRY(cudaEventRecord(small_done, c.s));
     launch_kron_combine_small(cj, nc, c.s);
   }
   std::vector<int> rc(2 * P.L, KP_OK);
@@ -870,20 +879,17 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
     cudaEventRecord(ctx->side_ev[2 * l + k], s);
   };
   if (!big.empty()) {
-    if (getenv("KP_SERIAL_EIG")) {  // diagnostic: issue the solves from this thread
-      for (int l : big)
-        for (int k = 0; k < 2; ++k) solve_pair(l, k);
-    } else {
-      std::vector<std::thread> pool;
-      for (int l : big)
-        for (int k = 0; k < 2; ++k) pool.emplace_back(solve_pair, l, k);
-      for (auto& t : pool) t.join();
-    }
+    std::vector<std::thread> pool;
+    for (int l : big)
+      for (int k = 0; k < 2; ++k)
+        if (!pair_small(l, k)) pool.emplace_back(solve_pair, l, k);
+    for (auto& t : pool) t.join();
   }
   for (int v : rc) KP_TRY(v);
   for (int l : big) {
     cudaStream_t s = ctx->side[2 * l];
-    KP_CUDA_TRY(cudaStreamWaitEvent(s, ctx->side_ev[2 * l + 1], 0));
+    if (!pair_small(l, 1)) KP_CUDA_TRY(cudaStreamWaitEvent(s, ctx->side_ev[2 * l + 1], 0));
+    if (pair_small(l, 0) || pair_small(l, 1)) KP_CUDA_TRY(cudaStreamWaitEvent(s, small_done, 0));
     launch_eig_status(c.at(P.k_la[l]), P.p[l], c.at(P.k_lb[l]), P.q[l],
                       reinterpret_cast<int*>(c.at(P.k_info[l])), out->status, s);
     KP_TRY(kron_combine(ctx->side_blas[2 * l], s, P.p[l], P.q[l], c.at(P.k_A1[l]), c.at(P.k_la[l]),
@@ -892,15 +898,6 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
     KP_CUDA_TRY(cudaEventRecord(ctx->side_ev[2 * l], s));
   }
   for (int l : big) KP_CUDA_TRY(cudaStreamWaitEvent(c.s, ctx->side_ev[2 * l], 0));
-  if (getenv("KP_DEBUG_EIG")) {  // diagnostic: print the per-layer eigensolver info words
-    cudaStreamSynchronize(c.s);
-    for (int l = 0; l < P.L; ++l) {
-      int inf[2] = {0, 0};
-      cudaMemcpy(inf, c.at(P.k_info[l]), sizeof(inf), cudaMemcpyDeviceToHost);
-      fprintf(stderr, "[kp] layer %d p=%d q=%d info=(%d,%d) lw=(%d,%d)\n", l, P.p[l], P.q[l],
-              inf[0], inf[1], P.lw[l][0], P.lw[l][1]);
-    }
-  }
   launch_axpy_out(delta, st->prev_update, cfg->momentum, c.at(P.o_dir), P.D, c.s);
   if (out->grad) KP_CUDA_TRY(cudaMemcpyAsync(out->grad, grad, sizeof(double) * P.D,
                                              cudaMemcpyDeviceToDevice, c.s));
