@@ -315,7 +315,30 @@ def affine_residual_terms(problem, x, rtol: float = 1e-12):
     return np.ascontiguousarray(r0), seeds
 
 
+_TERMS_CACHE: dict = {}
+
+
 def residual_terms(problem, x, rtol: float = 1e-12):
+    """Cached :func:`_residual_terms`: the split depends only on (problem, x), and the
+    harness keeps one batch for ``resample_every`` steps (reference harness.py:293-304).
+    The cache holds one entry, keyed on the problem object and the exact contents of x
+    (a full compare, a few ms, instead of the probing, ~100+ ms at N = 16384, d = 100).
+    The returned arrays are read-only."""
+    x = np.asarray(x, dtype=np.float64)
+    hit = _TERMS_CACHE.get("key")
+    if (hit is not None and hit[0] is problem and hit[1].shape == x.shape
+            and np.array_equal(hit[1], x)):
+        return _TERMS_CACHE["out"]
+    out = _residual_terms(problem, x, rtol)
+    for a in out:
+        if a is not None:
+            a.flags.writeable = False
+    _TERMS_CACHE["key"] = (problem, x.copy())
+    _TERMS_CACHE["out"] = out
+    return out
+
+
+def _residual_terms(problem, x, rtol: float = 1e-12):
     """Split an interior residual that is quadratic in the output gradient.
 
     Returns ``(r0, seeds, quad)`` such that, per point,
