@@ -21,7 +21,7 @@ class CpuShardEngine:
         self.b = [np.array(b) for b in biases]
         self.x, self.xb, self.tg = x_int, x_bnd, targets
         self.prob = problem
-        self.cd = np.diagonal(problem.coeffs.c).copy()
+        self.cd = orc.coeffs_of(problem)
         self.ng, self.nbg = float(n_glob), float(nb_glob)
         self.ema, self.lam, self.mu = ema, damping, momentum
         self.grid = [2.0 ** e for e in range(ls_min_exp, ls_max_exp + 1)]

@@ -24,7 +24,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, q, star=False):
+def _worker(rank, world, port, q, star=False, wkey="c3"):
     import sys
 
     here = os.path.dirname(os.path.abspath(__file__))
@@ -39,7 +39,7 @@ def _worker(rank, world, port, q, star=False):
         from paper_2405_15603_b200.dist import (ShardedKfacStarStep, ShardedKfacStep, shard_bounds,
                                                 torch_all_reduce)
 
-        wl = configs.WORKLOADS["c3"]
+        wl = configs.WORKLOADS[wkey]
         prob, params, batch = wl.build(0, 90, 31)
         i0, i1 = shard_bounds(90, rank, world)
         b0, b1 = shard_bounds(31, rank, world)
@@ -53,8 +53,9 @@ def _worker(rank, world, port, q, star=False):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("star", [False, True], ids=["kfac", "kfac_star"])
-def test_sharded_step_matches_single_process_oracle(star):
+@pytest.mark.parametrize("star,wkey", [(False, "c3"), (True, "c3"), (False, "dense")],
+                         ids=["kfac", "kfac_star", "kfac_dense_coeffs"])
+def test_sharded_step_matches_single_process_oracle(star, wkey):
     from oracle import kfac_oracle as orc
     from paper_2405_15603_b200 import configs
 
@@ -62,7 +63,7 @@ def test_sharded_step_matches_single_process_oracle(star):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, star)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, star, wkey)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
@@ -71,7 +72,7 @@ def test_sharded_step_matches_single_process_oracle(star):
         assert p.exitcode == 0
     res.sort(key=lambda t: t[0])
 
-    wl = configs.WORKLOADS["c3"]
+    wl = configs.WORKLOADS[wkey]
     prob, params, batch = wl.build(0, 90, 31)
     st = orc.init_state(params.weights, params.biases, ema=wl.ema, damping=wl.damping, momentum=0.3)
     step = orc.kfac_star_step if star else orc.kfac_step

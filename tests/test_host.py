@@ -160,3 +160,36 @@ def test_checkpoint_roundtrip(tmp_path):
     assert conf is None
     for a, b in zip(p.weights + p.biases, q.weights + q.biases):
         assert np.array_equal(a, b)
+
+
+def test_coeff_spectrum_diagonal_and_dense():
+    from paper_2405_15603_b200.taylor import coeff_spectrum
+    lam, rot = coeff_spectrum(np.diag([0.0, 1.0, 2.0]))
+    assert rot is None and np.array_equal(lam, [0.0, 1.0, 2.0])
+    lam, rot = coeff_spectrum(np.array([1.0, 3.0]))  # 1-D = the diagonal
+    assert rot is None and np.array_equal(lam, [1.0, 3.0])
+    r = np.random.default_rng(0).standard_normal((5, 5))
+    c = 0.5 * (r + r.T)
+    lam, rot = coeff_spectrum(c)
+    assert np.allclose(rot @ np.diag(lam) @ rot.T, c, atol=1e-13)
+    assert np.allclose(rot.T @ rot, np.eye(5), atol=1e-13)
+    # the rotated diagonal quadratic form equals the dense one (the device identity)
+    g = np.random.default_rng(1).standard_normal((7, 5))
+    gp = g @ rot
+    assert np.allclose(np.einsum("ni,ij,nj->n", g, c, g), (gp * gp) @ lam, atol=1e-12)
+    with pytest.raises(ValueError):
+        coeff_spectrum(np.zeros((2, 3)))
+
+
+def test_residual_terms_cache_tracks_batch_contents():
+    from paper_2405_15603_b200.pde import residual_terms
+    prob = make_problem("poisson_cos_sum")
+    x = sample_batch(prob, 40, 8, 3).interior.copy()
+    r0a, sa, _ = residual_terms(prob, x)
+    r0b, sb, _ = residual_terms(prob, x.copy())        # same contents: cached
+    assert r0b is r0a and sb is sa and not r0a.flags.writeable
+    x[0, 0] += 0.25                                     # in-place edit: recomputed
+    r0c, _, _ = residual_terms(prob, x)
+    assert r0c is not r0a and r0c[0] != r0a[0] and np.array_equal(r0c[1:], r0a[1:])
+    other = make_problem("poisson_cos_sum")             # another problem object: recomputed
+    assert residual_terms(other, x)[0] is not r0c
