@@ -275,11 +275,16 @@ def run_ours(args):
                          f"src/optim.py:251-263) on {n_s} interior + {n_s // 3} boundary points of "
                          f"{wl.name}, {dt:.2f} s"}
 
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "gemm_nt_traffic.json")
+    traffic, traffic_note = None, None
+    tp = os.path.join(ROOT, "profiles", "gemm_act_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+            tj = json.load(open(tp))
+            # only valid for the workload it was captured on (bytes scale with N)
+            if tj.get("n_interior") == args.n_interior and tj.get("workload") == wl.name:
+                traffic = tj.get("dram_bytes_per_launch")
+                traffic_note = {"launch": tj.get("kernel"),
+                                "algorithmic_bytes_per_launch": tj.get("algorithmic_bytes_per_launch")}
         except (OSError, ValueError):
             traffic = None
 
@@ -303,7 +308,7 @@ def run_ours(args):
                          "achieved": achieved_tflops, "peak": FP64_DMMA_PEAK_TFLOPS,
                          "unit": "TFLOP/s",
                          "frac": (achieved_tflops / FP64_DMMA_PEAK_TFLOPS) if achieved_tflops else None,
-                         "traffic": traffic, "launches_per_step": gemm_launches // max(args.steps, 1),
+                         "traffic": traffic, "traffic_of": traffic_note, "launches_per_step": gemm_launches // max(args.steps, 1),
                          "share_of_step": gemm_ms / ms_total if ms_total else None,
                          "peak_source": "measured DMMA issue peak, profiles/r01_fp64_peaks.txt "
                                         "(MEASURED_PEAKS.json has no FP64 entry; cuBLAS DGEMM 35.4)"},

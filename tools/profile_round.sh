@@ -10,6 +10,8 @@ python bench.py > $OUT/bench.json 2> $OUT/bench.err
 CMD16="python tools/phase_timing.py --workload c5 --n-interior 16384 --reps 1"
 $CMD16 > $OUT/phase16k.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_c5_n16384.csv $CMD16 > $OUT/ncu_launch.log 2>&1
+# the bench workload's own launches (one line-search candidate: LOSS, LOSS, LAST) -> traffic per launch
+ncu --set full --clock-control none -k regex:"k_gemm_act" -s 6 -c 3 -o $OUT/prof_gemm_act16k $CMD16 > $OUT/ncu0.log 2>&1
 CMD3="python tools/phase_timing.py --workload c5 --n-interior 3000 --reps 1"
 $CMD3 > $OUT/phase3k.log 2>&1 || exit 1
 # launch order per step: accumulate (interior: 3 STORE; boundary: 3 STORE), line search k=0 (LOSS, LOSS, LAST ...)
