@@ -213,6 +213,31 @@ __global__ void k_tn_reduce2(const double* __restrict__ partial, int64_t splits,
   }
 }
 
+// Many splits (small problems: few tiles, many row splits): 8 warps per 32 consecutive
+// entries, warp w summing splits w, w+8, ... in order, then the 8 warp sums in order.
+__global__ void __launch_bounds__(256) k_tn_reduce2_wide(const double* __restrict__ partial,
+                                                         int64_t splits, int nx, int ny, bool sym,
+                                                         double* __restrict__ acc, int64_t ldacc) {
+  __shared__ double red[8][33];
+  const int64_t n = (int64_t)nx * ny;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t e = (int64_t)blockIdx.x * 32 + lane;
+  double v = 0.0;
+  if (e < n)
+    for (int64_t s = w; s < splits; s += 8) v += partial[s * n + e];
+  red[w][lane] = v;
+  __syncthreads();
+  if (w == 0 && e < n) {
+    const int i = (int)(e / ny), j = (int)(e % ny);
+    if (!(sym && j > i)) {
+      double t = acc[(int64_t)i * ldacc + j];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t += red[k][lane];
+      acc[(int64_t)i * ldacc + j] = t;
+    }
+  }
+}
+
 }  // namespace
 
 size_t gemm_tn_tma_partial_doubles(int64_t R, int nx, int ny, bool sym) {
@@ -245,9 +270,14 @@ bool launch_gemm_tn_tma_accumulate(const double* X, int64_t ldx, int nx, const d
   count_launch();
   k_gemm_tn_tma<<<(unsigned)(t.splits * t.pairs), NW * 32, smem, s>>>(mx, my, a, t, partial);
   const int64_t n = (int64_t)nx * ny;
-  const int rb = (int)std::min<int64_t>(ceil_div(n, 256), 148 * 8);
   count_launch();
-  k_tn_reduce2<<<rb, 256, 0, s>>>(partial, t.splits, nx, ny, sym, acc, ldacc);
+  if (t.splits >= 16) {
+    k_tn_reduce2_wide<<<(unsigned)ceil_div(n, 32), 256, 0, s>>>(partial, t.splits, nx, ny, sym, acc,
+                                                                 ldacc);
+  } else {
+    const int rb = (int)std::min<int64_t>(ceil_div(n, 256), 148 * 8);
+    k_tn_reduce2<<<rb, 256, 0, s>>>(partial, t.splits, nx, ny, sym, acc, ldacc);
+  }
   return true;
 }
 
