@@ -40,6 +40,80 @@ __device__ __forceinline__ void set_status_dev(int32_t* status, int32_t code) {
   atomicCAS(status, 0, code);
 }
 
+// Parallel cyclic Jacobi on the symmetric C (n x n, pitch ld) accumulating V <- V G^T.
+// Round-robin ordering over m = n rounded up to even (index n is a dummy when n is odd):
+// m - 1 rounds of m/2 disjoint pairs per sweep.  Lane group k (G lanes) owns pair k of
+// every round: it computes the rotation redundantly in registers, then rotates rows p, q of
+// C, and (after a barrier) columns p, q of C and V.  Pair positions advance incrementally.
+template <int G>
+__device__ __forceinline__ void jacobi_sweeps(double* C, double* V, int n, int ld, int* flag) {
+  constexpr int GPW = 32 / G;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int k = warp * GPW + lane / G;  // pair slot of this lane group
+  const int gl = lane % G;
+  const int m = (n + 1) & ~1;
+  const int npair = m / 2;
+  const bool active = k < npair;
+  for (int sweep = 0; sweep < EIG_MAX_SWEEPS; ++sweep) {
+    if (tid == 0) *flag = 0;
+    __syncthreads();
+    // round 0 positions: a = 0 (k = 0) or 1 + (k - 1); b = 1 + (m - 2 - k)
+    int ia = k > 0 ? k - 1 : 0, ib = m - 2 - k;
+    for (int round = 0; round < m - 1; ++round) {
+      int p = 0, q = n;
+      double c = 1.0, sn = 0.0;
+      if (active) {
+        const int a = (k == 0) ? 0 : 1 + ia;
+        const int b = 1 + ib;
+        p = min(a, b);
+        q = max(a, b);
+        if (q < n) {
+          const double apq = C[p * ld + q];
+          const double app = C[p * ld + p], aqq = C[q * ld + q];
+          if (apq * apq > kJacobiTol * kJacobiTol * fabs(app * aqq) && fabs(apq) > 1e-300) {
+            // t = sign(theta) / (|theta| + sqrt(theta^2 + 1)), theta = (aqq - app) / (2 apq)
+            const double dd = aqq - app;
+            const double two_apq = 2.0 * apq;
+            const double den = fabs(dd) + sqrt(fma(dd, dd, two_apq * two_apq));
+            const double t = ((dd >= 0.0) == (apq >= 0.0) ? 1.0 : -1.0) * fabs(two_apq) / den;
+            c = rsqrt(fma(t, t, 1.0));
+            sn = t * c;
+            if (gl == 0) *flag = 1;
+          }
+        }
+        if (k != 0) ia = (ia + 1 == m - 1) ? 0 : ia + 1;
+        ib = (ib + 1 == m - 1) ? 0 : ib + 1;
+      }
+      __syncthreads();  // all rotation parameters read C before any row update
+      const bool rot = active && q < n && sn != 0.0;
+      if (rot) {
+        for (int col = gl; col < n; col += G) {
+          const double x = C[p * ld + col], y = C[q * ld + col];
+          C[p * ld + col] = c * x - sn * y;
+          C[q * ld + col] = sn * x + c * y;
+        }
+      }
+      __syncthreads();
+      if (rot) {
+        for (int row = gl; row < n; row += G) {
+          const double x = C[row * ld + p], y = C[row * ld + q];
+          C[row * ld + p] = c * x - sn * y;
+          C[row * ld + q] = sn * x + c * y;
+          const double vx = V[row * ld + p], vy = V[row * ld + q];
+          V[row * ld + p] = c * vx - sn * vy;
+          V[row * ld + q] = sn * vx + c * vy;
+        }
+      }
+      __syncthreads();
+    }
+    if (*flag == 0) {
+      if (tid == 0) atomicMax(&g_eig_sweeps_max, sweep + 1);
+      return;
+    }
+  }
+  if (tid == 0) atomicMax(&g_eig_sweeps_max, 1000 + EIG_MAX_SWEEPS);
+}
+
 // One CTA (32 warps) per factor pair.  smem: L, C, V (n x n each, row-major).
 __global__ void __launch_bounds__(EIG_THREADS) k_gen_eig_small(const SmallEigJobs jobs,
                                                               int32_t* status) {
@@ -122,78 +196,12 @@ __global__ void __launch_bounds__(EIG_THREADS) k_gen_eig_small(const SmallEigJob
   }
   __syncthreads();
 
-  // parallel cyclic Jacobi, round-robin ordering over m = n rounded up to even; warp w owns
-  // pairs w and w + 32 of every round and keeps their rotations in registers.
-  const int m = (n + 1) & ~1;
-  const int npair = m / 2;
-  for (int sweep = 0; sweep < EIG_MAX_SWEEPS; ++sweep) {
-    if (tid == 0) flag = 0;
-    __syncthreads();
-    for (int round = 0; round < m - 1; ++round) {
-      int pr[2], qr[2];
-      double cr[2], sr[2];
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int k = warp + u * NWARPS;
-        pr[u] = 0;
-        qr[u] = n;
-        cr[u] = 1.0;
-        sr[u] = 0.0;
-        if (k >= npair) continue;
-        const int a = (k == 0) ? 0 : 1 + (k - 1 + round) % (m - 1);
-        const int b = 1 + (m - 2 - k + round) % (m - 1);
-        const int p = min(a, b), q = max(a, b);
-        pr[u] = p;
-        qr[u] = q;
-        if (q >= n) continue;
-        const double apq = C[p * ld + q];
-        const double app = C[p * ld + p], aqq = C[q * ld + q];
-        if (apq * apq > kJacobiTol * kJacobiTol * fabs(app * aqq) && fabs(apq) > 1e-300) {
-          // t = sign(theta) / (|theta| + sqrt(theta^2 + 1)), theta = (aqq - app) / (2 apq)
-          const double dd = aqq - app;
-          const double two_apq = 2.0 * apq;
-          const double den = fabs(dd) + sqrt(fma(dd, dd, two_apq * two_apq));
-          const double t = ((dd >= 0.0) == (apq >= 0.0) ? 1.0 : -1.0) * fabs(two_apq) / den;
-          cr[u] = rsqrt(fma(t, t, 1.0));
-          sr[u] = t * cr[u];
-          if (lane == 0) flag = 1;
-        }
-      }
-      __syncthreads();  // all rotation parameters read C before any row update
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int p = pr[u], q = qr[u];
-        const double c = cr[u], s = sr[u];
-        if (q >= n || s == 0.0) continue;
-        for (int col = lane; col < n; col += 32) {
-          const double x = C[p * ld + col], y = C[q * ld + col];
-          C[p * ld + col] = c * x - s * y;
-          C[q * ld + col] = s * x + c * y;
-        }
-      }
-      __syncthreads();
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int p = pr[u], q = qr[u];
-        const double c = cr[u], s = sr[u];
-        if (q >= n || s == 0.0) continue;
-        for (int row = lane; row < n; row += 32) {
-          const double x = C[row * ld + p], y = C[row * ld + q];
-          C[row * ld + p] = c * x - s * y;
-          C[row * ld + q] = s * x + c * y;
-          const double vx = V[row * ld + p], vy = V[row * ld + q];
-          V[row * ld + p] = c * vx - s * vy;
-          V[row * ld + q] = s * vx + c * vy;
-        }
-      }
-      __syncthreads();
-    }
-    if (flag == 0) {
-      if (tid == 0) atomicMax(&g_eig_sweeps_max, sweep + 1);
-      break;
-    }
-    if (sweep == EIG_MAX_SWEEPS - 1 && tid == 0) atomicMax(&g_eig_sweeps_max, 1000 + sweep);
-  }
+  // parallel cyclic Jacobi (jacobi_sweeps): lane groups of 32 when the m/2 pairs fit the
+  // 32 warps, of 16 otherwise (n = 65..96), so no group ever handles two pairs per round
+  if (((n + 1) & ~1) / 2 <= NWARPS)
+    jacobi_sweeps<32>(C, V, n, ld, &flag);
+  else
+    jacobi_sweeps<16>(C, V, n, ld, &flag);
 
   // eigenvalues; T = L^-T V (back substitution, warp per column) written to global
   for (int i = tid; i < n; i += EIG_THREADS) jb.lam[i] = C[i * ld + i];

@@ -207,13 +207,22 @@ __global__ void __launch_bounds__(NW * 32, 8 / NW)
     else g.post[(grow + d + 1) * g.ldo + n0 + j] = o;
   }
   if (MODE == ACT_LAST) {
+    // one thread per row: a sequential dot over the tile's units against the last layer's
+    // weights (staged in smem), starting at unit (r mod 32) so that the 32 rows of a warp
+    // hit distinct banks (row pitch CPITCH + 1 is odd in 8-byte words)
+    __shared__ double wl[BN];
+    for (int j = threadIdx.x; j < BN; j += NWARP * 32) wl[j] = j < ncol ? g.wlast[n0 + j] : 0.0;
     __syncthreads();
     const int rows = (int)nsmp * S;
-    for (int r = warp; r < rows; r += NWARP) {
+    for (int r = threadIdx.x; r < rows; r += NWARP * 32) {
+      const double* cr = Cs + r * CPITCH;
       double a = 0.0;
-      for (int j = lane; j < ncol; j += 32) a = fma(Cs[r * CPITCH + j], g.wlast[n0 + j], a);
-      a = warp_sum(a);
-      if (lane == 0) g.upart[((int64_t)m0 + r) * tiles_n + tn] = a;
+      int j = (r & 31) % ncol;
+      for (int jj = 0; jj < ncol; ++jj) {
+        a = fma(cr[j], wl[j], a);
+        j = (j + 1 == ncol) ? 0 : j + 1;
+      }
+      g.upart[((int64_t)m0 + r) * tiles_n + tn] = a;
     }
   }
 }
