@@ -114,6 +114,25 @@ __device__ __forceinline__ void jacobi_sweeps(double* C, double* V, int n, int l
   if (tid == 0) atomicMax(&g_eig_sweeps_max, 1000 + EIG_MAX_SWEEPS);
 }
 
+// X <- V^T X V for symmetric X (smem, pitch ld), V in smem, through n x n global scratch.
+__device__ __forceinline__ void congruence(double* X, const double* V, double* scratch, int n,
+                                          int ld) {
+  for (int e = threadIdx.x; e < n * n; e += EIG_THREADS) {  // scratch = X V
+    const int i = e / n, j = e % n;
+    double a = 0.0;
+    for (int k = 0; k < n; ++k) a = fma(X[i * ld + k], V[k * ld + j], a);
+    scratch[e] = a;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < n * n; e += EIG_THREADS) {  // X = V^T scratch
+    const int i = e / n, j = e % n;
+    double a = 0.0;
+    for (int k = 0; k < n; ++k) a = fma(V[k * ld + i], scratch[k * n + j], a);
+    X[i * ld + j] = a;
+  }
+  __syncthreads();
+}
+
 // One CTA (32 warps) per factor pair.  smem: L, C, V (n x n each, row-major).
 __global__ void __launch_bounds__(EIG_THREADS) k_gen_eig_small(const SmallEigJobs jobs,
                                                               int32_t* status) {
@@ -138,6 +157,31 @@ __global__ void __launch_bounds__(EIG_THREADS) k_gen_eig_small(const SmallEigJob
   }
   if (tid == 0) flag = 0;
   __syncthreads();
+  // warm start: congruence by the previous step's T, kept only while T_prev^T M2 T_prev stays
+  // near I (its diagonal within [0.5, 2]); otherwise (first step, re-initialised factors)
+  // the cold path below runs on the untransformed pair
+  __shared__ int warm;
+  if (tid == 0) warm = (jb.warm_t != nullptr && *jb.warm_valid != 0) ? 1 : 0;
+  __syncthreads();
+  if (warm) {
+    for (int e2 = tid; e2 < n * n; e2 += EIG_THREADS) V[(e2 / n) * ld + e2 % n] = jb.warm_t[e2];
+    __syncthreads();
+    congruence(L, V, jb.warm_scratch, n, ld);
+    for (int i = tid; i < n; i += EIG_THREADS) {
+      const double dgl = L[i * ld + i];
+      if (!(dgl > 0.5 && dgl < 2.0)) warm = 0;
+    }
+    __syncthreads();
+    if (warm) {
+      congruence(C, V, jb.warm_scratch, n, ld);
+    } else {  // reload the untransformed M2
+      for (int e2 = tid; e2 < n * n; e2 += EIG_THREADS) {
+        const int i = e2 / n, j = e2 % n;
+        L[i * ld + j] = jb.f2[e2] + (i == j ? lam : 0.0);
+      }
+      __syncthreads();
+    }
+  }
 
   // right-looking Cholesky of M2 (lower triangle of L); warp w owns rows w, w+32, ...
   for (int k = 0; k < n; ++k) {
@@ -162,6 +206,7 @@ __global__ void __launch_bounds__(EIG_THREADS) k_gen_eig_small(const SmallEigJob
   if (flag != 0) {
     if (tid == 0) {
       if (jb.info) *jb.info = flag;
+      if (jb.warm_valid) *jb.warm_valid = 0;
       set_status_dev(status, KP_ERR_NOT_PSD);
     }
     return;
@@ -216,10 +261,23 @@ __global__ void __launch_bounds__(EIG_THREADS) k_gen_eig_small(const SmallEigJob
     }
   }
   __syncthreads();
+  const double* T = C;
+  if (warm) {  // T = T_prev T''  (T_prev from global, T'' in C; result in V)
+    for (int e2 = tid; e2 < n * n; e2 += EIG_THREADS) {
+      const int i = e2 / n, j = e2 % n;
+      double a = 0.0;
+      for (int k = 0; k < n; ++k) a = fma(jb.warm_t[i * n + k], C[k * ld + j], a);
+      V[i * ld + j] = a;
+    }
+    __syncthreads();
+    T = V;
+  }
   for (int e = tid; e < n * n; e += EIG_THREADS) {
     const int i = e / n, j = e % n;
-    jb.t[jb.col_major ? j * n + i : e] = C[i * ld + j];
+    jb.t[jb.col_major ? j * n + i : e] = T[i * ld + j];
+    if (jb.warm_t) jb.warm_t[e] = T[i * ld + j];
   }
+  if (tid == 0 && jb.warm_valid) *jb.warm_valid = 1;
   if (tid == 0 && jb.info) *jb.info = 0;
   // PSD check on the generalised eigenvalues (src/linalg.py:79-83, 165-166)
   if (tid == 0) {

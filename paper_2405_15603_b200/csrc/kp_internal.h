@@ -256,6 +256,13 @@ struct SmallEigJob {
   double* lam;       // n eigenvalues
   int* info;
   int col_major = 0;  // 1: write t column-major (the cuSOLVER layout, for a cuBLAS combine)
+  // Warm start (optional): the previous step's T (n x n row-major) and a validity flag, kept
+  // by the context across steps, plus n x n global scratch.  With a valid T_prev the pair is
+  // first congruence-transformed, (T_prev^T M1 T_prev, T_prev^T M2 T_prev), which the EMA
+  // keeps close to (diag, I), so Jacobi needs far fewer sweeps; T = T_prev T''.
+  double* warm_t = nullptr;
+  double* warm_scratch = nullptr;
+  int* warm_valid = nullptr;
 };
 struct SmallEigJobs {
   SmallEigJob job[32];

@@ -64,6 +64,12 @@ struct kp_context {
   cudaEvent_t cap_in = nullptr, cap_out = nullptr;
   std::vector<unsigned char> graph_key;
   cudaGraphExec_t graph_exec = nullptr;
+  // warm-start cache of the on-device eigensolver (previous T per small factor pair, scratch,
+  // validity flags), keyed on the layer shapes and the state's factor buffers
+  double* warm_buf = nullptr;
+  size_t warm_cap = 0;  // doubles
+  int* warm_flags = nullptr;
+  std::vector<unsigned char> warm_key;
   // cache of the last workspace plan (make_plan queries cuSOLVER workspace sizes: host cost)
   kp_problem plan_key{};
   bool plan_valid = false;
@@ -820,7 +826,52 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
     KP_CUDA_TRY(cudaEventRecord(ready, c.s));
   }
   std::vector<int> big;  // layers with at least one cuSOLVER pair
+  // warm-start cache for the small pairs (re-keyed when shapes or factor buffers change)
   {
+    std::vector<unsigned char> key;
+    auto put = [&](const void* p, size_t n) {
+      const unsigned char* b = static_cast<const unsigned char*>(p);
+      key.insert(key.end(), b, b + n);
+    };
+    size_t need = 0;
+    for (int l = 0; l < P.L; ++l) {
+      put(&P.p[l], sizeof(int));
+      put(&P.q[l], sizeof(int));
+      for (int k = 0; k < 2; ++k) {
+        const size_t nn = (size_t)(k == 0 ? P.p[l] : P.q[l]);
+        if (pair_small(l, k)) need += 2 * nn * nn;
+      }
+    }
+    put(&st->a_int, sizeof(double*));
+    put(&st->b_int, sizeof(double*));
+    put(&st->a_bnd, sizeof(double*));
+    put(&st->b_bnd, sizeof(double*));
+    if (key != ctx->warm_key) {
+      if (need + 32 > ctx->warm_cap) {
+        if (ctx->warm_buf) {
+          KP_CUDA_TRY(cudaDeviceSynchronize());
+          KP_CUDA_TRY(cudaFree(ctx->warm_buf));
+        }
+        ctx->warm_buf = nullptr;
+        ctx->warm_cap = 0;
+        ctx->warm_flags = nullptr;
+        KP_CUDA_TRY(cudaMalloc(&ctx->warm_buf, sizeof(double) * (need + 32)));
+        ctx->warm_cap = need + 32;
+        ctx->warm_flags = reinterpret_cast<int*>(ctx->warm_buf + need);
+      }
+      KP_CUDA_TRY(cudaMemsetAsync(ctx->warm_flags, 0, sizeof(int) * 64, c.s));
+      ctx->warm_key = key;
+    }
+  }
+  {
+    size_t woff = 0;
+    int wjob = 0;
+    auto warm = [&](SmallEigJob& j) {
+      j.warm_t = ctx->warm_buf + woff;
+      j.warm_scratch = ctx->warm_buf + woff + (size_t)j.n * j.n;
+      j.warm_valid = ctx->warm_flags + wjob++;
+      woff += 2 * (size_t)j.n * j.n;
+    };
     SmallEigJobs ej{};
     SmallCombineJobs cj{};
     int ne = 0, nc = 0, maxn = 1;
@@ -830,11 +881,13 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
       if (sa) {
         ej.job[ne++] = SmallEigJob{P.p[l], st->a_int + P.fa[l], st->a_bnd + P.fa[l], lam,
                                    c.at(P.k_A1[l]), c.at(P.k_la[l]), info, sb ? 0 : 1};
+        warm(ej.job[ne - 1]);
         maxn = std::max(maxn, P.p[l]);
       }
       if (sb) {
         ej.job[ne++] = SmallEigJob{P.q[l], st->b_int + P.fb[l], st->b_bnd + P.fb[l], lam,
                                    c.at(P.k_B1[l]), c.at(P.k_lb[l]), info + 1, sa ? 0 : 1};
+        warm(ej.job[ne - 1]);
         maxn = std::max(maxn, P.q[l]);
       }
       if (sa && sb)
@@ -1121,6 +1174,10 @@ int32_t kp_context_create(int32_t device, kp_context** out) {
 
 int32_t kp_context_destroy(kp_context* c) {
   if (!c) return KP_OK;
+  if (c->warm_buf) {
+    cudaDeviceSynchronize();
+    cudaFree(c->warm_buf);
+  }
   if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
   if (c->cap_stream) {
     cudaStreamSynchronize(c->cap_stream);
@@ -1221,6 +1278,8 @@ int32_t kp_init_state(kp_context* ctx, const kp_net* net, kp_state* st, int32_t 
     D += (int64_t)p * q;
   }
   KP_CUDA_TRY(cudaMemsetAsync(st->prev_update, 0, sizeof(double) * D, s));
+  if (ctx->warm_flags)  // re-initialised factors: cold-start the eigensolver
+    KP_CUDA_TRY(cudaMemsetAsync(ctx->warm_flags, 0, sizeof(int) * 64, s));
   KP_CUDA_TRY(cudaGetLastError());
   return KP_OK;
 }

@@ -348,3 +348,11 @@ def test_graph_replay_is_bit_identical(star):
     for fa, fb in zip(runs[0][2], runs[1][2]):
         for a, b in zip(fa, fb):
             assert np.array_equal(a, b)
+
+
+def test_ten_steps_match_oracle_warm_started_eigensolver():
+    """Ten steps (step 10 within 1e-8): from step 2 on, the on-device
+    eigensolver starts from the previous step's generalised eigenvectors."""
+    prob = make_problem("poisson2d_sin")
+    worst = _oracle_vs_device((2, 24, 24, 16, 1), prob, 120, 40, 10, momentum=0.3)
+    assert worst <= 1e-8
