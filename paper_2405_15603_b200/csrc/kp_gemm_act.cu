@@ -62,8 +62,12 @@ __global__ void __launch_bounds__(NW * 32, 8 / NW)
   double* sm = reinterpret_cast<double*>(act_raw + ((1024 - (smem_addr(act_raw) & 1023)) & 1023));
   double* As = sm;
   double* Bs = sm + STAGES * A_STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(Bs + STAGES * B_STAGE);
-  uint64_t* empty = full + STAGES;
+  // The pipeline barriers live outside the dynamic region: the epilogue's C staging reuses
+  // the whole pipeline smem, and overwriting live mbarrier objects (no mbarrier.inval) gave
+  // sporadic garbage rows (NaN in ~1 of 10^3 line-search launches).
+  __shared__ __align__(8) uint64_t bars[2 * STAGES];
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES;
   double* Cs = sm;  // epilogue staging, aliases the (drained) pipeline
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -236,7 +240,7 @@ bool run_act(const GemmAct& g, int box_rows, cudaStream_t s) {
   if (!make_tma_map_2d(&ma, g.A, (uint64_t)M, (uint64_t)g.K, (uint64_t)g.lda, box_rows)) return false;
   if (!make_tma_map_2d(&mb, g.B, (uint64_t)g.N * g.batch, (uint64_t)g.K, (uint64_t)g.ldb, BN))
     return false;
-  const size_t pipe = (size_t)STAGES * (TM * 8 + BN) * BK * sizeof(double) + 2 * STAGES * 8;
+  const size_t pipe = (size_t)STAGES * (TM * 8 + BN) * BK * sizeof(double);
   const size_t cst = (size_t)TM * 8 * CPITCH * sizeof(double);
   const size_t smem = std::max(pipe, cst) + 1024;
   auto kern = k_gemm_act<BK, STAGES, MODE, TM, NW, BN>;
