@@ -65,9 +65,14 @@ __global__ void __launch_bounds__(NW * 32, 8 / NW)
   // The pipeline barriers live outside the dynamic region: the epilogue's C staging reuses
   // the whole pipeline smem, and overwriting live mbarrier objects (no mbarrier.inval) gave
   // sporadic garbage rows (NaN in ~1 of 10^3 line-search launches).
-  __shared__ __align__(8) uint64_t bars[2 * STAGES];
-  uint64_t* full = bars;
-  uint64_t* empty = bars + STAGES;
+  // The pipeline barriers sit after both the pipeline stages and the epilogue's C staging
+  // (which reuses the stage smem): overwriting live mbarrier objects (no mbarrier.inval)
+  // gave sporadic garbage rows (NaN in ~1 of 10^3 line-search launches at c5 scale).
+  // (A static __shared__ array instead costs 2.5% on the line search.)
+  constexpr int CS_DOUBLES = AROWS * (BN + 4);
+  constexpr int PIPE_DOUBLES = STAGES * (A_STAGE + B_STAGE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + (CS_DOUBLES > PIPE_DOUBLES ? CS_DOUBLES : PIPE_DOUBLES));
+  uint64_t* empty = full + STAGES;
   double* Cs = sm;  // epilogue staging, aliases the (drained) pipeline
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -242,7 +247,7 @@ bool run_act(const GemmAct& g, int box_rows, cudaStream_t s) {
     return false;
   const size_t pipe = (size_t)STAGES * (TM * 8 + BN) * BK * sizeof(double);
   const size_t cst = (size_t)TM * 8 * CPITCH * sizeof(double);
-  const size_t smem = std::max(pipe, cst) + 1024;
+  const size_t smem = std::max(pipe, cst) + 2 * STAGES * 8 + 1024;
   auto kern = k_gemm_act<BK, STAGES, MODE, TM, NW, BN>;
   static bool attr_set = false;
   if (!attr_set) {
