@@ -106,7 +106,10 @@ __device__ __forceinline__ void jacobi_sweeps(double* C, double* V, int n, int l
       }
       __syncthreads();
     }
-    if (*flag == 0) {
+    // every thread reads the flag before thread 0 may reset it for the next sweep
+    const int rotated = *flag;
+    __syncthreads();
+    if (rotated == 0) {
       if (tid == 0) atomicMax(&g_eig_sweeps_max, sweep + 1);
       return;
     }
