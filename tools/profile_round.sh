@@ -18,5 +18,5 @@ $CMD3 > $OUT/phase3k.log 2>&1 || exit 1
 ncu --set full --clock-control none --import-source on -k regex:"k_gemm_act" -s 6 -c 3 -o $OUT/prof_gemm_act $CMD3 > $OUT/ncu1.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"k_gemm_tn_tma" -s 1 -c 2 -o $OUT/prof_gemm_tn $CMD3 > $OUT/ncu2.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"k_first_expand|k_act_bwd|k_gemm_nt_tma" -c 4 -o $OUT/prof_ew $CMD3 > $OUT/ncu3.log 2>&1
-for w in c1 c2 c3 c4; do python tools/phase_timing.py --workload $w --n-interior 3000 --reps 3 >> $OUT/phases_small.jsonl 2>&1; done
+for w in c1 c2 c3 c4; do python tools/phase_timing.py --workload $w --n-interior 3000 --reps 5 >> $OUT/phases_small.jsonl 2>&1; done
 ls -la $OUT
