@@ -67,6 +67,13 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_addr(bar)) : "memory");
 }
 
+// Orders this thread's (and, through the preceding mbarrier acquire, the consumers')
+// generic-proxy shared-memory accesses before subsequent async-proxy (TMA) accesses: the
+// refill of a pipeline stage must not overtake the reads of its previous contents.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"

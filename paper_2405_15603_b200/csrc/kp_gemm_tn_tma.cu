@@ -177,6 +177,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     if (lane == 0) mbar_arrive(&empty[s]);
     if (threadIdx.x == 0 && kt + STAGES < KT) {
       mbar_wait(&empty[s], par);
+      fence_proxy_async_smem();
       produce(kt + STAGES);
     }
   }
