@@ -175,9 +175,6 @@ void launch_last_from_partials(const double* upart, int ntn, int64_t n, TaylorDi
                                const double* targets, double* r, cudaStream_t s, int batch = 1,
                                int64_t bias_bstride = 0, int64_t r_bstride = 0,
                                const double* quad = nullptr);
-// Layer-0 gradient, derivative-row part: acc[j*(d+1)+i] += sum_n r_n gbar0[n, 1+i, j].
-void launch_grad0_deriv(const double* gbar0, const double* r, int64_t n, int d, int h1,
-                        double* acc, cudaStream_t s);
 // Batched deterministic sum of squares: out[k] = sum_i v[k*stride + i]^2, i < n.
 void launch_sumsq(const double* v, int64_t n, int64_t stride, int nvec, double* out,
                   int64_t out_stride, cudaStream_t s);

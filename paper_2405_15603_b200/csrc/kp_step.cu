@@ -53,7 +53,6 @@ struct kp_context {
   size_t ev_used = 0;
   double prof_flops = 0.0;
   int64_t prof_launches = 0;
-  double prof_ms_done = 0.0;
   // side streams for the per-layer Kronecker-sum solves (2 per layer: A and B factor pairs)
   std::vector<cudaStream_t> side;
   std::vector<cusolverDnHandle_t> side_solver;
@@ -339,8 +338,6 @@ int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
     }
   }
   P.lwork = lwork;
-  P.o_work = take(lwork);
-  P.o_info = take(8);
   for (int l = 0; l < P.L; ++l) {
     const int64_t p = P.p[l], q = P.q[l];
     P.k_A1[l] = take(p * p);

@@ -363,38 +363,6 @@ void launch_act_bwd(const ActBwd& a, int64_t n, int h, TaylorDims td, const doub
 }
 
 // ---------------------------------------------------------------------------
-// layer-0 gradient, derivative rows: Zhat_0 rows (e_i, 0) pick column i.
-
-__global__ void k_grad0_deriv(const double* __restrict__ gbar0, const double* __restrict__ r,
-                              int64_t n, int d, int h1, double* __restrict__ acc) {
-  const int64_t total = (int64_t)d * h1;
-  const int64_t S = d + 2;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(e / h1), j = (int)(e % h1);
-    const double* g = gbar0 + (int64_t)(1 + i) * h1 + j;
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-    int64_t k = 0;
-    for (; k + 4 <= n; k += 4) {
-      s0 += r[k] * g[(k)*S * h1];
-      s1 += r[k + 1] * g[(k + 1) * S * h1];
-      s2 += r[k + 2] * g[(k + 2) * S * h1];
-      s3 += r[k + 3] * g[(k + 3) * S * h1];
-    }
-    for (; k < n; ++k) s0 += r[k] * g[k * S * h1];
-    acc[(int64_t)j * (d + 1) + i] += (s0 + s1) + (s2 + s3);
-  }
-}
-
-void launch_grad0_deriv(const double* gbar0, const double* r, int64_t n, int d, int h1,
-                        double* acc, cudaStream_t s) {
-  const int64_t total = (int64_t)d * h1;
-  if (total <= 0 || n <= 0) return;
-  count_launch();
-  k_grad0_deriv<<<(unsigned)ceil_div(total, 128), 128, 0, s>>>(gbar0, r, n, d, h1, acc);
-}
-
-// ---------------------------------------------------------------------------
 // weighted value-row column sums: the bias row/column of the factors and of the
 // gradient (the virtual "1" entry of zhat, curvature.py:88-93), two passes with a
 // fixed summation order.
