@@ -251,7 +251,7 @@ def run_ours(args):
     ms_step = ms_total / args.steps
     steps_per_s = 1e3 / ms_step
     value = n_glob * steps_per_s
-    f_step = configs.flops_per_step(wl.widths, n_loc, nb_loc) * world
+    f_step = configs.flops_per_step(wl.widths, n_loc, nb_loc, optimizer=args.optimizer) * world
     achieved_tflops = gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
 
     # end to end through the public API (host numpy in, host numpy out), 1 GPU
@@ -330,7 +330,7 @@ def run_e2e(args, wl, prob, params, batch):
 
     from paper_2405_15603_b200.optim import OptimizerConfig, init_train_state, optimizer_step
 
-    cfg = OptimizerConfig(kind="kfac", damping=wl.damping, ema=wl.ema, momentum=wl.momentum)
+    cfg = OptimizerConfig(kind=args.optimizer, damping=wl.damping, ema=wl.ema, momentum=wl.momentum)
     state = init_train_state(params.copy(), cfg)
     # warm-up on the same state, as a training loop runs: the first call builds the device
     # engine (workspace, context, plans, solver handles) outside the timer

@@ -88,7 +88,8 @@ WORKLOADS["dense"] = Workload("dense_poisson5d", "poisson_cos_sum", (("dim", 5),
 C5_SWEEP = (3000, 16384, 65536)
 
 
-def flops_per_step(widths, n_int: int, n_bnd: int, n_candidates: int = 31) -> float:
+def flops_per_step(widths, n_int: int, n_bnd: int, n_candidates: int = 31,
+                   optimizer: str = "kfac") -> float:
     """Algorithmic FP64 flops of one KFAC step (SURVEY.md §8d formula).
 
     Forward: layer 0 on value rows only (its derivative rows are e_i, operator
@@ -111,6 +112,11 @@ def flops_per_step(widths, n_int: int, n_bnd: int, n_candidates: int = 31) -> fl
     f_a += sum(n_bnd * (h[l] + 1) * (h[l] + 2) for l in range(L))
     f_b = sum(M * h[l + 1] * (h[l + 1] + 1) for l in range(L))
     f_b += sum(n_bnd * h[l + 1] * (h[l + 1] + 1) for l in range(L))
+    if optimizer == "kfac_star":
+        # no line search; two exact Gramian-vector products G.delta, G.prev (optim.py:266-320),
+        # each a Jacobian-vector product (the forward GEMM shapes) plus a weighted gradient
+        # contraction
+        return f_fwd + f_bwd + f_grad + f_a + f_b + 2 * (f_fwd + f_grad)
     return (1 + n_candidates) * f_fwd + f_bwd + f_grad + f_a + f_b
 
 
