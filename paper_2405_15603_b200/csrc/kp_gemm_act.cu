@@ -48,8 +48,8 @@ __device__ __forceinline__ int sigma8(int g) { return (g >> 1) + ((g & 1) << 2);
 // NW warps, each owning BN / NW output units and all TM m8 tiles.  NW = 4 keeps the
 // per-CTA footprint small enough for two co-resident CTAs per SM (one's epilogue
 // overlaps the other's DMMA loop); NW = 8 serves the 15-16 tile shapes.
-template <int BK, int STAGES, int MODE, int TM, int NW, int BN>
-__global__ void __launch_bounds__(NW * 32, 8 / NW)
+template <int BK, int STAGES, int MODE, int TM, int NW, int BN, int MINB = 8 / NW>
+__global__ void __launch_bounds__(NW * 32, MINB)
     k_gemm_act(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                GemmAct g, int tiles_n, int box_rows) {
   constexpr int NWARP = NW;
@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(NW * 32, 8 / NW)
   }
 }
 
-template <int MODE, int TM, int NW, int BK, int STAGES, int BN = BN_MAX>
+template <int MODE, int TM, int NW, int BK, int STAGES, int BN = BN_MAX, int MINB = 8 / NW>
 bool run_act(const GemmAct& g, int box_rows, cudaStream_t s) {
   constexpr int CPITCH = BN + 4;
   CUtensorMap ma, mb;
@@ -249,7 +249,7 @@ bool run_act(const GemmAct& g, int box_rows, cudaStream_t s) {
   const size_t pipe = (size_t)STAGES * (TM * 8 + BN) * BK * sizeof(double);
   const size_t cst = (size_t)TM * 8 * CPITCH * sizeof(double);
   const size_t smem = std::max(pipe, cst) + 2 * STAGES * 8 + 1024;
-  auto kern = k_gemm_act<BK, STAGES, MODE, TM, NW, BN>;
+  auto kern = k_gemm_act<BK, STAGES, MODE, TM, NW, BN, MINB>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -262,10 +262,10 @@ bool run_act(const GemmAct& g, int box_rows, cudaStream_t s) {
   return true;
 }
 
-// tile shapes up to 13 m8 tiles: 4 warps, BK 16, 3 stages -> ~111 KB, two CTAs per SM;
-// 14-16 tiles: 8 warps, BK 32, 3 stages (one CTA per SM).  Narrow layers (N <= 64, the
-// small-d configs: many samples per tile, short K) use 64-unit tiles with 4 warps so two
-// or more CTAs share an SM and no tensor work is spent on padding columns.
+// Tile shapes up to 13 m8 tiles (one large sample per tile): 4 warps x 128 units, BK 16,
+// 3 stages -> ~111 KB, two CTAs per SM.  14-16 tiles (many small samples per tile): 4 warps
+// x 64 units; narrow layers (N <= 64, short K) with BK 32 and 2 stages, otherwise BK 16 and
+// 3 stages with three CTAs per SM.
 template <int MODE, int TM>
 bool run_act_tm(const GemmAct& g, int box_rows, cudaStream_t s) {
   if constexpr (TM <= 13) {
@@ -275,17 +275,26 @@ bool run_act_tm(const GemmAct& g, int box_rows, cudaStream_t s) {
     if (g.N <= 64) {
       if constexpr (TM != 15)
         if (g.K % 32 == 0 && g.K <= 64) return run_act<MODE, TM, 4, 32, 2, 64>(g, box_rows, s);
-      return run_act<MODE, TM, 4, 16, 3, 64>(g, box_rows, s);
+      return run_act<MODE, TM, 4, 16, 3, 64, 3>(g, box_rows, s);
     }
-    if constexpr (TM != 15)
-      if (g.K % 32 == 0) return run_act<MODE, TM, 8, 32, 3>(g, box_rows, s);
-    return run_act<MODE, TM, 8, 16, 6>(g, box_rows, s);
+    // wider layers: 64-unit tiles, 4 warps, three CTAs per SM (~72 KB each) so that
+    // epilogues overlap other CTAs' k loops (c4 line search -11% vs 8 warps x 128 units)
+    return run_act<MODE, TM, 4, 16, 3, 64, 3>(g, box_rows, s);
   }
 }
 
 }  // namespace
 
 int gemm_act_samples_per_tile(int S) { return S <= ROWS_MAX ? ROWS_MAX / S : 0; }
+
+// Unit width of the fused layer's tiles for this shape (mirrors run_act_tm); the LAST mode
+// leaves ceil(N / width) partial dots per row.
+int gemm_act_tile_width(int S, int N) {
+  const int nb = gemm_act_samples_per_tile(S);
+  const int tm = nb > 0 ? (nb * S + 7) / 8 : 0;
+  if (tm <= 13) return BN_MAX;
+  return 64;
+}
 
 bool gemm_act_ok(int S, int K, int64_t lda, int64_t ldb) {
   return S <= ROWS_MAX && K % 16 == 0 && lda % 2 == 0 && ldb % 2 == 0;

@@ -253,7 +253,7 @@ int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
   P.o_ping = take(P.Bc * Mc * P.maxh);
   P.o_pong = take(P.Bc * Mc * P.maxh);
   P.o_u = take(Mc);
-  P.o_upart = take(P.Bc * std::max(Mc, P.Nb) * ceil_div(std::max(P.maxh, 1), 128));
+  P.o_upart = take(P.Bc * std::max(Mc, P.Nb) * ceil_div(std::max(P.maxh, 1), 64));
   P.o_bzval0 = take(P.Bc * P.Nb * P.h[1]);
   for (int l = 1; l < P.L; ++l) P.o_bpost[l] = take(P.Nb * P.h[l]);
   for (int l = 1; l + 1 < P.L; ++l) P.o_bpre[l] = take(P.Nb * P.h[l + 1]);
@@ -541,7 +541,7 @@ void forward_loss(const Ctx& c, const double* theta, const double* wpad, const d
       ga.bias_bstride = P.D;
       if (l == L - 2 && u_out == nullptr) {
         // last hidden layer: fuse the h_out = 1 output layer, never store this state
-        const int ntn = (int)ceil_div(P.h[l + 1], 128);
+        const int ntn = (int)ceil_div(P.h[l + 1], gemm_act_tile_width(td.S, P.h[l + 1]));
         ga.wlast = theta + P.th[L - 1];
         ga.wlast_bstride = P.D;
         ga.upart = c.at(P.o_upart);
