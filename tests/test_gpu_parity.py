@@ -381,3 +381,10 @@ def test_line_search_phase_is_bit_reproducible():
             ref = ls
         assert torch.equal(ls, ref)
     eng.close()
+
+
+@pytest.mark.parametrize("n_int,n_bnd", [(1, 1), (2, 1), (5, 3)])
+def test_tiny_batches_match_oracle(n_int, n_bnd):
+    """Ragged edge: one or a few collocation points (single-sample tiles, partial splits)."""
+    _oracle_vs_device((2, 16, 8, 1), make_problem("poisson2d_sin"), n_int, n_bnd, 2)
+    _oracle_vs_device((5, 64, 64, 48, 48, 1), make_problem("heat", spatial_dim=4), n_int, n_bnd, 2)
