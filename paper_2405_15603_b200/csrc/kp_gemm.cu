@@ -187,7 +187,8 @@ size_t gemm_tn_partial_doubles(int64_t R, int P, int Q, bool sym) {
 }
 
 template <int BM, int BN, int WM, int WN, int BK, int STAGES>
-__global__ void __launch_bounds__(WM* WN * 32) k_gemm_tn(GemmTN g, TnGrid t, double* partial) {
+__device__ __forceinline__ void tn_block(const GemmTN& g, const TnGrid& t, double* partial,
+                                         int block) {
   constexpr int NT = WM * WN * 32;
   constexpr int LDX = BM + 4, LDY = BN + 4;  // pitch = 4 mod 16 doubles: conflict-free fragments
   constexpr int WTM = BM / WM, WTN = BN / WN;
@@ -199,8 +200,8 @@ __global__ void __launch_bounds__(WM* WN * 32) k_gemm_tn(GemmTN g, TnGrid t, dou
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp / WN, wn = warp % WN;
-  const int split = blockIdx.x / t.pairs;
-  const int pair = blockIdx.x % t.pairs;
+  const int split = block / t.pairs;
+  const int pair = block % t.pairs;
   int tp, tq;
   if (g.sym) {
     tp = (int)((sqrt(8.0 * pair + 1.0) - 1.0) * 0.5);
@@ -302,6 +303,50 @@ __global__ void __launch_bounds__(WM* WN * 32) k_gemm_tn(GemmTN g, TnGrid t, dou
   }
 }
 
+template <int BM, int BN, int WM, int WN, int BK, int STAGES>
+__global__ void __launch_bounds__(WM* WN * 32) k_gemm_tn(GemmTN g, TnGrid t, double* partial) {
+  tn_block<BM, BN, WM, WN, BK, STAGES>(g, t, partial, blockIdx.x);
+}
+
+// Grouped launch: many small contractions (every factor and gradient block of a pass of
+// a small network) share one grid; block b belongs to the job j with
+// begin[j] <= b < begin[j + 1].  Same arithmetic and split order as the single launch.
+constexpr int TN_GROUP_MAX = 40;
+struct TnGroup {
+  int njobs;
+  int begin[TN_GROUP_MAX + 1];
+  GemmTN g[TN_GROUP_MAX];
+  TnGrid t[TN_GROUP_MAX];
+  double* partial[TN_GROUP_MAX];
+  double* acc[TN_GROUP_MAX];
+  int64_t ebegin[TN_GROUP_MAX + 1];  // output-element prefix for the grouped reduce
+};
+
+template <int BM, int BN, int WM, int WN, int BK, int STAGES>
+__global__ void __launch_bounds__(WM* WN * 32) k_gemm_tn_grouped(const __grid_constant__ TnGroup G) {
+  int j = 0;
+  while (j + 1 < G.njobs && (int)blockIdx.x >= G.begin[j + 1]) ++j;
+  tn_block<BM, BN, WM, WN, BK, STAGES>(G.g[j], G.t[j], G.partial[j], blockIdx.x - G.begin[j]);
+}
+
+__global__ void k_tn_reduce_grouped(const __grid_constant__ TnGroup G) {
+  const int64_t total = G.ebegin[G.njobs];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int j = 0;
+    while (j + 1 < G.njobs && e >= G.ebegin[j + 1]) ++j;
+    const int64_t le = e - G.ebegin[j];
+    const int P = G.t[j].P, Q = G.t[j].Q;
+    const int i = (int)(le / Q), c = (int)(le % Q);
+    if (G.g[j].sym && c > i) continue;
+    const int64_t n = (int64_t)P * Q;
+    const double* part = G.partial[j];
+    double v = G.acc[j][le];
+    for (int64_t sp = 0; sp < G.t[j].splits; ++sp) v += part[sp * n + le];
+    G.acc[j][le] = v;
+  }
+}
+
 __global__ void k_tn_reduce(const double* __restrict__ partial, int64_t splits, int P, int Q,
                             bool sym, double* __restrict__ acc) {
   const int64_t n = (int64_t)P * Q;
@@ -335,6 +380,75 @@ void launch_gemm_tn_accumulate(const GemmTN& g, double* partial, double* acc, cu
   const int rb = (int)std::min<int64_t>(ceil_div(n, 256), 148 * 8);
   count_launch();
   k_tn_reduce<<<rb, 256, 0, s>>>(partial, t.splits, P, Q, g.sym, acc);
+}
+
+
+// Splits for a grouped pass: about TN_TARGET_CTAS CTAs in total, shared by the jobs in
+// proportion to their work (rows x tile pairs).
+static void tn_group_grids(const GemmTN* jobs, int n, TnGrid* out) {
+  double work = 0.0;
+  for (int j = 0; j < n; ++j) {
+    const int P = jobs[j].nx + (jobs[j].x_bias ? 1 : 0), Q = jobs[j].ny + (jobs[j].y_bias ? 1 : 0);
+    TnGrid t = tn_grid(jobs[j].R, P, Q, jobs[j].sym);
+    work += (double)std::max<int64_t>(jobs[j].R, 1) * t.pairs;
+    out[j] = t;
+  }
+  for (int j = 0; j < n; ++j) {
+    TnGrid& t = out[j];
+    const int64_t R = std::max<int64_t>(jobs[j].R, 1);
+    const double share = (double)R * t.pairs / std::max(work, 1.0);
+    int64_t splits = std::max<int64_t>(1, (int64_t)(share * TN_TARGET_CTAS / t.pairs));
+    splits = std::min<int64_t>(splits, std::max<int64_t>(1, ceil_div(R, 4 * TN_BK)));
+    const int64_t rps = ceil_div(ceil_div(R, splits), TN_BK) * TN_BK;
+    t.splits = ceil_div(R, rps);
+    t.rows_per_split = rps;
+  }
+}
+
+size_t gemm_tn_grouped_partial_doubles(const GemmTN* jobs, int n) {
+  if (n <= 0 || n > TN_GROUP_MAX) return 0;
+  TnGrid t[TN_GROUP_MAX];
+  tn_group_grids(jobs, n, t);
+  size_t tot = 0;
+  for (int j = 0; j < n; ++j) tot += (size_t)t[j].splits * t[j].P * t[j].Q;
+  return tot;
+}
+
+bool launch_gemm_tn_grouped(const GemmTN* jobs, double* const* accs, int n, double* partial,
+                            size_t partial_cap, cudaStream_t s) {
+  if (n <= 0) return true;
+  if (n > TN_GROUP_MAX) return false;
+  TnGroup G{};
+  G.njobs = n;
+  tn_group_grids(jobs, n, G.t);
+  size_t off = 0;
+  int blocks = 0;
+  int64_t elems = 0;
+  for (int j = 0; j < n; ++j) {
+    G.g[j] = jobs[j];
+    G.acc[j] = accs[j];
+    G.partial[j] = partial + off;
+    off += (size_t)G.t[j].splits * G.t[j].P * G.t[j].Q;
+    G.begin[j] = blocks;
+    blocks += (int)(G.t[j].splits * G.t[j].pairs);
+    G.ebegin[j] = elems;
+    elems += (int64_t)G.t[j].P * G.t[j].Q;
+  }
+  G.begin[n] = blocks;
+  G.ebegin[n] = elems;
+  if (off > partial_cap) return false;
+  auto kern = k_gemm_tn_grouped<TN_BM, TN_BN, TN_WM, TN_WN, TN_BK, TN_STAGES>;
+  const size_t smem = sizeof(double) * TN_STAGES * TN_BK * ((TN_BM + 4) + (TN_BN + 4) + 1);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = true;
+  }
+  count_launch();
+  kern<<<(unsigned)blocks, TN_WM * TN_WN * 32, smem, s>>>(G);
+  count_launch();
+  k_tn_reduce_grouped<<<(unsigned)std::min<int64_t>(ceil_div(elems, 256), 148 * 8), 256, 0, s>>>(G);
+  return true;
 }
 
 }  // namespace kp

@@ -77,6 +77,12 @@ struct GemmTN {
 };
 size_t gemm_tn_partial_doubles(int64_t R, int P, int Q, bool sym);
 void launch_gemm_tn_accumulate(const GemmTN& g, double* partial, double* acc, cudaStream_t s);
+// All of a pass's small contractions in one launch (+ one reduce): acc[j] += job j's
+// P x Q result (P = nx + x_bias, Q = ny + y_bias).  Returns false if the partial space
+// (gemm_tn_grouped_partial_doubles) or the job-table size (40) is exceeded.
+size_t gemm_tn_grouped_partial_doubles(const GemmTN* jobs, int n);
+bool launch_gemm_tn_grouped(const GemmTN* jobs, double* const* accs, int n, double* partial,
+                            size_t partial_cap, cudaStream_t s);
 
 // TMA-fed split-row reduction without bias columns (kp_gemm_tn_tma.cu):
 // acc[p*ldacc + q] += sum_r X[r,p] w(r) Y[r,q], p < nx, q < ny; w(r) = w[r / Sw].

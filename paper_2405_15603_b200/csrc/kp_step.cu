@@ -137,6 +137,8 @@ struct Plan {
   int64_t o_bzval0 = 0, o_bpost[MAXL] = {}, o_bpre[MAXL] = {}, o_bg[MAXL] = {};
   int64_t o_bping = 0, o_bpong = 0, o_ones = 0;
   int64_t o_r = 0, o_rb = 0, o_rls = 0, o_rbls = 0, o_u = 0, o_upart = 0;
+  bool tn_grouped = false;  // small network: grouped TN contractions (accumulate)
+  size_t partial_cap = 0;   // doubles at o_partial
   int64_t o_partial = 0, o_red = 0, o_grad = 0, o_delta = 0, o_dir = 0, o_thc = 0, o_ls = 0;
   int64_t o_A1 = 0, o_A2 = 0, o_B1 = 0, o_B2 = 0, o_la = 0, o_lb = 0, o_T1 = 0, o_T2 = 0;
   int64_t o_work = 0, o_info = 0;
@@ -184,6 +186,12 @@ int64_t per_point_doubles(const kp_net* net) {
   v += (int64_t)S;                                                       // u
   return v;
 }
+
+struct Plan;
+struct StateBufs;
+int tn_pass_jobs(const Plan& P, const double* x, int64_t n, const TaylorDims& td,
+                 const StateBufs* b, const double* gl_last, const double* w, double* accA,
+                 double* accB, double* accG, GemmTN* jobs, double** accs);
 
 int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
   KP_TRY(check_net(&pr->net));
@@ -285,6 +293,19 @@ int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
       upd(Rz, P.q[l], P.h[l], false);
     }
   }
+  if (P.maxh <= 128 && 3 * P.L <= 40) {
+    GemmTN jobs[3 * MAXL];
+    double* accs[3 * MAXL];
+    const TaylorDims tdi{P.S, P.d, true}, tdb{1, 0, false};
+    const int ki = tn_pass_jobs(P, nullptr, P.Nc, tdi, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                nullptr, jobs, accs);
+    part = std::max(part, gemm_tn_grouped_partial_doubles(jobs, ki));
+    const int kb = tn_pass_jobs(P, nullptr, P.Nb, tdb, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                nullptr, jobs, accs);
+    part = std::max(part, gemm_tn_grouped_partial_doubles(jobs, kb));
+    P.tn_grouped = true;
+  }
+  P.partial_cap = part;
   P.o_partial = take((int64_t)part);
   P.r_aint = 0;
   P.r_bint = P.r_aint + P.FA;
@@ -614,6 +635,36 @@ void backward(const Ctx& c, const double* theta, int64_t n, const TaylorDims& td
 // (optim.py:170-176, w = r) and, with w = J v, the exact Gramian-vector product of KFAC*
 // (curvature.py:253-260).  For layer 0 only the value rows of Z0 = [x; I; 0] are dense; the
 // derivative rows e_i contribute a weighted column sum.
+void contract_grad_deriv0(const Ctx& c, int64_t n, const TaylorDims& td, const double* G,
+                          const double* w, double* out);
+
+// The factor and gradient contractions of one pass (an interior chunk of n points or the
+// boundary) as cp.async TN jobs with synthesised bias columns, for the grouped launch of
+// small networks.  Null buffers give shape-only jobs (workspace sizing).
+int tn_pass_jobs(const Plan& P, const double* x, int64_t n, const TaylorDims& td,
+                 const StateBufs* b, const double* gl_last, const double* w, double* accA,
+                 double* accB, double* accG, GemmTN* jobs, double** accs) {
+  int k = 0;
+  const int64_t rows = n * td.S;
+  for (int l = 0; l < P.L; ++l) {
+    const int q = P.q[l], hz = P.h[l];
+    const double* G = (l == P.L - 1) ? gl_last : (b ? b->gout[l] : nullptr);
+    const double* Z = (l == 0) ? x : (b ? b->post[l] : nullptr);
+    const int64_t ldz = (l == 0) ? P.d : P.h[l];
+    const int64_t Rz = (l == 0) ? n : rows;
+    const int Sz = (l == 0) ? 1 : td.S;
+    const int64_t ldg = (l == 0) ? (int64_t)td.S * q : q;
+    const int Sw = (l == 0) ? 1 : td.S;
+    jobs[k] = GemmTN{Z, ldz, hz, true, Z, ldz, hz, true, nullptr, 1, Sz, Rz, true};
+    accs[k++] = accA ? accA + P.fa[l] : nullptr;
+    jobs[k] = GemmTN{G, q, q, false, G, q, q, false, nullptr, 1, 1, rows, true};
+    accs[k++] = accB ? accB + P.fb[l] : nullptr;
+    jobs[k] = GemmTN{G, ldg, q, false, Z, ldz, hz, true, w, Sw, Sz, Rz, false};
+    accs[k++] = accG ? accG + P.th[l] : nullptr;
+  }
+  return k;
+}
+
 void contract_grad_layer(const Ctx& c, const double* x, int64_t n, const TaylorDims& td,
                          const StateBufs& b, const double* gl_last, const double* w,
                          double* accG, int l) {
@@ -635,8 +686,17 @@ void contract_grad_layer(const Ctx& c, const double* x, int64_t n, const TaylorD
     GemmTN gg{G, ldg, q, false, Z, ldz, hz, true, w, Sw, Sz, Rz, false};
     launch_gemm_tn_accumulate(gg, part, out, c.s);
   }
-  // derivative rows e_i: out[j][i] += sum_n w_n Gbar0[n, 1+i, j] (contiguous d x q block)
-  if (l == 0 && td.taylor) {
+  if (l == 0 && td.taylor) contract_grad_deriv0(c, n, td, G, w, out);
+}
+
+// Layer-0 gradient, derivative rows e_i: out[j][i] += sum_n w_n Gbar0[n, 1+i, j] (the
+// contiguous d x q block after each sample's value row).
+void contract_grad_deriv0(const Ctx& c, int64_t n, const TaylorDims& td, const double* G,
+                          const double* w, double* out) {
+  const Plan& P = c.P;
+  double* part = c.at(P.o_partial);
+  const int q = P.q[0], p = P.p[0];
+  {
     if (!c.rot) {
       launch_colsum(G + q, (int64_t)td.S * q, n, P.d * q, w, out, p, 0.0, part, c.s, q);
     } else {  // rows along Q[:, k]: out[j][i] += sum_k (sum_n w_n Gbar0[n, 1+k, j]) Q[i][k]
@@ -660,6 +720,15 @@ void accumulate(const Ctx& c, const double* x, int64_t n, const TaylorDims& td,
   const int L = P.L;
   double* part = c.at(P.o_partial);
   const int64_t rows = n * td.S;
+  if (P.tn_grouped) {  // small network: every contraction of the pass in one launch
+    GemmTN jobs[3 * MAXL];
+    double* accs[3 * MAXL];
+    const int k = tn_pass_jobs(P, x, n, td, &b, gl_last, r, accA, accB, accG, jobs, accs);
+    if (launch_gemm_tn_grouped(jobs, accs, k, part, P.partial_cap, c.s)) {
+      if (td.taylor) contract_grad_deriv0(c, n, td, L == 1 ? gl_last : b.gout[0], r, accG);
+      return;
+    }
+  }
   for (int l = 0; l < L; ++l) {
     const int q = P.q[l], hz = P.h[l], p = P.p[l];
     const double* G = (l == L - 1) ? gl_last : b.gout[l];
