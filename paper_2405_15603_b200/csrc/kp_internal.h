@@ -202,8 +202,21 @@ void launch_split_u(const double* u, int64_t n, int d, double* value, double* gr
 void launch_initial_state(const double* x, int64_t n, int d, double* z, cudaStream_t s);
 
 // ---- optimizer bookkeeping (kp_optim.cu) ------------------------------------
-void launch_factor_finalize(const double* acc, double* F, int n, double scale, double ema,
-                            int diag_n, double diag_add, cudaStream_t s);
+struct FinalizeJob {
+  const double* acc;
+  double* F;
+  int n;
+  double scale;
+  int diag_n;
+  double diag_add;
+};
+struct FinalizeJobs {
+  int n;
+  FinalizeJob job[64];
+  int64_t ebegin[65];
+};
+// EMA update of every factor of a step in one launch.
+void launch_factor_finalize_grouped(FinalizeJobs& J, double ema, cudaStream_t s);
 void launch_grad_finalize(const double* gi, const double* gb, double ni, double nb,
                           double* grad, int64_t D, cudaStream_t s);
 void launch_axpy_out(const double* x, const double* y, double a, double* out, int64_t n,

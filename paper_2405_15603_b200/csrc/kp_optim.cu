@@ -23,26 +23,37 @@ __device__ __forceinline__ void set_status(int32_t* status, int32_t code) {
   atomicCAS(status, 0, code);
 }
 
-// new = lower(acc) (+ diag_add on the first diag_n diagonal entries) / scale;
-// F = ema * F + (1 - ema) * new.  `acc` holds a valid lower triangle.
-__global__ void k_factor_finalize(const double* __restrict__ acc, double* __restrict__ F, int n,
-                                  double scale, double ema, int diag_n, double diag_add) {
-  const int64_t total = (int64_t)n * n;
+// Per factor: new = lower(acc) (+ diag_add on the first diag_n diagonal entries) / scale;
+// F = ema * F + (1 - ema) * new (`acc` holds a valid lower triangle).  All factors of a
+// step in one launch; element e belongs to the job k with ebegin[k] <= e < ebegin[k + 1].
+__global__ void k_factor_finalize_grouped(const __grid_constant__ FinalizeJobs J, double ema) {
+  const int64_t total = J.ebegin[J.n];
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(e / n), j = (int)(e % n);
+    int k = 0;
+    while (k + 1 < J.n && e >= J.ebegin[k + 1]) ++k;
+    const FinalizeJob& jb = J.job[k];
+    const int64_t le = e - J.ebegin[k];
+    const int n = jb.n;
+    const int i = (int)(le / n), j = (int)(le % n);
     const int a = max(i, j), b = min(i, j);
-    double v = acc[(int64_t)a * n + b];
-    if (i == j && i < diag_n) v += diag_add;
-    const double nw = v / scale;
-    F[e] = ema * F[e] + (1.0 - ema) * nw;
+    double v = jb.acc[(int64_t)a * n + b];
+    if (i == j && i < jb.diag_n) v += jb.diag_add;
+    const double nw = v / jb.scale;
+    jb.F[le] = ema * jb.F[le] + (1.0 - ema) * nw;
   }
 }
 
-void launch_factor_finalize(const double* acc, double* F, int n, double scale, double ema,
-                            int diag_n, double diag_add, cudaStream_t s) {
+void launch_factor_finalize_grouped(FinalizeJobs& J, double ema, cudaStream_t s) {
+  if (J.n <= 0) return;
+  int64_t e = 0;
+  for (int k = 0; k < J.n; ++k) {
+    J.ebegin[k] = e;
+    e += (int64_t)J.job[k].n * J.job[k].n;
+  }
+  J.ebegin[J.n] = e;
   count_launch();
-  k_factor_finalize<<<grid1((int64_t)n * n), 256, 0, s>>>(acc, F, n, scale, ema, diag_n, diag_add);
+  k_factor_finalize_grouped<<<grid1(e), 256, 0, s>>>(J, ema);
 }
 
 __global__ void k_grad_finalize(const double* __restrict__ gi, const double* __restrict__ gb,

@@ -858,15 +858,16 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
   double* red = c.at(P.o_red);
   const double Ng = cfg->n_interior_global, Nbg = cfg->n_boundary_global;
   const double ema = cfg->ema;
-  for (int l = 0; l < P.L; ++l) {
-    launch_factor_finalize(red + P.r_aint + P.fa[l], st->a_int + P.fa[l], P.p[l], Ng * P.S, ema,
-                           l == 0 ? P.d : 0, Ng, c.s);
-    launch_factor_finalize(red + P.r_bint + P.fb[l], st->b_int + P.fb[l], P.q[l], Ng, ema, 0, 0.0,
-                           c.s);
-    launch_factor_finalize(red + P.r_abnd + P.fa[l], st->a_bnd + P.fa[l], P.p[l], Nbg, ema, 0,
-                           0.0, c.s);
-    launch_factor_finalize(red + P.r_bbnd + P.fb[l], st->b_bnd + P.fb[l], P.q[l], Nbg, ema, 0,
-                           0.0, c.s);
+  {  // EMA of the normalised factor sums (curvature.py:79-85, 112-115, 133-134), one launch
+    FinalizeJobs fj{};
+    for (int l = 0; l < P.L; ++l) {
+      fj.job[fj.n++] = FinalizeJob{red + P.r_aint + P.fa[l], st->a_int + P.fa[l], P.p[l], Ng * P.S,
+                                   l == 0 ? P.d : 0, Ng};
+      fj.job[fj.n++] = FinalizeJob{red + P.r_bint + P.fb[l], st->b_int + P.fb[l], P.q[l], Ng, 0, 0.0};
+      fj.job[fj.n++] = FinalizeJob{red + P.r_abnd + P.fa[l], st->a_bnd + P.fa[l], P.p[l], Nbg, 0, 0.0};
+      fj.job[fj.n++] = FinalizeJob{red + P.r_bbnd + P.fb[l], st->b_bnd + P.fb[l], P.q[l], Nbg, 0, 0.0};
+    }
+    launch_factor_finalize_grouped(fj, ema, c.s);
   }
   double* grad = c.at(P.o_grad);
   launch_grad_finalize(red + P.r_gint, red + P.r_gbnd, Ng, Nbg, grad, P.D, c.s);
