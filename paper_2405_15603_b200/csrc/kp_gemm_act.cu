@@ -264,21 +264,15 @@ bool run_act(const GemmAct& g, int box_rows, cudaStream_t s) {
 
 // Tile shapes up to 13 m8 tiles (one large sample per tile): 4 warps x 128 units, BK 16,
 // 3 stages -> ~111 KB, two CTAs per SM.  14-16 tiles (many small samples per tile): 4 warps
-// x 64 units; narrow layers (N <= 64, short K) with BK 32 and 2 stages, otherwise BK 16 and
-// 3 stages with three CTAs per SM.
+// x 64 units, BK 16, 3 stages, three CTAs per SM.
 template <int MODE, int TM>
 bool run_act_tm(const GemmAct& g, int box_rows, cudaStream_t s) {
   if constexpr (TM <= 13) {
     return run_act<MODE, TM, 4, 16, 3>(g, box_rows, s);
   } else {
-    // (15 m8 tiles with BK 32 exceed the register file: BK 16 only)
-    if (g.N <= 64) {
-      if constexpr (TM != 15)
-        if (g.K % 32 == 0 && g.K <= 64) return run_act<MODE, TM, 4, 32, 2, 64>(g, box_rows, s);
-      return run_act<MODE, TM, 4, 16, 3, 64, 3>(g, box_rows, s);
-    }
-    // wider layers: 64-unit tiles, 4 warps, three CTAs per SM (~72 KB each) so that
-    // epilogues overlap other CTAs' k loops (c4 line search -11% vs 8 warps x 128 units)
+    // 64-unit tiles, 4 warps, BK 16, 3 stages, three CTAs per SM (~72 KB each) so that
+    // epilogues overlap other CTAs' k loops (vs 8 warps x 128 units: c4 line search -11%;
+    // vs BK 32 x 2 stages for short K: c1-c3 line search -7%)
     return run_act<MODE, TM, 4, 16, 3, 64, 3>(g, box_rows, s);
   }
 }
@@ -292,8 +286,7 @@ int gemm_act_samples_per_tile(int S) { return S <= ROWS_MAX ? ROWS_MAX / S : 0; 
 int gemm_act_tile_width(int S, int N) {
   const int nb = gemm_act_samples_per_tile(S);
   const int tm = nb > 0 ? (nb * S + 7) / 8 : 0;
-  if (tm <= 13) return BN_MAX;
-  return 64;
+  return tm <= 13 ? BN_MAX : 64;
 }
 
 bool gemm_act_ok(int S, int K, int64_t lda, int64_t ldb) {
