@@ -182,8 +182,8 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2405_15603_b200 import configs
-    from paper_2405_15603_b200.dist import (ShardedKfacStarStep, ShardedKfacStep, make_rank_engine,
-                                            torch_all_reduce)
+    from paper_2405_15603_b200.dist import (ShardedKfacStarStep, ShardedKfacStep, layer_owners,
+                                            make_rank_engine, torch_all_reduce)
     from paper_2405_15603_b200.engine import KfacEngine
 
     rank, world, local = dist_env()
@@ -207,7 +207,7 @@ def run_ours(args):
         eng = make_rank_engine(wl.widths, batch, prob, rank, world, ema=wl.ema, damping=wl.damping,
                                momentum=wl.momentum, chunk=args.chunk or None)
         cls = ShardedKfacStarStep if args.optimizer == "kfac_star" else ShardedKfacStep
-        stepper = cls(eng, torch_all_reduce())
+        stepper = cls(eng, torch_all_reduce(), owners=layer_owners(wl.widths, world), rank=rank)
         do_step = stepper.step
     else:
         eng = make_rank_engine(wl.widths, batch, prob, 0, 1, ema=wl.ema, damping=wl.damping,

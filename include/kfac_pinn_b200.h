@@ -38,7 +38,7 @@ extern "C" {
 #endif
 
 #define KP_MAX_LAYERS 16
-#define KP_ABI_VERSION 3
+#define KP_ABI_VERSION 4
 
 typedef enum kp_status {
   KP_OK = 0,
@@ -176,6 +176,25 @@ int32_t kp_kfac_phase_linesearch(kp_context* ctx, const kp_problem* prob,
 int32_t kp_kfac_phase_update(kp_context* ctx, const kp_problem* prob, const kp_kfac_config* cfg,
                              kp_state* st, kp_step_out* out, void* workspace,
                              size_t workspace_bytes, void* stream);
+
+/* Distributed Kronecker solves.  The precondition phase split in
+ * two around a third exchange: kp_kfac_phase_precondition_owned normalises + EMAs every
+ * factor and the gradient like kp_kfac_phase_precondition, but solves only the layers with
+ * owned_layers[l] != 0 (host array, n_layers entries) and writes zeros to the other layers'
+ * Delta rows.  The caller then sum-all-reduces the buffer of kp_direction_buffer
+ * ([Delta (D) | 8 status slots]); with each layer owned by exactly one rank the sum is the
+ * owner's Delta bit for bit.  kp_kfac_phase_direction merges the status slots (every rank
+ * adopts the smallest failure code any rank saw) and forms delta^ = Delta + mu prev
+ * (src/optim.py:254).  Replaces the solve loop of src/curvature.py:150-163. */
+int32_t kp_direction_buffer(kp_context* ctx, const kp_problem* prob, void* workspace,
+                            double** ptr, int64_t* count);
+int32_t kp_kfac_phase_precondition_owned(kp_context* ctx, const kp_problem* prob,
+                                         const kp_kfac_config* cfg, kp_state* st,
+                                         kp_step_out* out, const int32_t* owned_layers,
+                                         void* workspace, size_t workspace_bytes, void* stream);
+int32_t kp_kfac_phase_direction(kp_context* ctx, const kp_problem* prob,
+                                const kp_kfac_config* cfg, kp_state* st, kp_step_out* out,
+                                void* workspace, size_t workspace_bytes, void* stream);
 
 /* KFAC* step (src/optim.py:266-320): the same factors and preconditioned direction
  * Delta as kp_kfac_step, then the exact Gramian-vector products G Delta and G prev

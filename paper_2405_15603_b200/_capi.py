@@ -13,7 +13,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libkfac_pinn_b200.so")
 MAX_LAYERS = 16
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 KP_OK = 0
 KP_ERR_INVALID = 1
@@ -79,6 +79,14 @@ _SIGS = {
     "kp_kfac_phase_precondition": (C.c_int32, [C.c_void_p, P(kp_problem), P(kp_kfac_config),
                                                P(kp_state), P(kp_step_out), C.c_void_p,
                                                C.c_size_t, C.c_void_p]),
+    "kp_direction_buffer": (C.c_int32, [C.c_void_p, P(kp_problem), C.c_void_p, P(C.c_void_p),
+                                        P(C.c_int64)]),
+    "kp_kfac_phase_precondition_owned": (C.c_int32, [C.c_void_p, P(kp_problem), P(kp_kfac_config),
+                                                     P(kp_state), P(kp_step_out), P(C.c_int32),
+                                                     C.c_void_p, C.c_size_t, C.c_void_p]),
+    "kp_kfac_phase_direction": (C.c_int32, [C.c_void_p, P(kp_problem), P(kp_kfac_config),
+                                            P(kp_state), P(kp_step_out), C.c_void_p, C.c_size_t,
+                                            C.c_void_p]),
     "kp_kfac_phase_linesearch": (C.c_int32, [C.c_void_p, P(kp_problem), P(kp_kfac_config),
                                              P(kp_state), P(kp_batch), P(kp_step_out), C.c_void_p,
                                              C.c_size_t, C.c_void_p]),

@@ -244,6 +244,8 @@ void launch_eig_status(const double* la, int p, const double* lb, int q, const i
 void launch_kron_scale(double* W, const double* la, int p, const double* lb, int q,
                        cudaStream_t s);
 void launch_set_status(int32_t* status, int32_t code, cudaStream_t s);
+void launch_status_slots(const int32_t* status, double* slots, cudaStream_t s);
+void launch_slots_status(const double* slots, int32_t* status, cudaStream_t s);
 // KFAC*: batched deterministic dot products, quadratic-model solve and update
 struct DotJobs {
   const double* a[8];

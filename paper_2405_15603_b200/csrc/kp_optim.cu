@@ -337,6 +337,32 @@ void launch_star_solve_update(const double* dots, double lam, double* theta, dou
   k_star_update<<<grid1(D), 256, 0, s>>>(theta, prev, delta, D, scalars, status);
 }
 
+// Status <-> exchange slots for the distributed Kronecker solves: slot k = 1 when this rank's
+// status is k; after the sum all-reduce, slot k counts the ranks that saw code k and every
+// rank adopts the smallest code seen anywhere (deterministic across ranks).
+__global__ void k_status_slots(const int32_t* status, double* slots) {
+  const int k = threadIdx.x;
+  if (k < 8) slots[k] = (k > 0 && *status == k) ? 1.0 : 0.0;
+}
+
+__global__ void k_slots_status(const double* slots, int32_t* status) {
+  for (int k = 1; k < 8; ++k)
+    if (slots[k] > 0.0) {
+      *status = k;
+      return;
+    }
+}
+
+void launch_status_slots(const int32_t* status, double* slots, cudaStream_t s) {
+  count_launch();
+  k_status_slots<<<1, 32, 0, s>>>(status, slots);
+}
+
+void launch_slots_status(const double* slots, int32_t* status, cudaStream_t s) {
+  count_launch();
+  k_slots_status<<<1, 1, 0, s>>>(slots, status);
+}
+
 __global__ void k_set_status(int32_t* status, int32_t code) { set_status(status, code); }
 
 void launch_set_status(int32_t* status, int32_t code, cudaStream_t s) {

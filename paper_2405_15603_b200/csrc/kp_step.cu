@@ -139,7 +139,7 @@ struct Plan {
   int64_t o_r = 0, o_rb = 0, o_rls = 0, o_rbls = 0, o_u = 0, o_upart = 0;
   bool tn_grouped = false;  // small network: grouped TN contractions (accumulate)
   size_t partial_cap = 0;   // doubles at o_partial
-  int64_t o_partial = 0, o_red = 0, o_grad = 0, o_delta = 0, o_dir = 0, o_thc = 0, o_ls = 0;
+  int64_t o_partial = 0, o_red = 0, o_grad = 0, o_delta = 0, o_dslot = 0, o_dir = 0, o_thc = 0, o_ls = 0;
   int64_t o_A1 = 0, o_A2 = 0, o_B1 = 0, o_B2 = 0, o_la = 0, o_lb = 0, o_T1 = 0, o_T2 = 0;
   int64_t o_work = 0, o_info = 0;
   // per-layer Kronecker-solve scratch (layers solve concurrently on side streams)
@@ -317,7 +317,8 @@ int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
   P.r_count = P.r_ss + 2;
   P.o_red = take(P.r_count);
   P.o_grad = take(P.D);
-  P.o_delta = take(P.D);
+  P.o_delta = take(P.D + 8);  // delta, then 8 status slots: the direction exchange buffer
+  P.o_dslot = P.o_delta + P.D;
   P.o_dir = take(P.D);
   P.o_thc = take(P.Bc * P.D);
   P.o_wpad = take(woff);
@@ -853,7 +854,17 @@ int kron_solve(kp_context* ctx, const Ctx& c, int p, int q, double* A1, double* 
                       c.at(P.o_T2));
 }
 
-int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp_step_out* out) {
+// `owned` (host, L flags) = nullptr: every layer's Kronecker solve runs here and the phase
+// ends with the momentum direction (phase_direction).  Otherwise only the flagged layers are
+// solved; the others' Delta rows are zeroed and the phase stops at the direction exchange
+// buffer [Delta | status slots] (kp_direction_buffer), which the ranks sum-all-reduce —
+// every layer is owned by exactly one rank, so the sum is that rank's Delta bit for bit —
+// before phase_direction.
+int phase_direction(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp_step_out* out,
+                    bool merge_slots);
+
+int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp_step_out* out,
+                       const int32_t* owned) {
   const Plan& P = c.P;
   double* red = c.at(P.o_red);
   const double Ng = cfg->n_interior_global, Nbg = cfg->n_boundary_global;
@@ -884,7 +895,8 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
   // combined with cuBLAS on its side stream.
   auto pair_small = [&](int l, int k) { return (k == 0 ? P.p[l] : P.q[l]) <= small_eig_max_n(); };
   bool any_big = false;
-  for (int l = 0; l < P.L; ++l) any_big |= !pair_small(l, 0) || !pair_small(l, 1);
+  for (int l = 0; l < P.L; ++l)
+    any_big |= (!owned || owned[l]) && (!pair_small(l, 0) || !pair_small(l, 1));
   cudaEvent_t ready = nullptr, small_done = nullptr;
   if (any_big) {
     KP_TRY(ensure_side_streams(ctx, 2 * P.L + 2));
@@ -945,6 +957,19 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
     for (int l = 0; l < P.L; ++l) {
       int* info = reinterpret_cast<int*>(c.at(P.k_info[l]));
       const bool sa = pair_small(l, 0), sb = pair_small(l, 1);
+      if (owned && !owned[l]) {  // another rank solves this layer; keep warm slots stable
+        SmallEigJob skip{};
+        if (sa) {
+          skip.n = P.p[l];
+          warm(skip);
+        }
+        if (sb) {
+          skip.n = P.q[l];
+          warm(skip);
+        }
+        KP_CUDA_TRY(cudaMemsetAsync(delta + P.th[l], 0, sizeof(double) * P.p[l] * P.q[l], c.s));
+        continue;
+      }
       if (sa) {
         ej.job[ne++] = SmallEigJob{P.p[l], st->a_int + P.fa[l], st->a_bnd + P.fa[l], lam,
                                    c.at(P.k_A1[l]), c.at(P.k_la[l]), info, sb ? 0 : 1};
@@ -1018,6 +1043,21 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
     KP_CUDA_TRY(cudaEventRecord(ctx->side_ev[2 * l], s));
   }
   for (int l : big) KP_CUDA_TRY(cudaStreamWaitEvent(c.s, ctx->side_ev[2 * l], 0));
+  if (owned) {
+    launch_status_slots(out->status, c.at(P.o_dslot), c.s);
+    return KP_OK;
+  }
+  return phase_direction(c, cfg, st, out, false);
+}
+
+// delta^ = Delta + mu prev (optim.py:254) and the optional grad / Delta outputs; after a
+// distributed solve the status slots summed over ranks are merged into *out->status first.
+int phase_direction(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp_step_out* out,
+                    bool merge_slots) {
+  const Plan& P = c.P;
+  double* grad = c.at(P.o_grad);
+  double* delta = c.at(P.o_delta);
+  if (merge_slots) launch_slots_status(c.at(P.o_dslot), out->status, c.s);
   launch_axpy_out(delta, st->prev_update, cfg->momentum, c.at(P.o_dir), P.D, c.s);
   if (out->grad) KP_CUDA_TRY(cudaMemcpyAsync(out->grad, grad, sizeof(double) * P.D,
                                              cudaMemcpyDeviceToDevice, c.s));
@@ -1360,6 +1400,15 @@ int32_t kp_reduce_buffer(kp_context* ctx, const kp_problem* pr, void* ws, double
   return KP_OK;
 }
 
+int32_t kp_direction_buffer(kp_context* ctx, const kp_problem* pr, void* ws, double** ptr,
+                            int64_t* count) {
+  Plan P;
+  KP_TRY(cached_plan(ctx, pr, P));
+  *ptr = static_cast<double*>(ws) + P.o_delta;
+  *count = P.D + 8;
+  return KP_OK;
+}
+
 int32_t kp_linesearch_buffer(kp_context* ctx, const kp_problem* pr, void* ws, double** ptr,
                              int64_t* count) {
   Plan P;
@@ -1416,7 +1465,27 @@ int32_t kp_kfac_phase_precondition(kp_context* ctx, const kp_problem* prob,
                                    const kp_kfac_config* cfg, kp_state* st, kp_step_out* out,
                                    void* ws, size_t ws_bytes, void* stream) {
   KP_PHASE_PROLOGUE
-  KP_TRY(phase_precondition(c, cfg, st, out));
+  KP_TRY(phase_precondition(c, cfg, st, out, nullptr));
+  KP_CUDA_TRY(cudaGetLastError());
+  return KP_OK;
+}
+
+int32_t kp_kfac_phase_precondition_owned(kp_context* ctx, const kp_problem* prob,
+                                         const kp_kfac_config* cfg, kp_state* st,
+                                         kp_step_out* out, const int32_t* owned_layers,
+                                         void* ws, size_t ws_bytes, void* stream) {
+  KP_PHASE_PROLOGUE
+  if (!owned_layers) return KP_ERR_INVALID;
+  KP_TRY(phase_precondition(c, cfg, st, out, owned_layers));
+  KP_CUDA_TRY(cudaGetLastError());
+  return KP_OK;
+}
+
+int32_t kp_kfac_phase_direction(kp_context* ctx, const kp_problem* prob,
+                                const kp_kfac_config* cfg, kp_state* st, kp_step_out* out,
+                                void* ws, size_t ws_bytes, void* stream) {
+  KP_PHASE_PROLOGUE
+  KP_TRY(phase_direction(c, cfg, st, out, true));
   KP_CUDA_TRY(cudaGetLastError());
   return KP_OK;
 }
@@ -1453,7 +1522,7 @@ int32_t kp_kfac_step(kp_context* ctx, const kp_problem* prob, const kp_kfac_conf
   KP_TRY(rotated_batch(c, bt_in, bt_rot, bt));
   KP_CUDA_TRY(cudaMemsetAsync(out->status, 0, sizeof(int32_t), c.s));
   KP_TRY(phase_accumulate(c, cfg, st, bt));
-  KP_TRY(phase_precondition(c, cfg, st, out));
+  KP_TRY(phase_precondition(c, cfg, st, out, nullptr));
   KP_TRY(phase_linesearch(c, cfg, st, bt));
   KP_TRY(phase_update(c, cfg, st, out));
   KP_CUDA_TRY(cudaGetLastError());
@@ -1502,7 +1571,7 @@ int32_t kp_kfac_star_step(kp_context* ctx, const kp_problem* prob, const kp_kfac
   KP_TRY(rotated_batch(c, bt_in, bt_rot, bt));
   KP_CUDA_TRY(cudaMemsetAsync(out->status, 0, sizeof(int32_t), c.s));
   KP_TRY(phase_accumulate(c, cfg, st, bt));
-  KP_TRY(phase_precondition(c, cfg, st, out));
+  KP_TRY(phase_precondition(c, cfg, st, out, nullptr));
   KP_TRY(phase_star_gvp(c, cfg, st, bt));
   KP_TRY(phase_star_update(c, cfg, st, out));
   KP_CUDA_TRY(cudaGetLastError());

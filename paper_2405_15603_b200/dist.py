@@ -12,9 +12,16 @@ device buffer:
 2. after the local line search: the 2 x 31 per-candidate sums of r^2
    (``kp_linesearch_buffer``).
 
-Normalisation by the global point counts, the EMA, the Kronecker-sum solves
-and the argmin are then computed redundantly — and bit-identically, since the
-all-reduced inputs are identical — on every rank.
+Normalisation by the global point counts, the EMA and the argmin are then
+computed redundantly — and bit-identically, since the all-reduced inputs are
+identical — on every rank.  The per-layer Kronecker-sum solves
+(src/curvature.py:150-163) are distributed by layer when any factor is too
+large for the on-device solver: each layer is owned by
+one rank (``layer_owners``), the owner writes its Delta rows and every other
+rank zeros, and a third sum all-reduce of ``kp_direction_buffer`` (Delta plus
+status slots) hands every rank the owners' Delta bit for bit.  Networks whose
+factors all fit the on-device solver (one launch for every layer) solve
+redundantly: an exchange would cost more than it saves.
 """
 
 from __future__ import annotations
@@ -33,6 +40,30 @@ def shard_bounds(n: int, rank: int, world: int):
     return lo, lo + base + (1 if rank < extra else 0)
 
 
+SMALL_EIG_MAX_N = 96  # factor pairs up to this size use the one-launch device solver (kp_step.cu)
+
+
+def layer_owners(widths, world: int):
+    """Owner rank of each layer's Kronecker solve, or None to solve redundantly.
+
+    Greedy longest-processing-time assignment on the solve cost p^3 + q^3 of the layer's
+    two generalised eigenproblems (p = h_l + 1, q = h_{l+1}); deterministic, so every
+    rank computes the same table.
+    """
+    widths = [int(w) for w in widths]
+    sizes = [(widths[l] + 1, widths[l + 1]) for l in range(len(widths) - 1)]
+    if world <= 1 or all(max(p, q) <= SMALL_EIG_MAX_N for p, q in sizes):
+        return None
+    cost = [float(p) ** 3 + float(q) ** 3 for p, q in sizes]
+    load = [0.0] * world
+    owners = [0] * len(sizes)
+    for l in sorted(range(len(sizes)), key=lambda i: (-cost[i], i)):
+        r = min(range(world), key=lambda k: (load[k], k))
+        owners[l] = r
+        load[r] += cost[l]
+    return owners
+
+
 class ShardedKfacStep:
     """Drives one rank's engine through the phased step with all-reduces in between.
 
@@ -41,15 +72,26 @@ class ShardedKfacStep:
     tests inject a CPU stand-in to check this orchestration under gloo).
     """
 
-    def __init__(self, engine, all_reduce):
+    def __init__(self, engine, all_reduce, owners=None, rank: int = 0):
         self.engine = engine
         self.all_reduce = all_reduce
+        # owners: per-layer owner rank (layer_owners) or None for redundant solves
+        self.owned = None if owners is None else [o == rank for o in owners]
+
+    def _precondition(self):
+        e = self.engine
+        if self.owned is None:
+            e.phase("precondition")
+            return
+        e.phase("precondition_owned", owned=self.owned)
+        self.all_reduce(e.direction_buffer())
+        e.phase("direction")
 
     def step(self):
         e = self.engine
         e.phase("accumulate")
         self.all_reduce(e.reduce_buffer())
-        e.phase("precondition")
+        self._precondition()
         e.phase("linesearch")
         self.all_reduce(e.linesearch_buffer())
         e.phase("update")
@@ -66,7 +108,7 @@ class ShardedKfacStarStep(ShardedKfacStep):
         e = self.engine
         e.phase("accumulate")
         self.all_reduce(e.reduce_buffer())
-        e.phase("precondition")
+        self._precondition()
         e.phase("star_gvp")
         self.all_reduce(e.gvp_buffer())
         e.phase("star_update")

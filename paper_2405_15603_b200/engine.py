@@ -310,6 +310,13 @@ class KfacEngine:
                                                        C.c_void_p(_ptr(self.ws)), C.byref(ptr), C.byref(cnt)))
         return self._view(ptr.value, cnt.value)
 
+    def direction_buffer(self):
+        ptr, cnt = C.c_void_p(), C.c_int64()
+        raise_for_status(self.lib.kp_direction_buffer(self.ctx, C.byref(self.prob),
+                                                      C.c_void_p(_ptr(self.ws)), C.byref(ptr),
+                                                      C.byref(cnt)))
+        return self._view(ptr.value, cnt.value)
+
     def gvp_buffer(self):
         ptr, cnt = C.c_void_p(), C.c_int64()
         raise_for_status(self.lib.kp_gvp_buffer(self.ctx, C.byref(self.prob), C.c_void_p(_ptr(self.ws)),
@@ -322,9 +329,15 @@ class KfacEngine:
         assert off % 8 == 0 and off >= 0
         return self.ws[off: off + 8 * count].view(self.torch.float64)
 
-    def phase(self, name: str):
+    def phase(self, name: str, owned=None):
+        """Run one phase; ``precondition_owned`` solves only the layers flagged in ``owned``."""
         a = self._args()
-        if name == "accumulate":
+        if name == "precondition_owned":
+            flags = (C.c_int32 * (len(self.widths) - 1))(*[1 if o else 0 for o in owned])
+            rc = self.lib.kp_kfac_phase_precondition_owned(*a[:4], *a[5:6], flags, *a[6:])
+        elif name == "direction":
+            rc = self.lib.kp_kfac_phase_direction(*a[:4], *a[5:])
+        elif name == "accumulate":
             rc = self.lib.kp_kfac_phase_accumulate(*a)
         elif name == "linesearch":
             rc = self.lib.kp_kfac_phase_linesearch(*a)

@@ -66,8 +66,14 @@ class CpuShardEngine:
                 off += n
         return out, v[off], v[off + 1]
 
-    def phase(self, name):
-        getattr(self, "_" + name)()
+    def direction_buffer(self):
+        return self.dirbuf
+
+    def phase(self, name, owned=None):
+        if name == "precondition_owned":
+            self._precondition_owned(owned)
+        else:
+            getattr(self, "_" + name)()
 
     def _accumulate(self):
         lin_in, pre, (u, gu, lu) = orc.taylor_forward(self.w, self.b, self.x, self.cd)
@@ -108,6 +114,23 @@ class CpuShardEngine:
         delta = orc.precondition(kf, grads)
         self.delta = delta
         self.grads = grads
+        self.dir = [d + self.mu * p for d, p in zip(delta, self.prev)]
+
+    # distributed solves: Delta of the owned layers, zeros elsewhere, + 8 status slots
+    def _precondition_owned(self, owned):
+        self._precondition()
+        parts = [d if own else np.zeros_like(d) for d, own in zip(self.delta, owned)]
+        self.dirbuf = torch.from_numpy(np.concatenate([p.ravel() for p in parts] + [np.zeros(8)]))
+        self.delta = None
+
+    def _direction(self):
+        v = self.dirbuf.numpy()
+        assert not v[-8:].any()
+        off, delta = 0, []
+        for p in self.prev:
+            delta.append(v[off:off + p.size].reshape(p.shape).copy())
+            off += p.size
+        self.delta = delta
         self.dir = [d + self.mu * p for d, p in zip(delta, self.prev)]
 
     def _linesearch(self):

@@ -24,7 +24,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, q, star=False, wkey="c3"):
+def _worker(rank, world, port, q, star=False, wkey="c3", owners=None):
     import sys
 
     here = os.path.dirname(os.path.abspath(__file__))
@@ -46,16 +46,20 @@ def _worker(rank, world, port, q, star=False, wkey="c3"):
         eng = CpuShardEngine(params.weights, params.biases, batch.interior[i0:i1],
                              batch.boundary[b0:b1], batch.boundary_targets[b0:b1], prob, 90, 31,
                              ema=wl.ema, damping=wl.damping, momentum=0.3)
-        stepper = (ShardedKfacStarStep if star else ShardedKfacStep)(eng, torch_all_reduce())
+        stepper = (ShardedKfacStarStep if star else ShardedKfacStep)(eng, torch_all_reduce(),
+                                                                      owners=owners, rank=rank)
         infos = [stepper.step() for _ in range(3)]
         q.put((rank, infos, [w.copy() for w in eng.w]))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("star,wkey", [(False, "c3"), (True, "c3"), (False, "dense")],
-                         ids=["kfac", "kfac_star", "kfac_dense_coeffs"])
-def test_sharded_step_matches_single_process_oracle(star, wkey):
+@pytest.mark.parametrize("star,wkey,owners", [(False, "c3", None), (True, "c3", None),
+                                               (False, "dense", None), (False, "c3", [0, 1, 1, 0, 1]),
+                                               (True, "c3", [1, 0, 0, 1, 0])],
+                         ids=["kfac", "kfac_star", "kfac_dense_coeffs", "kfac_distributed_solves",
+                              "kfac_star_distributed_solves"])
+def test_sharded_step_matches_single_process_oracle(star, wkey, owners):
     from oracle import kfac_oracle as orc
     from paper_2405_15603_b200 import configs
 
@@ -63,7 +67,7 @@ def test_sharded_step_matches_single_process_oracle(star, wkey):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, star, wkey)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, star, wkey, owners)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
@@ -90,3 +94,19 @@ def test_sharded_step_matches_single_process_oracle(star, wkey):
     # every rank ends with identical parameters (replicated state)
     for w0, w1 in zip(res[0][2], res[1][2]):
         assert np.array_equal(w0, w1)
+
+
+def test_layer_owners():
+    from paper_2405_15603_b200.dist import layer_owners
+
+    # all factors fit the one-launch device solver: redundant solves, no exchange
+    assert layer_owners([2, 64, 64, 48, 48, 1], 4) is None
+    c5 = [100, 768, 768, 512, 512, 1]
+    assert layer_owners(c5, 1) is None
+    # one owner per layer, the two largest layers on different ranks, deterministic
+    o2 = layer_owners(c5, 2)
+    assert o2 == layer_owners(c5, 2) and set(o2) == {0, 1} and o2[1] != o2[2]
+    assert sorted(layer_owners(c5, 8)) == [0, 1, 2, 3, 4]
+    c4 = [10, 256, 256, 128, 128, 1]
+    o4 = layer_owners(c4, 4)
+    assert len(o4) == 5 and set(o4) == {0, 1, 2, 3}

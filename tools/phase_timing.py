@@ -1,6 +1,11 @@
 """Per-phase CUDA-event timing of one KFAC step (diagnostic, not the bench).
 
     python tools/phase_timing.py --workload c5 --n-interior 3000 [--chunk 0] [--reps 3]
+                                 [--owned-world W]
+
+--owned-world W: also time the precondition phase as each rank r < W of a W-GPU run does it
+with distributed Kronecker solves (dist.layer_owners; the direction all-reduce excluded) and
+report the slowest rank's time as "precondition_owned_max_ms".
 """
 import argparse
 import json
@@ -18,11 +23,12 @@ def main():
     ap.add_argument("--n-boundary", type=int, default=None)
     ap.add_argument("--chunk", type=int, default=0)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--owned-world", type=int, default=0)
     a = ap.parse_args()
     import torch
 
     from paper_2405_15603_b200 import configs
-    from paper_2405_15603_b200.dist import make_rank_engine
+    from paper_2405_15603_b200.dist import layer_owners, make_rank_engine
 
     wl = configs.WORKLOADS[a.workload]
     nb = a.n_boundary if a.n_boundary is not None else (wl.n_boundary if a.n_interior == wl.n_interior else a.n_interior // 3)
@@ -49,6 +55,22 @@ def main():
         res["total_ms"] = evs[0].elapsed_time(evs[4])
         res["status"] = code
         res["alpha"] = float(sc[2])
+    owners = layer_owners(wl.widths, a.owned_world) if a.owned_world > 1 else None
+    if owners is not None:
+        worst = 0.0
+        for r in range(a.owned_world):
+            t = []
+            for rep in range(a.reps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                eng.phase("accumulate")
+                e0.record()
+                eng.phase("precondition_owned", owned=[o == r for o in owners])
+                e1.record()
+                torch.cuda.synchronize()
+                t.append(e0.elapsed_time(e1))
+            worst = max(worst, min(t))
+        res["owners"] = owners
+        res["precondition_owned_max_ms"] = worst
     f = configs.flops_per_step(wl.widths, a.n_interior, nb)
     res["alg_tflops_per_s"] = f / (res["total_ms"] / 1e3) / 1e12
     res["workload"] = wl.name
