@@ -301,8 +301,14 @@ void launch_last_layer(const double* post, int64_t n, int h, const double* theta
 // ---------------------------------------------------------------------------
 // activation backward (taylor.py:206-239)
 
-__global__ void k_act_bwd(ActBwd a, int64_t n, int h, TaylorDims td,
-                          const double* __restrict__ cdiag) {
+// One thread per (sample, unit) walks the sample's S rows (coalesced across the warp's units).
+// Variants: PRE = stored pre-activation state (else layer 0: value z + W0^T rows);
+// GIN = full upstream adjoint (else the rank-1 seed x w_last of the h_out = 1 layer).
+// Derivative rows go in batches of 8 loads in flight (memory-level parallelism) through
+// running row pointers, two CTAs of 256 per SM.
+template <bool PRE, bool GIN>
+__global__ void __launch_bounds__(256, 2) k_act_bwd(ActBwd a, int64_t n, int h, TaylorDims td,
+                                                    const double* __restrict__ cdiag) {
   const int64_t total = n * h;
   const int d = td.d;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -310,47 +316,52 @@ __global__ void k_act_bwd(ActBwd a, int64_t n, int h, TaylorDims td,
     const int64_t smp = e / h;
     const int j = (int)(e % h);
     const int64_t base = smp * td.S * h + j;
-    const double z = a.pre ? a.pre[base] : a.zval[e];
+    const double z = PRE ? a.pre[base] : a.zval[e];
     const TanhD t = tanh_derivs(z, td.taylor);
-    const double wl = a.gin ? 0.0 : a.wlast[j];
-    auto gin_at = [&](int s) -> double {
-      if (a.gin) return a.gin[base + (int64_t)s * h];
-      const double sd = a.seeds ? a.seeds[smp * td.S + s] : 1.0;
-      return sd * wl;
-    };
-    const double vb = gin_at(0);
+    const double wl = GIN ? 0.0 : a.wlast[j];
+    const double* sd = GIN ? nullptr : (a.seeds ? a.seeds + smp * td.S : nullptr);
+    const double vb = GIN ? a.gin[base] : (sd ? sd[0] * wl : wl);
+    double* go = a.gout + base;
     if (!td.taylor) {
-      a.gout[base] = t.s1 * vb;  // network.py:229-231
+      go[0] = t.s1 * vb;  // network.py:229-231
       continue;
     }
-    const double lb = gin_at(d + 1);
-    const double ell = a.pre ? a.pre[base + (int64_t)(d + 1) * h] : 0.0;
+    const int64_t hl = h;
+    const double lb = GIN ? a.gin[base + (int64_t)(d + 1) * hl] : (sd ? sd[d + 1] * wl : wl);
+    const double ell = PRE ? a.pre[base + (int64_t)(d + 1) * hl] : 0.0;
     double quad = 0.0, ggb = 0.0;
     const double two_s2 = 2.0 * t.s2;
-    // derivative rows in batches of 4: issue the loads first (memory-level parallelism)
-    for (int i0 = 1; i0 <= d; i0 += 4) {
-      double gv[4], gbv[4];
+    const double* pg = PRE ? a.pre + base + hl : a.w0t + j;   // derivative row i = 1
+    const double* pb = GIN ? a.gin + base + hl : nullptr;
+    double* po = go + hl;
+    auto row = [&](double g, double gb, int i, double* o) {
+      const double cg = g * cdiag[i - 1];
+      quad += cg * g;
+      ggb += g * gb;
+      *o = t.s1 * gb + two_s2 * cg * lb;
+    };
+    int i0 = 1;
+    for (; i0 + 7 <= d; i0 += 8) {  // full batches: 8 loads in flight
+      double gv[8], gbv[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int i = i0 + u;
-        if (i <= d) {
-          gv[u] = a.pre ? a.pre[base + (int64_t)i * h] : a.w0t[(int64_t)(i - 1) * h + j];
-          gbv[u] = gin_at(i);
-        }
+      for (int u = 0; u < 8; ++u) {
+        gv[u] = pg[u * hl];
+        gbv[u] = GIN ? pb[u * hl] : (sd ? sd[i0 + u] * wl : wl);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int i = i0 + u;
-        if (i <= d) {
-          const double cg = gv[u] * cdiag[i - 1];
-          quad += cg * gv[u];
-          ggb += gv[u] * gbv[u];
-          a.gout[base + (int64_t)i * h] = t.s1 * gbv[u] + two_s2 * cg * lb;
-        }
-      }
+      for (int u = 0; u < 8; ++u) row(gv[u], gbv[u], i0 + u, po + u * hl);
+      pg += 8 * hl;
+      if (GIN) pb += 8 * hl;
+      po += 8 * hl;
     }
-    a.gout[base + (int64_t)(d + 1) * h] = t.s1 * lb;
-    a.gout[base] = t.s1 * vb + t.s2 * ggb + t.s2 * ell * lb + t.s3 * quad * lb;
+    for (; i0 <= d; ++i0) {
+      row(*pg, GIN ? *pb : (sd ? sd[i0] * wl : wl), i0, po);
+      pg += hl;
+      if (GIN) pb += hl;
+      po += hl;
+    }
+    go[(int64_t)(d + 1) * hl] = t.s1 * lb;
+    go[0] = t.s1 * vb + t.s2 * ggb + t.s2 * ell * lb + t.s3 * quad * lb;
   }
 }
 
@@ -359,7 +370,11 @@ void launch_act_bwd(const ActBwd& a, int64_t n, int h, TaylorDims td, const doub
   const int64_t total = n * h;
   if (total <= 0) return;
   count_launch();
-  k_act_bwd<<<grid_for(total, 256), 256, 0, s>>>(a, n, h, td, cdiag);
+  const unsigned g = grid_for(total, 256);
+  if (a.pre && a.gin) k_act_bwd<true, true><<<g, 256, 0, s>>>(a, n, h, td, cdiag);
+  else if (a.pre) k_act_bwd<true, false><<<g, 256, 0, s>>>(a, n, h, td, cdiag);
+  else if (a.gin) k_act_bwd<false, true><<<g, 256, 0, s>>>(a, n, h, td, cdiag);
+  else k_act_bwd<false, false><<<g, 256, 0, s>>>(a, n, h, td, cdiag);
 }
 
 // ---------------------------------------------------------------------------

@@ -61,6 +61,18 @@ PLAN = {
     "dense_star": ("dense", 300, 100, 3),
 }
 
+# Ten-step runs of the five BASELINE configs (north star: 1e-10 after one step, 1e-8 after
+# ten).  c1 at its full size; c2-c5 reduced so the reference finishes in seconds.  Arrays are
+# recorded at steps 1 and 10 only; every step records losses, alpha and the line search.
+PLAN10 = {
+    "c1_10": ("c1", 3000, 500, 10),
+    "c2_10": ("c2", 1000, 200, 10),
+    "c3_10": ("c3", 1000, 400, 10),
+    "c4_10": ("c4", 400, 130, 10),
+    "c5_10": ("c5", 24, 8, 10),
+}
+FULL_RECORD_STEPS = {1, 10}
+
 
 def ref_problem(wl):
     """Reference PdeProblem for a workload (catalog where it exists, else rigged)."""
@@ -98,7 +110,8 @@ def put(out, key, arr):
 
 def main():
     only = set(sys.argv[1:])
-    for name, (wkey, n_int, n_bnd, steps) in PLAN.items():
+    for name, (wkey, n_int, n_bnd, steps) in {**PLAN, **PLAN10}.items():
+        ten = name in PLAN10
         if only and name not in only:
             continue
         wl = cfgs.WORKLOADS[wkey]
@@ -147,6 +160,10 @@ def main():
             out[pre + "loss_boundary"] = np.array(info.loss_boundary)
             out[pre + "alpha"] = np.array(info.alpha)
             out[pre + "mu"] = np.array(info.mu)
+            if ten and t not in FULL_RECORD_STEPS:
+                print(f"{name} step {t}: loss={info.loss_total:.6e} alpha={info.alpha:.10g}",
+                      flush=True)
+                continue
             put(out, pre + "grad", network.mats_to_vec(ev.grad_mats))
             put(out, pre + "delta", network.mats_to_vec(delta))
             put(out, pre + "theta", network.params_to_vec(state.params))
