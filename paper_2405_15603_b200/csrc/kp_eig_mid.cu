@@ -1,0 +1,385 @@
+// Mid-size symmetric eigensolver (96 < n <= 288) for the damped Kronecker-sum solve:
+// one-sided (Hestenes) Jacobi on a Cholesky factor, the columns resident in the shared
+// memory of a thread-block cluster (16 CTAs, or 8 where 16-CTA clusters cannot be
+// scheduled), FP64, sm_100a.
+//
+// Used for the factor pairs that are too large for the one-CTA solver of kp_eig_small.cu
+// (BASELINE c4: 128-257; c5 layer 0's A: 101).  The generalised problem M1 x = l M2 x
+// (reference src/linalg.py:136-174 via curvature.py:150-161) is reduced with library calls
+// that never block the host (kp_step.cu gen_eig_mid): M2 = L L^T (potrf), C = L^-1 M1 L^-T
+// (two trsm), C = R^T R (potrf, upper).  This kernel then orthogonalises the columns of R
+// by plane rotations, R J1 J2 ... = R V with mutually orthogonal columns, so that
+//   C V = V diag(||R v_i||^2)      (eigenpairs of C, V orthogonal),
+// and T = L^-T V (trsm) satisfies T^T M2 T = I, T^T M1 T = diag(lambda).
+//
+// Parallel ordering: the n columns (padded with zero columns to 2 CL ppc for a cluster of
+// CL CTAs) form CL ppc disjoint pairs per round; CTA c owns pairs [c ppc, (c+1) ppc), one
+// warp per pair.  Between rounds the pairing advances by the circle method (one column
+// fixed, the rest rotate one position), so every pair of columns meets once per sweep of
+// 2 CL ppc - 1 rounds.  Inside a CTA a column moves by re-indexing only; at a CTA boundary
+// the warp that rotated the outgoing column also stores it (R and V parts, 2n doubles) into
+// the neighbour's mailbox through distributed shared memory.  One cluster barrier per
+// round; mailboxes and slot tables are double-buffered by round parity, so a mailbox
+// written in round t + 2 was drained before the barrier of round t + 1.
+//
+// A rotation is applied when |<r_p, r_q>| > tol ||r_p|| ||r_q|| (tol = max(1e-14, 2 n eps));
+// the sweep loop ends after a sweep without rotations anywhere in the cluster.
+#include <cooperative_groups.h>
+
+#include <cfloat>
+
+#include "kp_common.cuh"
+#include "kp_internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace kp {
+
+namespace {
+
+constexpr int MID_MAXN = 288;
+constexpr int MID_MAX_SWEEPS = 40;
+constexpr int MID_EPL = (MID_MAXN + 31) / 32;  // column elements per lane
+
+__device__ int g_mid_sweeps_max = 0;  // diagnostic: most sweeps used by any solve
+
+__host__ __device__ inline int mid_ppc(int n, int cl) { return ((n + 1) / 2 + cl - 1) / cl; }
+
+__device__ __forceinline__ double warp_allsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Sum a, b, g over the warp with 4-value butterfly folding (9 shuffles of doubles instead of
+// 15): after the first two levels each lane holds one of the four partial sums.
+__device__ __forceinline__ void warp_sum3(double& a, double& b, double& g, int lane) {
+  double d = 0.0;
+  {  // level 16: lanes < 16 keep (a, b), lanes >= 16 keep (g, d)
+    const bool hi = lane & 16;
+    const double s0 = hi ? a : g, s1 = hi ? b : d;
+    const double r0 = __shfl_xor_sync(0xffffffffu, s0, 16);
+    const double r1 = __shfl_xor_sync(0xffffffffu, s1, 16);
+    if (hi) {
+      g += r0;
+      d += r1;
+    } else {
+      a += r0;
+      b += r1;
+    }
+    a = hi ? g : a;  // x0 = a (lo) or g (hi)
+    b = hi ? d : b;  // x1 = b (lo) or d (hi)
+  }
+  {  // level 8: lanes with bit 3 clear keep x0, set keep x1
+    const bool hi = lane & 8;
+    const double snd = hi ? a : b;
+    const double r = __shfl_xor_sync(0xffffffffu, snd, 8);
+    a = (hi ? b : a) + r;
+  }
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  // lane 0: sum a, lane 8: sum b, lane 16: sum g
+  const double sa = __shfl_sync(0xffffffffu, a, 0);
+  const double sb = __shfl_sync(0xffffffffu, a, 8);
+  const double sg = __shfl_sync(0xffffffffu, a, 16);
+  a = sa;
+  b = sb;
+  g = sg;
+}
+
+// rv: n x n column-major.  In: the upper-triangular Cholesky factor R of C (the strictly
+// lower part is ignored).  Out: the eigenvectors V of C = R^T R (column i = vector i).
+// lam[i] = eigenvalue i.  info: 0 ok, 1 no convergence in MID_MAX_SWEEPS sweeps, n + 1 when
+// one of the two upstream Cholesky factorisations (chol_info[0..1]) failed (not PD).
+// warm_valid (optional): set to 1 on success, 0 otherwise (the caller's warm-start flag).
+//
+// smem: 2 ppc column records + 4 mailboxes ([from left, from right] x round parity), each
+// record R | V (2n doubles).  A round: every pair warp loads its two R columns into
+// registers, forms the three dot products and rotates R and V; the warps owning the CTA's
+// outgoing columns (last top slot -> right neighbour, first bottom slot -> left neighbour)
+// also store them into the neighbour's mailbox.  One cluster barrier; then each CTA copies
+// its mailboxes into the records it handed over and writes the next round's slot table.
+template <int CL>
+__global__ void __launch_bounds__(((MID_MAXN / 2 + CL - 1) / CL) * 32, 1)
+    k_eig_mid(int n, double* __restrict__ rv, double* __restrict__ lam, int* __restrict__ info,
+              const int* __restrict__ chol_info, double tol, int* __restrict__ warm_valid,
+              long long* prof) {
+  constexpr int MAXPPC = (MID_MAXN / 2 + CL - 1) / CL;
+  cg::cluster_group cluster = cg::this_cluster();
+  long long t_rot = 0, t_sync = 0, t_upd = 0, t0 = 0;
+  const int c = (int)cluster.block_rank();
+  if (chol_info[0] != 0 || chol_info[1] != 0) {  // uniform across the cluster: no DSMEM yet
+    if (c == 0 && threadIdx.x == 0) {
+      *info = n + 1;
+      if (warm_valid) *warm_valid = 0;
+    }
+    return;
+  }
+  extern __shared__ double msm[];
+  const int ppc = mid_ppc(n, CL);
+  const int m = 2 * CL * ppc;  // padded column count (columns >= n are zero)
+  const size_t cs2 = 2 * (size_t)n;  // one column record: R (n) then V (n)
+  double* buf = msm;                          // 2 ppc records
+  double* mbox = msm + (size_t)2 * ppc * cs2;  // [dir][par]: dir 0 = from the left
+  __shared__ int top[2][MAXPPC], bot[2][MAXPPC], colid[2 * MAXPPC];
+  __shared__ int mcol[2][2];
+  __shared__ int rotated;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nthr = blockDim.x;
+  double* const mbox_left = cluster.map_shared_rank(mbox, c > 0 ? c - 1 : c);
+  double* const mbox_right = cluster.map_shared_rank(mbox, c < CL - 1 ? c + 1 : c);
+  int* const mcol_left = cluster.map_shared_rank(&mcol[0][0], c > 0 ? c - 1 : c);
+  int* const mcol_right = cluster.map_shared_rank(&mcol[0][0], c < CL - 1 ? c + 1 : c);
+  const double tol2 = tol * tol;
+
+  if (tid < ppc) {
+    const int g = c * ppc + tid;
+    top[0][tid] = tid;
+    bot[0][tid] = ppc + tid;
+    colid[tid] = 2 * g;
+    colid[ppc + tid] = 2 * g + 1;
+  }
+  for (int e = tid; e < 2 * ppc * n; e += nthr) {
+    const int b = e / n, i = e % n;
+    const int k = b < ppc ? b : b - ppc;
+    const int col = 2 * (c * ppc + k) + (b < ppc ? 0 : 1);
+    buf[b * cs2 + i] = (col < n && i <= col) ? rv[(size_t)col * n + i] : 0.0;
+    buf[b * cs2 + n + i] = (i == col) ? 1.0 : 0.0;
+  }
+  cluster.sync();  // every CTA initialised before any mailbox store
+
+  int sweep = 0, cur = 0;  // cur: slot table of the current round
+  bool converged = false;
+  for (; sweep < MID_MAX_SWEEPS; ++sweep) {
+    if (tid == 0) rotated = 0;
+    __syncthreads();
+    for (int round = 0; round < m - 1; ++round) {
+      const int par = round & 1;
+      if (prof) t0 = clock64();
+      if (warp < ppc) {
+        const int bp = top[cur][warp], bq = bot[cur][warp];
+        const int cp = colid[bp], cq = colid[bq];
+        double* rp = buf + bp * cs2;
+        double* rq = buf + bq * cs2;
+        // this warp forwards its top column to the right / its bottom column to the left
+        const bool send_r = warp == ppc - 1 && c < CL - 1;
+        const bool send_l = warp == 0 && c > 0;
+        double x[MID_EPL], y[MID_EPL];
+        double a = 0.0, b = 0.0, gm = 0.0;
+#pragma unroll
+        for (int u = 0; u < MID_EPL; ++u) {
+          const int i = lane + 32 * u;
+          x[u] = i < n ? rp[i] : 0.0;
+          y[u] = i < n ? rq[i] : 0.0;
+          a = fma(x[u], x[u], a);
+          b = fma(y[u], y[u], b);
+          gm = fma(x[u], y[u], gm);
+        }
+        warp_sum3(a, b, gm, lane);
+        const bool rot = cp < n && cq < n && gm * gm > tol2 * (a * b) && fabs(gm) > 1e-300;
+        double* dr = send_r ? mbox_right + (size_t)(0 * 2 + par) * cs2 : nullptr;  // their "from left"
+        double* dl = send_l ? mbox_left + (size_t)(1 * 2 + par) * cs2 : nullptr;   // their "from right"
+        if (rot) {
+          // t = tan of the rotation angle: 2g sign(b - a) / (|b - a| + sqrt((b - a)^2 + 4 g^2))
+          const double dba = b - a, g2 = 2.0 * gm;
+          const double t = (dba >= 0.0 ? g2 : -g2) / (fabs(dba) + sqrt(fma(dba, dba, g2 * g2)));
+          const double cs = rsqrt(fma(t, t, 1.0));
+          const double sn = cs * t;
+          double* vp = rp + n;
+          double* vq = rq + n;
+#pragma unroll
+          for (int u = 0; u < MID_EPL; ++u) {
+            const int i = lane + 32 * u;
+            if (i < n) {
+              const double xr = cs * x[u] - sn * y[u], yr = sn * x[u] + cs * y[u];
+              const double pu = vp[i], qu = vq[i];
+              const double xv = cs * pu - sn * qu, yv = sn * pu + cs * qu;
+              rp[i] = xr;
+              rq[i] = yr;
+              vp[i] = xv;
+              vq[i] = yv;
+              if (send_r) {
+                dr[i] = xr;
+                dr[n + i] = xv;
+              }
+              if (send_l) {
+                dl[i] = yr;
+                dl[n + i] = yv;
+              }
+            }
+          }
+          if (lane == 0) rotated = 1;
+        } else if (send_r || send_l) {
+#pragma unroll
+          for (int u = 0; u < MID_EPL; ++u) {
+            const int i = lane + 32 * u;
+            if (i < n) {
+              if (send_r) {
+                dr[i] = x[u];
+                dr[n + i] = rp[n + i];
+              }
+              if (send_l) {
+                dl[i] = y[u];
+                dl[n + i] = rq[n + i];
+              }
+            }
+          }
+        }
+        if (lane == 0) {
+          if (send_r) mcol_right[0 * 2 + par] = cp;
+          if (send_l) mcol_left[1 * 2 + par] = cq;
+        }
+      }
+      if (prof) { __syncthreads(); const long long t1 = clock64(); t_rot += t1 - t0; t0 = t1; }
+      cluster.sync();  // rotations done, mailboxes filled (release / acquire)
+      if (prof) { const long long t1 = clock64(); t_sync += t1 - t0; t0 = t1; }
+      // mailboxes -> the records this CTA handed over; next slot table by the circle method:
+      // top[k] <- top[k-1], bot[k] <- bot[k+1]; cluster ends: global top[0] stays,
+      // global bot[0] -> top[1], global top[last] -> bot[last]
+      const int ot = top[cur][ppc - 1], ob = bot[cur][0];
+      const int recv_l = (c == CL - 1) ? ob : ot;
+      const int recv_r = (c == 0) ? ot : ob;
+      if (c > 0) {
+        const double* src = mbox + (size_t)(0 * 2 + par) * cs2;
+        double* dst = buf + recv_l * cs2;
+        for (int i = tid; i < 2 * n; i += nthr) dst[i] = src[i];
+      }
+      if (c < CL - 1) {
+        const double* src = mbox + (size_t)(1 * 2 + par) * cs2;
+        double* dst = buf + recv_r * cs2;
+        for (int i = tid; i < 2 * n; i += nthr) dst[i] = src[i];
+      }
+      if (tid < ppc) {
+        const int k = tid;
+        top[cur ^ 1][k] =
+            k == 0 ? (c == 0 ? top[cur][0] : recv_l) : ((c == 0 && k == 1) ? ob : top[cur][k - 1]);
+        bot[cur ^ 1][k] = k == ppc - 1 ? (c == CL - 1 ? ot : recv_r) : bot[cur][k + 1];
+      }
+      if (tid == 32) {
+        if (c > 0) colid[recv_l] = mcol[0][par];
+        if (c < CL - 1) colid[recv_r] = mcol[1][par];
+      }
+      cur ^= 1;
+      __syncthreads();
+      if (prof) t_upd += clock64() - t0;
+    }
+    // every flag of this sweep was set before the last round's cluster barrier
+    int any = 0;
+    for (int r = 0; r < CL; ++r) any |= *cluster.map_shared_rank(&rotated, r);
+    cluster.sync();  // all flags read before any CTA resets its own
+    if (!any) {
+      converged = true;
+      break;
+    }
+  }
+  // eigenvalues ||R v_i||^2 and eigenvectors V (column col of rv)
+  for (int sl = warp; sl < 2 * ppc; sl += nthr / 32) {
+    const int bidx = sl < ppc ? top[cur][sl] : bot[cur][sl - ppc];
+    const int col = colid[bidx];
+    if (col < 0 || col >= n) continue;
+    const double* r = buf + bidx * cs2;
+    double a = 0.0;
+    for (int i = lane; i < n; i += 32) {
+      a = fma(r[i], r[i], a);
+      rv[(size_t)col * n + i] = r[n + i];
+    }
+    a = warp_allsum(a);
+    if (lane == 0) lam[col] = a;
+  }
+  if (prof && tid == 0) {
+    prof[5 * c + 0] = t_rot;
+    prof[5 * c + 1] = t_sync;
+    prof[5 * c + 2] = 0;
+    prof[5 * c + 3] = t_upd;
+    prof[5 * c + 4] = sweep;
+  }
+  if (c == 0 && tid == 0) {
+    *info = converged ? 0 : 1;
+    if (warm_valid) *warm_valid = converged ? 1 : 0;
+    atomicMax(&g_mid_sweeps_max, converged ? sweep + 1 : 1000 + sweep);
+  }
+}
+
+template <int CL>
+size_t mid_smem(int n) {
+  return (size_t)(2 * mid_ppc(n, CL) + 4) * 2 * n * sizeof(double);
+}
+
+// Cluster size: 16 when the device can co-schedule 16-CTA clusters of this kernel
+// (non-portable size), else 8.
+template <int CL>
+bool mid_setup() {
+  auto kern = k_eig_mid<CL>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)mid_smem<CL>(MID_MAXN)) != cudaSuccess)
+    return false;
+  if (CL > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                    cudaSuccess)
+    return false;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CL);
+  cfg.blockDim = dim3(mid_ppc(MID_MAXN, CL) * 32);
+  cfg.dynamicSmemBytes = mid_smem<CL>(MID_MAXN);
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int nc = 0;
+  if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) != cudaSuccess || nc < 1) {
+    cudaGetLastError();
+    return false;
+  }
+  return true;
+}
+
+template <int CL>
+void launch_mid(int n, double* rv, double* lam, int* info, const int* chol_info,
+                cudaStream_t s, int* warm_valid, long long* prof) {
+  const double tol = fmax(1e-14, 2.0 * n * DBL_EPSILON);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CL);
+  cfg.blockDim = dim3(mid_ppc(n, CL) * 32);
+  cfg.dynamicSmemBytes = mid_smem<CL>(n);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_eig_mid<CL>, n, rv, lam, info, chol_info, tol, warm_valid, prof);
+}
+
+int g_mid_cl = 0;  // 0: not chosen yet
+
+}  // namespace
+
+int mid_eig_max_n() { return MID_MAXN; }
+
+int mid_eig_sweeps_used() {
+  int v = 0;
+  cudaMemcpyFromSymbol(&v, g_mid_sweeps_max, sizeof(int));
+  return v;
+}
+
+int mid_eig_cluster_size() {
+  if (g_mid_cl == 0) {
+    const char* env = getenv("KP_MID_CLUSTER");
+    const int want = env ? atoi(env) : 16;
+    g_mid_cl = (want == 16 && mid_setup<16>()) ? 16 : (mid_setup<8>() ? 8 : -1);
+  }
+  return g_mid_cl;
+}
+
+void launch_eig_mid(int n, double* rv, double* lam, int* info, const int* chol_info,
+                    cudaStream_t s, int* warm_valid, long long* prof) {
+  count_launch();
+  if (mid_eig_cluster_size() == 16) launch_mid<16>(n, rv, lam, info, chol_info, s, warm_valid, prof);
+  else launch_mid<8>(n, rv, lam, info, chol_info, s, warm_valid, prof);
+}
+
+}  // namespace kp

@@ -244,6 +244,7 @@ void launch_eig_status(const double* la, int p, const double* lb, int q, const i
 void launch_kron_scale(double* W, const double* la, int p, const double* lb, int q,
                        cudaStream_t s);
 void launch_set_status(int32_t* status, int32_t code, cudaStream_t s);
+void launch_warm_identity(double* T, int n, const int* valid, cudaStream_t s);
 void launch_status_slots(const int32_t* status, double* slots, cudaStream_t s);
 void launch_slots_status(const double* slots, int32_t* status, cudaStream_t s);
 // KFAC*: batched deterministic dot products, quadratic-model solve and update
@@ -302,6 +303,12 @@ struct SmallCombineJobs {
   SmallCombineJob job[16];
 };
 int small_eig_max_n();
+// kp_eig_mid.cu: one-sided Jacobi in an 8-CTA cluster for small_eig_max_n() < n <= mid_eig_max_n()
+int mid_eig_max_n();
+int mid_eig_sweeps_used();
+int mid_eig_cluster_size();  // 16, 8, or -1 when no cluster launch is possible
+void launch_eig_mid(int n, double* rv, double* lam, int* info, const int* chol_info,
+                    cudaStream_t s, int* warm_valid = nullptr, long long* prof = nullptr);
 size_t small_eig_smem_bytes(int n);
 void launch_gen_eig_small(const SmallEigJobs& jobs, int njobs, int max_n, int32_t* status,
                           cudaStream_t s);

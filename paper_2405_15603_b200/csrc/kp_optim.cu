@@ -198,25 +198,39 @@ void launch_damped_copy(const double* F, double lam, int n, double* out, cudaStr
 __global__ void k_eig_status(const double* la, int p, const double* lb, int q, const int* info,
                              int32_t* status) {
   const double tol = 1e-6;
-  for (int k = 0; k < 2; ++k) {
-    const int n = k == 0 ? p : q;
-    if (info[k] > n) set_status(status, KP_ERR_NOT_PSD);
-    else if (info[k] != 0) set_status(status, KP_ERR_EIG);
-  }
+  const int lane = threadIdx.x;
   const double* ls[2] = {la, lb};
   const int ns[2] = {p, q};
   for (int k = 0; k < 2; ++k) {
-    if (info[k] != 0) continue;
-    const double lo = ls[k][0], hi = ls[k][ns[k] - 1];
-    const double norm = fmax(fabs(lo), fabs(hi));
-    if (lo < -tol * fmax(norm, 1e-300)) set_status(status, KP_ERR_NOT_PSD);
+    const int n = ns[k];
+    if (info[k] > n) {
+      if (lane == 0) set_status(status, KP_ERR_NOT_PSD);
+      continue;
+    }
+    if (info[k] != 0) {
+      if (lane == 0) set_status(status, KP_ERR_EIG);
+      continue;
+    }
+    // min / max |.| by a warp scan (the mid-size Jacobi solver leaves them unordered)
+    double lo = INFINITY, hi = 0.0;
+    for (int i = lane; i < n; i += 32) {
+      const double v = ls[k][i];
+      lo = fmin(lo, v);
+      hi = fmax(hi, fabs(v));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (lane == 0 && lo < -tol * fmax(hi, 1e-300)) set_status(status, KP_ERR_NOT_PSD);
   }
 }
 
 void launch_eig_status(const double* la, int p, const double* lb, int q, const int* info,
                        int32_t* status, cudaStream_t s) {
   count_launch();
-  k_eig_status<<<1, 1, 0, s>>>(la, p, lb, q, info, status);
+  k_eig_status<<<1, 32, 0, s>>>(la, p, lb, q, info, status);
 }
 
 // W (p x q column-major) /= (lb_i la_j + 1)   (linalg.py:171)
@@ -361,6 +375,20 @@ void launch_status_slots(const int32_t* status, double* slots, cudaStream_t s) {
 void launch_slots_status(const double* slots, int32_t* status, cudaStream_t s) {
   count_launch();
   k_slots_status<<<1, 1, 0, s>>>(slots, status);
+}
+
+// Warm-start basis of a mid-size pair: the identity unless the previous solve succeeded.
+__global__ void k_warm_identity(double* T, int n, const int* valid) {
+  if (*valid) return;
+  const int64_t total = (int64_t)n * n;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x)
+    T[e] = (e / n == e % n) ? 1.0 : 0.0;
+}
+
+void launch_warm_identity(double* T, int n, const int* valid, cudaStream_t s) {
+  count_launch();
+  k_warm_identity<<<grid1((int64_t)n * n), 256, 0, s>>>(T, n, valid);
 }
 
 __global__ void k_set_status(int32_t* status, int32_t code) { set_status(status, code); }

@@ -63,6 +63,7 @@ struct kp_context {
   cudaEvent_t cap_in = nullptr, cap_out = nullptr;
   std::vector<unsigned char> graph_key;
   cudaGraphExec_t graph_exec = nullptr;
+  std::vector<unsigned char> graph_failed_key;  // arguments whose capture failed: run plain
   // warm-start cache of the on-device eigensolver (previous T per small factor pair, scratch,
   // validity flags), keyed on the layer shapes and the state's factor buffers
   double* warm_buf = nullptr;
@@ -355,6 +356,10 @@ int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
       KP_SOLVER_TRY(cusolverDnDsygvd_bufferSize(ctx->solver, CUSOLVER_EIG_TYPE_1,
                                                 CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
                                                 n, nullptr, n, nullptr, n, nullptr, &lw));
+      int lwp = 0;  // the mid-size route (potrf twice) shares the pair's workspace
+      KP_SOLVER_TRY(cusolverDnDpotrf_bufferSize(ctx->solver, CUBLAS_FILL_MODE_LOWER, n, nullptr,
+                                                n, &lwp));
+      lw = std::max(lw, lwp);
       P.lw[l][k] = std::max(lw, 1);
       lwork = std::max(lwork, lw);
     }
@@ -372,7 +377,7 @@ int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
     P.k_T2[l] = take(p * q);
     P.k_wa[l] = take(P.lw[l][0]);
     P.k_wb[l] = take(P.lw[l][1]);
-    P.k_info[l] = take(4);
+    P.k_info[l] = take(4);  // 8 ints: eig info (A, B), Cholesky infos (A: M2, C; B: M2, C)
   }
   P.total = o;
   return KP_OK;
@@ -854,6 +859,41 @@ int kron_solve(kp_context* ctx, const Ctx& c, int p, int q, double* A1, double* 
                       c.at(P.o_T2));
 }
 
+// Generalised eigenproblem of a mid-size pair (small_eig_max_n() < n <= mid_eig_max_n()),
+// entirely asynchronous on stream s (no host-blocking library call).  Warm start as in the
+// small solver: the pair is first congruence-transformed by the previous step's T (kept in
+// tp; the identity until a solve of this pair has succeeded, decided on the device by
+// *valid, so the same launches serve cold and warm steps and can be graph-captured):
+//   M_i' = Tp^T (F_i + lam I) Tp,  M2' = L L^T (potrf),  C = L^-1 M1' L^-T (two trsm),
+//   C = R^T R (potrf), one-sided Jacobi on R in an 8-CTA cluster (kp_eig_mid.cu) ->
+//   C V = V diag(ev),  T = Tp L^-T V, left in m1 (column-major, like sygvd's) and in tp.
+int gen_eig_mid(cusolverDnHandle_t hs, cublasHandle_t hb, cudaStream_t s, int n, const double* f1,
+                const double* f2, double lam, double* m1, double* m2, double* ev, double* work,
+                int lwork, int* info, int* chol_info, double* tp, double* w, int* valid) {
+  const double one = 1.0, zero = 0.0;
+  KP_CUDA_TRY(cudaMemsetAsync(chol_info, 0, 2 * sizeof(int), s));
+  launch_damped_copy(f1, lam, n, m1, s);
+  launch_damped_copy(f2, lam, n, m2, s);
+  launch_warm_identity(tp, n, valid, s);
+  for (double* m : {m2, m1}) {
+    KP_BLAS_TRY(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, n, n, n, &one, m, n, tp, n, &zero, w, n));
+    KP_BLAS_TRY(cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, n, n, n, &one, tp, n, w, n, &zero, m, n));
+  }
+  KP_SOLVER_TRY(cusolverDnDpotrf(hs, CUBLAS_FILL_MODE_LOWER, n, m2, n, work, lwork, chol_info));
+  KP_BLAS_TRY(cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N,
+                          CUBLAS_DIAG_NON_UNIT, n, n, &one, m2, n, m1, n));
+  KP_BLAS_TRY(cublasDtrsm(hb, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T,
+                          CUBLAS_DIAG_NON_UNIT, n, n, &one, m2, n, m1, n));
+  KP_SOLVER_TRY(cusolverDnDpotrf(hs, CUBLAS_FILL_MODE_UPPER, n, m1, n, work, lwork, chol_info + 1));
+  launch_eig_mid(n, m1, ev, info, chol_info, s, valid);
+  KP_BLAS_TRY(cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T,
+                          CUBLAS_DIAG_NON_UNIT, n, n, &one, m2, n, m1, n));
+  KP_BLAS_TRY(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, n, n, n, &one, tp, n, m1, n, &zero, w, n));
+  KP_CUDA_TRY(cudaMemcpyAsync(m1, w, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s));
+  KP_CUDA_TRY(cudaMemcpyAsync(tp, w, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s));
+  return KP_OK;
+}
+
 // `owned` (host, L flags) = nullptr: every layer's Kronecker solve runs here and the phase
 // ends with the momentum direction (phase_direction).  Otherwise only the flagged layers are
 // solved; the others' Delta rows are zeroed and the phase stops at the direction exchange
@@ -894,6 +934,10 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
   // is issued from its own host thread (own handle + stream); a layer with a large pair is
   // combined with cuBLAS on its side stream.
   auto pair_small = [&](int l, int k) { return (k == 0 ? P.p[l] : P.q[l]) <= small_eig_max_n(); };
+  auto pair_mid = [&](int l, int k) {
+    const int n = k == 0 ? P.p[l] : P.q[l];
+    return n > small_eig_max_n() && n <= mid_eig_max_n();
+  };
   bool any_big = false;
   for (int l = 0; l < P.L; ++l)
     any_big |= (!owned || owned[l]) && (!pair_small(l, 0) || !pair_small(l, 1));
@@ -904,7 +948,13 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
     small_done = ctx->side_ev[2 * P.L + 1];
     KP_CUDA_TRY(cudaEventRecord(ready, c.s));
   }
-  std::vector<int> big;  // layers with at least one cuSOLVER pair
+  std::vector<int> big;  // layers with at least one pair outside the one-launch small solver
+  struct MidWarm {
+    double* t;
+    double* scratch;
+    int* valid;
+  };
+  std::vector<MidWarm> mid_warm(2 * P.L, MidWarm{nullptr, nullptr, nullptr});
   // warm-start cache for the small pairs (re-keyed when shapes or factor buffers change)
   {
     std::vector<unsigned char> key;
@@ -918,7 +968,7 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
       put(&P.q[l], sizeof(int));
       for (int k = 0; k < 2; ++k) {
         const size_t nn = (size_t)(k == 0 ? P.p[l] : P.q[l]);
-        if (pair_small(l, k)) need += 2 * nn * nn;
+        if (pair_small(l, k) || pair_mid(l, k)) need += 2 * nn * nn;
       }
     }
     put(&st->a_int, sizeof(double*));
@@ -989,10 +1039,38 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
       else
         big.push_back(l);
     }
+    // warm-start slots of the mid-size pairs follow the small ones (owned or not: stable)
+    for (int l = 0; l < P.L; ++l)
+      for (int k = 0; k < 2; ++k) {
+        if (!pair_mid(l, k)) continue;
+        SmallEigJob tmp{};
+        tmp.n = k == 0 ? P.p[l] : P.q[l];
+        warm(tmp);
+        mid_warm[2 * l + k] = MidWarm{tmp.warm_t, tmp.warm_scratch, tmp.warm_valid};
+      }
     launch_gen_eig_small(ej, ne, maxn, out->status, c.s);
     if (any_big) KP_CUDA_TRY(cudaEventRecord(small_done, c.s));
     launch_kron_combine_small(cj, nc, c.s);
   }
+  // mid-size pairs: asynchronous route issued from this thread on the pair's side stream
+  for (int l : big)
+    for (int k = 0; k < 2; ++k) {
+      if (!pair_mid(l, k)) continue;
+      cudaStream_t s = ctx->side[2 * l + k];
+      KP_CUDA_TRY(cudaStreamWaitEvent(s, ready, 0));
+      int* info = reinterpret_cast<int*>(c.at(P.k_info[l])) + k;
+      KP_CUDA_TRY(cudaMemsetAsync(info, 0, sizeof(int), s));
+      KP_TRY(gen_eig_mid(ctx->side_solver[2 * l + k], ctx->side_blas[2 * l + k], s,
+                         k == 0 ? P.p[l] : P.q[l],
+                         k == 0 ? st->a_int + P.fa[l] : st->b_int + P.fb[l],
+                         k == 0 ? st->a_bnd + P.fa[l] : st->b_bnd + P.fb[l], lam,
+                         c.at(k == 0 ? P.k_A1[l] : P.k_B1[l]), c.at(k == 0 ? P.k_A2[l] : P.k_B2[l]),
+                         c.at(k == 0 ? P.k_la[l] : P.k_lb[l]), c.at(k == 0 ? P.k_wa[l] : P.k_wb[l]),
+                         P.lw[l][k], info, reinterpret_cast<int*>(c.at(P.k_info[l])) + 2 + 2 * k,
+                         mid_warm[2 * l + k].t, mid_warm[2 * l + k].scratch,
+                         mid_warm[2 * l + k].valid));
+      KP_CUDA_TRY(cudaEventRecord(ctx->side_ev[2 * l + k], s));
+    }
   std::vector<int> rc(2 * P.L, KP_OK);
   auto solve_pair = [&](int l, int k) {
     cudaSetDevice(ctx->device);
@@ -1027,7 +1105,7 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
     std::vector<std::thread> pool;
     for (int l : big)
       for (int k = 0; k < 2; ++k)
-        if (!pair_small(l, k)) pool.emplace_back(solve_pair, l, k);
+        if (!pair_small(l, k) && !pair_mid(l, k)) pool.emplace_back(solve_pair, l, k);
     for (auto& t : pool) t.join();
   }
   for (int v : rc) KP_TRY(v);
@@ -1594,7 +1672,7 @@ int32_t kp_kfac_step_graphed(kp_context* ctx, const kp_problem* prob, const kp_k
   Plan P;
   KP_TRY(prepare(ctx, prob, P, ws_bytes));
   bool capturable = !ctx->profile;
-  for (int l = 0; l < P.L; ++l) capturable &= std::max(P.p[l], P.q[l]) <= small_eig_max_n();
+  for (int l = 0; l < P.L; ++l) capturable &= std::max(P.p[l], P.q[l]) <= mid_eig_max_n();
   if (!capturable) return plain();
   std::vector<unsigned char> key;
   auto put = [&](const void* p, size_t n) {
@@ -1615,6 +1693,7 @@ int32_t kp_kfac_step_graphed(kp_context* ctx, const kp_problem* prob, const kp_k
     KP_CUDA_TRY(cudaEventCreateWithFlags(&ctx->cap_in, cudaEventDisableTiming));
     KP_CUDA_TRY(cudaEventCreateWithFlags(&ctx->cap_out, cudaEventDisableTiming));
   }
+  if (key == ctx->graph_failed_key) return plain();
   if (!ctx->graph_exec || key != ctx->graph_key) {
     if (ctx->graph_exec) {
       cudaGraphExecDestroy(ctx->graph_exec);
@@ -1631,15 +1710,20 @@ int32_t kp_kfac_step_graphed(kp_context* ctx, const kp_problem* prob, const kp_k
     cudaGraph_t graph = nullptr;
     const cudaError_t ce = cudaStreamEndCapture(ctx->cap_stream, &graph);
     if (rc != KP_OK || ce != cudaSuccess || !graph) {
+      // not capturable (a library call refused the capture): this call's step already ran
+      // uncaptured above; later calls with these arguments run plain
       if (graph) cudaGraphDestroy(graph);
       cudaGetLastError();
-      return rc != KP_OK ? rc : KP_ERR_CUDA;
+      ctx->graph_failed_key = key;
+      return KP_OK;
     }
     const cudaError_t ie = cudaGraphInstantiate(&ctx->graph_exec, graph, 0);
     cudaGraphDestroy(graph);
     if (ie != cudaSuccess) {
       ctx->graph_exec = nullptr;
-      return KP_ERR_CUDA;
+      cudaGetLastError();
+      ctx->graph_failed_key = key;
+      return KP_OK;
     }
     ctx->graph_key = key;
     KP_CUDA_TRY(cudaEventRecord(ctx->cap_out, ctx->cap_stream));
