@@ -8,11 +8,11 @@
 //   M1 = F1 + lam I, M2 = F2 + lam I
 //   M2 = L L^T (Cholesky; failure -> not positive definite, src/linalg.py:128-132)
 //   C  = L^-1 M1 L^-T (two forward substitutions, C symmetric)
-//   C  = V diag(lam) V^T  (parallel cyclic Jacobi, round-robin pairing)
+//   C  = G G^T (Cholesky), one-sided Jacobi on the rows of G -> C = V diag(lam) V^T
 //   T  = L^-T V           (so T^T M2 T = I, T^T M1 T = diag(lam))
 // Combine (src/linalg.py:168-173 restated on the generalised basis):
 //   out = -T_B [(T_B^T G T_A) / (lb la^T + 1)] T_A^T.
-// Jacobi is accurate to a few ulps relative to each eigenpair; the solution of the
+// One-sided Jacobi is accurate to a few ulps relative to each eigenpair; the solution of the
 // Kronecker-sum system is unique, so it matches the reference's LAPACK route to
 // roundoff (tests/test_gpu_parity.py).
 #include <algorithm>
@@ -40,73 +40,81 @@ __device__ __forceinline__ void set_status_dev(int32_t* status, int32_t code) {
   atomicCAS(status, 0, code);
 }
 
-// Parallel cyclic Jacobi on the symmetric C (n x n, pitch ld) accumulating V <- V G^T.
-// Round-robin ordering over m = n rounded up to even (index n is a dummy when n is odd):
-// m - 1 rounds of m/2 disjoint pairs per sweep.  Lane group k (G lanes) owns pair k of
-// every round: it computes the rotation redundantly in registers, then rotates rows p, q of
-// C, and (after a barrier) columns p, q of C and V.  Pair positions advance incrementally.
-template <int G>
-__device__ __forceinline__ void jacobi_sweeps(double* C, double* V, int n, int ld, int* flag) {
-  constexpr int GPW = 32 / G;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int k = warp * GPW + lane / G;  // pair slot of this lane group
-  const int gl = lane % G;
+// One-sided (Hestenes) Jacobi on the ROWS of a lower-triangular factor G (C = G G^T), with
+// the same rotations applied to the rows of W (start: W = I).  On return the rows of G are
+// mutually orthogonal: row i of W is eigenvector i of C and ||row i of G||^2 its eigenvalue.
+// Half-warp k owns pair k of each round (circle-method ordering over m = n rounded up to
+// even, index n a dummy when n is odd): it loads the two rows into registers, forms the three
+// dot products with a 4-level shuffle reduction and rotates both rows of G and W.  Rows do
+// not move, only the pairing changes, so a round is one CTA barrier.
+constexpr int OS_EPL = (EIG_MAXN + 15) / 16;  // row elements per lane of a half-warp
+
+__device__ __forceinline__ void jacobi_rows(double* G, double* W, int n, int ld, int* flag,
+                                            double tol) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int hl = lane & 15;                 // lane inside the half-warp
+  const int k = (tid >> 5) * 2 + (lane >> 4);  // pair slot of this half-warp
+  const unsigned hmask = (lane & 16) ? 0xffff0000u : 0x0000ffffu;
   const int m = (n + 1) & ~1;
   const int npair = m / 2;
   const bool active = k < npair;
+  const double tol2 = tol * tol;
   for (int sweep = 0; sweep < EIG_MAX_SWEEPS; ++sweep) {
     if (tid == 0) *flag = 0;
     __syncthreads();
-    // round 0 positions: a = 0 (k = 0) or 1 + (k - 1); b = 1 + (m - 2 - k)
     int ia = k > 0 ? k - 1 : 0, ib = m - 2 - k;
     for (int round = 0; round < m - 1; ++round) {
-      int p = 0, q = n;
-      double c = 1.0, sn = 0.0;
       if (active) {
         const int a = (k == 0) ? 0 : 1 + ia;
         const int b = 1 + ib;
-        p = min(a, b);
-        q = max(a, b);
-        if (q < n) {
-          const double apq = C[p * ld + q];
-          const double app = C[p * ld + p], aqq = C[q * ld + q];
-          if (apq * apq > kJacobiTol * kJacobiTol * fabs(app * aqq) && fabs(apq) > 1e-300) {
-            // t = sign(theta) / (|theta| + sqrt(theta^2 + 1)), theta = (aqq - app) / (2 apq)
-            const double dd = aqq - app;
-            const double two_apq = 2.0 * apq;
-            const double den = fabs(dd) + sqrt(fma(dd, dd, two_apq * two_apq));
-            const double t = ((dd >= 0.0) == (apq >= 0.0) ? 1.0 : -1.0) * fabs(two_apq) / den;
-            c = rsqrt(fma(t, t, 1.0));
-            sn = t * c;
-            if (gl == 0) *flag = 1;
-          }
-        }
+        const int p = min(a, b), q = max(a, b);
         if (k != 0) ia = (ia + 1 == m - 1) ? 0 : ia + 1;
         ib = (ib + 1 == m - 1) ? 0 : ib + 1;
-      }
-      __syncthreads();  // all rotation parameters read C before any row update
-      const bool rot = active && q < n && sn != 0.0;
-      if (rot) {
-        for (int col = gl; col < n; col += G) {
-          const double x = C[p * ld + col], y = C[q * ld + col];
-          C[p * ld + col] = c * x - sn * y;
-          C[q * ld + col] = sn * x + c * y;
-        }
-      }
-      __syncthreads();
-      if (rot) {
-        for (int row = gl; row < n; row += G) {
-          const double x = C[row * ld + p], y = C[row * ld + q];
-          C[row * ld + p] = c * x - sn * y;
-          C[row * ld + q] = sn * x + c * y;
-          const double vx = V[row * ld + p], vy = V[row * ld + q];
-          V[row * ld + p] = c * vx - sn * vy;
-          V[row * ld + q] = sn * vx + c * vy;
+        if (q < n) {
+          double* gp = G + p * ld;
+          double* gq = G + q * ld;
+          double x[OS_EPL], y[OS_EPL];
+          double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+          for (int u = 0; u < OS_EPL; ++u) {
+            const int i = hl + 16 * u;
+            x[u] = i < n ? gp[i] : 0.0;
+            y[u] = i < n ? gq[i] : 0.0;
+            al = fma(x[u], x[u], al);
+            be = fma(y[u], y[u], be);
+            ga = fma(x[u], y[u], ga);
+          }
+#pragma unroll
+          for (int o = 8; o > 0; o >>= 1) {
+            al += __shfl_xor_sync(hmask, al, o);
+            be += __shfl_xor_sync(hmask, be, o);
+            ga += __shfl_xor_sync(hmask, ga, o);
+          }
+          if (ga * ga > tol2 * (al * be) && fabs(ga) > 1e-300) {
+            // tan of the angle: 2g sign(b - a) / (|b - a| + sqrt((b - a)^2 + 4 g^2))
+            const double dba = be - al, g2 = 2.0 * ga;
+            const double t = (dba >= 0.0 ? g2 : -g2) / (fabs(dba) + sqrt(fma(dba, dba, g2 * g2)));
+            const double cs = rsqrt(fma(t, t, 1.0));
+            const double sn = cs * t;
+            double* wp = W + p * ld;
+            double* wq = W + q * ld;
+#pragma unroll
+            for (int u = 0; u < OS_EPL; ++u) {
+              const int i = hl + 16 * u;
+              if (i < n) {
+                gp[i] = cs * x[u] - sn * y[u];
+                gq[i] = sn * x[u] + cs * y[u];
+                const double wx = wp[i], wy = wq[i];
+                wp[i] = cs * wx - sn * wy;
+                wq[i] = sn * wx + cs * wy;
+              }
+            }
+            if (hl == 0) *flag = 1;
+          }
         }
       }
       __syncthreads();
     }
-    // every thread reads the flag before thread 0 may reset it for the next sweep
     const int rotated = *flag;
     __syncthreads();
     if (rotated == 0) {
@@ -136,6 +144,72 @@ __device__ __forceinline__ void congruence(double* X, const double* V, double* s
   __syncthreads();
 }
 
+// X = L^-1 B (UPPER = false) or X = L^-T B (UPPER = true) for lower-triangular L (smem,
+// pitch ld, invd[k] = 1 / L[k][k]); B read as B[i][j] or, with trans_b, B[j][i].  Warp per
+// column j; lane l owns rows l, l + 32, l + 64 in registers.  Right-looking: once x_k is
+// known (broadcast from its lane) every lane updates its remaining rows, so a column costs
+// n shuffle + FMA steps and no reductions.
+template <bool UPPER>
+__device__ __forceinline__ void tri_solve_cols(const double* L, const double* invd,
+                                               const double* B, bool trans_b, double* X, int n,
+                                               int ld) {
+  constexpr int R = (EIG_MAXN + 31) / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NWARPS = EIG_THREADS / 32;
+  for (int j = warp; j < n; j += NWARPS) {
+    double b[R];
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+      const int i = lane + 32 * t;
+      b[t] = i < n ? (trans_b ? B[j * ld + i] : B[i * ld + j]) : 0.0;
+    }
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      const int sb = UPPER ? R - 1 - s : s;  // register slot of the rows of this block
+      for (int kk = 0; kk < 32; ++kk) {
+        const int kl = UPPER ? 31 - kk : kk;
+        const int k = 32 * sb + kl;
+        if (k >= n) continue;
+        const double xk = __shfl_sync(0xffffffffu, b[sb], kl) * invd[k];
+        if (lane == kl) X[k * ld + j] = xk;
+#pragma unroll
+        for (int t = 0; t < R; ++t) {
+          const int i = lane + 32 * t;
+          if (UPPER ? (i < k) : (i > k && i < n))
+            b[t] = fma(-(UPPER ? L[k * ld + i] : L[i * ld + k]), xk, b[t]);
+        }
+      }
+    }
+  }
+}
+
+// Right-looking Cholesky of the symmetric A (lower triangle, smem, pitch ld) in place; warp w
+// owns rows w, w+32, ...  On failure at pivot k, *flag = n + k + 1 (LAPACK's info > n
+// convention for the second matrix of a pencil).  Ends with a barrier.
+__device__ __forceinline__ void chol_lower(double* A, int n, int ld, int* flag) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NWARPS = EIG_THREADS / 32;
+  for (int k = 0; k < n; ++k) {
+    const double a = A[k * ld + k];
+    if (!(a > 0.0)) {
+      if (tid == 0) *flag = n + k + 1;
+      break;
+    }
+    const double dk = sqrt(a);
+    const double inv = 1.0 / dk;
+    __syncthreads();  // everyone has read A[k][k]
+    if (tid == 0) A[k * ld + k] = dk;
+    for (int i = k + 1 + tid; i < n; i += EIG_THREADS) A[i * ld + k] *= inv;
+    __syncthreads();
+    for (int i = k + 1 + warp; i < n; i += NWARPS) {
+      const double lik = A[i * ld + k];
+      for (int j = k + 1 + lane; j <= i; j += 32) A[i * ld + j] -= lik * A[j * ld + k];
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+}
+
 // One CTA (32 warps) per factor pair.  smem: L, C, V (n x n each, row-major).
 __global__ void __launch_bounds__(EIG_THREADS) k_gen_eig_small(const SmallEigJobs jobs,
                                                               int32_t* status) {
@@ -146,6 +220,7 @@ __global__ void __launch_bounds__(EIG_THREADS) k_gen_eig_small(const SmallEigJob
   double* L = esm;
   double* C = L + n * ld;
   double* V = C + n * ld;
+  double* invd = V + n * ld;  // 1 / diag of the Cholesky factor of M2
   __shared__ int flag;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -186,26 +261,8 @@ __global__ void __launch_bounds__(EIG_THREADS) k_gen_eig_small(const SmallEigJob
     }
   }
 
-  // right-looking Cholesky of M2 (lower triangle of L); warp w owns rows w, w+32, ...
-  for (int k = 0; k < n; ++k) {
-    const double a = L[k * ld + k];
-    if (!(a > 0.0)) {
-      if (tid == 0) flag = n + k + 1;  // LAPACK convention: info > n -> second matrix not PD
-      break;
-    }
-    const double dk = sqrt(a);
-    const double inv = 1.0 / dk;
-    __syncthreads();  // everyone has read L[k][k]
-    if (tid == 0) L[k * ld + k] = dk;
-    for (int i = k + 1 + tid; i < n; i += EIG_THREADS) L[i * ld + k] *= inv;
-    __syncthreads();
-    for (int i = k + 1 + warp; i < n; i += NWARPS) {
-      const double lik = L[i * ld + k];
-      for (int j = k + 1 + lane; j <= i; j += 32) L[i * ld + j] -= lik * L[j * ld + k];
-    }
-    __syncthreads();
-  }
-  __syncthreads();
+  // Cholesky of M2 (lower triangle of L); failure -> info > n (second matrix not PD)
+  chol_lower(L, n, ld, &flag);
   if (flag != 0) {
     if (tid == 0) {
       if (jb.info) *jb.info = flag;
@@ -215,24 +272,16 @@ __global__ void __launch_bounds__(EIG_THREADS) k_gen_eig_small(const SmallEigJob
     return;
   }
 
-  // C <- L^-1 C then C <- L^-1 C^T (C symmetric).  Warp per column, lanes split the dot
-  // product of each forward-substitution row.
-  for (int pass = 0; pass < 2; ++pass) {
-    for (int j = warp; j < n; j += NWARPS) {
-      for (int i = 0; i < n; ++i) {
-        double acc = 0.0;
-        for (int k = lane; k < i; k += 32) acc += L[i * ld + k] * V[k * ld + j];
-        acc = warp_sum(acc);
-        const double rhs = pass == 0 ? C[i * ld + j] : C[j * ld + i];
-        if (lane == 0) V[i * ld + j] = (rhs - acc) / L[i * ld + i];
-        __syncwarp();
-      }
-    }
-    __syncthreads();
-    for (int e = tid; e < n * ld; e += EIG_THREADS) C[e] = V[e];
-    __syncthreads();
-  }
-  // symmetrise (roundoff) and V = I
+  // C <- L^-1 C (into V), then C <- L^-1 (L^-1 C)^T (from V back into C): right-looking
+  // triangular solves, warp per column (tri_solve_cols)
+  for (int i = tid; i < n; i += EIG_THREADS) invd[i] = 1.0 / L[i * ld + i];
+  __syncthreads();
+  tri_solve_cols<false>(L, invd, C, false, V, n, ld);
+  __syncthreads();
+  tri_solve_cols<false>(L, invd, V, true, C, n, ld);
+  __syncthreads();
+  // symmetrise (roundoff), C = G G^T (Cholesky, G lower; strictly upper part zeroed) and
+  // W = I; one-sided Jacobi on the rows of G (jacobi_rows): C W^T = W^T diag(||g_i||^2)
   for (int e = tid; e < n * n; e += EIG_THREADS) {
     const int i = e / n, j = e % n;
     if (i < j) {
@@ -243,26 +292,40 @@ __global__ void __launch_bounds__(EIG_THREADS) k_gen_eig_small(const SmallEigJob
     V[i * ld + j] = (i == j) ? 1.0 : 0.0;
   }
   __syncthreads();
-
-  // parallel cyclic Jacobi (jacobi_sweeps): lane groups of 32 when the m/2 pairs fit the
-  // 32 warps, of 16 otherwise (n = 65..96), so no group ever handles two pairs per round
-  if (((n + 1) & ~1) / 2 <= NWARPS)
-    jacobi_sweeps<32>(C, V, n, ld, &flag);
-  else
-    jacobi_sweeps<16>(C, V, n, ld, &flag);
-
-  // eigenvalues; T = L^-T V (back substitution, warp per column) written to global
-  for (int i = tid; i < n; i += EIG_THREADS) jb.lam[i] = C[i * ld + i];
+  chol_lower(C, n, ld, &flag);
+  if (flag != 0) {  // M1 not PD
+    if (tid == 0) {
+      if (jb.info) *jb.info = n + 1;
+      if (jb.warm_valid) *jb.warm_valid = 0;
+      set_status_dev(status, KP_ERR_NOT_PSD);
+    }
+    return;
+  }
+  for (int e = tid; e < n * n; e += EIG_THREADS) {
+    const int i = e / n, j = e % n;
+    if (j > i) C[i * ld + j] = 0.0;
+  }
   __syncthreads();
-  for (int j = warp; j < n; j += NWARPS) {
-    for (int i = n - 1; i >= 0; --i) {
-      double acc = 0.0;
-      for (int k = i + 1 + lane; k < n; k += 32) acc += L[k * ld + i] * C[k * ld + j];
-      acc = warp_sum(acc);
-      if (lane == 0) C[i * ld + j] = (V[i * ld + j] - acc) / L[i * ld + i];  // C reused as T
-      __syncwarp();
+  jacobi_rows(C, V, n, ld, &flag, fmax(1e-14, 2.0 * n * 2.220446049250313e-16));
+
+  // eigenvalues; V <- W^T (column j = eigenvector j); T = L^-T V (back substitution, warp per
+  // column) written to global
+  for (int i = warp; i < n; i += NWARPS) {
+    double a = 0.0;
+    for (int j = lane; j < n; j += 32) a = fma(C[i * ld + j], C[i * ld + j], a);
+    a = warp_sum(a);
+    if (lane == 0) jb.lam[i] = a;
+  }
+  for (int e = tid; e < n * n; e += EIG_THREADS) {
+    const int i = e / n, j = e % n;
+    if (i < j) {
+      const double a = V[i * ld + j];
+      V[i * ld + j] = V[j * ld + i];
+      V[j * ld + i] = a;
     }
   }
+  __syncthreads();
+  tri_solve_cols<true>(L, invd, V, false, C, n, ld);  // C reused as T = L^-T V
   __syncthreads();
   const double* T = C;
   if (warm) {  // T = T_prev T''  (T_prev from global, T'' in C; result in V)
@@ -343,7 +406,9 @@ int small_eig_sweeps_used() {
   return v;
 }
 
-size_t small_eig_smem_bytes(int n) { return sizeof(double) * 3 * (size_t)n * eig_pitch(n); }
+size_t small_eig_smem_bytes(int n) {
+  return sizeof(double) * (3 * (size_t)n * eig_pitch(n) + (size_t)n);
+}
 
 void launch_gen_eig_small(const SmallEigJobs& jobs, int njobs, int max_n, int32_t* status,
                           cudaStream_t s) {
