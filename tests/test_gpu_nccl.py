@@ -138,3 +138,43 @@ def test_two_rank_distributed_solves_bit_identical(wkey):
     for e in ranks:
         assert np.array_equal(e.theta_numpy(), ref_theta)
         e.close()
+
+
+@pytest.mark.parametrize("wkey", ["c4", "c1"])
+def test_distributed_solve_failure_reaches_every_rank(wkey):
+    """A not-positive-definite factor pair detected by the owner of its layer must fail the
+    step on every rank (status slots of the direction buffer): both ranks end with
+    NotPositiveSemidefiniteError's code."""
+    from paper_2405_15603_b200 import configs
+    from paper_2405_15603_b200.dist import make_rank_engine
+    wl = configs.WORKLOADS[wkey]
+    prob, params, batch = wl.build(0, 200, 60)
+    L = len(wl.widths) - 1
+    owners = [l % 2 for l in range(L)]  # layer 1 belongs to rank 1
+    ranks = []
+    for _ in range(2):
+        e = make_rank_engine(wl.widths, batch, prob, 0, 1, ema=wl.ema, damping=wl.damping,
+                             momentum=0.0)
+        e.use_graph = False
+        e.load_params(params)
+        e.init_factors(True)
+        a_int, b_int, a_bnd, b_bnd = e.factor_lists()
+        a_bnd[1] = -100.0 * np.eye(a_bnd[1].shape[0])  # EMA keeps it indefinite
+        e.set_factor_lists(a_int, b_int, a_bnd, b_bnd)
+        ranks.append(e)
+    for e in ranks:
+        e.phase("accumulate")
+    for r, e in enumerate(ranks):
+        e.phase("precondition_owned", owned=[o == r for o in owners])
+    b0, b1 = ranks[0].direction_buffer(), ranks[1].direction_buffer()
+    total = b0 + b1
+    b0.copy_(total)
+    b1.copy_(total)
+    codes = []
+    for e in ranks:
+        e.phase("direction")
+        e.phase("linesearch")
+        e.phase("update")
+        codes.append(e.finish_step()[1])
+        e.close()
+    assert codes == [2, 2], codes  # KP_ERR_NOT_PSD on both ranks
