@@ -243,13 +243,16 @@ def test_damping_only_gives_half_negative_gradient():
     assert np.allclose(-x, -g / 2.0, atol=1e-12)
 
 
-def test_step_is_bit_deterministic():
-    wl = cfgs.WORKLOADS["c2"]
+@pytest.mark.parametrize("wkey,steps", [("c2", 2), ("c4", 4)])
+def test_step_is_bit_deterministic(wkey, steps):
+    """Two fresh runs give bitwise-identical parameters (c4: the cluster eigensolver, cold
+    and warm-started, and its DSMEM exchange)."""
+    wl = cfgs.WORKLOADS[wkey]
     prob, params, batch = wl.build(0, 500, 100)
     out = []
     for _ in range(2):
         state = init_train_state(params.copy(), OptimizerConfig(kind="kfac", damping=1e-3, ema=0.95))
-        for _ in range(2):
+        for _ in range(steps):
             optimizer_step(state, batch, prob)
         out.append(np.concatenate([w.ravel() for w in state.params.weights]))
     assert np.array_equal(out[0], out[1])
