@@ -51,42 +51,6 @@ __device__ __forceinline__ double warp_allsum(double v) {
   return v;
 }
 
-// Sum a, b, g over the warp with 4-value butterfly folding (9 shuffles of doubles instead of
-// 15): after the first two levels each lane holds one of the four partial sums.
-__device__ __forceinline__ void warp_sum3(double& a, double& b, double& g, int lane) {
-  double d = 0.0;
-  {  // level 16: lanes < 16 keep (a, b), lanes >= 16 keep (g, d)
-    const bool hi = lane & 16;
-    const double s0 = hi ? a : g, s1 = hi ? b : d;
-    const double r0 = __shfl_xor_sync(0xffffffffu, s0, 16);
-    const double r1 = __shfl_xor_sync(0xffffffffu, s1, 16);
-    if (hi) {
-      g += r0;
-      d += r1;
-    } else {
-      a += r0;
-      b += r1;
-    }
-    a = hi ? g : a;  // x0 = a (lo) or g (hi)
-    b = hi ? d : b;  // x1 = b (lo) or d (hi)
-  }
-  {  // level 8: lanes with bit 3 clear keep x0, set keep x1
-    const bool hi = lane & 8;
-    const double snd = hi ? a : b;
-    const double r = __shfl_xor_sync(0xffffffffu, snd, 8);
-    a = (hi ? b : a) + r;
-  }
-#pragma unroll
-  for (int o = 4; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-  // lane 0: sum a, lane 8: sum b, lane 16: sum g
-  const double sa = __shfl_sync(0xffffffffu, a, 0);
-  const double sb = __shfl_sync(0xffffffffu, a, 8);
-  const double sg = __shfl_sync(0xffffffffu, a, 16);
-  a = sa;
-  b = sb;
-  g = sg;
-}
-
 // rv: n x n column-major.  In: the upper-triangular Cholesky factor R of C (the strictly
 // lower part is ignored).  Out: the eigenvectors V of C = R^T R (column i = vector i).
 // lam[i] = eigenvalue i.  info: 0 ok, 1 no convergence in MID_MAX_SWEEPS sweeps, n + 1 when
@@ -175,7 +139,12 @@ __global__ void __launch_bounds__(((MID_MAXN / 2 + CL - 1) / CL) * 32, 1)
           b = fma(y[u], y[u], b);
           gm = fma(x[u], y[u], gm);
         }
-        warp_sum3(a, b, gm, lane);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {  // three interleaved butterflies: 5 dependent steps
+          a += __shfl_xor_sync(0xffffffffu, a, o);
+          b += __shfl_xor_sync(0xffffffffu, b, o);
+          gm += __shfl_xor_sync(0xffffffffu, gm, o);
+        }
         const bool rot = cp < n && cq < n && gm * gm > tol2 * (a * b) && fabs(gm) > 1e-300;
         double* dr = send_r ? mbox_right + (size_t)(0 * 2 + par) * cs2 : nullptr;  // their "from left"
         double* dl = send_l ? mbox_left + (size_t)(1 * 2 + par) * cs2 : nullptr;   // their "from right"
