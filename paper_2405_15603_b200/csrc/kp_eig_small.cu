@@ -396,6 +396,57 @@ __global__ void __launch_bounds__(1024) k_kron_combine_small(const SmallCombineJ
   }
 }
 
+// The same with every operand staged in shared memory (odd pitches: conflict-free column
+// walks); used when p^2 + q^2 + 2pq doubles fit (every layer up to 64 wide).
+__host__ __device__ inline int comb_pitch(int n) { return n | 1; }
+__host__ __device__ inline size_t comb_smem_doubles(int p, int q) {
+  return (size_t)p * comb_pitch(p) + (size_t)q * comb_pitch(q) + 2 * (size_t)q * comb_pitch(p);
+}
+constexpr size_t COMB_SMEM_MAX = 200 * 1024;
+
+__global__ void __launch_bounds__(1024) k_kron_combine_small_smem(const SmallCombineJobs jobs) {
+  extern __shared__ double csm[];
+  const SmallCombineJob jb = jobs.job[blockIdx.x];
+  const int p = jb.p, q = jb.q;
+  const int lp = comb_pitch(p), lq = comb_pitch(q);
+  double* TA = csm;              // p x p
+  double* TB = TA + p * lp;      // q x q
+  double* X = TB + q * lq;       // q x p
+  double* Y = X + q * lp;        // q x p
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int e = tid; e < p * p; e += nt) TA[(e / p) * lp + e % p] = jb.ta[e];
+  for (int e = tid; e < q * q; e += nt) TB[(e / q) * lq + e % q] = jb.tb[e];
+  for (int e = tid; e < q * p; e += nt) X[(e / p) * lp + e % p] = jb.g[e];
+  __syncthreads();
+  for (int e = tid; e < q * p; e += nt) {  // Y = G T_A
+    const int i = e / p, j = e % p;
+    double v = 0.0;
+    for (int k = 0; k < p; ++k) v = fma(X[i * lp + k], TA[k * lp + j], v);
+    Y[i * lp + j] = v;
+  }
+  __syncthreads();
+  for (int e = tid; e < q * p; e += nt) {  // X = (T_B^T Y) / (lb_i la_j + 1)
+    const int i = e / p, j = e % p;
+    double v = 0.0;
+    for (int k = 0; k < q; ++k) v = fma(TB[k * lq + i], Y[k * lp + j], v);
+    X[i * lp + j] = v / (jb.lb[i] * jb.la[j] + 1.0);
+  }
+  __syncthreads();
+  for (int e = tid; e < q * p; e += nt) {  // Y = X T_A^T
+    const int i = e / p, j = e % p;
+    double v = 0.0;
+    for (int k = 0; k < p; ++k) v = fma(X[i * lp + k], TA[j * lp + k], v);
+    Y[i * lp + j] = v;
+  }
+  __syncthreads();
+  for (int e = tid; e < q * p; e += nt) {  // out = sign T_B Y
+    const int i = e / p, j = e % p;
+    double v = 0.0;
+    for (int k = 0; k < q; ++k) v = fma(TB[i * lq + k], Y[k * lp + j], v);
+    jb.out[e] = jb.sign * v;
+  }
+}
+
 }  // namespace
 
 int small_eig_max_n() { return EIG_MAXN; }
@@ -426,8 +477,21 @@ void launch_gen_eig_small(const SmallEigJobs& jobs, int njobs, int max_n, int32_
 
 void launch_kron_combine_small(const SmallCombineJobs& jobs, int njobs, cudaStream_t s) {
   if (njobs <= 0) return;
+  size_t need = 0;
+  for (int j = 0; j < njobs; ++j)
+    need = std::max(need, sizeof(double) * comb_smem_doubles(jobs.job[j].p, jobs.job[j].q));
   count_launch();
-  k_kron_combine_small<<<njobs, 1024, 0, s>>>(jobs);
+  if (need <= COMB_SMEM_MAX) {
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(k_kron_combine_small_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)COMB_SMEM_MAX);
+      attr_set = true;
+    }
+    k_kron_combine_small_smem<<<njobs, 1024, need, s>>>(jobs);
+  } else {
+    k_kron_combine_small<<<njobs, 1024, 0, s>>>(jobs);
+  }
 }
 
 }  // namespace kp
