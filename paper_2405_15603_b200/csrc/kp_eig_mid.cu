@@ -327,21 +327,22 @@ int g_mid_cl = 0;  // 0: not chosen yet
 
 }  // namespace
 
-int mid_eig_max_n() { return MID_MAXN; }
+int mid_eig_cluster_size() {
+  if (g_mid_cl == 0) {
+    const char* env = getenv("KP_MID_CLUSTER");
+    const int want = env ? atoi(env) : 16;  // 16 (default), 8, or 0 = off (cuSOLVER route)
+    g_mid_cl = want == 0 ? -1 : (want == 16 && mid_setup<16>()) ? 16 : (mid_setup<8>() ? 8 : -1);
+  }
+  return g_mid_cl;
+}
+
+// 0 when no cluster launch of the kernel can be scheduled: the pairs then take the cuSOLVER route.
+int mid_eig_max_n() { return mid_eig_cluster_size() > 0 ? MID_MAXN : 0; }
 
 int mid_eig_sweeps_used() {
   int v = 0;
   cudaMemcpyFromSymbol(&v, g_mid_sweeps_max, sizeof(int));
   return v;
-}
-
-int mid_eig_cluster_size() {
-  if (g_mid_cl == 0) {
-    const char* env = getenv("KP_MID_CLUSTER");
-    const int want = env ? atoi(env) : 16;
-    g_mid_cl = (want == 16 && mid_setup<16>()) ? 16 : (mid_setup<8>() ? 8 : -1);
-  }
-  return g_mid_cl;
 }
 
 void launch_eig_mid(int n, double* rv, double* lam, int* info, const int* chol_info,

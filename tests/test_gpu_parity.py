@@ -396,3 +396,21 @@ def test_tiny_batches_match_oracle(n_int, n_bnd):
     """Ragged edge: one or a few collocation points (single-sample tiles, partial splits)."""
     _oracle_vs_device((2, 16, 8, 1), make_problem("poisson2d_sin"), n_int, n_bnd, 2)
     _oracle_vs_device((5, 64, 64, 48, 48, 1), make_problem("heat", spatial_dim=4), n_int, n_bnd, 2)
+
+
+@pytest.mark.parametrize("cluster", ["8", "0"], ids=["cluster8", "cusolver"])
+def test_mid_size_pairs_other_routes_match_reference(cluster):
+    """c4's mid-size factor pairs through the 8-CTA-cluster solver and through the cuSOLVER
+    fallback (taken when no cluster launch can be scheduled) match the reference goldens too
+    (KP_MID_CLUSTER is read once per process, hence the subprocess)."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, KP_MID_CLUSTER=cluster)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_parity.py"), "-k",
+                        "test_kfac_steps_match_reference_golden and c4"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "2 passed" in r.stdout, r.stdout[-500:]
