@@ -25,14 +25,16 @@ namespace kp {
 
 namespace {
 
-constexpr int EIG_THREADS = 1024;
+constexpr int EIG_THREADS = 768;  // 24 warps: 48 half-warp pairs (n <= 96)
 constexpr int EIG_MAXN = 96;
 constexpr int EIG_MAX_SWEEPS = 30;
 // Rotate only when |a_pq| > tol * sqrt(|a_pp a_qq|): relative accuracy ~1e-14 per eigenpair
 // (the KFAC parity bar is 1e-10); tighter values let roundoff re-trigger rotations forever.
 constexpr double kJacobiTol = 1e-14;
 
-__host__ __device__ inline int eig_pitch(int n) { return ((n - 1 + 15) / 16) * 16 + 1; }
+// 16k+1 doubles with 16k >= n: column walks hit 32 distinct banks, and a row holds the
+// 16 * ceil(n / 16) elements the Jacobi rounds read without bounds checks (zero padded)
+__host__ __device__ inline int eig_pitch(int n) { return ((n + 15) / 16) * 16 + 1; }
 
 __device__ int g_eig_sweeps_max = 0;  // diagnostic: most Jacobi sweeps used by any job
 
@@ -40,15 +42,42 @@ __device__ __forceinline__ void set_status_dev(int32_t* status, int32_t code) {
   atomicCAS(status, 0, code);
 }
 
+// 2^-e for the binary exponent e of x > 0 (exact power of two; x normal).
+__device__ __forceinline__ double pow2_neg_exponent(double x) {
+  const int e = ((__double2hiint(x) >> 20) & 0x7ff) - 1023;
+  return __hiloint2double((1023 - e) << 20, 0);
+}
+
+// Rotation (cs, sn) that orthogonalises two rows with squared norms a, b and inner product
+// g: tan = 2g sign(b - a) / (|b - a| + sqrt((b - a)^2 + 4 g^2)), formed in FP32 after a
+// power-of-two rescaling (the angle only steers convergence: an inexact one leaves a tiny
+// remainder for the next sweep); cs = (1 + t^2)^-1/2 from an FP32 estimate refined by two
+// FP64 Newton steps, sn = cs t, so cs^2 + sn^2 = 1 to FP64 precision.  Branch-free.
+__device__ __forceinline__ void jacobi_angle(double a, double b, double g, double& cs,
+                                             double& sn) {
+  const double d = b - a, g2 = 2.0 * g;
+  const double sc = pow2_neg_exponent(fmax(fabs(d), fabs(g2)));
+  const float df = (float)(d * sc), gf = (float)(g2 * sc);
+  const float den = fabsf(df) + sqrtf(fmaf(df, df, gf * gf));
+  const float tf = (df >= 0.0f ? gf : -gf) * __frcp_rn(den);
+  const double t = (double)tf;
+  const double q1 = fma(t, t, 1.0);
+  double y = (double)rsqrtf((float)q1);
+  y = y * fma(-0.5 * q1 * y, y, 1.5);
+  y = y * fma(-0.5 * q1 * y, y, 1.5);
+  cs = y;
+  sn = y * t;
+}
+
 // One-sided (Hestenes) Jacobi on the ROWS of a lower-triangular factor G (C = G G^T), with
 // the same rotations applied to the rows of W (start: W = I).  On return the rows of G are
 // mutually orthogonal: row i of W is eigenvector i of C and ||row i of G||^2 its eigenvalue.
 // Half-warp k owns pair k of each round (circle-method ordering over m = n rounded up to
-// even, index n a dummy when n is odd): it loads the two rows into registers, forms the three
-// dot products with a 4-level shuffle reduction and rotates both rows of G and W.  Rows do
-// not move, only the pairing changes, so a round is one CTA barrier.
-constexpr int OS_EPL = (EIG_MAXN + 15) / 16;  // row elements per lane of a half-warp
-
+// even, index n a dummy when n is odd): it loads the two rows into registers (EPL elements
+// per lane; rows zero-padded to 16 EPL, so no bounds checks), forms the three dot products
+// with a 4-level shuffle reduction and rotates both rows of G and W.  Rows do not move,
+// only the pairing changes, so a round is one CTA barrier.
+template <int EPL>
 __device__ __forceinline__ void jacobi_rows(double* G, double* W, int n, int ld, int* flag,
                                             double tol) {
   const int tid = threadIdx.x, lane = tid & 31;
@@ -71,15 +100,14 @@ __device__ __forceinline__ void jacobi_rows(double* G, double* W, int n, int ld,
         if (k != 0) ia = (ia + 1 == m - 1) ? 0 : ia + 1;
         ib = (ib + 1 == m - 1) ? 0 : ib + 1;
         if (q < n) {
-          double* gp = G + p * ld;
-          double* gq = G + q * ld;
-          double x[OS_EPL], y[OS_EPL];
+          double* gp = G + p * ld + hl;
+          double* gq = G + q * ld + hl;
+          double x[EPL], y[EPL];
           double al = 0.0, be = 0.0, ga = 0.0;
 #pragma unroll
-          for (int u = 0; u < OS_EPL; ++u) {
-            const int i = hl + 16 * u;
-            x[u] = i < n ? gp[i] : 0.0;
-            y[u] = i < n ? gq[i] : 0.0;
+          for (int u = 0; u < EPL; ++u) {
+            x[u] = gp[16 * u];
+            y[u] = gq[16 * u];
             al = fma(x[u], x[u], al);
             be = fma(y[u], y[u], be);
             ga = fma(x[u], y[u], ga);
@@ -91,23 +119,17 @@ __device__ __forceinline__ void jacobi_rows(double* G, double* W, int n, int ld,
             ga += __shfl_xor_sync(hmask, ga, o);
           }
           if (ga * ga > tol2 * (al * be) && fabs(ga) > 1e-300) {
-            // tan of the angle: 2g sign(b - a) / (|b - a| + sqrt((b - a)^2 + 4 g^2))
-            const double dba = be - al, g2 = 2.0 * ga;
-            const double t = (dba >= 0.0 ? g2 : -g2) / (fabs(dba) + sqrt(fma(dba, dba, g2 * g2)));
-            const double cs = rsqrt(fma(t, t, 1.0));
-            const double sn = cs * t;
-            double* wp = W + p * ld;
-            double* wq = W + q * ld;
+            double cs, sn;
+            jacobi_angle(al, be, ga, cs, sn);
+            double* wp = W + p * ld + hl;
+            double* wq = W + q * ld + hl;
 #pragma unroll
-            for (int u = 0; u < OS_EPL; ++u) {
-              const int i = hl + 16 * u;
-              if (i < n) {
-                gp[i] = cs * x[u] - sn * y[u];
-                gq[i] = sn * x[u] + cs * y[u];
-                const double wx = wp[i], wy = wq[i];
-                wp[i] = cs * wx - sn * wy;
-                wq[i] = sn * wx + cs * wy;
-              }
+            for (int u = 0; u < EPL; ++u) {
+              gp[16 * u] = cs * x[u] - sn * y[u];
+              gq[16 * u] = sn * x[u] + cs * y[u];
+              const double wx = wp[16 * u], wy = wq[16 * u];
+              wp[16 * u] = cs * wx - sn * wy;
+              wq[16 * u] = sn * wx + cs * wy;
             }
             if (hl == 0) *flag = 1;
           }
@@ -301,12 +323,24 @@ __global__ void __launch_bounds__(EIG_THREADS) k_gen_eig_small(const SmallEigJob
     }
     return;
   }
-  for (int e = tid; e < n * n; e += EIG_THREADS) {
-    const int i = e / n, j = e % n;
+  const int nr = ((n + 15) / 16) * 16;  // padded row length read by the Jacobi rounds
+  for (int e = tid; e < n * nr; e += EIG_THREADS) {
+    const int i = e / nr, j = e % nr;
     if (j > i) C[i * ld + j] = 0.0;
+    if (j >= n) V[i * ld + j] = 0.0;
   }
   __syncthreads();
-  jacobi_rows(C, V, n, ld, &flag, fmax(1e-14, 2.0 * n * 2.220446049250313e-16));
+  {
+    const double tol = fmax(1e-14, 2.0 * n * 2.220446049250313e-16);
+    switch (nr / 16) {
+      case 1: jacobi_rows<1>(C, V, n, ld, &flag, tol); break;
+      case 2: jacobi_rows<2>(C, V, n, ld, &flag, tol); break;
+      case 3: jacobi_rows<3>(C, V, n, ld, &flag, tol); break;
+      case 4: jacobi_rows<4>(C, V, n, ld, &flag, tol); break;
+      case 5: jacobi_rows<5>(C, V, n, ld, &flag, tol); break;
+      default: jacobi_rows<6>(C, V, n, ld, &flag, tol); break;
+    }
+  }
 
   // eigenvalues; V <- W^T (column j = eigenvector j); T = L^-T V (back substitution, warp per
   // column) written to global
