@@ -119,4 +119,31 @@ __device__ __forceinline__ TanhD tanh_derivs(double z, bool third) {
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// 2^-e for the binary exponent e of x > 0 (exact power of two; x normal).
+__device__ __forceinline__ double pow2_neg_exponent(double x) {
+  const int e = ((__double2hiint(x) >> 20) & 0x7ff) - 1023;
+  return __hiloint2double((1023 - e) << 20, 0);
+}
+
+// Rotation (cs, sn) that orthogonalises two rows with squared norms a, b and inner product
+// g: tan = 2g sign(b - a) / (|b - a| + sqrt((b - a)^2 + 4 g^2)), formed in FP32 after a
+// power-of-two rescaling (the angle only steers convergence: an inexact one leaves a tiny
+// remainder for the next sweep); cs = (1 + t^2)^-1/2 from an FP32 estimate refined by two
+// FP64 Newton steps, sn = cs t, so cs^2 + sn^2 = 1 to FP64 precision.  Branch-free.
+__device__ __forceinline__ void jacobi_angle(double a, double b, double g, double& cs,
+                                             double& sn) {
+  const double d = b - a, g2 = 2.0 * g;
+  const double sc = pow2_neg_exponent(fmax(fabs(d), fabs(g2)));
+  const float df = (float)(d * sc), gf = (float)(g2 * sc);
+  const float den = fabsf(df) + sqrtf(fmaf(df, df, gf * gf));
+  const float tf = (df >= 0.0f ? gf : -gf) * __frcp_rn(den);
+  const double t = (double)tf;
+  const double q1 = fma(t, t, 1.0);
+  double y = (double)rsqrtf((float)q1);
+  y = y * fma(-0.5 * q1 * y, y, 1.5);
+  y = y * fma(-0.5 * q1 * y, y, 1.5);
+  cs = y;
+  sn = y * t;
+}
+
 }  // namespace kp

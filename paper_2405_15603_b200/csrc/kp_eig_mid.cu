@@ -39,7 +39,6 @@ namespace {
 
 constexpr int MID_MAXN = 288;
 constexpr int MID_MAX_SWEEPS = 40;
-constexpr int MID_EPL = (MID_MAXN + 31) / 32;  // column elements per lane
 
 __device__ int g_mid_sweeps_max = 0;  // diagnostic: most sweeps used by any solve
 
@@ -63,7 +62,7 @@ __device__ __forceinline__ double warp_allsum(double v) {
 // outgoing columns (last top slot -> right neighbour, first bottom slot -> left neighbour)
 // also store them into the neighbour's mailbox.  One cluster barrier; then each CTA copies
 // its mailboxes into the records it handed over and writes the next round's slot table.
-template <int CL>
+template <int CL, int EF>
 __global__ void __launch_bounds__(((MID_MAXN / 2 + CL - 1) / CL) * 32, 1)
     k_eig_mid(int n, double* __restrict__ rv, double* __restrict__ lam, int* __restrict__ info,
               const int* __restrict__ chol_info, double tol, int* __restrict__ warm_valid,
@@ -128,13 +127,21 @@ __global__ void __launch_bounds__(((MID_MAXN / 2 + CL - 1) / CL) * 32, 1)
         // this warp forwards its top column to the right / its bottom column to the left
         const bool send_r = warp == ppc - 1 && c < CL - 1;
         const bool send_l = warp == 0 && c > 0;
-        double x[MID_EPL], y[MID_EPL];
+        // EF = n / 32 full 32-element slices per column (no bounds checks) + a tail of
+        // n - 32 EF elements (lanes below it)
+        const int tail = n - 32 * EF;
+        const bool tl = lane < tail;
+        double x[EF + 1], y[EF + 1];
         double a = 0.0, b = 0.0, gm = 0.0;
 #pragma unroll
-        for (int u = 0; u < MID_EPL; ++u) {
-          const int i = lane + 32 * u;
-          x[u] = i < n ? rp[i] : 0.0;
-          y[u] = i < n ? rq[i] : 0.0;
+        for (int u = 0; u < EF; ++u) {
+          x[u] = rp[lane + 32 * u];
+          y[u] = rq[lane + 32 * u];
+        }
+        x[EF] = tl ? rp[32 * EF + lane] : 0.0;
+        y[EF] = tl ? rq[32 * EF + lane] : 0.0;
+#pragma unroll
+        for (int u = 0; u <= EF; ++u) {
           a = fma(x[u], x[u], a);
           b = fma(y[u], y[u], b);
           gm = fma(x[u], y[u], gm);
@@ -148,18 +155,15 @@ __global__ void __launch_bounds__(((MID_MAXN / 2 + CL - 1) / CL) * 32, 1)
         const bool rot = cp < n && cq < n && gm * gm > tol2 * (a * b) && fabs(gm) > 1e-300;
         double* dr = send_r ? mbox_right + (size_t)(0 * 2 + par) * cs2 : nullptr;  // their "from left"
         double* dl = send_l ? mbox_left + (size_t)(1 * 2 + par) * cs2 : nullptr;   // their "from right"
+        double* vp = rp + n;
+        double* vq = rq + n;
         if (rot) {
-          // t = tan of the rotation angle: 2g sign(b - a) / (|b - a| + sqrt((b - a)^2 + 4 g^2))
-          const double dba = b - a, g2 = 2.0 * gm;
-          const double t = (dba >= 0.0 ? g2 : -g2) / (fabs(dba) + sqrt(fma(dba, dba, g2 * g2)));
-          const double cs = rsqrt(fma(t, t, 1.0));
-          const double sn = cs * t;
-          double* vp = rp + n;
-          double* vq = rq + n;
+          double cs, sn;
+          jacobi_angle(a, b, gm, cs, sn);
 #pragma unroll
-          for (int u = 0; u < MID_EPL; ++u) {
+          for (int u = 0; u <= EF; ++u) {
             const int i = lane + 32 * u;
-            if (i < n) {
+            if (u < EF || tl) {
               const double xr = cs * x[u] - sn * y[u], yr = sn * x[u] + cs * y[u];
               const double pu = vp[i], qu = vq[i];
               const double xv = cs * pu - sn * qu, yv = sn * pu + cs * qu;
@@ -180,16 +184,16 @@ __global__ void __launch_bounds__(((MID_MAXN / 2 + CL - 1) / CL) * 32, 1)
           if (lane == 0) rotated = 1;
         } else if (send_r || send_l) {
 #pragma unroll
-          for (int u = 0; u < MID_EPL; ++u) {
+          for (int u = 0; u <= EF; ++u) {
             const int i = lane + 32 * u;
-            if (i < n) {
+            if (u < EF || tl) {
               if (send_r) {
                 dr[i] = x[u];
-                dr[n + i] = rp[n + i];
+                dr[n + i] = vp[i];
               }
               if (send_l) {
                 dl[i] = y[u];
-                dl[n + i] = rq[n + i];
+                dl[n + i] = vq[i];
               }
             }
           }
@@ -278,13 +282,26 @@ size_t mid_smem(int n) {
 // (non-portable size), else 8.
 template <int CL>
 bool mid_setup() {
-  auto kern = k_eig_mid<CL>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)mid_smem<CL>(MID_MAXN)) != cudaSuccess)
+  auto kern = k_eig_mid<CL, MID_MAXN / 32>;
+  bool ok = true;
+  auto attrs = [&](auto k) {
+    ok = ok && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)mid_smem<CL>(MID_MAXN)) == cudaSuccess;
+    if (CL > 8)
+      ok = ok && cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                     cudaSuccess;
+  };
+  attrs(k_eig_mid<CL, 3>);
+  attrs(k_eig_mid<CL, 4>);
+  attrs(k_eig_mid<CL, 5>);
+  attrs(k_eig_mid<CL, 6>);
+  attrs(k_eig_mid<CL, 7>);
+  attrs(k_eig_mid<CL, 8>);
+  attrs(k_eig_mid<CL, 9>);
+  if (!ok) {
+    cudaGetLastError();
     return false;
-  if (CL > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
-                    cudaSuccess)
-    return false;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(CL);
   cfg.blockDim = dim3(mid_ppc(MID_MAXN, CL) * 32);
@@ -320,7 +337,23 @@ void launch_mid(int n, double* rv, double* lam, int* info, const int* chol_info,
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_eig_mid<CL>, n, rv, lam, info, chol_info, tol, warm_valid, prof);
+  switch (n / 32) {
+#define KP_MID_CASE(E)                                                                     \
+  case E:                                                                                  \
+    cudaLaunchKernelEx(&cfg, k_eig_mid<CL, E>, n, rv, lam, info, chol_info, tol, warm_valid, \
+                       prof);                                                              \
+    break;
+    KP_MID_CASE(3)
+    KP_MID_CASE(4)
+    KP_MID_CASE(5)
+    KP_MID_CASE(6)
+    KP_MID_CASE(7)
+    KP_MID_CASE(8)
+    KP_MID_CASE(9)
+#undef KP_MID_CASE
+    default:
+      break;
+  }
 }
 
 int g_mid_cl = 0;  // 0: not chosen yet
