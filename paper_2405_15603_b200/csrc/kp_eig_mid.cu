@@ -82,17 +82,21 @@ __global__ void __launch_bounds__(((MID_MAXN / 2 + CL - 1) / CL) * 32, 1)
   const int ppc = mid_ppc(n, CL);
   const int m = 2 * CL * ppc;  // padded column count (columns >= n are zero)
   const size_t cs2 = 2 * (size_t)n;  // one column record: R (n) then V (n)
-  double* buf = msm;                          // 2 ppc records
-  double* mbox = msm + (size_t)2 * ppc * cs2;  // [dir][par]: dir 0 = from the left
-  __shared__ int top[2][MAXPPC], bot[2][MAXPPC], colid[2 * MAXPPC];
-  __shared__ int mcol[2][2];
+  double* buf = msm;  // 2 ppc + 4 records: the slots' columns and 4 landing records
+  // land[dir][par]: the record a neighbour stores its handed-over column into in rounds of
+  // parity par (dir 0: from the left, 1: from the right).  After the round the record joins
+  // the slot table and the record this CTA handed over in that direction takes its place.
+  __shared__ int top[2][MAXPPC], bot[2][MAXPPC], colid[2 * MAXPPC + 4];
+  __shared__ int land[2][2];
   __shared__ int rotated;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* const buf_left = cluster.map_shared_rank(buf, c > 0 ? c - 1 : c);
+  double* const buf_right = cluster.map_shared_rank(buf, c < CL - 1 ? c + 1 : c);
+  int* const colid_left = cluster.map_shared_rank(colid, c > 0 ? c - 1 : c);
+  int* const colid_right = cluster.map_shared_rank(colid, c < CL - 1 ? c + 1 : c);
+  const int* const land_left = cluster.map_shared_rank(&land[0][0], c > 0 ? c - 1 : c);
+  const int* const land_right = cluster.map_shared_rank(&land[0][0], c < CL - 1 ? c + 1 : c);
   const int nthr = blockDim.x;
-  double* const mbox_left = cluster.map_shared_rank(mbox, c > 0 ? c - 1 : c);
-  double* const mbox_right = cluster.map_shared_rank(mbox, c < CL - 1 ? c + 1 : c);
-  int* const mcol_left = cluster.map_shared_rank(&mcol[0][0], c > 0 ? c - 1 : c);
-  int* const mcol_right = cluster.map_shared_rank(&mcol[0][0], c < CL - 1 ? c + 1 : c);
   const double tol2 = tol * tol;
 
   if (tid < ppc) {
@@ -102,6 +106,10 @@ __global__ void __launch_bounds__(((MID_MAXN / 2 + CL - 1) / CL) * 32, 1)
     colid[tid] = 2 * g;
     colid[ppc + tid] = 2 * g + 1;
   }
+  if (tid < 4) {
+    land[tid >> 1][tid & 1] = 2 * ppc + tid;
+    colid[2 * ppc + tid] = -1;
+  }
   for (int e = tid; e < 2 * ppc * n; e += nthr) {
     const int b = e / n, i = e % n;
     const int k = b < ppc ? b : b - ppc;
@@ -109,15 +117,16 @@ __global__ void __launch_bounds__(((MID_MAXN / 2 + CL - 1) / CL) * 32, 1)
     buf[b * cs2 + i] = (col < n && i <= col) ? rv[(size_t)col * n + i] : 0.0;
     buf[b * cs2 + n + i] = (i == col) ? 1.0 : 0.0;
   }
-  cluster.sync();  // every CTA initialised before any mailbox store
+  cluster.sync();  // every CTA initialised before any remote store
 
-  int sweep = 0, cur = 0;  // cur: slot table of the current round
+  int sweep = 0, cur = 0;  // cur: slot table of the current round (= parity of gr)
+  int gr = 0;              // rounds so far, across sweeps
   bool converged = false;
   for (; sweep < MID_MAX_SWEEPS; ++sweep) {
     if (tid == 0) rotated = 0;
     __syncthreads();
-    for (int round = 0; round < m - 1; ++round) {
-      const int par = round & 1;
+    for (int round = 0; round < m - 1; ++round, ++gr) {
+      const int par = gr & 1;
       if (prof) t0 = clock64();
       if (warp < ppc) {
         const int bp = top[cur][warp], bq = bot[cur][warp];
@@ -127,6 +136,9 @@ __global__ void __launch_bounds__(((MID_MAXN / 2 + CL - 1) / CL) * 32, 1)
         // this warp forwards its top column to the right / its bottom column to the left
         const bool send_r = warp == ppc - 1 && c < CL - 1;
         const bool send_l = warp == 0 && c > 0;
+        // the neighbour's landing record for this round (set two rounds ago, see land[])
+        const int dst_r = send_r ? land_right[0 * 2 + par] : 0;  // their "from the left"
+        const int dst_l = send_l ? land_left[1 * 2 + par] : 0;   // their "from the right"
         // EF = n / 32 full 32-element slices per column (no bounds checks) + a tail of
         // n - 32 EF elements (lanes below it)
         const int tail = n - 32 * EF;
@@ -153,8 +165,8 @@ __global__ void __launch_bounds__(((MID_MAXN / 2 + CL - 1) / CL) * 32, 1)
           gm += __shfl_xor_sync(0xffffffffu, gm, o);
         }
         const bool rot = cp < n && cq < n && gm * gm > tol2 * (a * b) && fabs(gm) > 1e-300;
-        double* dr = send_r ? mbox_right + (size_t)(0 * 2 + par) * cs2 : nullptr;  // their "from left"
-        double* dl = send_l ? mbox_left + (size_t)(1 * 2 + par) * cs2 : nullptr;   // their "from right"
+        double* dr = send_r ? buf_right + (size_t)dst_r * cs2 : nullptr;
+        double* dl = send_l ? buf_left + (size_t)dst_l * cs2 : nullptr;
         double* vp = rp + n;
         double* vq = rq + n;
         if (rot) {
@@ -199,38 +211,29 @@ __global__ void __launch_bounds__(((MID_MAXN / 2 + CL - 1) / CL) * 32, 1)
           }
         }
         if (lane == 0) {
-          if (send_r) mcol_right[0 * 2 + par] = cp;
-          if (send_l) mcol_left[1 * 2 + par] = cq;
+          if (send_r) colid_right[dst_r] = cp;
+          if (send_l) colid_left[dst_l] = cq;
         }
       }
       if (prof) { __syncthreads(); const long long t1 = clock64(); t_rot += t1 - t0; t0 = t1; }
       cluster.sync();  // rotations done, mailboxes filled (release / acquire)
       if (prof) { const long long t1 = clock64(); t_sync += t1 - t0; t0 = t1; }
-      // mailboxes -> the records this CTA handed over; next slot table by the circle method:
-      // top[k] <- top[k-1], bot[k] <- bot[k+1]; cluster ends: global top[0] stays,
-      // global bot[0] -> top[1], global top[last] -> bot[last]
+      // next slot table by the circle method: top[k] <- top[k-1], bot[k] <- bot[k+1];
+      // cluster ends: global top[0] stays, global bot[0] -> top[1], global top[last] ->
+      // bot[last]; the columns that arrived sit in land[.][par], the records handed over
+      // become the landing records of round + 2
       const int ot = top[cur][ppc - 1], ob = bot[cur][0];
-      const int recv_l = (c == CL - 1) ? ob : ot;
-      const int recv_r = (c == 0) ? ot : ob;
-      if (c > 0) {
-        const double* src = mbox + (size_t)(0 * 2 + par) * cs2;
-        double* dst = buf + recv_l * cs2;
-        for (int i = tid; i < 2 * n; i += nthr) dst[i] = src[i];
-      }
-      if (c < CL - 1) {
-        const double* src = mbox + (size_t)(1 * 2 + par) * cs2;
-        double* dst = buf + recv_r * cs2;
-        for (int i = tid; i < 2 * n; i += nthr) dst[i] = src[i];
-      }
+      const int in_l = land[0][par], in_r = land[1][par];
       if (tid < ppc) {
         const int k = tid;
         top[cur ^ 1][k] =
-            k == 0 ? (c == 0 ? top[cur][0] : recv_l) : ((c == 0 && k == 1) ? ob : top[cur][k - 1]);
-        bot[cur ^ 1][k] = k == ppc - 1 ? (c == CL - 1 ? ot : recv_r) : bot[cur][k + 1];
+            k == 0 ? (c == 0 ? top[cur][0] : in_l) : ((c == 0 && k == 1) ? ob : top[cur][k - 1]);
+        bot[cur ^ 1][k] = k == ppc - 1 ? (c == CL - 1 ? ot : in_r) : bot[cur][k + 1];
       }
-      if (tid == 32) {
-        if (c > 0) colid[recv_l] = mcol[0][par];
-        if (c < CL - 1) colid[recv_r] = mcol[1][par];
+      __syncthreads();  // everyone has read land[.][par] and the old slot table
+      if (tid == 0) {
+        if (c > 0) land[0][par] = ob;       // handed to the left this round
+        if (c < CL - 1) land[1][par] = ot;  // handed to the right this round
       }
       cur ^= 1;
       __syncthreads();
@@ -275,7 +278,7 @@ __global__ void __launch_bounds__(((MID_MAXN / 2 + CL - 1) / CL) * 32, 1)
 
 template <int CL>
 size_t mid_smem(int n) {
-  return (size_t)(2 * mid_ppc(n, CL) + 4) * 2 * n * sizeof(double);
+  return (size_t)(2 * mid_ppc(n, CL) + 4) * 2 * n * sizeof(double);  // slots + landing records
 }
 
 // Cluster size: 16 when the device can co-schedule 16-CTA clusters of this kernel
