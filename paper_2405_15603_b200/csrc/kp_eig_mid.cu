@@ -216,21 +216,27 @@ __global__ void __launch_bounds__(((MID_MAXN / 2 + CL - 1) / CL) * 32, 1)
         }
       }
       if (prof) { __syncthreads(); const long long t1 = clock64(); t_rot += t1 - t0; t0 = t1; }
-      cluster.sync();  // rotations done, mailboxes filled (release / acquire)
-      if (prof) { const long long t1 = clock64(); t_sync += t1 - t0; t0 = t1; }
       // next slot table by the circle method: top[k] <- top[k-1], bot[k] <- bot[k+1];
       // cluster ends: global top[0] stays, global bot[0] -> top[1], global top[last] ->
       // bot[last]; the columns that arrived sit in land[.][par], the records handed over
-      // become the landing records of round + 2
+      // become the landing records of round + 2.  The table is local, so it is written
+      // between the two halves of the cluster barrier; land[.][par] (which neighbours read
+      // during the rotation phase) is read before the arrive and rewritten after the wait.
       const int ot = top[cur][ppc - 1], ob = bot[cur][0];
       const int in_l = land[0][par], in_r = land[1][par];
+      int ntop = 0, nbot = 0;
       if (tid < ppc) {
         const int k = tid;
-        top[cur ^ 1][k] =
-            k == 0 ? (c == 0 ? top[cur][0] : in_l) : ((c == 0 && k == 1) ? ob : top[cur][k - 1]);
-        bot[cur ^ 1][k] = k == ppc - 1 ? (c == CL - 1 ? ot : in_r) : bot[cur][k + 1];
+        ntop = k == 0 ? (c == 0 ? top[cur][0] : in_l) : ((c == 0 && k == 1) ? ob : top[cur][k - 1]);
+        nbot = k == ppc - 1 ? (c == CL - 1 ? ot : in_r) : bot[cur][k + 1];
       }
-      __syncthreads();  // everyone has read land[.][par] and the old slot table
+      asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+      if (tid < ppc) {
+        top[cur ^ 1][tid] = ntop;
+        bot[cur ^ 1][tid] = nbot;
+      }
+      asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+      if (prof) { const long long t1 = clock64(); t_sync += t1 - t0; t0 = t1; }
       if (tid == 0) {
         if (c > 0) land[0][par] = ob;       // handed to the left this round
         if (c < CL - 1) land[1][par] = ot;  // handed to the right this round
