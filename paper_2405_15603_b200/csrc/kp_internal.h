@@ -245,6 +245,7 @@ void launch_kron_scale(double* W, const double* la, int p, const double* lb, int
                        cudaStream_t s);
 void launch_set_status(int32_t* status, int32_t code, cudaStream_t s);
 void launch_warm_identity(double* T, int n, const int* valid, cudaStream_t s);
+void launch_merge_chol_info(const int* chol_info, int* info, int n, cudaStream_t s);
 void launch_status_slots(const int32_t* status, double* slots, cudaStream_t s);
 void launch_slots_status(const double* slots, int32_t* status, cudaStream_t s);
 // KFAC*: batched deterministic dot products, quadratic-model solve and update

@@ -391,6 +391,17 @@ void launch_warm_identity(double* T, int n, const int* valid, cudaStream_t s) {
   k_warm_identity<<<grid1((int64_t)n * n), 256, 0, s>>>(T, n, valid);
 }
 
+// A failed Cholesky of the second matrix of a pencil (potrf info k > 0) reported the way
+// sygvd does: info = n + k (not positive definite).
+__global__ void k_merge_chol_info(const int* chol_info, int* info, int n) {
+  if (*chol_info != 0) *info = n + *chol_info;
+}
+
+void launch_merge_chol_info(const int* chol_info, int* info, int n, cudaStream_t s) {
+  count_launch();
+  k_merge_chol_info<<<1, 1, 0, s>>>(chol_info, info, n);
+}
+
 __global__ void k_set_status(int32_t* status, int32_t code) { set_status(status, code); }
 
 void launch_set_status(int32_t* status, int32_t code, cudaStream_t s) {

@@ -356,10 +356,13 @@ int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
       KP_SOLVER_TRY(cusolverDnDsygvd_bufferSize(ctx->solver, CUSOLVER_EIG_TYPE_1,
                                                 CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
                                                 n, nullptr, n, nullptr, n, nullptr, &lw));
-      int lwp = 0;  // the mid-size route (potrf twice) shares the pair's workspace
+      int lwp = 0, lwe = 0;  // potrf (mid route, large route) and syevd share the workspace
       KP_SOLVER_TRY(cusolverDnDpotrf_bufferSize(ctx->solver, CUBLAS_FILL_MODE_LOWER, n, nullptr,
                                                 n, &lwp));
-      lw = std::max(lw, lwp);
+      KP_SOLVER_TRY(cusolverDnDsyevd_bufferSize(ctx->solver, CUSOLVER_EIG_MODE_VECTOR,
+                                                CUBLAS_FILL_MODE_LOWER, n, nullptr, n, nullptr,
+                                                &lwe));
+      lw = std::max(lw, std::max(lwp, lwe));
       P.lw[l][k] = std::max(lw, 1);
       lwork = std::max(lwork, lw);
     }
@@ -1071,33 +1074,56 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
                          mid_warm[2 * l + k].valid));
       KP_CUDA_TRY(cudaEventRecord(ctx->side_ev[2 * l + k], s));
     }
+  // Large pairs (n > mid_eig_max_n()): M2 = L L^T and C = L^-1 M1 L^-T are issued here
+  // (asynchronous); only the symmetric eigensolver (cuSOLVER syevd, which blocks its calling
+  // thread) runs on one host thread per pair, followed by T = L^-T V.  (Measured on c5's eight
+  // pairs: 42.6 ms vs 47.3 ms for sygvd per thread, tools/syevd_threads_bench.cu.)
+  auto big_pair = [&](int l, int k) { return !pair_small(l, k) && !pair_mid(l, k); };
+  for (int l : big)
+    for (int k = 0; k < 2; ++k) {
+      if (!big_pair(l, k)) continue;
+      cudaStream_t s = ctx->side[2 * l + k];
+      const int n = k == 0 ? P.p[l] : P.q[l];
+      int* iw = reinterpret_cast<int*>(c.at(P.k_info[l]));
+      const double one = 1.0;
+      double* m1 = c.at(k == 0 ? P.k_A1[l] : P.k_B1[l]);
+      double* m2 = c.at(k == 0 ? P.k_A2[l] : P.k_B2[l]);
+      KP_CUDA_TRY(cudaStreamWaitEvent(s, ready, 0));
+      // info words must not depend on what the workspace held before
+      KP_CUDA_TRY(cudaMemsetAsync(iw + k, 0, sizeof(int), s));
+      KP_CUDA_TRY(cudaMemsetAsync(iw + 2 + 2 * k, 0, sizeof(int), s));
+      launch_damped_copy(k == 0 ? st->a_int + P.fa[l] : st->b_int + P.fb[l], lam, n, m1, s);
+      launch_damped_copy(k == 0 ? st->a_bnd + P.fa[l] : st->b_bnd + P.fb[l], lam, n, m2, s);
+      cublasHandle_t hb = ctx->side_blas[2 * l + k];
+      KP_SOLVER_TRY(cusolverDnDpotrf(ctx->side_solver[2 * l + k], CUBLAS_FILL_MODE_LOWER, n, m2, n,
+                                     c.at(k == 0 ? P.k_wa[l] : P.k_wb[l]), P.lw[l][k],
+                                     iw + 2 + 2 * k));
+      KP_BLAS_TRY(cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N,
+                              CUBLAS_DIAG_NON_UNIT, n, n, &one, m2, n, m1, n));
+      KP_BLAS_TRY(cublasDtrsm(hb, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T,
+                              CUBLAS_DIAG_NON_UNIT, n, n, &one, m2, n, m1, n));
+    }
   std::vector<int> rc(2 * P.L, KP_OK);
   auto solve_pair = [&](int l, int k) {
     cudaSetDevice(ctx->device);
     cudaStream_t s = ctx->side[2 * l + k];
-    if (cudaStreamWaitEvent(s, ready, 0) != cudaSuccess) {
-      rc[2 * l + k] = KP_ERR_CUDA;
-      return;
-    }
-    int* info = reinterpret_cast<int*>(c.at(P.k_info[l])) + k;
-    // zero the info word first: it must not depend on what the workspace held before
-    if (cudaMemsetAsync(info, 0, sizeof(int), s) != cudaSuccess) {
-      rc[2 * l + k] = KP_ERR_CUDA;
-      return;
-    }
     const int n = k == 0 ? P.p[l] : P.q[l];
-    const double* f1 = k == 0 ? st->a_int + P.fa[l] : st->b_int + P.fb[l];
-    const double* f2 = k == 0 ? st->a_bnd + P.fa[l] : st->b_bnd + P.fb[l];
+    int* iw = reinterpret_cast<int*>(c.at(P.k_info[l]));
     double* m1 = c.at(k == 0 ? P.k_A1[l] : P.k_B1[l]);
     double* m2 = c.at(k == 0 ? P.k_A2[l] : P.k_B2[l]);
-    double* ev = c.at(k == 0 ? P.k_la[l] : P.k_lb[l]);
-    if (n == 1) {
-      launch_gen_eig_1x1(f1, f2, lam, m1, ev, info, s);
-    } else {
-      launch_damped_copy(f1, lam, n, m1, s);
-      launch_damped_copy(f2, lam, n, m2, s);
-      rc[2 * l + k] = gen_eig(ctx->side_solver[2 * l + k], n, m1, m2, ev,
-                              c.at(k == 0 ? P.k_wa[l] : P.k_wb[l]), P.lw[l][k], info);
+    const double one = 1.0;
+    if (cusolverDnDsyevd(ctx->side_solver[2 * l + k], CUSOLVER_EIG_MODE_VECTOR,
+                         CUBLAS_FILL_MODE_LOWER, n, m1, n, c.at(k == 0 ? P.k_la[l] : P.k_lb[l]),
+                         c.at(k == 0 ? P.k_wa[l] : P.k_wb[l]), P.lw[l][k],
+                         iw + k) != CUSOLVER_STATUS_SUCCESS) {
+      rc[2 * l + k] = KP_ERR_CUDA;
+      return;
+    }
+    launch_merge_chol_info(iw + 2 + 2 * k, iw + k, n, s);  // M2 not PD -> info > n
+    if (cublasDtrsm(ctx->side_blas[2 * l + k], CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T,
+                    CUBLAS_DIAG_NON_UNIT, n, n, &one, m2, n, m1, n) != CUBLAS_STATUS_SUCCESS) {
+      rc[2 * l + k] = KP_ERR_CUDA;
+      return;
     }
     cudaEventRecord(ctx->side_ev[2 * l + k], s);
   };
@@ -1105,7 +1131,7 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
     std::vector<std::thread> pool;
     for (int l : big)
       for (int k = 0; k < 2; ++k)
-        if (!pair_small(l, k) && !pair_mid(l, k)) pool.emplace_back(solve_pair, l, k);
+        if (big_pair(l, k)) pool.emplace_back(solve_pair, l, k);
     for (auto& t : pool) t.join();
   }
   for (int v : rc) KP_TRY(v);
