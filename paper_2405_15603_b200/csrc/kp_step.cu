@@ -139,6 +139,7 @@ struct Plan {
   int64_t o_bping = 0, o_bpong = 0, o_ones = 0;
   int64_t o_r = 0, o_rb = 0, o_rls = 0, o_rbls = 0, o_u = 0, o_upart = 0;
   bool tn_grouped = false;  // small network: grouped TN contractions (accumulate)
+  bool tn_grouped_bnd = false;  // boundary pass (few rows): grouped TN contractions
   size_t partial_cap = 0;   // doubles at o_partial
   int64_t o_partial = 0, o_red = 0, o_grad = 0, o_delta = 0, o_dslot = 0, o_dir = 0, o_thc = 0, o_ls = 0;
   int64_t o_A1 = 0, o_A2 = 0, o_B1 = 0, o_B2 = 0, o_la = 0, o_lb = 0, o_T1 = 0, o_T2 = 0;
@@ -193,6 +194,11 @@ struct StateBufs;
 int tn_pass_jobs(const Plan& P, const double* x, int64_t n, const TaylorDims& td,
                  const StateBufs* b, const double* gl_last, const double* w, double* accA,
                  double* accB, double* accG, GemmTN* jobs, double** accs);
+
+// Boundary passes with at most this much contraction work (points x widest layer^2) use
+// the grouped TN launch (c4: 1000 x 256^2; c5's 768-wide layers stay on the TMA kernel,
+// where the grouped cp.async kernel measured slower).
+constexpr double kBndGroupMaxWork = 134217728.0;  // 2^27
 
 int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
   KP_TRY(check_net(&pr->net));
@@ -305,6 +311,17 @@ int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
                                 nullptr, jobs, accs);
     part = std::max(part, gemm_tn_grouped_partial_doubles(jobs, kb));
     P.tn_grouped = true;
+  }
+  // Wider networks: the boundary pass alone (S = 1, few rows: one launch per contraction
+  // would be launch-latency bound) still goes through the grouped launch.
+  if (!P.tn_grouped && 3 * P.L <= 40 && (double)P.Nb * P.maxh * P.maxh <= kBndGroupMaxWork) {
+    GemmTN jobs[3 * MAXL];
+    double* accs[3 * MAXL];
+    const TaylorDims tdb{1, 0, false};
+    const int kb = tn_pass_jobs(P, nullptr, P.Nb, tdb, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                nullptr, jobs, accs);
+    part = std::max(part, gemm_tn_grouped_partial_doubles(jobs, kb));
+    P.tn_grouped_bnd = true;
   }
   P.partial_cap = part;
   P.o_partial = take((int64_t)part);
@@ -729,7 +746,7 @@ void accumulate(const Ctx& c, const double* x, int64_t n, const TaylorDims& td,
   const int L = P.L;
   double* part = c.at(P.o_partial);
   const int64_t rows = n * td.S;
-  if (P.tn_grouped) {  // small network: every contraction of the pass in one launch
+  if (P.tn_grouped || (P.tn_grouped_bnd && td.S == 1)) {  // every contraction in one launch
     GemmTN jobs[3 * MAXL];
     double* accs[3 * MAXL];
     const int k = tn_pass_jobs(P, x, n, td, &b, gl_last, r, accA, accB, accG, jobs, accs);
