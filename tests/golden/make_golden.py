@@ -70,6 +70,12 @@ PLAN10 = {
     "c3_10": ("c3", 1000, 400, 10),
     "c4_10": ("c4", 400, 130, 10),
     "c5_10": ("c5", 24, 8, 10),
+    # the section-8(f) paths over ten steps: KFAC* (c1 at full size), the log-Fokker-Planck
+    # residual (KFAC and KFAC*) and dense operator coefficients
+    "c1_star_10": ("c1", 3000, 500, 10),
+    "lfp_10": ("lfp", 300, 100, 10),
+    "lfp_star_10": ("lfp", 300, 100, 10),
+    "dense_10": ("dense", 400, 100, 10),
 }
 FULL_RECORD_STEPS = {1, 10}
 
@@ -120,7 +126,7 @@ def main():
         params = network.init_params(arch, _stream_seed(0, 0))
         batch = pde.sample_batch(prob, n_int, n_bnd, _stream_seed(0, 1, 0))
         momentum = 0.9 if name.endswith("momentum") else wl.momentum
-        kind = "kfac_star" if name.endswith("_star") else "kfac"
+        kind = "kfac_star" if "_star" in name else "kfac"
         cfg = optim.OptimizerConfig(kind=kind, damping=wl.damping, ema=wl.ema,
                                     momentum=momentum, init_mode="identity")
         state = optim.init_train_state(params, cfg)

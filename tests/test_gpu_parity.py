@@ -8,7 +8,7 @@ per array.
 import numpy as np
 import pytest
 
-from golden_util import NAMES, NAMES10, STAR_NAMES, compare, has, load, pack_factors
+from golden_util import NAMES, NAMES10, STAR10, STAR_NAMES, compare, has, load, pack_factors
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -22,7 +22,8 @@ from paper_2405_15603_b200.pde import make_problem, sample_batch  # noqa: E402
 WL_OF = {"c1": "c1", "c2": "c2", "c3": "c3", "c4": "c4", "c5": "c5", "c1_momentum": "c1",
          "c1_star": "c1", "c3_star": "c3", "c5_star": "c5", "lfp": "lfp", "lfp_star": "lfp",
          "dense": "dense", "dense_star": "dense",
-         "c1_10": "c1", "c2_10": "c2", "c3_10": "c3", "c4_10": "c4", "c5_10": "c5"}
+         "c1_10": "c1", "c2_10": "c2", "c3_10": "c3", "c4_10": "c4", "c5_10": "c5",
+         "lfp_10": "lfp", "dense_10": "dense", "c1_star_10": "c1", "lfp_star_10": "lfp"}
 
 
 def _theta_colstack(params):
@@ -282,7 +283,7 @@ def test_unsupported_residual_rejected():
         optimizer_step(state, batch, prob)
 
 
-@pytest.mark.parametrize("name", STAR_NAMES)
+@pytest.mark.parametrize("name", STAR_NAMES + STAR10)
 def test_kfac_star_steps_match_reference_golden(name):
     """KFAC* on the device (kp_kfac_star_step): exact Gramian-vector products via JVP +
     weighted reverse contraction vs the reference's Jacobian-row route."""
@@ -303,12 +304,16 @@ def test_kfac_star_steps_match_reference_golden(name):
         for key, val in (("loss_interior", info.loss_interior), ("loss_boundary", info.loss_boundary)):
             ref = float(g[p + key])
             assert abs(val - ref) <= tol * abs(ref), (key, val, ref)
+        if not has(g, p + "theta"):  # ten-step runs record arrays at steps 1 and 10 only
+            t += 1
+            continue
         eng = state._engine
         widths = eng.widths
         assert compare(g, p + "delta", _device_mats_to_vec(eng.delta.cpu().numpy(), widths), tol) <= tol
         assert compare(g, p + "theta", _theta_colstack(state.params), tol) <= tol
         assert compare(g, p + "prev_update", mats_to_vec(state.prev_update), tol) <= tol
         t += 1
+    assert t > (10 if name in STAR10 else 1)
 
 
 def test_kfac_star_chunked_matches_single_chunk():

@@ -9,7 +9,7 @@ reference's seeded parameters and batches bit-for-bit.
 import numpy as np
 import pytest
 
-from golden_util import NAMES, NAMES10, STAR_NAMES, compare, has, load, pack_factors
+from golden_util import NAMES, NAMES10, STAR10, STAR_NAMES, compare, has, load, pack_factors
 from oracle import kfac_oracle as orc
 from paper_2405_15603_b200 import configs as cfgs
 from paper_2405_15603_b200.network import params_to_vec
@@ -17,7 +17,8 @@ from paper_2405_15603_b200.network import params_to_vec
 WL_OF = {"c1": "c1", "c2": "c2", "c3": "c3", "c4": "c4", "c5": "c5", "c1_momentum": "c1",
          "c1_star": "c1", "c3_star": "c3", "c5_star": "c5", "lfp": "lfp", "lfp_star": "lfp",
          "dense": "dense", "dense_star": "dense",
-         "c1_10": "c1", "c2_10": "c2", "c3_10": "c3", "c4_10": "c4", "c5_10": "c5"}
+         "c1_10": "c1", "c2_10": "c2", "c3_10": "c3", "c4_10": "c4", "c5_10": "c5",
+         "lfp_10": "lfp", "dense_10": "dense", "c1_star_10": "c1", "lfp_star_10": "lfp"}
 
 
 def build(name):
@@ -27,7 +28,7 @@ def build(name):
     return g, wl, prob, params, batch
 
 
-@pytest.mark.parametrize("name", NAMES + STAR_NAMES + NAMES10)
+@pytest.mark.parametrize("name", NAMES + STAR_NAMES + NAMES10 + STAR10)
 def test_inputs_bit_identical_to_reference(name):
     g, wl, prob, params, batch = build(name)
     assert compare(g, "in/interior", batch.interior, 0) == 0.0
@@ -48,7 +49,7 @@ def test_oracle_dense_coefficient_taylor_forward():
         assert compare(g, "taylor/" + key, arr, 1e-12) <= 1e-12
 
 
-@pytest.mark.parametrize("name", NAMES + ("c4_10", "c5_10"))
+@pytest.mark.parametrize("name", NAMES + ("c4_10", "c5_10", "lfp_10", "dense_10"))
 def test_oracle_matches_reference_steps(name):
     g, wl, prob, params, batch = build(name)
     st = orc.init_state(params.weights, params.biases, ema=float(g["ema"]),
@@ -86,7 +87,7 @@ def rel(a, b):
     return abs(a - b) / max(abs(b), 1e-300)
 
 
-@pytest.mark.parametrize("name", STAR_NAMES)
+@pytest.mark.parametrize("name", STAR_NAMES + ("lfp_star_10",))
 def test_oracle_matches_reference_kfac_star(name):
     """KFAC* (src/optim.py:266-320): alpha/mu from the exact-Gramian quadratic model."""
     from paper_2405_15603_b200.network import mats_to_vec
@@ -103,6 +104,9 @@ def test_oracle_matches_reference_kfac_star(name):
         assert abs(mu - float(g[p + "mu"])) <= tol * max(abs(float(g[p + "mu"])), 1.0)
         assert rel(li, float(g[p + "loss_interior"])) <= tol
         assert rel(lb, float(g[p + "loss_boundary"])) <= tol
+        if not has(g, p + "theta"):  # ten-step runs record arrays at steps 1 and 10 only
+            t += 1
+            continue
         assert compare(g, p + "delta", mats_to_vec(rec["delta"]), tol) <= tol
         theta = np.concatenate([np.hstack([w, b[:, None]]).ravel(order="F")
                                 for w, b in zip(st.weights, st.biases)])
