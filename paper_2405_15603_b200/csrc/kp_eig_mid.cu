@@ -17,10 +17,12 @@
 // warp per pair.  Between rounds the pairing advances by the circle method (one column
 // fixed, the rest rotate one position), so every pair of columns meets once per sweep of
 // 2 CL ppc - 1 rounds.  Inside a CTA a column moves by re-indexing only; at a CTA boundary
-// the warp that rotated the outgoing column also stores it (R and V parts, 2n doubles) into
-// the neighbour's mailbox through distributed shared memory.  One cluster barrier per
-// round; mailboxes and slot tables are double-buffered by round parity, so a mailbox
-// written in round t + 2 was drained before the barrier of round t + 1.
+// the warp that rotated the outgoing column also stores it (R and V parts, 2n doubles)
+// straight into a landing record of the neighbour through distributed shared memory.  The
+// landing records rotate with the hand-overs (the record a CTA hands over in round t is its
+// landing record for round t + 2), so nothing is copied.  One split cluster barrier per
+// round; the slot tables are double-buffered by round parity.  Pairs up to 160 use 8-CTA
+// clusters, larger ones 16.
 //
 // A rotation is applied when |<r_p, r_q>| > tol ||r_p|| ||r_q|| (tol = max(1e-14, 2 n eps));
 // the sweep loop ends after a sweep without rotations anywhere in the cluster.
@@ -56,12 +58,12 @@ __device__ __forceinline__ double warp_allsum(double v) {
 // one of the two upstream Cholesky factorisations (chol_info[0..1]) failed (not PD).
 // warm_valid (optional): set to 1 on success, 0 otherwise (the caller's warm-start flag).
 //
-// smem: 2 ppc column records + 4 mailboxes ([from left, from right] x round parity), each
-// record R | V (2n doubles).  A round: every pair warp loads its two R columns into
+// smem: 2 ppc column records + 4 landing records ([from left, from right] x round parity),
+// each record R | V (2n doubles).  A round: every pair warp loads its two R columns into
 // registers, forms the three dot products and rotates R and V; the warps owning the CTA's
 // outgoing columns (last top slot -> right neighbour, first bottom slot -> left neighbour)
-// also store them into the neighbour's mailbox.  One cluster barrier; then each CTA copies
-// its mailboxes into the records it handed over and writes the next round's slot table.
+// also store them into the neighbour's landing record.  Between the two halves of the
+// cluster barrier each CTA writes the next round's slot table.
 template <int CL, int EF>
 __global__ void __launch_bounds__(((MID_MAXN / 2 + CL - 1) / CL) * 32, 1)
     k_eig_mid(int n, double* __restrict__ rv, double* __restrict__ lam, int* __restrict__ info,
