@@ -51,7 +51,8 @@ int main(int argc, char** argv) {
   cudaMalloc(&dl, 8 * n);
   cudaMalloc(&dinfo, 4);
   cudaMalloc(&dci, 8);
-  cudaMalloc(&dprof, 8 * 40);
+  cudaMalloc(&dprof, 8 * 512);
+  cudaMemset(dprof, 0, 8 * 512);
   cudaMemset(dci, 0, 8);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
@@ -75,9 +76,15 @@ int main(int argc, char** argv) {
     printf("n=%d eps=%g: %.3f ms info=%d sweeps(max so far)=%d err=%s\n", n, eps, ms, info,
            kp::mid_eig_sweeps_used(), cudaGetErrorString(err));
   }
-  long long prof[40];
-  cudaMemcpy(prof, dprof, 8 * 40, cudaMemcpyDeviceToHost);
-  for (int c = 0; c < 8; ++c)
+  long long prof[512];
+  cudaMemcpy(prof, dprof, 8 * 512, cudaMemcpyDeviceToHost);
+  for (int w = 0; w < 20; ++w)
+    if (prof[256 + w * 4 + 3] > 0)
+      printf("cta 1 warp %d: reduce %.0f angle %.0f rotate %.0f cycles per rotation (%lld)\n", w,
+             (double)prof[256 + w * 4] / prof[256 + w * 4 + 3],
+             (double)prof[256 + w * 4 + 1] / prof[256 + w * 4 + 3],
+             (double)prof[256 + w * 4 + 2] / prof[256 + w * 4 + 3], prof[256 + w * 4 + 3]);
+  for (int c = 0; c < 16; ++c)
     printf("cta %d: rot %lld sync %lld xchg %lld upd %lld cycles, sweeps %lld\n", c, prof[5 * c],
            prof[5 * c + 1], prof[5 * c + 2], prof[5 * c + 3], prof[5 * c + 4]);
   cudaMemcpy(V.data(), dR, 8 * n * n, cudaMemcpyDeviceToHost);
