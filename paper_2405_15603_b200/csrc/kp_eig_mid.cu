@@ -160,16 +160,12 @@ __global__ void __launch_bounds__(((MID_MAXN / 2 + CL - 1) / CL) * 32, 1)
           b = fma(y[u], y[u], b);
           gm = fma(x[u], y[u], gm);
         }
-        const bool fine = prof && c == 1 && lane == 0;
-        long long f0 = 0, f1 = 0, f2 = 0, f3 = 0;
-        if (fine) f0 = clock64() + 0 * (long long)(a + b + gm);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {  // three interleaved butterflies: 5 dependent steps
           a += __shfl_xor_sync(0xffffffffu, a, o);
           b += __shfl_xor_sync(0xffffffffu, b, o);
           gm += __shfl_xor_sync(0xffffffffu, gm, o);
         }
-        if (fine) f1 = clock64() + 0 * (long long)(a + b + gm);
         const bool rot = cp < n && cq < n && gm * gm > tol2 * (a * b) && fabs(gm) > 1e-300;
         double* dr = send_r ? buf_right + (size_t)dst_r * cs2 : nullptr;
         double* dl = send_l ? buf_left + (size_t)dst_l * cs2 : nullptr;
@@ -178,7 +174,6 @@ __global__ void __launch_bounds__(((MID_MAXN / 2 + CL - 1) / CL) * 32, 1)
         if (rot) {
           double cs, sn;
           jacobi_angle(a, b, gm, cs, sn);
-          if (fine) f2 = clock64() + 0 * (long long)(cs + sn);
 #pragma unroll
           for (int u = 0; u <= EF; ++u) {
             const int i = lane + 32 * u;
@@ -220,16 +215,6 @@ __global__ void __launch_bounds__(((MID_MAXN / 2 + CL - 1) / CL) * 32, 1)
         if (lane == 0) {
           if (send_r) colid_right[dst_r] = cp;
           if (send_l) colid_left[dst_l] = cq;
-        }
-        if (fine) {
-          f3 = clock64();
-          if (f2 != 0) {
-            long long* fp = prof + 256 + warp * 4;
-            fp[0] += f1 - f0;  // warp reductions
-            fp[1] += f2 - f1;  // angle
-            fp[2] += f3 - f2;  // rotation (+ remote stores for the boundary warps)
-            fp[3] += 1;
-          }
         }
       }
       if (prof) { __syncthreads(); const long long t1 = clock64(); t_rot += t1 - t0; t0 = t1; }

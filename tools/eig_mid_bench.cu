@@ -78,12 +78,6 @@ int main(int argc, char** argv) {
   }
   long long prof[512];
   cudaMemcpy(prof, dprof, 8 * 512, cudaMemcpyDeviceToHost);
-  for (int w = 0; w < 20; ++w)
-    if (prof[256 + w * 4 + 3] > 0)
-      printf("cta 1 warp %d: reduce %.0f angle %.0f rotate %.0f cycles per rotation (%lld)\n", w,
-             (double)prof[256 + w * 4] / prof[256 + w * 4 + 3],
-             (double)prof[256 + w * 4 + 1] / prof[256 + w * 4 + 3],
-             (double)prof[256 + w * 4 + 2] / prof[256 + w * 4 + 3], prof[256 + w * 4 + 3]);
   for (int c = 0; c < 16; ++c)
     printf("cta %d: rot %lld sync %lld xchg %lld upd %lld cycles, sweeps %lld\n", c, prof[5 * c],
            prof[5 * c + 1], prof[5 * c + 2], prof[5 * c + 3], prof[5 * c + 4]);
