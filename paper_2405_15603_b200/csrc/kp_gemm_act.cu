@@ -267,7 +267,10 @@ bool run_act(const GemmAct& g, int box_rows, cudaStream_t s) {
 // x 64 units, BK 16, 3 stages, three CTAs per SM.
 template <int MODE, int TM>
 bool run_act_tm(const GemmAct& g, int box_rows, cudaStream_t s) {
-  if constexpr (TM <= 13) {
+  if constexpr (TM <= 8) {
+    // 64-row tiles for short K (<= 64: c1-c3): 64-unit tiles, four CTAs per SM (~50 KB each)
+    return run_act<MODE, TM, 4, 16, 3, 64, 4>(g, box_rows, s);
+  } else if constexpr (TM <= 13) {
     return run_act<MODE, TM, 4, 16, 3>(g, box_rows, s);
   } else {
     // 64-unit tiles, 4 warps, BK 16, 3 stages, three CTAs per SM (~72 KB each) so that
@@ -279,14 +282,27 @@ bool run_act_tm(const GemmAct& g, int box_rows, cudaStream_t s) {
 
 }  // namespace
 
-int gemm_act_samples_per_tile(int S) { return S <= ROWS_MAX ? ROWS_MAX / S : 0; }
+// State rows per tile: 64 for short K (the tiles are latency-bound; smaller ones let four
+// CTAs share an SM), else 128.  KP_ACT_SMALL_ROWS=0 keeps 128 (measurements).
+static int act_rows(int K) {
+  static const bool small = [] {
+    const char* e = getenv("KP_ACT_SMALL_ROWS");
+    return !(e && atoi(e) == 0);
+  }();
+  return (small && K <= 64) ? 64 : ROWS_MAX;
+}
+
+int gemm_act_samples_per_tile(int S, int K) {
+  const int rows = act_rows(K);
+  return S <= rows ? rows / S : 0;
+}
 
 // Unit width of the fused layer's tiles for this shape (mirrors run_act_tm); the LAST mode
 // leaves ceil(N / width) partial dots per row.
-int gemm_act_tile_width(int S, int N) {
-  const int nb = gemm_act_samples_per_tile(S);
+int gemm_act_tile_width(int S, int N, int K) {
+  const int nb = gemm_act_samples_per_tile(S, K);
   const int tm = nb > 0 ? (nb * S + 7) / 8 : 0;
-  return tm <= 13 ? BN_MAX : 64;
+  return (tm <= 8 || tm > 13) ? 64 : BN_MAX;
 }
 
 bool gemm_act_ok(int S, int K, int64_t lda, int64_t ldb) {
@@ -299,7 +315,8 @@ bool launch_gemm_act(GemmAct g, int mode, cudaStream_t s) {
   if (g.S > ROWS_MAX || g.K % 16 != 0 || g.lda % 2 || g.ldb % 2 || !al16(g.A) || !al16(g.B) ||
       g.n_samples * g.S * g.batch >= (int64_t(1) << 31) || g.N * (int64_t)g.batch >= (int64_t(1) << 31))
     return false;
-  g.nb = gemm_act_samples_per_tile(g.S);
+  g.nb = gemm_act_samples_per_tile(g.S, g.K);
+  if (g.nb <= 0) return false;
   const int box_rows = (g.nb * g.S + 7) / 8 * 8;
   // the m8-tile count is a template parameter: predicated-off DMMAs still occupy the
   // tensor pipe, so a runtime guard over a 16-tile array wastes up to 16/tm of it
@@ -309,6 +326,10 @@ bool launch_gemm_act(GemmAct g, int mode, cudaStream_t s) {
     if (mode == ACT_STORE) return run_act_tm<ACT_STORE, T>(g, box_rows, s); \
     if (mode == ACT_LOSS) return run_act_tm<ACT_LOSS, T>(g, box_rows, s);   \
     return run_act_tm<ACT_LAST, T>(g, box_rows, s);
+    KP_ACT_CASE(5)
+    KP_ACT_CASE(6)
+    KP_ACT_CASE(7)
+    KP_ACT_CASE(8)
     KP_ACT_CASE(9)
     KP_ACT_CASE(10)
     KP_ACT_CASE(11)

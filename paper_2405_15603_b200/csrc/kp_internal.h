@@ -122,8 +122,8 @@ struct GemmAct {
 };
 // Whether launch_gemm_act can run this layer shape (fused path available).
 bool gemm_act_ok(int S, int K, int64_t lda, int64_t ldb);
-int gemm_act_samples_per_tile(int S);
-int gemm_act_tile_width(int S, int N);
+int gemm_act_samples_per_tile(int S, int K);
+int gemm_act_tile_width(int S, int N, int K);
 bool launch_gemm_act(GemmAct g, int mode, cudaStream_t s);
 
 // ---- Taylor-mode elementwise kernels (kp_taylor.cu) ------------------------

@@ -588,7 +588,7 @@ void forward_loss(const Ctx& c, const double* theta, const double* wpad, const d
       ga.bias_bstride = P.D;
       if (l == L - 2 && u_out == nullptr) {
         // last hidden layer: fuse the h_out = 1 output layer, never store this state
-        const int ntn = (int)ceil_div(P.h[l + 1], gemm_act_tile_width(td.S, P.h[l + 1]));
+        const int ntn = (int)ceil_div(P.h[l + 1], gemm_act_tile_width(td.S, P.h[l + 1], P.h[l]));
         ga.wlast = theta + P.th[L - 1];
         ga.wlast_bstride = P.D;
         ga.upart = c.at(P.o_upart);
