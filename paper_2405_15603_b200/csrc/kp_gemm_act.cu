@@ -268,8 +268,9 @@ bool run_act(const GemmAct& g, int box_rows, cudaStream_t s) {
 template <int MODE, int TM>
 bool run_act_tm(const GemmAct& g, int box_rows, cudaStream_t s) {
   if constexpr (TM <= 8) {
-    // 64-row tiles for short K (<= 64: c1-c3): 64-unit tiles, four CTAs per SM (~50 KB each)
-    return run_act<MODE, TM, 4, 16, 3, 64, 4>(g, box_rows, s);
+    // 64-row tiles for short K (<= 64: c1-c3): 64-unit tiles, 2 stages, five CTAs per SM
+    // (~36 KB each; 3 stages / 4 CTAs: c2 line search 1.03 ms, this 0.95; 6 CTAs spill)
+    return run_act<MODE, TM, 4, 16, 2, 64, 5>(g, box_rows, s);
   } else if constexpr (TM <= 13) {
     return run_act<MODE, TM, 4, 16, 3>(g, box_rows, s);
   } else {
