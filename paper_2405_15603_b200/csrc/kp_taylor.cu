@@ -290,7 +290,9 @@ void launch_last_layer(const double* post, int64_t n, int h, const double* theta
                        const double* targets, double* r, double* u_out, cudaStream_t s,
                        const double* quad, double* seeds_out) {
   if (n <= 0) return;
-  const int spb = std::max(1, std::min(LAST_MAX_ROWS / td.S, 64));
+  // enough blocks for ~4 per SM (a warp per row: short rows are latency-bound)
+  const int64_t want = std::max<int64_t>(1, ceil_div(n, 148 * 4));
+  const int spb = (int)std::max<int64_t>(1, std::min<int64_t>(std::min(LAST_MAX_ROWS / td.S, 64), want));
   const int64_t blocks = ceil_div(n, spb);
   count_launch();
   k_last_layer<<<(unsigned)blocks, LAST_THREADS, 0, s>>>(post, n, h, theta_last, td, spb, r0,
