@@ -161,7 +161,10 @@ void launch_first_layer(const double* x, int64_t n, int d, const double* theta0,
   g.sC = n * h1;
   launch_gemm_nt(g, s);
   const unsigned tiles = (unsigned)ceil_div(h1, 32);
-  const int64_t groups = std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, EXP_WARPS), 148LL * 8 / tiles + 1));
+  // about 8 blocks per SM over the whole (tiles x groups x candidates) grid
+  const int64_t groups = std::max<int64_t>(
+      1, std::min<int64_t>(ceil_div(n, EXP_WARPS),
+                           std::max<int64_t>(8, (148LL * 8 / tiles + 1) / std::max(batch, 1))));
   const int64_t spb = ceil_div(n, groups);
   const size_t smem = td.taylor ? sizeof(double) * (size_t)(td.d * 32 + 32) : 0;
   count_launch();
