@@ -122,13 +122,16 @@ void launch_candidate(const double* theta, const double* dir, int exp2, double* 
   k_candidate<<<dim3(grid1(D), (unsigned)batch), 256, 0, s>>>(theta, dir, exp2, out, D, wp, wpad);
 }
 
-// Grid argmin (optim.py:195-211) then theta += alpha dir, prev = alpha dir.
+// Grid argmin (optim.py:195-211) then theta += alpha dir, prev = alpha dir.  One warp:
+// lane k takes candidates k, k+32, ...; the smallest finite loss wins, ties go to the
+// smaller step (the reference's ascending scan keeps the first strict minimum).
 __global__ void k_argmin(const double* __restrict__ ls_sums, int ncand, int min_exp, double ni,
                          double nb, double* scalars, double* ls_losses, int32_t* status,
                          double mu) {
+  const int lane = threadIdx.x;
   double best = INFINITY;
   int best_k = -1;
-  for (int k = 0; k < ncand; ++k) {
+  for (int k = lane; k < ncand; k += 32) {
     const double li = ls_sums[2 * k] / (2.0 * ni);
     const double lb = ls_sums[2 * k + 1] / (2.0 * nb);
     if (ls_losses) {
@@ -141,6 +144,16 @@ __global__ void k_argmin(const double* __restrict__ ls_sums, int ncand, int min_
       best_k = k;
     }
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int ok = __shfl_xor_sync(0xffffffffu, best_k, o);
+    if (ok >= 0 && (best_k < 0 || ob < best || (ob == best && ok < best_k))) {
+      best = ob;
+      best_k = ok;
+    }
+  }
+  if (lane != 0) return;
   if (best_k < 0) {
     set_status(status, KP_ERR_LINE_SEARCH);
     scalars[2] = 0.0;
@@ -171,7 +184,7 @@ void launch_argmin_update(const double* ls_sums, int ncand, int min_exp, double 
                           double* scalars, double* ls_losses, int32_t* status, double mu,
                           cudaStream_t s) {
   count_launch();
-  k_argmin<<<1, 1, 0, s>>>(ls_sums, ncand, min_exp, ni, nb, scalars, ls_losses, status, mu);
+  k_argmin<<<1, 32, 0, s>>>(ls_sums, ncand, min_exp, ni, nb, scalars, ls_losses, status, mu);
   count_launch();
   k_update<<<grid1(D), 256, 0, s>>>(theta, prev, dir, D, scalars, status);
 }
