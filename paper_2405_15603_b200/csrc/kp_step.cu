@@ -58,6 +58,9 @@ struct kp_context {
   std::vector<cusolverDnHandle_t> side_solver;
   std::vector<cublasHandle_t> side_blas;
   std::vector<cudaEvent_t> side_ev;
+  // early preconditioning (single-call steps): layer l's factor contractions done / its factor
+  // EMA done, so the layer's eigenproblems start while later layers are still contracted
+  std::vector<cudaEvent_t> layer_ev, fin_ev;
   // CUDA-graph replay of whole steps (only when every layer uses the on-device solver)
   cudaStream_t cap_stream = nullptr;
   cudaEvent_t cap_in = nullptr, cap_out = nullptr;
@@ -77,6 +80,13 @@ struct kp_context {
 };
 
 static int ensure_side_streams(kp_context* c, int n) {
+  while ((int)c->layer_ev.size() < n / 2) {  // per-layer events of the early preconditioning
+    cudaEvent_t a, b;
+    KP_CUDA_TRY(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+    KP_CUDA_TRY(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+    c->layer_ev.push_back(a);
+    c->fin_ev.push_back(b);
+  }
   while ((int)c->side.size() < n) {
     cudaStream_t s;
     KP_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -409,6 +419,10 @@ struct Ctx {
   double* W;  // workspace base
   cudaStream_t s;
   const double* rot = nullptr;  // Q of dense operator coefficients (kp_batch.coeff_rot)
+  // single-call step with per-layer contractions and off-launch (mid-size / large) factor
+  // pairs: the accumulate phase records ctx->layer_ev and the precondition phase starts each
+  // such layer's EMA and eigenproblems as soon as its factors are complete
+  bool early = false;
   double* at(int64_t off) const { return W + off; }
 };
 
@@ -741,7 +755,7 @@ void contract_grad_deriv0(const Ctx& c, int64_t n, const TaylorDims& td, const d
 // which synthesises the bias column itself.
 void accumulate(const Ctx& c, const double* x, int64_t n, const TaylorDims& td,
                 const StateBufs& b, const double* gl_last, const double* r, double* accA,
-                double* accB, double* accG) {
+                double* accB, double* accG, bool record_layers = false) {
   const Plan& P = c.P;
   const int L = P.L;
   double* part = c.at(P.o_partial);
@@ -780,6 +794,7 @@ void accumulate(const Ctx& c, const double* x, int64_t n, const TaylorDims& td,
       GemmTN bb{G, q, q, false, G, q, q, false, nullptr, 1, 1, rows, true};
       launch_gemm_tn_accumulate(bb, part, accB + P.fb[l], c.s);
     }
+    if (record_layers) cudaEventRecord(c.ctx->layer_ev[l], c.s);  // A_l, B_l complete
     contract_grad_layer(c, x, n, td, b, gl_last, r, accG, l);
   }
 }
@@ -795,6 +810,20 @@ int phase_accumulate(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, cons
     launch_prep_layer0(st->theta, P.d, P.h[1], bt->coeff_diag, bt->coeff_rot, c.at(P.o_w0t), c.at(P.o_q0), c.s);
   const TaylorDims tdi{P.S, P.d, true};
   const TaylorDims tdb{1, 0, false};
+  auto boundary_pass = [&]() {
+    const StateBufs bb = boundary_bufs(c);
+    double* ones = c.at(P.o_ones);
+    launch_fill(ones, P.Nb, 1.0, c.s);
+    ResidualIn rb{nullptr, nullptr, bt->targets};
+    forward_store(c, st->theta, c.at(P.o_wpad), bt->x_bnd, P.Nb, tdb, bt->coeff_diag, bb, rb,
+                  c.at(P.o_rb), nullptr);
+    backward(c, st->theta, P.Nb, tdb, bt->coeff_diag, bb, nullptr);
+    accumulate(c, bt->x_bnd, P.Nb, tdb, bb, ones, c.at(P.o_rb), red + P.r_abnd, red + P.r_bbnd,
+               red + P.r_gbnd);
+  };
+  // early preconditioning: the boundary sums first, so that each layer's factors are
+  // complete right after its interior contractions (last chunk)
+  if (c.early) boundary_pass();
   const StateBufs bi = interior_bufs(c);
   for (int64_t n0 = 0; n0 < P.N; n0 += P.Nc) {
     const int64_t nc = std::min(P.Nc, P.N - n0);
@@ -809,17 +838,10 @@ int phase_accumulate(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, cons
     }
     forward_store(c, st->theta, c.at(P.o_wpad), x, nc, tdi, bt->coeff_diag, bi, ri, r, nullptr);
     backward(c, st->theta, nc, tdi, bt->coeff_diag, bi, seeds);
-    accumulate(c, x, nc, tdi, bi, seeds, r, red + P.r_aint, red + P.r_bint, red + P.r_gint);
+    accumulate(c, x, nc, tdi, bi, seeds, r, red + P.r_aint, red + P.r_bint, red + P.r_gint,
+               c.early && n0 + nc >= P.N);
   }
-  const StateBufs bb = boundary_bufs(c);
-  double* ones = c.at(P.o_ones);
-  launch_fill(ones, P.Nb, 1.0, c.s);
-  ResidualIn rb{nullptr, nullptr, bt->targets};
-  forward_store(c, st->theta, c.at(P.o_wpad), bt->x_bnd, P.Nb, tdb, bt->coeff_diag, bb, rb,
-                c.at(P.o_rb), nullptr);
-  backward(c, st->theta, P.Nb, tdb, bt->coeff_diag, bb, nullptr);
-  accumulate(c, bt->x_bnd, P.Nb, tdb, bb, ones, c.at(P.o_rb), red + P.r_abnd, red + P.r_bbnd,
-             red + P.r_gbnd);
+  if (!c.early) boundary_pass();
   launch_sumsq(c.at(P.o_r), P.N, 0, 1, red + P.r_ss, 1, c.s);
   launch_sumsq(c.at(P.o_rb), P.Nb, 0, 1, red + P.r_ss + 1, 1, c.s);
   return KP_OK;
@@ -929,16 +951,39 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
   double* red = c.at(P.o_red);
   const double Ng = cfg->n_interior_global, Nbg = cfg->n_boundary_global;
   const double ema = cfg->ema;
+  kp_context* ctx = c.ctx;
+  auto pair_small = [&](int l, int k) { return (k == 0 ? P.p[l] : P.q[l]) <= small_eig_max_n(); };
+  auto pair_mid = [&](int l, int k) {
+    const int n = k == 0 ? P.p[l] : P.q[l];
+    return n > small_eig_max_n() && n <= mid_eig_max_n();
+  };
+  // early layers: their factors were completed (c.early: ctx->layer_ev) before the end of the
+  // accumulate phase; their EMA and eigenproblems start on the side streams right then
+  std::vector<char> early(P.L, 0);
+  if (c.early && !owned) {
+    KP_TRY(ensure_side_streams(ctx, 2 * P.L + 2));
+    for (int l = 0; l < P.L; ++l) early[l] = !pair_small(l, 0) || !pair_small(l, 1);
+  }
   {  // EMA of the normalised factor sums (curvature.py:79-85, 112-115, 133-134), one launch
     FinalizeJobs fj{};
     for (int l = 0; l < P.L; ++l) {
-      fj.job[fj.n++] = FinalizeJob{red + P.r_aint + P.fa[l], st->a_int + P.fa[l], P.p[l], Ng * P.S,
-                                   l == 0 ? P.d : 0, Ng};
-      fj.job[fj.n++] = FinalizeJob{red + P.r_bint + P.fb[l], st->b_int + P.fb[l], P.q[l], Ng, 0, 0.0};
-      fj.job[fj.n++] = FinalizeJob{red + P.r_abnd + P.fa[l], st->a_bnd + P.fa[l], P.p[l], Nbg, 0, 0.0};
-      fj.job[fj.n++] = FinalizeJob{red + P.r_bbnd + P.fb[l], st->b_bnd + P.fb[l], P.q[l], Nbg, 0, 0.0};
+      FinalizeJobs lj{};
+      FinalizeJobs& j = early[l] ? lj : fj;
+      j.job[j.n++] = FinalizeJob{red + P.r_aint + P.fa[l], st->a_int + P.fa[l], P.p[l], Ng * P.S,
+                                 l == 0 ? P.d : 0, Ng};
+      j.job[j.n++] = FinalizeJob{red + P.r_bint + P.fb[l], st->b_int + P.fb[l], P.q[l], Ng, 0, 0.0};
+      j.job[j.n++] = FinalizeJob{red + P.r_abnd + P.fa[l], st->a_bnd + P.fa[l], P.p[l], Nbg, 0, 0.0};
+      j.job[j.n++] = FinalizeJob{red + P.r_bbnd + P.fb[l], st->b_bnd + P.fb[l], P.q[l], Nbg, 0, 0.0};
+      if (early[l]) {  // this layer's EMA on its A-side stream, after its contractions
+        cudaStream_t s2 = ctx->side[2 * l];
+        KP_CUDA_TRY(cudaStreamWaitEvent(s2, ctx->layer_ev[l], 0));
+        launch_factor_finalize_grouped(lj, ema, s2);
+        KP_CUDA_TRY(cudaEventRecord(ctx->fin_ev[l], s2));
+      }
     }
-    launch_factor_finalize_grouped(fj, ema, c.s);
+    if (fj.n > 0) launch_factor_finalize_grouped(fj, ema, c.s);
+    for (int l = 0; l < P.L; ++l)  // the one-launch small solver reads every layer's factors
+      if (early[l]) KP_CUDA_TRY(cudaStreamWaitEvent(c.s, ctx->fin_ev[l], 0));
   }
   double* grad = c.at(P.o_grad);
   launch_grad_finalize(red + P.r_gint, red + P.r_gbnd, Ng, Nbg, grad, P.D, c.s);
@@ -947,17 +992,11 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
   const double lam = cfg->damping;
   // The 2L generalised eigenproblems are independent: fan out over side streams (A and B
   // factor pair of layer l on streams 2l and 2l+1), combine on 2l, join back.
-  kp_context* ctx = c.ctx;
   // Factor pairs up to small_eig_max_n(): on-device Cholesky + Jacobi solver, all of them in
   // one launch on the main stream (plus one combine launch for the layers whose two pairs are
   // both small).  Larger pairs: cuSOLVER sygvd, which blocks the calling host thread, so each
   // is issued from its own host thread (own handle + stream); a layer with a large pair is
   // combined with cuBLAS on its side stream.
-  auto pair_small = [&](int l, int k) { return (k == 0 ? P.p[l] : P.q[l]) <= small_eig_max_n(); };
-  auto pair_mid = [&](int l, int k) {
-    const int n = k == 0 ? P.p[l] : P.q[l];
-    return n > small_eig_max_n() && n <= mid_eig_max_n();
-  };
   bool any_big = false;
   for (int l = 0; l < P.L; ++l)
     any_big |= (!owned || owned[l]) && (!pair_small(l, 0) || !pair_small(l, 1));
@@ -1077,7 +1116,7 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
     for (int k = 0; k < 2; ++k) {
       if (!pair_mid(l, k)) continue;
       cudaStream_t s = ctx->side[2 * l + k];
-      KP_CUDA_TRY(cudaStreamWaitEvent(s, ready, 0));
+      KP_CUDA_TRY(cudaStreamWaitEvent(s, early[l] ? ctx->fin_ev[l] : ready, 0));
       int* info = reinterpret_cast<int*>(c.at(P.k_info[l])) + k;
       KP_CUDA_TRY(cudaMemsetAsync(info, 0, sizeof(int), s));
       KP_TRY(gen_eig_mid(ctx->side_solver[2 * l + k], ctx->side_blas[2 * l + k], s,
@@ -1105,7 +1144,7 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
       const double one = 1.0;
       double* m1 = c.at(k == 0 ? P.k_A1[l] : P.k_B1[l]);
       double* m2 = c.at(k == 0 ? P.k_A2[l] : P.k_B2[l]);
-      KP_CUDA_TRY(cudaStreamWaitEvent(s, ready, 0));
+      KP_CUDA_TRY(cudaStreamWaitEvent(s, early[l] ? ctx->fin_ev[l] : ready, 0));
       // info words must not depend on what the workspace held before
       KP_CUDA_TRY(cudaMemsetAsync(iw + k, 0, sizeof(int), s));
       KP_CUDA_TRY(cudaMemsetAsync(iw + 2 + 2 * k, 0, sizeof(int), s));
@@ -1156,6 +1195,7 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
     cudaStream_t s = ctx->side[2 * l];
     if (!pair_small(l, 1)) KP_CUDA_TRY(cudaStreamWaitEvent(s, ctx->side_ev[2 * l + 1], 0));
     if (pair_small(l, 0) || pair_small(l, 1)) KP_CUDA_TRY(cudaStreamWaitEvent(s, small_done, 0));
+    if (early[l]) KP_CUDA_TRY(cudaStreamWaitEvent(s, ready, 0));  // the finalized gradient
     launch_eig_status(c.at(P.k_la[l]), P.p[l], c.at(P.k_lb[l]), P.q[l],
                       reinterpret_cast<int*>(c.at(P.k_info[l])), out->status, s);
     KP_TRY(kron_combine(ctx->side_blas[2 * l], s, P.p[l], P.q[l], c.at(P.k_A1[l]), c.at(P.k_la[l]),
@@ -1421,6 +1461,8 @@ int32_t kp_context_destroy(kp_context* c) {
     cudaStreamDestroy(c->side[k]);
   }
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->layer_ev) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->fin_ev) cudaEventDestroy(e);
   if (c->blas) cublasDestroy(c->blas);
   if (c->solver) cusolverDnDestroy(c->solver);
   delete c;
@@ -1633,11 +1675,31 @@ int32_t kp_kfac_phase_update(kp_context* ctx, const kp_problem* prob, const kp_k
   return KP_OK;
 }
 
+// Early preconditioning for single-call steps (Ctx::early): per-layer contractions (not the
+// grouped small-network launch) and at least one factor pair outside the one-launch small
+// solver.  KP_EARLY_PRECOND=0 turns it off (measurements).
+static int setup_early(Ctx& c) {
+  static const bool enabled = [] {
+    const char* e = getenv("KP_EARLY_PRECOND");
+    return !(e && atoi(e) == 0);
+  }();
+  const Plan& P = c.P;
+  if (!enabled || P.tn_grouped) return KP_OK;
+  bool any = false;
+  for (int l = 0; l < P.L; ++l)
+    any |= std::max(P.p[l], P.q[l]) > small_eig_max_n();
+  if (!any) return KP_OK;
+  KP_TRY(ensure_side_streams(c.ctx, 2 * P.L + 2));
+  c.early = true;
+  return KP_OK;
+}
+
 int32_t kp_kfac_step(kp_context* ctx, const kp_problem* prob, const kp_kfac_config* cfg,
                      kp_state* st, const kp_batch* bt, kp_step_out* out, void* ws,
                      size_t ws_bytes, void* stream) {
   KP_PHASE_PROLOGUE
   if (!bt) return KP_ERR_INVALID;
+  KP_TRY(setup_early(c));
   kp_batch bt_rot;
   const kp_batch* bt_in = bt;
   KP_TRY(rotated_batch(c, bt_in, bt_rot, bt));
@@ -1687,6 +1749,7 @@ int32_t kp_kfac_star_step(kp_context* ctx, const kp_problem* prob, const kp_kfac
                           size_t ws_bytes, void* stream) {
   KP_PHASE_PROLOGUE
   if (!bt) return KP_ERR_INVALID;
+  KP_TRY(setup_early(c));
   kp_batch bt_rot;
   const kp_batch* bt_in = bt;
   KP_TRY(rotated_batch(c, bt_in, bt_rot, bt));
