@@ -192,6 +192,13 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     sharded = world > 1 or args.force_dist
     if sharded:
+        if "RANK" not in os.environ:  # --force-dist outside torchrun: a world of one
+            import socket
+            with socket.socket() as sk:
+                sk.bind(("127.0.0.1", 0))
+                port = sk.getsockname()[1]
+            os.environ.update({"RANK": "0", "WORLD_SIZE": "1", "LOCAL_RANK": "0",
+                               "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
         dist.init_process_group("nccl", device_id=dev)
     wl = configs.WORKLOADS[args.workload]
     n_loc = args.n_interior
