@@ -186,6 +186,13 @@ def test_chunked_interior_matches_unchunked():
     _oracle_vs_device((5, 64, 48, 1), prob, 300, 50, 2, chunk=70)
 
 
+def test_chunked_mid_size_pairs_match_oracle():
+    """Chunked interior with factor pairs on the cluster solver (n = 131, 130) and early
+    preconditioning: the per-layer events come from the last chunk's contractions."""
+    prob = make_problem("poisson_harmonic_mixed")
+    _oracle_vs_device((10, 130, 70, 1), prob, 240, 60, 3, chunk=70)
+
+
 def test_taylor_forward_matches_oracle():
     from paper_2405_15603_b200.engine import KfacEngine, pack_params
     prob = make_problem("heat", spatial_dim=4)
