@@ -76,6 +76,9 @@ PLAN10 = {
     "lfp_10": ("lfp", 300, 100, 10),
     "lfp_star_10": ("lfp", 300, 100, 10),
     "dense_10": ("dense", 400, 100, 10),
+    "c3_star_10": ("c3", 400, 200, 10),
+    "c5_star_10": ("c5", 24, 8, 10),
+    "c1_momentum_10": ("c1", 600, 150, 10),
 }
 FULL_RECORD_STEPS = {1, 10}
 
@@ -125,7 +128,7 @@ def main():
         arch = network.Architecture(wl.widths)
         params = network.init_params(arch, _stream_seed(0, 0))
         batch = pde.sample_batch(prob, n_int, n_bnd, _stream_seed(0, 1, 0))
-        momentum = 0.9 if name.endswith("momentum") else wl.momentum
+        momentum = 0.9 if "momentum" in name else wl.momentum
         kind = "kfac_star" if "_star" in name else "kfac"
         cfg = optim.OptimizerConfig(kind=kind, damping=wl.damping, ema=wl.ema,
                                     momentum=momentum, init_mode="identity")

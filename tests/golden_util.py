@@ -8,8 +8,8 @@ GOLDEN_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 NAMES = ("c1", "c2", "c3", "c4", "c5", "c1_momentum", "lfp", "dense")
 STAR_NAMES = ("c1_star", "c3_star", "c5_star", "lfp_star", "dense_star")
 # ten-step runs of the five BASELINE configs (arrays recorded at steps 1 and 10)
-NAMES10 = ("c1_10", "c2_10", "c3_10", "c4_10", "c5_10", "lfp_10", "dense_10")
-STAR10 = ("c1_star_10", "lfp_star_10")
+NAMES10 = ("c1_10", "c2_10", "c3_10", "c4_10", "c5_10", "lfp_10", "dense_10", "c1_momentum_10")
+STAR10 = ("c1_star_10", "lfp_star_10", "c3_star_10", "c5_star_10")
 
 
 def load(name):

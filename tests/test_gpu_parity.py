@@ -23,7 +23,8 @@ WL_OF = {"c1": "c1", "c2": "c2", "c3": "c3", "c4": "c4", "c5": "c5", "c1_momentu
          "c1_star": "c1", "c3_star": "c3", "c5_star": "c5", "lfp": "lfp", "lfp_star": "lfp",
          "dense": "dense", "dense_star": "dense",
          "c1_10": "c1", "c2_10": "c2", "c3_10": "c3", "c4_10": "c4", "c5_10": "c5",
-         "lfp_10": "lfp", "dense_10": "dense", "c1_star_10": "c1", "lfp_star_10": "lfp"}
+         "lfp_10": "lfp", "dense_10": "dense", "c1_star_10": "c1", "lfp_star_10": "lfp",
+         "c3_star_10": "c3", "c5_star_10": "c5", "c1_momentum_10": "c1"}
 
 
 def _theta_colstack(params):

@@ -18,7 +18,8 @@ WL_OF = {"c1": "c1", "c2": "c2", "c3": "c3", "c4": "c4", "c5": "c5", "c1_momentu
          "c1_star": "c1", "c3_star": "c3", "c5_star": "c5", "lfp": "lfp", "lfp_star": "lfp",
          "dense": "dense", "dense_star": "dense",
          "c1_10": "c1", "c2_10": "c2", "c3_10": "c3", "c4_10": "c4", "c5_10": "c5",
-         "lfp_10": "lfp", "dense_10": "dense", "c1_star_10": "c1", "lfp_star_10": "lfp"}
+         "lfp_10": "lfp", "dense_10": "dense", "c1_star_10": "c1", "lfp_star_10": "lfp",
+         "c3_star_10": "c3", "c5_star_10": "c5", "c1_momentum_10": "c1"}
 
 
 def build(name):
@@ -49,7 +50,7 @@ def test_oracle_dense_coefficient_taylor_forward():
         assert compare(g, "taylor/" + key, arr, 1e-12) <= 1e-12
 
 
-@pytest.mark.parametrize("name", NAMES + ("c4_10", "c5_10", "lfp_10", "dense_10"))
+@pytest.mark.parametrize("name", NAMES + ("c4_10", "c5_10", "lfp_10", "dense_10", "c1_momentum_10"))
 def test_oracle_matches_reference_steps(name):
     g, wl, prob, params, batch = build(name)
     st = orc.init_state(params.weights, params.biases, ema=float(g["ema"]),
@@ -87,7 +88,7 @@ def rel(a, b):
     return abs(a - b) / max(abs(b), 1e-300)
 
 
-@pytest.mark.parametrize("name", STAR_NAMES + ("lfp_star_10",))
+@pytest.mark.parametrize("name", STAR_NAMES + ("lfp_star_10", "c5_star_10"))
 def test_oracle_matches_reference_kfac_star(name):
     """KFAC* (src/optim.py:266-320): alpha/mu from the exact-Gramian quadratic model."""
     from paper_2405_15603_b200.network import mats_to_vec
