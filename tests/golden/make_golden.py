@@ -79,6 +79,7 @@ PLAN10 = {
     "c3_star_10": ("c3", 400, 200, 10),
     "c5_star_10": ("c5", 24, 8, 10),
     "c1_momentum_10": ("c1", 600, 150, 10),
+    "c4_zero_10": ("c4", 400, 130, 10),  # init_mode="zero" (src/curvature.py:62-76)
 }
 FULL_RECORD_STEPS = {1, 10}
 
@@ -131,9 +132,11 @@ def main():
         momentum = 0.9 if "momentum" in name else wl.momentum
         kind = "kfac_star" if "_star" in name else "kfac"
         cfg = optim.OptimizerConfig(kind=kind, damping=wl.damping, ema=wl.ema,
-                                    momentum=momentum, init_mode="identity")
+                                    momentum=momentum,
+                                    init_mode="zero" if "zero" in name else "identity")
         state = optim.init_train_state(params, cfg)
         out = {"widths": np.array(wl.widths), "n_interior": np.array(n_int),
+               "init_zero": np.array(1 if "zero" in name else 0),
                "n_boundary": np.array(n_bnd), "momentum": np.array(momentum),
                "damping": np.array(wl.damping), "ema": np.array(wl.ema)}
         put(out, "in/interior", batch.interior)

@@ -9,7 +9,8 @@ reference's seeded parameters and batches bit-for-bit.
 import numpy as np
 import pytest
 
-from golden_util import NAMES, NAMES10, STAR10, STAR_NAMES, compare, has, load, pack_factors
+from golden_util import (NAMES, NAMES10, STAR10, STAR_NAMES, compare, has, line_search_rel, load,
+                         pack_factors)
 from oracle import kfac_oracle as orc
 from paper_2405_15603_b200 import configs as cfgs
 from paper_2405_15603_b200.network import params_to_vec
@@ -19,7 +20,7 @@ WL_OF = {"c1": "c1", "c2": "c2", "c3": "c3", "c4": "c4", "c5": "c5", "c1_momentu
          "dense": "dense", "dense_star": "dense",
          "c1_10": "c1", "c2_10": "c2", "c3_10": "c3", "c4_10": "c4", "c5_10": "c5",
          "lfp_10": "lfp", "dense_10": "dense", "c1_star_10": "c1", "lfp_star_10": "lfp",
-         "c3_star_10": "c3", "c5_star_10": "c5", "c1_momentum_10": "c1"}
+         "c3_star_10": "c3", "c5_star_10": "c5", "c1_momentum_10": "c1", "c4_zero_10": "c4"}
 
 
 def build(name):
@@ -50,11 +51,13 @@ def test_oracle_dense_coefficient_taylor_forward():
         assert compare(g, "taylor/" + key, arr, 1e-12) <= 1e-12
 
 
-@pytest.mark.parametrize("name", NAMES + ("c4_10", "c5_10", "lfp_10", "dense_10", "c1_momentum_10"))
+@pytest.mark.parametrize("name", NAMES + ("c4_10", "c5_10", "lfp_10", "dense_10", "c1_momentum_10",
+                                           "c4_zero_10"))
 def test_oracle_matches_reference_steps(name):
     g, wl, prob, params, batch = build(name)
     st = orc.init_state(params.weights, params.biases, ema=float(g["ema"]),
-                        damping=float(g["damping"]), momentum=float(g["momentum"]))
+                        damping=float(g["damping"]), momentum=float(g["momentum"]),
+                        init_mode="zero" if int(g.get("init_zero", 0)) else "identity")
     t = 1
     while f"s{t}/alpha" in g:
         rec = {}
@@ -64,8 +67,7 @@ def test_oracle_matches_reference_steps(name):
         assert alpha == float(g[p + "alpha"])
         assert abs(li - float(g[p + "loss_interior"])) <= tol * abs(float(g[p + "loss_interior"]))
         assert abs(lb - float(g[p + "loss_boundary"])) <= tol * abs(float(g[p + "loss_boundary"]))
-        ls = np.asarray(rec["ls_losses"])
-        assert np.max(np.abs(ls - g[p + "ls_losses"]) / np.maximum(np.abs(g[p + "ls_losses"]), 1e-300)) <= tol
+        assert line_search_rel(rec["ls_losses"], g[p + "ls_losses"]) <= tol
         if not has(g, p + "theta"):  # ten-step runs record arrays at steps 1 and 10 only
             t += 1
             continue
