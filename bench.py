@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--chunk", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-points", type=int, default=CPU_SAMPLE_POINTS,
+                    help="interior points per CPU-oracle step (reference arm and cpu_baseline)")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--force-dist", action="store_true",
                     help="use the sharded NCCL step even at world size 1 (plumbing check)")
@@ -109,20 +111,29 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference_step_time(wl, n_points, n_bnd, threads_note):
+def oracle_step_fn(optimizer):
+    """The oracle's step for --optimizer (reference src/optim.py:251-263 / :266-320)."""
+    from oracle import kfac_oracle as orc
+
+    return orc.kfac_star_step if optimizer == "kfac_star" else orc.kfac_step
+
+
+def cpu_reference_step_time(wl, n_points, n_bnd, threads_note, optimizer="kfac"):
     """Time one oracle KFAC step (the reference algorithm, NumPy/OpenBLAS) on this host."""
     from oracle import kfac_oracle as orc
+
+    step = oracle_step_fn(optimizer)
 
     prob, params, batch = wl.build(0, n_points, n_bnd)
     # warm the BLAS/LAPACK paths on a tiny batch first
     _, _, small = wl.build(0, 4, 2)
     st0 = orc.init_state(params.weights, params.biases, ema=wl.ema, damping=wl.damping,
                          momentum=wl.momentum)
-    orc.kfac_step(st0, small, prob)
+    step(st0, small, prob)
     st = orc.init_state(params.weights, params.biases, ema=wl.ema, damping=wl.damping,
                         momentum=wl.momentum)
     t0 = time.perf_counter()
-    orc.kfac_step(st, batch, prob)
+    step(st, batch, prob)
     return time.perf_counter() - t0
 
 
@@ -141,18 +152,21 @@ def run_reference(args):
     from paper_2405_15603_b200 import configs
 
     wl = configs.WORKLOADS[args.workload]
-    n_s = CPU_SAMPLE_POINTS
+    n_s = args.cpu_points
     nb_s = max(1, n_s // 3)
     prob, params, batch = wl.build(0, n_s, nb_s)
     from oracle import kfac_oracle as orc
 
+    step = oracle_step_fn(args.optimizer)
+    ref_lines = "266-320" if args.optimizer == "kfac_star" else "251-263"
+
     st = orc.init_state(params.weights, params.biases, ema=wl.ema, damping=wl.damping,
                         momentum=wl.momentum)
     for _ in range(args.warmup):
-        orc.kfac_step(st, batch, prob)
+        step(st, batch, prob)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        orc.kfac_step(st, batch, prob)
+        step(st, batch, prob)
     dt = (time.perf_counter() - t0) / max(args.steps, 1)
     value = n_s / dt
     cores = host_cores()
@@ -163,13 +177,13 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference seeding recipe, SURVEY.md §8d)",
-        "config": {"workload": wl.name, "widths": list(wl.widths),
+        "config": {"workload": wl.name, "optimizer": args.optimizer, "widths": list(wl.widths),
                    "n_interior_per_step": n_s, "n_boundary_per_step": nb_s,
                    "arm_n_interior_total": n_int_full},
         "cpu_baseline": {"value": value, "unit": "interior collocation points/s", "cores": cores,
                          "kind": "port",
-                         "sample": f"oracle/kfac_oracle.py kfac_step (NumPy/OpenBLAS restatement of the "
-                                   f"reference src/optim.py:251-263) on {n_s} interior + {nb_s} boundary "
+                         "sample": f"oracle/kfac_oracle.py {step.__name__} (NumPy/OpenBLAS restatement of "
+                                   f"the reference src/optim.py:{ref_lines}) on {n_s} interior + {nb_s} boundary "
                                    f"points of {wl.name}; per-point work is N-linear except the "
                                    f"N-independent Kronecker solve"},
         "e2e": {"value": value, "unit": "interior collocation points/s", "h2d_bytes_per_step": 0,
@@ -275,12 +289,13 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        n_s = CPU_SAMPLE_POINTS
-        dt = cpu_reference_step_time(wl, n_s, max(1, n_s // 3), None)
+        n_s = args.cpu_points
+        dt = cpu_reference_step_time(wl, n_s, max(1, n_s // 3), None, args.optimizer)
         cpu = {"value": n_s / dt, "unit": "interior collocation points/s", "cores": host_cores(),
                "kind": "port",
-               "sample": f"one oracle kfac_step (NumPy/OpenBLAS restatement of reference "
-                         f"src/optim.py:251-263) on {n_s} interior + {n_s // 3} boundary points of "
+               "sample": f"one oracle {args.optimizer}_step (NumPy/OpenBLAS restatement of "
+                         f"reference src/optim.py:"
+                         f"{'266-320' if args.optimizer == 'kfac_star' else '251-263'}) on {n_s} interior + {n_s // 3} boundary points of "
                          f"{wl.name}, {dt:.2f} s"}
 
     traffic, traffic_note = None, None
