@@ -117,3 +117,19 @@ def test_oracle_matches_reference_kfac_star(name):
         assert compare(g, p + "prev_update", mats_to_vec(st.prev_update), tol) <= tol
         t += 1
     assert t > 1
+
+
+@pytest.mark.parametrize("name", NAMES + NAMES10)
+def test_line_search_gap_dwarfs_parity_tolerance(name):
+    """exact α equality is a sound assertion only if the best and second-best
+    line-search losses of the reference are separated far beyond the parity tolerance.  Every
+    golden step keeps a relative gap of at least 100 x 1e-8 (smallest: c3 step 3, 4.7e-6)."""
+    g = load(name)
+    t, gaps = 1, []
+    while f"s{t}/ls_losses" in g:
+        tot = np.asarray(g[f"s{t}/ls_losses"], dtype=np.float64).reshape(-1, 2).sum(axis=1)
+        fin = np.sort(tot[np.isfinite(tot)])
+        assert fin.size >= 2
+        gaps.append((fin[1] - fin[0]) / abs(fin[0]))
+        t += 1
+    assert gaps and min(gaps) >= 100 * 1e-8, gaps
