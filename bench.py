@@ -202,6 +202,12 @@ def run_ours(args):
     from paper_2405_15603_b200.engine import KfacEngine
 
     rank, world, local = dist_env()
+    # KP_BENCH_DIST_BACKEND=gloo: plumbing check of the N > 1 path with every rank on the one
+    # GPU of a test box (host-side collectives; no kernel waits on another rank).  Never a
+    # bench number.
+    backend = os.environ.get("KP_BENCH_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     sharded = world > 1 or args.force_dist
@@ -213,7 +219,10 @@ def run_ours(args):
                 port = sk.getsockname()[1]
             os.environ.update({"RANK": "0", "WORLD_SIZE": "1", "LOCAL_RANK": "0",
                                "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     wl = configs.WORKLOADS[args.workload]
     n_loc = args.n_interior
     nb_loc = args.n_boundary if args.n_boundary is not None else max(1, n_loc // 3)
