@@ -62,9 +62,6 @@ __global__ void __launch_bounds__(NW * 32, MINB)
   double* sm = reinterpret_cast<double*>(act_raw + ((1024 - (smem_addr(act_raw) & 1023)) & 1023));
   double* As = sm;
   double* Bs = sm + STAGES * A_STAGE;
-  // The pipeline barriers live outside the dynamic region: the epilogue's C staging reuses
-  // the whole pipeline smem, and overwriting live mbarrier objects (no mbarrier.inval) gave
-  // sporadic garbage rows (NaN in ~1 of 10^3 line-search launches).
   // The pipeline barriers sit after both the pipeline stages and the epilogue's C staging
   // (which reuses the stage smem): overwriting live mbarrier objects (no mbarrier.inval)
   // gave sporadic garbage rows (NaN in ~1 of 10^3 line-search launches at c5 scale).
