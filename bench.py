@@ -118,8 +118,28 @@ def oracle_step_fn(optimizer):
     return orc.kfac_star_step if optimizer == "kfac_star" else orc.kfac_step
 
 
-def cpu_reference_step_time(wl, n_points, n_bnd, threads_note, optimizer="kfac"):
-    """Time one oracle KFAC step (the reference algorithm, NumPy/OpenBLAS) on this host."""
+def all_host_blas_threads():
+    """Context giving the oracle's BLAS every host core: torchrun exports OMP_NUM_THREADS=1,
+    which OpenBLAS reads when NumPy loads."""
+    from threadpoolctl import threadpool_limits
+
+    return threadpool_limits(limits=host_cores(), user_api="blas")
+
+
+def blas_threads():
+    from threadpoolctl import threadpool_info
+
+    return max([d["num_threads"] for d in threadpool_info() if d["user_api"] == "blas"] or [1])
+
+
+def cpu_reference_step_time(wl, n_points, n_bnd, optimizer="kfac"):
+    """Time one oracle KFAC step (the reference algorithm, NumPy/OpenBLAS) on this host with
+    every host core; returns (seconds, BLAS threads used)."""
+    with all_host_blas_threads():
+        return _cpu_reference_step_time(wl, n_points, n_bnd, optimizer), blas_threads()
+
+
+def _cpu_reference_step_time(wl, n_points, n_bnd, optimizer):
     from oracle import kfac_oracle as orc
 
     step = oracle_step_fn(optimizer)
@@ -162,14 +182,15 @@ def run_reference(args):
 
     st = orc.init_state(params.weights, params.biases, ema=wl.ema, damping=wl.damping,
                         momentum=wl.momentum)
-    for _ in range(args.warmup):
-        step(st, batch, prob)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        step(st, batch, prob)
-    dt = (time.perf_counter() - t0) / max(args.steps, 1)
+    with all_host_blas_threads():
+        cores = blas_threads()
+        for _ in range(args.warmup):
+            step(st, batch, prob)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            step(st, batch, prob)
+        dt = (time.perf_counter() - t0) / max(args.steps, 1)
     value = n_s / dt
-    cores = host_cores()
     n_int_full = args.n_interior * args.gpus
     line = {
         "impl": "reference", "metric": "collocation_pts_per_s", "value": value,
@@ -299,8 +320,8 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         n_s = args.cpu_points
-        dt = cpu_reference_step_time(wl, n_s, max(1, n_s // 3), None, args.optimizer)
-        cpu = {"value": n_s / dt, "unit": "interior collocation points/s", "cores": host_cores(),
+        dt, cores = cpu_reference_step_time(wl, n_s, max(1, n_s // 3), args.optimizer)
+        cpu = {"value": n_s / dt, "unit": "interior collocation points/s", "cores": cores,
                "kind": "port",
                "sample": f"one oracle {args.optimizer}_step (NumPy/OpenBLAS restatement of "
                          f"reference src/optim.py:"

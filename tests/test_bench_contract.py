@@ -46,3 +46,5 @@ def test_reference_arm_under_torchrun_prints_once():
     assert r.returncode == 0, r.stderr[-2000:]
     lines = _json_lines(r.stdout)
     assert len(lines) == 1 and lines[0]["n_gpus"] == 2
+    # torchrun exports OMP_NUM_THREADS=1; the reference arm still uses every host core
+    assert lines[0]["cpu_baseline"]["cores"] == len(os.sched_getaffinity(0))
