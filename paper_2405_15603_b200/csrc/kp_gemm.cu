@@ -184,9 +184,100 @@ static TnGrid tn_grid(int64_t R, int P, int Q, bool sym) {
   return t;
 }
 
+// One-column contractions (the h_out = 1 output layer's B factor and gradient:
+// X = Gbar_L, one column): acc[j] += sum_r x_r w_{r/Sw} y_{r,j} (+ y's bias column) is a
+// weighted column sum over the rows of Y, HBM-bound; the 64 x 64 DMMA tiles would compute
+// 63 wasted rows of every tile (c5: 9.3 ms for a 6.8 GB read).  Rows are split over about
+// four blocks per SM, one partial row per block, reduced by k_tn_reduce (fixed order).
+constexpr int COL1_THREADS = 256, COL1_WIDE = 4, COL1_TINY = 8;
+constexpr int64_t COL1_TARGET_BLOCKS = 148 * 4;
+
+static int64_t col1_splits(int64_t R) {
+  return std::max<int64_t>(1, std::min<int64_t>(COL1_TARGET_BLOCKS, ceil_div(R, 4 * COL1_THREADS)));
+}
+
 size_t gemm_tn_partial_doubles(int64_t R, int P, int Q, bool sym) {
   TnGrid t = tn_grid(R, P, Q, sym);
-  return (size_t)t.splits * P * Q;
+  size_t need = (size_t)t.splits * P * Q;
+  if (P == 1) need = std::max(need, (size_t)col1_splits(R) * Q);
+  return need;
+}
+
+__device__ __forceinline__ double col1_x(const GemmTN& g, int64_t r) {
+  const double x = g.X[r * g.ldx];
+  return g.w ? x * g.w[r / g.Sw] : x;
+}
+
+// Q > COL1_TINY: thread t owns columns t + 256 k; the block's rows go through shared memory
+// 256 at a time (x_r w_r staged once), each row of Y read coalesced.
+__global__ void __launch_bounds__(COL1_THREADS) k_tn_col1_wide(GemmTN g, int Q, int64_t rpb,
+                                                             double* __restrict__ partial) {
+  __shared__ double xs[COL1_THREADS];
+  const int tid = threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.x * rpb;
+  const int64_t r1 = g.R < r0 + rpb ? g.R : r0 + rpb;
+  double acc[COL1_WIDE];
+#pragma unroll
+  for (int k = 0; k < COL1_WIDE; ++k) acc[k] = 0.0;
+  for (int64_t rb = r0; rb < r1; rb += COL1_THREADS) {
+    const int nr = (int)(r1 - rb < COL1_THREADS ? r1 - rb : COL1_THREADS);
+    __syncthreads();
+    if (tid < nr) xs[tid] = col1_x(g, rb + tid);
+    __syncthreads();
+#pragma unroll 4
+    for (int i = 0; i < nr; ++i) {
+      const double xv = xs[i];
+      const int64_t r = rb + i;
+      const double* yr = g.Y + r * g.ldy;
+      const bool brow = g.y_bias && (r % g.S) == 0;
+#pragma unroll
+      for (int k = 0; k < COL1_WIDE; ++k) {
+        const int j = tid + COL1_THREADS * k;
+        if (j < g.ny) acc[k] = fma(xv, yr[j], acc[k]);
+        else if (j == g.ny && brow) acc[k] += xv;
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < COL1_WIDE; ++k) {
+    const int j = tid + COL1_THREADS * k;
+    if (j < Q) partial[(int64_t)blockIdx.x * Q + j] = acc[k];
+  }
+}
+
+// Q <= COL1_TINY (the 1 x 1 B factor of the output layer): thread per row, block reduction.
+__global__ void __launch_bounds__(COL1_THREADS) k_tn_col1_tiny(GemmTN g, int Q, int64_t rpb,
+                                                             double* __restrict__ partial) {
+  __shared__ double red[COL1_THREADS / 32][COL1_TINY];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t r0 = (int64_t)blockIdx.x * rpb;
+  const int64_t r1 = g.R < r0 + rpb ? g.R : r0 + rpb;
+  double acc[COL1_TINY];
+#pragma unroll
+  for (int k = 0; k < COL1_TINY; ++k) acc[k] = 0.0;
+  for (int64_t r = r0 + tid; r < r1; r += COL1_THREADS) {
+    const double xv = col1_x(g, r);
+    const double* yr = g.Y + r * g.ldy;
+    const bool brow = g.y_bias && (r % g.S) == 0;
+#pragma unroll
+    for (int k = 0; k < COL1_TINY; ++k) {
+      if (k < g.ny) acc[k] = fma(xv, yr[k], acc[k]);
+      else if (k == g.ny && brow) acc[k] += xv;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < COL1_TINY; ++k) {
+    double v = acc[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp][k] = v;
+  }
+  __syncthreads();
+  if (tid < Q) {
+    double v = 0.0;
+    for (int w = 0; w < COL1_THREADS / 32; ++w) v += red[w][tid];
+    partial[(int64_t)blockIdx.x * Q + tid] = v;
+  }
 }
 
 template <int BM, int BN, int WM, int WN, int BK, int STAGES>
@@ -367,6 +458,20 @@ void launch_gemm_tn_accumulate(const GemmTN& g, double* partial, double* acc, cu
   const int P = g.nx + (g.x_bias ? 1 : 0);
   const int Q = g.ny + (g.y_bias ? 1 : 0);
   if (g.R <= 0 || P <= 0 || Q <= 0) return;
+  if (g.nx == 1 && !g.x_bias && Q <= COL1_THREADS * COL1_WIDE) {
+    const int64_t splits = col1_splits(g.R);
+    const int64_t rpb = ceil_div(ceil_div(g.R, splits), COL1_THREADS) * COL1_THREADS;
+    const int64_t blocks = ceil_div(g.R, rpb);
+    count_launch();
+    if (Q <= COL1_TINY)
+      k_tn_col1_tiny<<<(unsigned)blocks, COL1_THREADS, 0, s>>>(g, Q, rpb, partial);
+    else
+      k_tn_col1_wide<<<(unsigned)blocks, COL1_THREADS, 0, s>>>(g, Q, rpb, partial);
+    count_launch();
+    k_tn_reduce<<<(int)std::min<int64_t>(ceil_div(Q, 256), 148 * 8), 256, 0, s>>>(
+        partial, blocks, 1, Q, false, acc);
+    return;
+  }
   TnGrid t = tn_grid(g.R, P, Q, g.sym);
   const unsigned blocks = (unsigned)(t.splits * t.pairs);
   auto kern = k_gemm_tn<TN_BM, TN_BN, TN_WM, TN_WN, TN_BK, TN_STAGES>;

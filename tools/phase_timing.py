@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--chunk", type=int, default=0)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--owned-world", type=int, default=0)
+    ap.add_argument("--star", action="store_true", help="KFAC* phases (star_gvp, star_update)")
     a = ap.parse_args()
     import torch
 
@@ -45,12 +46,13 @@ def main():
         evs[1].record()
         eng.phase("precondition")
         evs[2].record()
-        eng.phase("linesearch")
+        eng.phase("star_gvp" if a.star else "linesearch")
         evs[3].record()
-        eng.phase("update")
+        eng.phase("star_update" if a.star else "update")
         evs[4].record()
         sc, code = eng.finish_step()
-        names = ["accumulate", "precondition", "linesearch", "update"]
+        names = (["accumulate", "precondition", "star_gvp", "star_update"] if a.star
+                 else ["accumulate", "precondition", "linesearch", "update"])
         res = {n: evs[i].elapsed_time(evs[i + 1]) for i, n in enumerate(names)}
         res["total_ms"] = evs[0].elapsed_time(evs[4])
         res["status"] = code
@@ -71,7 +73,18 @@ def main():
             worst = max(worst, min(t))
         res["owners"] = owners
         res["precondition_owned_max_ms"] = worst
-    f = configs.flops_per_step(wl.widths, a.n_interior, nb)
+    # the single-call step (early preconditioning overlaps the accumulate) for comparison
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fn = eng.star_step if a.star else eng.step
+    eng.use_graph = False
+    fn()
+    e0.record()
+    fn()
+    e1.record()
+    torch.cuda.synchronize()
+    res["single_call_ms"] = e0.elapsed_time(e1)
+    f = configs.flops_per_step(wl.widths, a.n_interior, nb,
+                               optimizer="kfac_star" if a.star else "kfac")
     res["alg_tflops_per_s"] = f / (res["total_ms"] / 1e3) / 1e12
     res["workload"] = wl.name
     res["n_interior"] = a.n_interior
