@@ -261,6 +261,8 @@ void launch_star_solve_update(const double* dots, double lam, double* theta, dou
 void launch_rowdot_accum(const double* G, const double* Y, int q, int64_t n, int S, double* jv,
                          cudaStream_t s);
 // layer-0 Jacobian-vector product (value rows from y0val, derivative rows from V0^T)
+bool launch_jvp_last(const double* G, const double* Z, int64_t ldz, int K, const double* v,
+                     const double* b, int64_t n, int S, double* jv, cudaStream_t s);
 void launch_jvp_layer0(const double* G, const double* y0val, const double* v0t, int64_t n, int d,
                        int h1, double* jv, cudaStream_t s);
 void launch_gen_eig_1x1(const double* f1, const double* f2, double lam, double* t, double* eig,

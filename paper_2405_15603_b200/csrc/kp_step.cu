@@ -1292,6 +1292,9 @@ void jvp_pass(const Ctx& c, const double* x, int64_t n, const TaylorDims& td, co
       if (td.taylor) launch_jvp_layer0(G, y0, c.at(P.o_v0t), n, P.d, q, jv, c.s);
       else launch_rowdot_accum(G, y0, q, n, 1, jv, c.s);
     } else {
+      if (q == 1 && launch_jvp_last(G, b.post[l], P.h[l], P.h[l], wv + P.wo[l],
+                                    V + P.th[l] + P.h[l], n, td.S, jv, c.s))
+        continue;
       double* y = c.at(P.o_ping);
       GemmNT g{b.post[l], P.h[l], wv + P.wo[l], P.h[l], y, q, n * td.S, q, P.h[l],
                V + P.th[l] + P.h[l], P.p[l], td.S};

@@ -463,6 +463,44 @@ void launch_rowdot_accum(const double* G, const double* Y, int q, int64_t n, int
   k_rowdot_accum<<<(unsigned)ceil_div(n, 8), 256, 0, s>>>(G, Y, q, n, S, jv);
 }
 
+// Output layer with h_out = 1 (q = 1): jv[n] += sum_s G[n,s] (z_{n,s} . v + (s == 0) b) in one
+// read of the last hidden state (warp per sample, the K/32 entries of v in registers, one
+// reduction per sample) instead of an (n S x 1) GEMM output plus a row-dot pass.
+constexpr int JVP_LAST_MAXK = 1024;
+__global__ void __launch_bounds__(256) k_jvp_last(const double* __restrict__ G,
+                                                  const double* __restrict__ Z, int64_t ldz, int K,
+                                                  const double* __restrict__ v, const double* __restrict__ b,
+                                                  int64_t n, int S, double* __restrict__ jv) {
+  const int lane = threadIdx.x & 31;
+  const int64_t smp = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (smp >= n) return;
+  constexpr int U = JVP_LAST_MAXK / 32;
+  double vr[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) vr[u] = (lane + 32 * u < K) ? v[lane + 32 * u] : 0.0;
+  const double* g = G + smp * S;
+  double acc = 0.0;
+  for (int s = 0; s < S; ++s) {
+    const double* z = Z + (smp * S + s) * ldz;
+    double t = 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (lane + 32 * u < K) t = fma(z[lane + 32 * u], vr[u], t);
+    acc = fma(g[s], t, acc);
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) jv[smp] += fma(g[0], b[0], acc);
+}
+
+bool launch_jvp_last(const double* G, const double* Z, int64_t ldz, int K, const double* v,
+                     const double* b, int64_t n, int S, double* jv, cudaStream_t s) {
+  if (K > JVP_LAST_MAXK) return false;
+  if (n <= 0) return true;
+  count_launch();
+  k_jvp_last<<<(unsigned)ceil_div(n, 8), 256, 0, s>>>(G, Z, ldz, K, v, b, n, S, jv);
+  return true;
+}
+
 // Layer 0: zhat rows are [x; 1] (value), [e_i; 0] (derivatives), 0 (operator), so
 // y_value = V0[:, :d] x + V0[:, d] (y0val, from a GEMM) and y_i = V0[:, i].
 __global__ void k_jvp_layer0(const double* __restrict__ G, const double* __restrict__ y0val,
