@@ -72,6 +72,7 @@ struct kp_context {
   double* warm_buf = nullptr;
   size_t warm_cap = 0;  // doubles
   int* warm_flags = nullptr;
+  cudaEvent_t warm_ev = nullptr;  // the flags' reset on the main stream, for the side streams
   std::vector<unsigned char> warm_key;
   // cache of the last workspace plan (make_plan queries cuSOLVER workspace sizes: host cost)
   kp_problem plan_key{};
@@ -1015,6 +1016,7 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
   };
   std::vector<MidWarm> mid_warm(2 * P.L, MidWarm{nullptr, nullptr, nullptr});
   // warm-start cache for the small pairs (re-keyed when shapes or factor buffers change)
+  bool warm_reset = false;
   {
     std::vector<unsigned char> key;
     auto put = [&](const void* p, size_t n) {
@@ -1049,6 +1051,11 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
       }
       KP_CUDA_TRY(cudaMemsetAsync(ctx->warm_flags, 0, sizeof(int) * 64, c.s));
       ctx->warm_key = key;
+      // the mid-size pairs read their flags on side streams that (for early layers) wait
+      // only on their own factors: order them after this reset
+      if (!ctx->warm_ev) KP_CUDA_TRY(cudaEventCreateWithFlags(&ctx->warm_ev, cudaEventDisableTiming));
+      KP_CUDA_TRY(cudaEventRecord(ctx->warm_ev, c.s));
+      warm_reset = true;
     }
   }
   {
@@ -1117,6 +1124,7 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
       if (!pair_mid(l, k)) continue;
       cudaStream_t s = ctx->side[2 * l + k];
       KP_CUDA_TRY(cudaStreamWaitEvent(s, early[l] ? ctx->fin_ev[l] : ready, 0));
+      if (warm_reset) KP_CUDA_TRY(cudaStreamWaitEvent(s, ctx->warm_ev, 0));
       int* info = reinterpret_cast<int*>(c.at(P.k_info[l])) + k;
       KP_CUDA_TRY(cudaMemsetAsync(info, 0, sizeof(int), s));
       KP_TRY(gen_eig_mid(ctx->side_solver[2 * l + k], ctx->side_blas[2 * l + k], s,
@@ -1304,10 +1312,13 @@ void jvp_pass(const Ctx& c, const double* x, int64_t n, const TaylorDims& td, co
   }
 }
 
-int phase_star_gvp(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, const kp_batch* bt) {
+// Gramian-vector products of vectors [v0, v1) of {Delta, prev}: each vector owns its two
+// slots of o_gv (interior, boundary), so the vectors can be computed in either order.
+static int star_gvp_range(const Ctx& c, const kp_kfac_config* cfg, kp_state* st,
+                          const kp_batch* bt, int v0, int v1) {
   const Plan& P = c.P;
   double* gv = c.at(P.o_gv);
-  KP_CUDA_TRY(cudaMemsetAsync(gv, 0, sizeof(double) * 4 * P.D, c.s));
+  KP_CUDA_TRY(cudaMemsetAsync(gv + 2 * v0 * P.D, 0, sizeof(double) * 2 * (v1 - v0) * P.D, c.s));
   const TaylorDims tdi{P.S, P.d, true};
   const TaylorDims tdb{1, 0, false};
   const bool single = P.Nc >= P.N;  // else the interior states are recomputed per chunk
@@ -1336,7 +1347,7 @@ int phase_star_gvp(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, const 
                     c.at(P.o_r) + n0, nullptr);
       backward(c, st->theta, nc, tdi, bt->coeff_diag, bi, seeds);
     }
-    for (int v = 0; v < 2; ++v) {
+    for (int v = v0; v < v1; ++v) {
       prep(vecs[v]);
       jvp_pass(c, x, nc, tdi, bi, seeds, vecs[v], c.at(P.o_jv));
       for (int l = 0; l < P.L; ++l)
@@ -1344,7 +1355,7 @@ int phase_star_gvp(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, const 
     }
   }
   const StateBufs bb = boundary_bufs(c);
-  for (int v = 0; v < 2; ++v) {
+  for (int v = v0; v < v1; ++v) {
     prep(vecs[v]);
     jvp_pass(c, bt->x_bnd, P.Nb, tdb, bb, c.at(P.o_ones), vecs[v], c.at(P.o_jvb));
     for (int l = 0; l < P.L; ++l)
@@ -1352,6 +1363,10 @@ int phase_star_gvp(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, const 
                           gv + (2 * v + 1) * P.D, l);
   }
   return KP_OK;
+}
+
+int phase_star_gvp(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, const kp_batch* bt) {
+  return star_gvp_range(c, cfg, st, bt, 0, 2);
 }
 
 int phase_star_update(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp_step_out* out) {
@@ -1449,6 +1464,7 @@ int32_t kp_context_destroy(kp_context* c) {
     cudaDeviceSynchronize();
     cudaFree(c->warm_buf);
   }
+  if (c->warm_ev) cudaEventDestroy(c->warm_ev);
   if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
   if (c->cap_stream) {
     cudaStreamSynchronize(c->cap_stream);
@@ -1758,8 +1774,17 @@ int32_t kp_kfac_star_step(kp_context* ctx, const kp_problem* prob, const kp_kfac
   KP_TRY(rotated_batch(c, bt_in, bt_rot, bt));
   KP_CUDA_TRY(cudaMemsetAsync(out->status, 0, sizeof(int32_t), c.s));
   KP_TRY(phase_accumulate(c, cfg, st, bt));
+  // G prev needs no Delta: with early preconditioning (the large eigenproblems on side
+  // streams / host threads) and the states of a single pass still resident, it is issued
+  // before the preconditioner so that the GPU computes it while the solves run
+  static const bool ahead_on = [] {  // KP_STAR_AHEAD=0: Delta first (measurements)
+    const char* e = getenv("KP_STAR_AHEAD");
+    return !(e && atoi(e) == 0);
+  }();
+  const bool ahead = ahead_on && c.early && c.P.Nc >= c.P.N;
+  if (ahead) KP_TRY(star_gvp_range(c, cfg, st, bt, 1, 2));
   KP_TRY(phase_precondition(c, cfg, st, out, nullptr));
-  KP_TRY(phase_star_gvp(c, cfg, st, bt));
+  KP_TRY(star_gvp_range(c, cfg, st, bt, 0, ahead ? 1 : 2));
   KP_TRY(phase_star_update(c, cfg, st, out));
   KP_CUDA_TRY(cudaGetLastError());
   return KP_OK;
