@@ -188,9 +188,9 @@ static TnGrid tn_grid(int64_t R, int P, int Q, bool sym) {
 // X = Gbar_L, one column): acc[j] += sum_r x_r w_{r/Sw} y_{r,j} (+ y's bias column) is a
 // weighted column sum over the rows of Y, HBM-bound; the 64 x 64 DMMA tiles would compute
 // 63 wasted rows of every tile (c5: 9.3 ms for a 6.8 GB read).  Rows are split over about
-// four blocks per SM, one partial row per block, reduced by k_tn_reduce (fixed order).
+// eight blocks per SM, one partial row per block, reduced by k_tn_reduce (fixed order).
 constexpr int COL1_THREADS = 256, COL1_WIDE = 4, COL1_TINY = 8;
-constexpr int64_t COL1_TARGET_BLOCKS = 148 * 4;
+constexpr int64_t COL1_TARGET_BLOCKS = 148 * 8;
 
 static int64_t col1_splits(int64_t R) {
   return std::max<int64_t>(1, std::min<int64_t>(COL1_TARGET_BLOCKS, ceil_div(R, 4 * COL1_THREADS)));
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(COL1_THREADS) k_tn_col1_wide(GemmTN g, int Q, 
     __syncthreads();
     if (tid < nr) xs[tid] = col1_x(g, rb + tid);
     __syncthreads();
-#pragma unroll 4
+#pragma unroll 8
     for (int i = 0; i < nr; ++i) {
       const double xv = xs[i];
       const int64_t r = rb + i;
