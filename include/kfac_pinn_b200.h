@@ -38,7 +38,7 @@ extern "C" {
 #endif
 
 #define KP_MAX_LAYERS 16
-#define KP_ABI_VERSION 4
+#define KP_ABI_VERSION 5
 
 typedef enum kp_status {
   KP_OK = 0,
@@ -81,6 +81,11 @@ typedef struct kp_kfac_config {
   int32_t ls_max_exp;
   double n_interior_global;
   double n_boundary_global;
+  /* KFAC* only: the damping of the 2x2 quadratic model, OptimizerConfig.damping
+   * (src/optim.py:303), while the factor damping above is KfacState.damping
+   * (src/curvature.py:150-152).  Equal unless the caller edits one of them; <= 0: use
+   * damping. */
+  double model_damping;
 } kp_kfac_config;
 
 /* Persistent optimizer state (TrainState/KfacState, src/optim.py:81-92,

@@ -332,6 +332,9 @@ class OracleState:
     grid: list
     prev_update: list = field(default_factory=list)
     step: int = 0
+    # KFAC*'s quadratic-model damping is OptimizerConfig.damping (optim.py:303), the factor
+    # damping KfacState.damping (curvature.py:150-152); None: the same value
+    model_damping: float | None = None
 
 
 def init_state(weights, biases, ema=0.9, damping=1e-2, momentum=0.0, init_mode="identity",
@@ -467,7 +470,7 @@ def kfac_star_step(st: OracleState, batch, problem, record=None):
         return out + rb.T @ (rb @ v) / rb.shape[0]
 
     dv, pv, gv = _vec(delta), _vec(st.prev_update), _vec(ev.grad_mats)
-    lam = kf.damping
+    lam = kf.damping if st.model_damping is None else st.model_damping
     g_dv = gvp(dv)
     m11 = float(dv @ g_dv + lam * dv @ dv)
     rhs1 = float(dv @ gv)

@@ -13,7 +13,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libkfac_pinn_b200.so")
 MAX_LAYERS = 16
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 KP_OK = 0
 KP_ERR_INVALID = 1
@@ -37,7 +37,8 @@ class kp_problem(C.Structure):
 class kp_kfac_config(C.Structure):
     _fields_ = [("ema", C.c_double), ("damping", C.c_double), ("momentum", C.c_double),
                 ("ls_min_exp", C.c_int32), ("ls_max_exp", C.c_int32),
-                ("n_interior_global", C.c_double), ("n_boundary_global", C.c_double)]
+                ("n_interior_global", C.c_double), ("n_boundary_global", C.c_double),
+                ("model_damping", C.c_double)]
 
 
 class kp_state(C.Structure):

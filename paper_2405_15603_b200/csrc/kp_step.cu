@@ -1381,7 +1381,7 @@ int phase_star_update(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp_
   const double* g = c.at(P.o_grad);
   DotJobs dj{{d, d, d, p, d, d, p, p}, {c.at(P.o_gvd), d, g, p, c.at(P.o_gvp), p, c.at(P.o_gvp), g}};
   launch_dots(dj, 8, P.D, c.at(P.o_dots), c.s);
-  launch_star_solve_update(c.at(P.o_dots), cfg->damping, st->theta, st->prev_update, d, P.D,
+  launch_star_solve_update(c.at(P.o_dots), cfg->model_damping > 0.0 ? cfg->model_damping : cfg->damping, st->theta, st->prev_update, d, P.D,
                            out->scalars, out->status, c.s);
   return KP_OK;
 }

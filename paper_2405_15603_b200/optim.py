@@ -44,6 +44,10 @@ __all__ = [
 
 OPTIMIZER_KINDS = ("kfac", "kfac_star", "engd", "sgd", "adam")
 
+# The device engine class.  The only substitute is the CPU stand-in of the plug-in tests
+# (tests/cpu_step_engine.py), which checks the host-side state plumbing without a GPU.
+ENGINE_FACTORY = KfacEngine
+
 
 @dataclass
 class OptimizerConfig:
@@ -170,7 +174,7 @@ def _engine_for(state: TrainState, batch, widths) -> KfacEngine:
     # (re)build: carry the current host-visible optimizer state onto the device
     kf = state.kfac
     prev = state.prev_update
-    eng = KfacEngine(widths, ni, nb, ema=cfg.ema, damping=cfg.damping, momentum=cfg.momentum,
+    eng = ENGINE_FACTORY(widths, ni, nb, ema=cfg.ema, damping=cfg.damping, momentum=cfg.momentum,
                      ls_min_exp=cfg.line_search_min_exp, ls_max_exp=cfg.line_search_max_exp)
     eng.set_factor_lists(kf.a_interior, kf.b_interior, kf.a_boundary, kf.b_boundary)
     eng.set_prev_mats(prev)
@@ -196,7 +200,14 @@ def _sync_host_edits(state: TrainState, eng: KfacEngine):
             eng.set_prev_mats(state._prev_host)
 
 
-def _kfac_device_step(state: TrainState, batch, problem) -> StepInfo:
+def device_step(state: TrainState, batch, problem) -> tuple:
+    """One step on the device; returns (StepInfo, status code) without raising.
+
+    On success and on non-finite parameters (status 4) the state is updated the way the
+    reference's step mutates it before ``optimizer_step`` raises (src/optim.py:259-262,
+    396-402): new params, previous update and ``step += 1``.  The factors always carry the
+    step's EMA update (the reference updates them before the line search can fail,
+    src/optim.py:237-248)."""
     params = state.params
     widths = (params.weights[0].shape[1],) + tuple(w.shape[0] for w in params.weights)
     cdiag = coeff_matrix(problem.coeffs)
@@ -207,6 +218,7 @@ def _kfac_device_step(state: TrainState, batch, problem) -> StepInfo:
     if state._kfac_host is not None:
         eng.cfg.ema = float(state._kfac_host.ema)
         eng.cfg.damping = float(state._kfac_host.damping)
+        eng.cfg.model_damping = float(state.config.damping)  # KFAC* model (optim.py:303)
         if eng.cfg.damping <= 0:
             raise ValueError("damping must be positive for Kronecker preconditioning")
     eng.set_batch(x, r0, seeds, np.asarray(batch.boundary, dtype=np.float64),
@@ -216,23 +228,27 @@ def _kfac_device_step(state: TrainState, batch, problem) -> StepInfo:
     else:
         eng.launch_step()
     sc, code = eng.finish_step()
-    # mirror the device state back to the reference-visible fields
-    mats = eng.param_mats()
-    cls = type(params) if hasattr(type(params), "__dataclass_fields__") else network.Parameters
-    new_params = cls([m[:, :-1].copy() for m in mats], [m[:, -1].copy() for m in mats],
-                     getattr(params, "activation", "tanh"))
     if state._kfac_host is not None:
         state._kfac_host._stale = True
     state._prev_snapshot = None
-    from .engine import raise_for_status
-
     if code == 0 or code == 4:  # ok, or non-finite params (params were replaced first)
+        # mirror the device state back to the reference-visible fields
+        mats = eng.param_mats()
+        cls = type(params) if hasattr(type(params), "__dataclass_fields__") else network.Parameters
+        new_params = cls([m[:, :-1].copy() for m in mats], [m[:, -1].copy() for m in mats],
+                         getattr(params, "activation", "tanh"))
         state.params = new_params
         state._params_seen = new_params
-    if code == 0:
         state.step += 1
+    return StepInfo(float(sc[2]), float(sc[3]), float(sc[0]), float(sc[1])), code
+
+
+def _kfac_device_step(state: TrainState, batch, problem) -> StepInfo:
+    from .engine import raise_for_status
+
+    info, code = device_step(state, batch, problem)
     raise_for_status(code, "optimizer_step")
-    return StepInfo(float(sc[2]), float(sc[3]), float(sc[0]), float(sc[1]))
+    return info
 
 
 def optimizer_step(state: TrainState, batch, problem) -> StepInfo:

@@ -47,7 +47,7 @@ def test_ctypes_struct_layout_matches_header():
     assert C.sizeof(_capi.kp_net) == 4 * 18
     assert _capi.kp_problem.n_interior.offset == 72
     assert C.sizeof(_capi.kp_problem) == 104
-    assert C.sizeof(_capi.kp_kfac_config) == 48
+    assert C.sizeof(_capi.kp_kfac_config) == 56
     assert C.sizeof(_capi.kp_step_out) == 5 * 8
 
 
