@@ -9,14 +9,20 @@ accumulation, the damped Kronecker-sum preconditioner, momentum, the 31-point
 grid line search (31 more forward passes) and the update.  Metric: interior
 collocation points processed per second (N_Omega x KFAC steps/s), whole job.
 
-Multi-GPU (torchrun, one process per GPU, NCCL): weak scaling — every rank owns
-``--n-interior`` interior and ``--n-interior // 3`` boundary points of one global
-batch; factor sums / gradient and line-search losses are all-reduced.
+Multi-GPU (one process per GPU, NCCL): ``--gpus N`` outside torchrun re-executes itself
+under ``torch.distributed.run --nproc-per-node N``.  N > 1 defaults to strong scaling:
+one global batch of ``--n-total`` (default 65536, the top of the BASELINE c5 sweep)
+interior and ``--n-total // 3`` boundary points split contiguously across the ranks;
+``--scaling weak`` gives every rank ``--n-interior`` points instead.  Factor sums /
+gradient and line-search losses are all-reduced; the per-layer Kronecker solves are
+distributed across ranks.
 
 Printed JSON also carries: ``roofline`` for the dominant kernel (the FP64 DMMA
 forward GEMM, k_gemm_nt) measured with CUDA events inside the timed region;
-``cpu_baseline`` (the CPU oracle restating the reference, bounded sample on
-this host); ``e2e`` (the public optimizer_step API with host numpy buffers,
+``roofline_hbm`` for the HBM-bound activation adjoint (k_act_bwd), also timed with
+CUDA events in the timed region; ``cpu_baseline`` (the CPU oracle restating the
+reference, timed on this host at two bounded sample sizes and extrapolated to the
+arm's N with a fixed + per-point cost fit); ``e2e`` (the public optimizer_step API with host numpy buffers,
 H2D of the batch and D2H of parameters + StepInfo inside the timed region);
 ``clocks`` sampled by nvidia-smi during the timed region; ``gpu_launches``.
 """
@@ -36,8 +42,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FP64_DMMA_PEAK_TFLOPS = 37.1  # measured, profiles/r01_fp64_peaks.txt (register-only DMMA, 1965 MHz)
-CPU_SAMPLE_POINTS = 128       # interior points per CPU-oracle step (bounded sample, ~10 s on the box;
-                              # the per-point rate is within 1% of a 192-point step)
+HBM_COPY_PEAK_GBS = 6552.6    # measured copy bandwidth (profiles/r01_fp64_peaks.txt) when
+                              # MEASURED_PEAKS.json is absent
+CPU_SAMPLE_POINTS = 128       # mean interior points per CPU-oracle step: the steps alternate
+                              # between 64 and 192 points (bounded samples, ~5 / ~15 s on the box)
+STRONG_N_TOTAL = 65536        # BASELINE c5's largest sweep point (global batch for N > 1)
 
 
 def parse():
@@ -49,7 +58,12 @@ def parse():
     ap.add_argument("--workload", default="c5")
     ap.add_argument("--optimizer", choices=("kfac", "kfac_star"), default="kfac",
                     help="kfac (the BASELINE metric) or kfac_star (src/optim.py:266-320)")
-    ap.add_argument("--n-interior", type=int, default=16384, help="interior points per GPU")
+    ap.add_argument("--n-interior", type=int, default=16384,
+                    help="interior points per GPU (N = 1, and every N under --scaling weak)")
+    ap.add_argument("--n-total", type=int, default=STRONG_N_TOTAL,
+                    help="global interior points under --scaling strong (N > 1)")
+    ap.add_argument("--scaling", choices=("weak", "strong"), default=None,
+                    help="N > 1: strong (default, fixed --n-total) or weak (--n-interior per GPU)")
     ap.add_argument("--n-boundary", type=int, default=None, help="boundary points per GPU")
     ap.add_argument("--chunk", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
@@ -132,11 +146,32 @@ def blas_threads():
     return max([d["num_threads"] for d in threadpool_info() if d["user_api"] == "blas"] or [1])
 
 
-def cpu_reference_step_time(wl, n_points, n_bnd, optimizer="kfac"):
-    """Time one oracle KFAC step (the reference algorithm, NumPy/OpenBLAS) on this host with
-    every host core; returns (seconds, BLAS threads used)."""
+def cpu_sizes(args):
+    """The two bounded CPU sample sizes (interior points): mean = --cpu-points."""
+    n1 = max(2, args.cpu_points // 2)
+    return n1, max(n1 + 1, (3 * args.cpu_points) // 2)
+
+
+def fit_fixed_per_point(samples):
+    """Least-squares t(n) = fixed + per_point * n over (n, seconds) samples.  The step is
+    linear in N except for the N-independent Kronecker solves."""
+    n = np.array([s[0] for s in samples], dtype=np.float64)
+    t = np.array([s[1] for s in samples], dtype=np.float64)
+    if np.ptp(n) == 0:
+        return 0.0, float(t.mean() / n.mean())
+    b = float(np.sum((n - n.mean()) * (t - t.mean())) / np.sum((n - n.mean()) ** 2))
+    a = float(t.mean() - b * n.mean())
+    if a < 0 or b <= 0:  # noisy samples: fall back to a pure per-point rate
+        return 0.0, float(t.sum() / n.sum())
+    return a, b
+
+
+def cpu_reference_fit(wl, sizes, optimizer="kfac"):
+    """One oracle step (the reference algorithm, NumPy/OpenBLAS, every host core) at each
+    sample size; returns ([(n, seconds)], BLAS threads used)."""
     with all_host_blas_threads():
-        return _cpu_reference_step_time(wl, n_points, n_bnd, optimizer), blas_threads()
+        return [(n, _cpu_reference_step_time(wl, n, max(1, n // 3), optimizer)) for n in sizes], \
+            blas_threads()
 
 
 def _cpu_reference_step_time(wl, n_points, n_bnd, optimizer):
@@ -157,6 +192,26 @@ def _cpu_reference_step_time(wl, n_points, n_bnd, optimizer):
     return time.perf_counter() - t0
 
 
+def cpu_line(samples, cores, n_arm, nb_arm, wl, optimizer, what):
+    """cpu_baseline object: the fit extrapolated to the GPU arm's interior batch."""
+    a, b = fit_fixed_per_point(samples)
+    t_arm = a + b * n_arm
+    ref_lines = "266-320" if optimizer == "kfac_star" else "251-263"
+    desc = ", ".join(f"{n} pts: {t:.2f} s" for n, t in samples)
+    return {"value": n_arm / t_arm, "unit": "interior collocation points/s", "cores": cores,
+            "kind": "port", "extrapolated": True, "same_config": True,
+            "n_interior": n_arm, "n_boundary": nb_arm,
+            "fit": {"fixed_s": a, "per_point_s": b, "step_s_at_n": t_arm},
+            "samples": [{"n_interior": n, "n_boundary": max(1, n // 3), "s_per_step": t}
+                        for n, t in samples],
+            "sample": f"{what} oracle {optimizer}_step (NumPy/OpenBLAS restatement of reference "
+                      f"src/optim.py:{ref_lines}) on {wl.name} at bounded sample sizes ({desc}); "
+                      f"t(N) = fixed + per_point * N fitted over the samples and evaluated at "
+                      f"the GPU arm's N = {n_arm} interior / {nb_arm} boundary points "
+                      f"(extrapolated: the reference step is linear in N apart from the "
+                      f"N-independent Kronecker solves)"}
+
+
 def host_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -164,49 +219,70 @@ def host_cores():
         return os.cpu_count() or 1
 
 
+def resolve_scaling(args, world):
+    return args.scaling or ("strong" if world > 1 else "weak")
+
+
+def job_points(args, world):
+    """(interior, boundary) points of the whole job and the scaling mode."""
+    scaling = resolve_scaling(args, world)
+    n = args.n_total if scaling == "strong" else args.n_interior * world
+    if args.n_boundary is not None:
+        nb = args.n_boundary * (world if scaling == "weak" else 1)
+    else:
+        nb = max(1, n // 3)
+    return n, nb, scaling
+
+
 def run_reference(args):
-    """--impl reference: the reference KFAC step (restated CPU oracle) on host cores."""
+    """--impl reference: the reference KFAC step (restated CPU oracle) on host cores.
+
+    Steps alternate between two bounded sample sizes of the arm's workload; the per-step
+    times are fitted as fixed + per-point cost and evaluated at the GPU arm's N (value =
+    that N / the fitted step time).  Under torchrun only rank 0 runs and prints."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     from paper_2405_15603_b200 import configs
-
-    wl = configs.WORKLOADS[args.workload]
-    n_s = args.cpu_points
-    nb_s = max(1, n_s // 3)
-    prob, params, batch = wl.build(0, n_s, nb_s)
     from oracle import kfac_oracle as orc
 
+    wl = configs.WORKLOADS[args.workload]
     step = oracle_step_fn(args.optimizer)
-    ref_lines = "266-320" if args.optimizer == "kfac_star" else "251-263"
-
-    st = orc.init_state(params.weights, params.biases, ema=wl.ema, damping=wl.damping,
-                        momentum=wl.momentum)
+    n_arm, nb_arm, scaling = job_points(args, max(world, args.gpus))
+    runs = []
+    for n_s in cpu_sizes(args):
+        prob, params, batch = wl.build(0, n_s, max(1, n_s // 3))
+        st = orc.init_state(params.weights, params.biases, ema=wl.ema, damping=wl.damping,
+                            momentum=wl.momentum)
+        runs.append((n_s, st, batch, prob))
+    samples = []
     with all_host_blas_threads():
         cores = blas_threads()
-        for _ in range(args.warmup):
+        for k in range(max(args.warmup, 0)):
+            n_s, st, batch, prob = runs[k % 2]
             step(st, batch, prob)
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
+        for k in range(max(args.steps, 2)):  # at least one step per sample size
+            n_s, st, batch, prob = runs[k % 2]
+            t0 = time.perf_counter()
             step(st, batch, prob)
-        dt = (time.perf_counter() - t0) / max(args.steps, 1)
-    value = n_s / dt
-    n_int_full = args.n_interior * args.gpus
+            samples.append((n_s, time.perf_counter() - t0))
+    per_size = [(n, float(np.median([t for m, t in samples if m == n]))) for n in cpu_sizes(args)]
+    cpu = cpu_line(samples, cores, n_arm, nb_arm, wl, args.optimizer,
+                   f"{len(samples)} timed steps (alternating sizes) of the")
+    cpu["samples"] = [{"n_interior": n, "n_boundary": max(1, n // 3), "s_per_step": t}
+                      for n, t in per_size]
+    value = cpu["value"]
     line = {
         "impl": "reference", "metric": "collocation_pts_per_s", "value": value,
         "unit": "interior collocation points/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "warmup": args.warmup, "ms_per_step": cpu["fit"]["step_s_at_n"] * 1e3,
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference seeding recipe, SURVEY.md §8d)",
         "config": {"workload": wl.name, "optimizer": args.optimizer, "widths": list(wl.widths),
-                   "n_interior_per_step": n_s, "n_boundary_per_step": nb_s,
-                   "arm_n_interior_total": n_int_full},
-        "cpu_baseline": {"value": value, "unit": "interior collocation points/s", "cores": cores,
-                         "kind": "port",
-                         "sample": f"oracle/kfac_oracle.py {step.__name__} (NumPy/OpenBLAS restatement of "
-                                   f"the reference src/optim.py:{ref_lines}) on {n_s} interior + {nb_s} boundary "
-                                   f"points of {wl.name}; per-point work is N-linear except the "
-                                   f"N-independent Kronecker solve"},
+                   "n_interior_total": n_arm, "n_boundary_total": nb_arm,
+                   "parallelism": f"dp{args.gpus}"},
+        "extrapolated": True,
+        "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": "interior collocation points/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -245,9 +321,7 @@ def run_ours(args):
         else:
             dist.init_process_group(backend)
     wl = configs.WORKLOADS[args.workload]
-    n_loc = args.n_interior
-    nb_loc = args.n_boundary if args.n_boundary is not None else max(1, n_loc // 3)
-    n_glob, nb_glob = n_loc * world, nb_loc * world
+    n_glob, nb_glob, scaling = job_points(args, world)
     prob, params, batch = wl.build(0, n_glob, nb_glob)
 
     def barrier():
@@ -291,20 +365,31 @@ def run_ours(args):
     barrier()
     ms_total = e0.elapsed_time(e1)
     gemm_ms, gemm_flops, gemm_launches, k1 = eng.profile_read()
+    hbm_ms, hbm_bytes, hbm_launches = eng.profile_read_hbm()
     eng.profile(False)
+    n_loc, nb_loc = eng.n_interior, eng.n_boundary
     clk = clocks.stop()
     launches = (k1 - k0) // max(args.steps, 1)
     chunk = int(eng.prob.chunk)
 
-    t = torch.tensor([ms_total, gemm_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([ms_total, gemm_ms, hbm_ms], dtype=torch.float64, device=dev)
     if sharded:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total, gemm_ms_max = float(t[0]), float(t[1])
     ms_step = ms_total / args.steps
     steps_per_s = 1e3 / ms_step
     value = n_glob * steps_per_s
-    f_step = configs.flops_per_step(wl.widths, n_loc, nb_loc, optimizer=args.optimizer) * world
+    f_step = configs.flops_per_step(wl.widths, n_glob, nb_glob, optimizer=args.optimizer)
     achieved_tflops = gemm_flops / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
+    hbm_peak, hbm_peak_src = HBM_COPY_PEAK_GBS, "measured copy bandwidth, profiles/r01_fp64_peaks.txt"
+    mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(mp):
+        try:
+            hbm_peak = float(json.load(open(mp))["hbm_gbs"])
+            hbm_peak_src = "MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth)"
+        except (OSError, ValueError, KeyError):
+            pass
+    hbm_gbs = hbm_bytes / (hbm_ms / 1e3) / 1e9 if hbm_ms > 0 else None
 
     # end to end through the public API (host numpy in, host numpy out), 1 GPU
     e2e = None
@@ -319,14 +404,8 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        n_s = args.cpu_points
-        dt, cores = cpu_reference_step_time(wl, n_s, max(1, n_s // 3), args.optimizer)
-        cpu = {"value": n_s / dt, "unit": "interior collocation points/s", "cores": cores,
-               "kind": "port",
-               "sample": f"one oracle {args.optimizer}_step (NumPy/OpenBLAS restatement of "
-                         f"reference src/optim.py:"
-                         f"{'266-320' if args.optimizer == 'kfac_star' else '251-263'}) on {n_s} interior + {n_s // 3} boundary points of "
-                         f"{wl.name}, {dt:.2f} s"}
+        samples, cores = cpu_reference_fit(wl, cpu_sizes(args), args.optimizer)
+        cpu = cpu_line(samples, cores, n_glob, nb_glob, wl, args.optimizer, "one")
 
     traffic, traffic_note = None, None
     tp = os.path.join(ROOT, "profiles", "gemm_act_traffic.json")
@@ -337,7 +416,10 @@ def run_ours(args):
             if tj.get("n_interior") == args.n_interior and tj.get("workload") == wl.name:
                 traffic = tj.get("dram_bytes_per_launch")
                 traffic_note = {"launch": tj.get("kernel"),
-                                "algorithmic_bytes_per_launch": tj.get("algorithmic_bytes_per_launch")}
+                                "algorithmic_bytes_per_launch": tj.get("algorithmic_bytes_per_launch"),
+                                "source": "stored ncu --set full capture of the same launch "
+                                          "(profiles/gemm_act_traffic.json), not measured in "
+                                          "this run"}
         except (OSError, ValueError):
             traffic = None
 
@@ -346,7 +428,7 @@ def run_ours(args):
             "metric": "collocation_pts_per_s", "value": value,
             "unit": "interior collocation points/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference seeding recipe, SURVEY.md §8d)",
             "config": {"workload": wl.name, "optimizer": args.optimizer,
                        "widths": list(wl.widths), "n_interior_per_gpu": n_loc,
@@ -365,6 +447,15 @@ def run_ours(args):
                          "share_of_step": gemm_ms / ms_total if ms_total else None,
                          "peak_source": "measured DMMA issue peak, profiles/r01_fp64_peaks.txt "
                                         "(MEASURED_PEAKS.json has no FP64 entry; cuBLAS DGEMM 35.4)"},
+            "roofline_hbm": {"bound": "hbm", "kernel": "k_act_bwd (activation adjoint, src/taylor.py:206-239)",
+                             "achieved": hbm_gbs, "peak": hbm_peak, "unit": "GB/s",
+                             "frac": (hbm_gbs / hbm_peak) if hbm_gbs else None,
+                             "frac_of_8tbs": (hbm_gbs / 8000.0) if hbm_gbs else None,
+                             "traffic": None, "launches_per_step": hbm_launches // max(args.steps, 1),
+                             "share_of_step": hbm_ms / ms_total if ms_total else None,
+                             "peak_source": hbm_peak_src,
+                             "bytes": "algorithmic: stored pre-activation state + incoming "
+                                      "adjoint + outgoing adjoint, 8 B each per (point, row, unit)"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
@@ -435,12 +526,31 @@ def run_e2e_sharded(args, wl, prob, params, batch, rank, world, eng, stepper):
             "ms_per_step": float(dt[0]) * 1e3, "api": "dist.ShardedKfacStep + host shard upload"}
 
 
+def reexec_under_torchrun(n):
+    """``--gpus N`` (N > 1) outside torchrun: one process per GPU through torch.distributed.run."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_ours(args)
+        return
+    under_torchrun = "RANK" in os.environ and "WORLD_SIZE" in os.environ
+    if args.gpus > 1 and not under_torchrun:
+        reexec_under_torchrun(args.gpus)
+    if under_torchrun and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}")
+    run_ours(args)
 
 
 if __name__ == "__main__":

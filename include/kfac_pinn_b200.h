@@ -140,6 +140,9 @@ int32_t kp_context_destroy(kp_context* ctx);
 int32_t kp_profile_enable(kp_context* ctx, int32_t enable);
 int32_t kp_profile_read(kp_context* ctx, double* gemm_ms, double* gemm_flops, int64_t* launches,
                         int64_t* kernel_launches);
+/* The same for the HBM-bound activation adjoint (k_act_bwd, src/taylor.py:206-239): summed
+ * CUDA-event time, algorithmic DRAM bytes and launches since kp_profile_enable. */
+int32_t kp_profile_read_hbm(kp_context* ctx, double* ms, double* bytes, int64_t* launches);
 
 /* Sizes. */
 int64_t kp_param_count(const kp_net* net);              /* D */

@@ -53,6 +53,11 @@ struct kp_context {
   size_t ev_used = 0;
   double prof_flops = 0.0;
   int64_t prof_launches = 0;
+  // the same for the HBM-bound activation adjoint (k_act_bwd): event pairs + algorithmic bytes
+  std::vector<cudaEvent_t> ev_hbm;
+  size_t ev_hbm_used = 0;
+  double prof_hbm_bytes = 0.0;
+  int64_t prof_hbm_launches = 0;
   // side streams for the per-layer Kronecker-sum solves (2 per layer: A and B factor pairs)
   std::vector<cudaStream_t> side;
   std::vector<cusolverDnHandle_t> side_solver;
@@ -450,6 +455,39 @@ void prof_launch(const Ctx& c, double flops, F&& launch) {
   ctx->prof_launches += 1;
 }
 
+// Optional CUDA-event timing of the HBM-bound activation adjoint; ``bytes`` = algorithmic
+// DRAM bytes of the launch (every operand read once, the output written once).
+template <typename F>
+void prof_hbm_launch(const Ctx& c, double bytes, F&& launch) {
+  kp_context* ctx = c.ctx;
+  if (!ctx->profile) {
+    launch();
+    return;
+  }
+  if (ctx->ev_hbm_used + 2 > ctx->ev_hbm.size()) {
+    for (int k = 0; k < 64; ++k) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ctx->ev_hbm.push_back(e);
+    }
+  }
+  cudaEventRecord(ctx->ev_hbm[ctx->ev_hbm_used], c.s);
+  launch();
+  cudaEventRecord(ctx->ev_hbm[ctx->ev_hbm_used + 1], c.s);
+  ctx->ev_hbm_used += 2;
+  ctx->prof_hbm_bytes += bytes;
+  ctx->prof_hbm_launches += 1;
+}
+
+// Algorithmic bytes of one k_act_bwd launch per (sample, unit): the stored pre-activation
+// state (S rows, or the one value row of layer 0), the incoming adjoint (S rows, or the
+// per-sample rank-1 seed, negligible) and the outgoing adjoint (S rows).
+double act_bwd_bytes(const ActBwd& a, int64_t n, int h, const TaylorDims& td) {
+  const double S = td.S;
+  const double per = 8.0 * ((a.pre ? S : 1.0) + (a.gin ? S : 0.0) + S);
+  return per * (double)n * h;
+}
+
 void prof_gemm(const Ctx& c, const GemmNT& g) {
   prof_launch(c, 2.0 * (double)g.M * g.N * g.K, [&] { launch_gemm_nt(g, c.s); });
 }
@@ -656,7 +694,8 @@ void backward(const Ctx& c, const double* theta, int64_t n, const TaylorDims& td
     a.seeds = seeds;
     a.wlast = theta + P.th[L - 1];
     a.gout = b.gout[L - 2];
-    launch_act_bwd(a, n, P.h[L - 1], td, cdiag, c.s);
+    prof_hbm_launch(c, act_bwd_bytes(a, n, P.h[L - 1], td),
+                    [&] { launch_act_bwd(a, n, P.h[L - 1], td, cdiag, c.s); });
   }
   for (int l = L - 2; l >= 1; --l) {
     GemmNT g{b.gout[l], P.h[l + 1], c.at(P.o_wT[l]), P.h[l + 1], b.ping, P.h[l],
@@ -668,7 +707,8 @@ void backward(const Ctx& c, const double* theta, int64_t n, const TaylorDims& td
     a.w0t = c.at(P.o_w0t);
     a.gin = b.ping;
     a.gout = b.gout[l - 1];
-    launch_act_bwd(a, n, P.h[l], td, cdiag, c.s);
+    prof_hbm_launch(c, act_bwd_bytes(a, n, P.h[l], td),
+                    [&] { launch_act_bwd(a, n, P.h[l], td, cdiag, c.s); });
   }
 }
 
@@ -1494,6 +1534,27 @@ int32_t kp_profile_enable(kp_context* c, int32_t enable) {
   c->ev_used = 0;
   c->prof_flops = 0.0;
   c->prof_launches = 0;
+  c->ev_hbm_used = 0;
+  c->prof_hbm_bytes = 0.0;
+  c->prof_hbm_launches = 0;
+  return KP_OK;
+}
+
+int32_t kp_profile_read_hbm(kp_context* c, double* ms_out, double* bytes, int64_t* launches) {
+  if (!c) return KP_ERR_INVALID;
+  double ms = 0.0;
+  for (size_t k = 0; k + 1 < c->ev_hbm_used; k += 2) {
+    KP_CUDA_TRY(cudaEventSynchronize(c->ev_hbm[k + 1]));
+    float t = 0.f;
+    KP_CUDA_TRY(cudaEventElapsedTime(&t, c->ev_hbm[k], c->ev_hbm[k + 1]));
+    ms += t;
+  }
+  if (ms_out) *ms_out = ms;
+  if (bytes) *bytes = c->prof_hbm_bytes;
+  if (launches) *launches = c->prof_hbm_launches;
+  c->ev_hbm_used = 0;
+  c->prof_hbm_bytes = 0.0;
+  c->prof_hbm_launches = 0;
   return KP_OK;
 }
 

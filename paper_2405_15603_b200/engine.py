@@ -388,6 +388,12 @@ class KfacEngine:
                                                   C.byref(k)))
         return ms.value, fl.value, n.value, k.value
 
+    def profile_read_hbm(self):
+        """(ms, algorithmic bytes, launches) of the activation-adjoint kernel since enable."""
+        ms, by, n = C.c_double(), C.c_double(), C.c_int64()
+        raise_for_status(self.lib.kp_profile_read_hbm(self.ctx, C.byref(ms), C.byref(by), C.byref(n)))
+        return ms.value, by.value, n.value
+
     def close(self):
         if getattr(self, "ctx", None) is not None and self.ctx.value:
             self.stream.synchronize()

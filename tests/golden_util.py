@@ -10,6 +10,12 @@ STAR_NAMES = ("c1_star", "c3_star", "c5_star", "lfp_star", "dense_star")
 # ten-step runs of the five BASELINE configs (arrays recorded at steps 1 and 10)
 NAMES10 = ("c1_10", "c2_10", "c3_10", "c4_10", "c5_10", "lfp_10", "dense_10", "c1_momentum_10", "c4_zero_10")
 STAR10 = ("c1_star_10", "lfp_star_10", "c3_star_10", "c5_star_10")
+# the BASELINE sizes themselves (tests/golden/make_golden_full.py): c2-c4 at N_Omega = 3000,
+# ten steps; c5 at 3000 / 1000, three steps (the benched code path); c5 KFAC* at 1000 / 333
+NAMES_FULL = ("c2_full10", "c3_full10", "c4_full10", "c5_full3")
+STAR_FULL = ("c5_star_n1000",)
+FULL_WL = {"c2_full10": "c2", "c3_full10": "c3", "c4_full10": "c4", "c5_full3": "c5",
+           "c5_star_n1000": "c5"}
 
 
 def load(name):

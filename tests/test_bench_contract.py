@@ -48,3 +48,29 @@ def test_reference_arm_under_torchrun_prints_once():
     assert len(lines) == 1 and lines[0]["n_gpus"] == 2
     # torchrun exports OMP_NUM_THREADS=1; the reference arm still uses every host core
     assert lines[0]["cpu_baseline"]["cores"] == len(os.sched_getaffinity(0))
+
+
+def test_reference_arm_describes_the_gpu_arms_batch():
+    """The reference arm times bounded samples and reports the fitted step time at the GPU
+    arm's own N (BASELINE c5: 16384 on one GPU, 65536 global under strong scaling)."""
+    for extra, n in (([], 16384), (["--gpus", "4"], 65536), (["--gpus", "2", "--scaling", "weak"], 32768)):
+        r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", *TINY, *extra],
+                           cwd=ROOT, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        ln = _json_lines(r.stdout)[0]
+        cb = ln["cpu_baseline"]
+        assert ln["extrapolated"] and cb["extrapolated"] and cb["same_config"]
+        assert ln["config"]["n_interior_total"] == n == cb["n_interior"]
+        assert [s["n_interior"] for s in cb["samples"]] == [4, 12]
+        assert abs(ln["value"] - n / (cb["fit"]["fixed_s"] + cb["fit"]["per_point_s"] * n)) <= 1e-9 * ln["value"]
+
+
+def test_fixed_plus_per_point_fit():
+    sys.path.insert(0, ROOT)
+    import bench
+
+    a, b = bench.fit_fixed_per_point([(64, 1.0 + 64 * 0.01), (192, 1.0 + 192 * 0.01),
+                                      (64, 1.0 + 64 * 0.01)])
+    assert abs(a - 1.0) < 1e-12 and abs(b - 0.01) < 1e-14
+    a, b = bench.fit_fixed_per_point([(64, 2.0), (192, 1.0)])  # noisy: pure per-point rate
+    assert a == 0.0 and abs(b - 3.0 / 256) < 1e-15

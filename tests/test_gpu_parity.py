@@ -8,7 +8,7 @@ per array.
 import numpy as np
 import pytest
 
-from golden_util import (NAMES, NAMES10, STAR10, STAR_NAMES, compare, has, line_search_rel, load,
+from golden_util import (FULL_WL, NAMES, NAMES10, NAMES_FULL, STAR10, STAR_FULL, STAR_NAMES, compare, has, line_search_rel, load,
                          pack_factors)
 
 torch = pytest.importorskip("torch")
@@ -25,7 +25,8 @@ WL_OF = {"c1": "c1", "c2": "c2", "c3": "c3", "c4": "c4", "c5": "c5", "c1_momentu
          "dense": "dense", "dense_star": "dense",
          "c1_10": "c1", "c2_10": "c2", "c3_10": "c3", "c4_10": "c4", "c5_10": "c5",
          "lfp_10": "lfp", "dense_10": "dense", "c1_star_10": "c1", "lfp_star_10": "lfp",
-         "c3_star_10": "c3", "c5_star_10": "c5", "c1_momentum_10": "c1", "c4_zero_10": "c4"}
+         "c3_star_10": "c3", "c5_star_10": "c5", "c1_momentum_10": "c1", "c4_zero_10": "c4",
+         **FULL_WL}
 
 
 def _theta_colstack(params):
@@ -43,7 +44,7 @@ def _device_mats_to_vec(vec, widths):
     return np.concatenate(out)
 
 
-@pytest.mark.parametrize("name", NAMES + NAMES10)
+@pytest.mark.parametrize("name", NAMES + NAMES10 + NAMES_FULL)
 def test_kfac_steps_match_reference_golden(name):
     g = load(name)
     wl = cfgs.WORKLOADS[WL_OF[name]]
@@ -77,7 +78,7 @@ def test_kfac_steps_match_reference_golden(name):
                           ("a_boundary", kf.a_boundary), ("b_boundary", kf.b_boundary)):
             assert compare(g, p + key, pack_factors(mats), tol) <= tol, key
         t += 1
-    assert t > (10 if name in NAMES10 else 1)
+    assert t > (10 if name in NAMES10 or name.endswith("full10") else 3 if name in NAMES_FULL else 1)
 
 
 def _oracle_vs_device(widths, problem, n_int, n_bnd, steps, momentum=0.0, ema=0.95, damping=1e-3,
@@ -292,7 +293,7 @@ def test_unsupported_residual_rejected():
         optimizer_step(state, batch, prob)
 
 
-@pytest.mark.parametrize("name", STAR_NAMES + STAR10)
+@pytest.mark.parametrize("name", STAR_NAMES + STAR10 + STAR_FULL)
 def test_kfac_star_steps_match_reference_golden(name):
     """KFAC* on the device (kp_kfac_star_step): exact Gramian-vector products via JVP +
     weighted reverse contraction vs the reference's Jacobian-row route."""

@@ -9,7 +9,7 @@ reference's seeded parameters and batches bit-for-bit.
 import numpy as np
 import pytest
 
-from golden_util import (NAMES, NAMES10, STAR10, STAR_NAMES, compare, has, line_search_rel, load,
+from golden_util import (FULL_WL, NAMES, NAMES10, NAMES_FULL, STAR10, STAR_FULL, STAR_NAMES, compare, has, line_search_rel, load,
                          pack_factors)
 from oracle import kfac_oracle as orc
 from paper_2405_15603_b200 import configs as cfgs
@@ -20,7 +20,8 @@ WL_OF = {"c1": "c1", "c2": "c2", "c3": "c3", "c4": "c4", "c5": "c5", "c1_momentu
          "dense": "dense", "dense_star": "dense",
          "c1_10": "c1", "c2_10": "c2", "c3_10": "c3", "c4_10": "c4", "c5_10": "c5",
          "lfp_10": "lfp", "dense_10": "dense", "c1_star_10": "c1", "lfp_star_10": "lfp",
-         "c3_star_10": "c3", "c5_star_10": "c5", "c1_momentum_10": "c1", "c4_zero_10": "c4"}
+         "c3_star_10": "c3", "c5_star_10": "c5", "c1_momentum_10": "c1", "c4_zero_10": "c4",
+         **FULL_WL}
 
 
 def build(name):
@@ -30,7 +31,7 @@ def build(name):
     return g, wl, prob, params, batch
 
 
-@pytest.mark.parametrize("name", NAMES + STAR_NAMES + NAMES10 + STAR10)
+@pytest.mark.parametrize("name", NAMES + STAR_NAMES + NAMES10 + STAR10 + NAMES_FULL + STAR_FULL)
 def test_inputs_bit_identical_to_reference(name):
     g, wl, prob, params, batch = build(name)
     assert compare(g, "in/interior", batch.interior, 0) == 0.0
@@ -119,7 +120,7 @@ def test_oracle_matches_reference_kfac_star(name):
     assert t > 1
 
 
-@pytest.mark.parametrize("name", NAMES + NAMES10)
+@pytest.mark.parametrize("name", NAMES + NAMES10 + NAMES_FULL)
 def test_line_search_gap_dwarfs_parity_tolerance(name):
     """exact α equality is a sound assertion only if the best and second-best
     line-search losses of the reference are separated far beyond the parity tolerance.  Every

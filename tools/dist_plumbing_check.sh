@@ -1,7 +1,7 @@
 set -x
 export KP_BENCH_DIST_BACKEND=gloo
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 2 --warmup 3 --n-interior 2048 --n-boundary 600 --no-cpu > gpurun_out/dp2.log 2>&1; echo rc=$?
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29512 bench.py --gpus 4 --steps 2 --warmup 3 --n-interior 1024 --n-boundary 300 --no-cpu --optimizer kfac_star > gpurun_out/dp4s.log 2>&1; echo rc=$?
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --scaling weak --steps 2 --warmup 3 --n-interior 2048 --n-boundary 600 --no-cpu > gpurun_out/dp2.log 2>&1; echo rc=$?
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29512 bench.py --gpus 4 --scaling weak --steps 2 --warmup 3 --n-interior 1024 --n-boundary 300 --no-cpu --optimizer kfac_star > gpurun_out/dp4s.log 2>&1; echo rc=$?
 unset KP_BENCH_DIST_BACKEND
 timeout 600 python bench.py --steps 2 --warmup 3 --n-interior 4096 --n-boundary 1200 --no-cpu > gpurun_out/dp1.log 2>&1; echo rc=$?
 timeout 600 python bench.py --steps 2 --warmup 3 --n-interior 4096 --n-boundary 1200 --no-cpu --optimizer kfac_star > gpurun_out/dp1s.log 2>&1; echo rc=$?
