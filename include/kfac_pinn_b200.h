@@ -46,7 +46,7 @@ typedef enum kp_status {
   KP_ERR_NOT_PSD = 2,       /* NotPositiveSemidefiniteError (src/linalg.py:39-44,79-83,128-132) */
   KP_ERR_LINE_SEARCH = 3,   /* LineSearchError (src/optim.py:37-38,209-210) */
   KP_ERR_NONFINITE = 4,     /* FloatingPointError (src/optim.py:398-401) */
-  KP_ERR_CUDA = 5,          /* CUDA / cuSOLVER / cuBLAS failure */
+  KP_ERR_CUDA = 5,          /* CUDA failure */
   KP_ERR_EIG = 6,           /* numpy.linalg.LinAlgError: eigensolver did not converge */
   KP_ERR_WORKSPACE = 7      /* workspace too small */
 } kp_status;
@@ -143,6 +143,12 @@ int32_t kp_profile_read(kp_context* ctx, double* gemm_ms, double* gemm_flops, in
 /* The same for the HBM-bound activation adjoint (k_act_bwd, src/taylor.py:206-239): summed
  * CUDA-event time, algorithmic DRAM bytes and launches since kp_profile_enable. */
 int32_t kp_profile_read_hbm(kp_context* ctx, double* ms, double* bytes, int64_t* launches);
+/* Diagnostics: the most Jacobi sweeps any solve of each device eigensolver route used in this
+ * process since the last reset (small: one CTA, mid: cluster shared memory, large:
+ * L2-resident cluster); 1000 + s marks a solve that did not converge in s sweeps.  Call after
+ * the stream has completed; reset != 0 zeroes the counters. */
+int32_t kp_solver_sweeps(int32_t* small_max, int32_t* mid_max, int32_t* large_max,
+                         int32_t reset);
 
 /* Sizes. */
 int64_t kp_param_count(const kp_net* net);              /* D */

@@ -63,6 +63,7 @@ _SIGS = {
     "kp_profile_enable": (C.c_int32, [C.c_void_p, C.c_int32]),
     "kp_profile_read": (C.c_int32, [C.c_void_p, P(C.c_double), P(C.c_double), P(C.c_int64),
                                     P(C.c_int64)]),
+    "kp_solver_sweeps": (C.c_int32, [P(C.c_int32), P(C.c_int32), P(C.c_int32), C.c_int32]),
     "kp_profile_read_hbm": (C.c_int32, [C.c_void_p, P(C.c_double), P(C.c_double), P(C.c_int64)]),
     "kp_param_count": (C.c_int64, [P(kp_net)]),
     "kp_factor_count": (C.c_int64, [P(kp_net), C.c_int32]),

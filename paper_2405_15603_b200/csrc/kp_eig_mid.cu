@@ -374,18 +374,23 @@ int g_mid_cl = 0;  // 0: not chosen yet
 int mid_eig_cluster_size() {
   if (g_mid_cl == 0) {
     const char* env = getenv("KP_MID_CLUSTER");
-    const int want = env ? atoi(env) : 16;  // 16 (default), 8, or 0 = off (cuSOLVER route)
+    const int want = env ? atoi(env) : 16;  // 16 (default), 8, or 0 = off (large-pair route)
     g_mid_cl = want == 0 ? -1 : (want == 16 && mid_setup<16>()) ? 16 : (mid_setup<8>() ? 8 : -1);
   }
   return g_mid_cl;
 }
 
-// 0 when no cluster launch of the kernel can be scheduled: the pairs then take the cuSOLVER route.
+// 0 when no cluster launch of the kernel can be scheduled: the pairs then take the large-pair
+// route (kp_eig_large.cu).
 int mid_eig_max_n() { return mid_eig_cluster_size() > 0 ? MID_MAXN : 0; }
 
-int mid_eig_sweeps_used() {
+int mid_eig_sweeps_used(bool reset) {
   int v = 0;
   cudaMemcpyFromSymbol(&v, g_mid_sweeps_max, sizeof(int));
+  if (reset) {
+    const int z = 0;
+    cudaMemcpyToSymbol(g_mid_sweeps_max, &z, sizeof(int));
+  }
   return v;
 }
 

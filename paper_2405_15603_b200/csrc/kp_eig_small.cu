@@ -1,7 +1,8 @@
 // On-device generalised symmetric-definite eigensolver for small factors (n <= 96)
 // and the Kronecker-sum combine, FP64, sm_100a.  Used for the layers whose factors
 // fit in one CTA's shared memory (every layer of BASELINE configs c1-c3); larger
-// layers go through cuSOLVER sygvd.  Everything stays on the device: no host sync,
+// layers go through the mid / large device routes (kp_step.cu gen_eig_pair).  Everything
+// stays on the device: no host sync,
 // one launch for all small factor pairs, one for all small combines.
 //
 // For a pair (F1, F2) with damping lam (reference src/curvature.py:150-161):
@@ -458,9 +459,13 @@ __global__ void __launch_bounds__(1024) k_kron_combine_small_smem(const SmallCom
 
 int small_eig_max_n() { return EIG_MAXN; }
 
-int small_eig_sweeps_used() {
+int small_eig_sweeps_used(bool reset) {
   int v = 0;
   cudaMemcpyFromSymbol(&v, g_eig_sweeps_max, sizeof(int));
+  if (reset) {
+    const int z = 0;
+    cudaMemcpyToSymbol(g_eig_sweeps_max, &z, sizeof(int));
+  }
   return v;
 }
 

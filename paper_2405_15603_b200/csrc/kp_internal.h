@@ -269,6 +269,33 @@ void launch_gen_eig_1x1(const double* f1, const double* f2, double lam, double* 
                         int* info, cudaStream_t s);
 void launch_identity(double* F, int n, double v, cudaStream_t s);
 
+// ---- dense row-major FP64 linear algebra without library calls (kp_dense.cu) ----
+// C (M x N) = alpha op(A) op(B) + beta C; op(A) M x K (A stored K x M when ta), op(B) K x N
+// (B stored N x K when tb).  lower_only: tiles strictly above the diagonal are skipped.
+struct DenseGemm {
+  int M, N, K;
+  const double* A;
+  int64_t lda;
+  bool ta;
+  const double* B;
+  int64_t ldb;
+  bool tb;
+  double* C;
+  int64_t ldc;
+  double alpha, beta;
+  bool lower_only;
+};
+void launch_dense_gemm(const DenseGemm& g, cudaStream_t s);
+// In-place lower Cholesky A = L L^T (row-major; the strict upper triangle is overwritten
+// with scratch values).  info: 0 or the 1-based index of the first non-positive pivot.
+void launch_cholesky(int n, double* A, int64_t lda, int* info, cudaStream_t s);
+// X = L^-1 B (lower triangular L; X holds B on entry, or b_identity: B = I).
+void launch_trsm_lower(int n, const double* L, int64_t ldl, double* X, int64_t ldx, int m,
+                       bool b_identity, cudaStream_t s);
+void launch_copy_matrix(const double* src, int64_t lds, int rows, int cols, double* dst,
+                        int64_t ldd, cudaStream_t s);
+void launch_zero_upper(int n, double* A, int64_t lda, cudaStream_t s);
+
 // ---- small on-device generalised eigensolver + combine (kp_eig_small.cu) ---------
 struct SmallEigJob {
   int n;
@@ -278,7 +305,7 @@ struct SmallEigJob {
   double* t;         // n x n row-major, column k = generalised eigenvector k
   double* lam;       // n eigenvalues
   int* info;
-  int col_major = 0;  // 1: write t column-major (the cuSOLVER layout, for a cuBLAS combine)
+  int col_major = 0;  // 1: write t column-major (= T^T row-major, for the DMMA combine)
   // Warm start (optional): the previous step's T (n x n row-major) and a validity flag, kept
   // by the context across steps, plus n x n global scratch.  With a valid T_prev the pair is
   // first congruence-transformed, (T_prev^T M1 T_prev, T_prev^T M2 T_prev), which the EMA
@@ -308,10 +335,21 @@ struct SmallCombineJobs {
 int small_eig_max_n();
 // kp_eig_mid.cu: one-sided Jacobi in an 8-CTA cluster for small_eig_max_n() < n <= mid_eig_max_n()
 int mid_eig_max_n();
-int mid_eig_sweeps_used();
+int mid_eig_sweeps_used(bool reset = false);
+int small_eig_sweeps_used(bool reset = false);
 int mid_eig_cluster_size();  // 16, 8, or -1 when no cluster launch is possible
 void launch_eig_mid(int n, double* rv, double* lam, int* info, const int* chol_info,
                     cudaStream_t s, int* warm_valid = nullptr, long long* prof = nullptr);
+// kp_eig_large.cu: one-sided Jacobi with the vectors in L2, one 16-CTA cluster per pair, for
+// mid_eig_max_n() < n <= large_eig_max_n(); U (n x n row-major): the rows of L_C in,
+// orthogonalised rows out; V (n x n): the eigenvectors of C as rows
+int large_eig_max_n();
+// T^T = U^T K^-1 from the orthogonalised rows U (default), or KP_LARGE_ACCV=1: V accumulated
+// in the kernel and T^T = V^T L^-1
+bool large_eig_accumulate_v();
+int large_eig_sweeps_used(bool reset = false);
+void launch_eig_large(int n, double* U, double* V, double* lam, int* info, const int* chol_info,
+                      cudaStream_t s, int* warm_valid = nullptr);
 size_t small_eig_smem_bytes(int n);
 void launch_gen_eig_small(const SmallEigJobs& jobs, int njobs, int max_n, int32_t* status,
                           cudaStream_t s);

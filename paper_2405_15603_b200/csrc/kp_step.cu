@@ -13,12 +13,9 @@
 //      per-candidate sums of r^2 into a second small buffer (all-reduce #2).
 //   4. update — device argmin (ascending grid, finite, strict <), theta += a dir,
 //      prev = a dir, non-finite check (optim.py:260-262, 398-401).
-#include <cublas_v2.h>
-#include <cusolverDn.h>
 
 #include <algorithm>
 #include <atomic>
-#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -46,8 +43,6 @@ using namespace kp;
 
 struct kp_context {
   int device = 0;
-  cusolverDnHandle_t solver = nullptr;
-  cublasHandle_t blas = nullptr;
   bool profile = false;
   std::vector<cudaEvent_t> ev;  // pairs
   size_t ev_used = 0;
@@ -60,8 +55,6 @@ struct kp_context {
   int64_t prof_hbm_launches = 0;
   // side streams for the per-layer Kronecker-sum solves (2 per layer: A and B factor pairs)
   std::vector<cudaStream_t> side;
-  std::vector<cusolverDnHandle_t> side_solver;
-  std::vector<cublasHandle_t> side_blas;
   std::vector<cudaEvent_t> side_ev;
   // early preconditioning (single-call steps): layer l's factor contractions done / its factor
   // EMA done, so the layer's eigenproblems start while later layers are still contracted
@@ -79,7 +72,7 @@ struct kp_context {
   int* warm_flags = nullptr;
   cudaEvent_t warm_ev = nullptr;  // the flags' reset on the main stream, for the side streams
   std::vector<unsigned char> warm_key;
-  // cache of the last workspace plan (make_plan queries cuSOLVER workspace sizes: host cost)
+  // cache of the last workspace plan (make_plan: host cost)
   kp_problem plan_key{};
   bool plan_valid = false;
   std::vector<unsigned char> plan_blob;
@@ -96,39 +89,13 @@ static int ensure_side_streams(kp_context* c, int n) {
   while ((int)c->side.size() < n) {
     cudaStream_t s;
     KP_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    cusolverDnHandle_t h;
-    if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) return KP_ERR_CUDA;
-    cusolverDnSetStream(h, s);
-    cublasHandle_t b;
-    if (cublasCreate(&b) != CUBLAS_STATUS_SUCCESS) return KP_ERR_CUDA;
-    cublasSetStream(b, s);
     cudaEvent_t e;
     KP_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     c->side.push_back(s);
-    c->side_solver.push_back(h);
-    c->side_blas.push_back(b);
     c->side_ev.push_back(e);
   }
   return KP_OK;
 }
-
-#define KP_SOLVER_TRY(expr)                                                          \
-  do {                                                                               \
-    cusolverStatus_t s__ = (expr);                                                   \
-    if (s__ != CUSOLVER_STATUS_SUCCESS) {                                            \
-      fprintf(stderr, "[kfac_pinn_b200] cuSOLVER status %d in %s\n", (int)s__, #expr); \
-      return KP_ERR_CUDA;                                                            \
-    }                                                                                \
-  } while (0)
-
-#define KP_BLAS_TRY(expr)                                                            \
-  do {                                                                               \
-    cublasStatus_t s__ = (expr);                                                     \
-    if (s__ != CUBLAS_STATUS_SUCCESS) {                                              \
-      fprintf(stderr, "[kfac_pinn_b200] cuBLAS status %d in %s\n", (int)s__, #expr);  \
-      return KP_ERR_CUDA;                                                            \
-    }                                                                                \
-  } while (0)
 
 #define KP_TRY(expr)          \
   do {                        \
@@ -164,7 +131,6 @@ struct Plan {
   int64_t k_A1[MAXL] = {}, k_A2[MAXL] = {}, k_B1[MAXL] = {}, k_B2[MAXL] = {}, k_la[MAXL] = {},
           k_lb[MAXL] = {}, k_T1[MAXL] = {}, k_T2[MAXL] = {}, k_wa[MAXL] = {}, k_wb[MAXL] = {},
           k_info[MAXL] = {};
-  int lw[MAXL][2] = {};
   int64_t o_wpad = 0, o_wpadc = 0, wo[MAXL] = {};
   int64_t o_w0t = 0, o_q0 = 0, o_w0tc = 0, o_q0c = 0;
   WPack wp{};   // layout of the padded copy of theta
@@ -176,12 +142,20 @@ struct Plan {
                             // (or the rotated seeds of dense coefficients)
   int64_t o_rotg = 0;       // layer-0 derivative-row gradient in the rotated basis (h1 x d)
   int Bc = 1;   // line-search candidates evaluated per batched launch
-  int64_t lwork = 0;
   int64_t total = 0;  // doubles
   // reduce-buffer sub-offsets (relative to o_red)
   int64_t r_aint = 0, r_bint = 0, r_abnd = 0, r_bbnd = 0, r_gint = 0, r_gbnd = 0, r_ss = 0,
           r_count = 0;
 };
+
+// Scratch of the device generalised eigensolver per factor pair (gen_eig_pair): M1 / K, and
+// two n x n work matrices.
+inline int64_t pair_scratch_doubles(int n) { return 3LL * n * n; }
+
+// Largest factor size the device solvers handle (small / mid / large route).
+inline int max_pair_n() {
+  return std::max(small_eig_max_n(), std::max(mid_eig_max_n(), large_eig_max_n()));
+}
 
 int check_net(const kp_net* net) {
   if (!net || net->n_layers < 1 || net->n_layers > MAXL) return KP_ERR_INVALID;
@@ -218,6 +192,8 @@ constexpr double kBndGroupMaxWork = 134217728.0;  // 2^27
 
 int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
   KP_TRY(check_net(&pr->net));
+  for (int l = 0; l <= pr->net.n_layers; ++l)  // factor sizes h + 1 (A) and h (B)
+    if (pr->net.widths[l] + (l < pr->net.n_layers ? 1 : 0) > max_pair_n()) return KP_ERR_INVALID;
   if (pr->n_interior < 1 || pr->n_boundary < 1 || pr->n_candidates < 1) return KP_ERR_INVALID;
   P.L = pr->net.n_layers;
   for (int l = 0; l <= P.L; ++l) P.h[l] = pr->net.widths[l];
@@ -381,26 +357,6 @@ int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
   P.o_lb = take(P.maxq);
   P.o_T1 = take((int64_t)P.maxp * P.maxq);
   P.o_T2 = take((int64_t)P.maxp * P.maxq);
-  int lwork = 1;
-  for (int l = 0; l < P.L; ++l) {
-    for (int k = 0; k < 2; ++k) {
-      const int n = k == 0 ? P.p[l] : P.q[l];
-      int lw = 0;
-      KP_SOLVER_TRY(cusolverDnDsygvd_bufferSize(ctx->solver, CUSOLVER_EIG_TYPE_1,
-                                                CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
-                                                n, nullptr, n, nullptr, n, nullptr, &lw));
-      int lwp = 0, lwe = 0;  // potrf (mid route, large route) and syevd share the workspace
-      KP_SOLVER_TRY(cusolverDnDpotrf_bufferSize(ctx->solver, CUBLAS_FILL_MODE_LOWER, n, nullptr,
-                                                n, &lwp));
-      KP_SOLVER_TRY(cusolverDnDsyevd_bufferSize(ctx->solver, CUSOLVER_EIG_MODE_VECTOR,
-                                                CUBLAS_FILL_MODE_LOWER, n, nullptr, n, nullptr,
-                                                &lwe));
-      lw = std::max(lw, std::max(lwp, lwe));
-      P.lw[l][k] = std::max(lw, 1);
-      lwork = std::max(lwork, lw);
-    }
-  }
-  P.lwork = lwork;
   for (int l = 0; l < P.L; ++l) {
     const int64_t p = P.p[l], q = P.q[l];
     P.k_A1[l] = take(p * p);
@@ -411,8 +367,8 @@ int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
     P.k_lb[l] = take(q);
     P.k_T1[l] = take(p * q);
     P.k_T2[l] = take(p * q);
-    P.k_wa[l] = take(P.lw[l][0]);
-    P.k_wb[l] = take(P.lw[l][1]);
+    P.k_wa[l] = take(pair_scratch_doubles(P.p[l]));  // device generalised eigensolver scratch
+    P.k_wb[l] = take(pair_scratch_doubles(P.q[l]));
     P.k_info[l] = take(4);  // 8 ints: eig info (A, B), Cholesky infos (A: M2, C; B: M2, C)
   }
   P.total = o;
@@ -888,93 +844,70 @@ int phase_accumulate(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, cons
   return KP_OK;
 }
 
-// Damped two-term Kronecker-sum solve for one layer (linalg.py:136-174) by the
-// generalised symmetric-definite eigenproblems A1 x = l A2 x, B1 y = m B2 y
-// (Cholesky of A2/B2 + eigh, cuSOLVER sygvd): with T_A^T A2 T_A = I,
-// T_A^T A1 T_A = diag(la) (likewise B), X = T_B [(T_B^T G T_A) / (lb la^T + 1)] T_A^T
-// solves B1 X A1 + B2 X A2 = G — the same unique solution as the reference's
-// inverse-square-root route.  Writes out = sign * X (q x p row-major).
-// Generalised symmetric-definite eigenproblem M1 x = lam M2 x (cuSOLVER sygvd, type 1):
-// Cholesky of M2 + eigh; on return M1 holds T with T^T M2 T = I, T^T M1 T = diag(lam).
-int gen_eig(cusolverDnHandle_t h, int n, double* M1, double* M2, double* lam, double* work,
-            int lwork, int* info) {
-  KP_SOLVER_TRY(cusolverDnDsygvd(h, CUSOLVER_EIG_TYPE_1, CUSOLVER_EIG_MODE_VECTOR,
-                                 CUBLAS_FILL_MODE_LOWER, n, M1, n, M2, n, lam, work, lwork, info));
-  return KP_OK;
-}
-
-// out (q x p row-major) = sign * T_B [(T_B^T G T_A) / (lb la^T + 1)] T_A^T.  Column-major
-// views: G^T is p x q (ld p), T_A = A1 (p x p), T_B = B1 (q x q).
-int kron_combine(cublasHandle_t h, cudaStream_t s, int p, int q, const double* TA,
-                 const double* la, const double* TB, const double* lb, const double* G,
-                 double* out, double sign, double* T1, double* T2) {
-  const double one = 1.0, zero = 0.0;
-  KP_BLAS_TRY(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, p, q, q, &one, G, p, TB, q, &zero, T1, p));
-  KP_BLAS_TRY(cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, p, q, p, &one, TA, p, T1, p, &zero, T2, p));
-  launch_kron_scale(T2, la, p, lb, q, s);
-  KP_BLAS_TRY(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, p, q, q, &one, T2, p, TB, q, &zero, T1, p));
-  KP_BLAS_TRY(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, p, q, p, &sign, TA, p, T1, p, &zero, out, p));
-  return KP_OK;
-}
-
-// Damped two-term Kronecker-sum solve for one layer (linalg.py:136-174) by the
-// generalised symmetric-definite eigenproblems A1 x = l A2 x, B1 y = m B2 y:
-// with T_A^T A2 T_A = I, T_A^T A1 T_A = diag(la) (likewise B),
-// X = T_B [(T_B^T G T_A) / (lb la^T + 1)] T_A^T solves B1 X A1 + B2 X A2 = G — the
-// same unique solution as the reference's inverse-square-root route.  Single stream.
-int kron_solve(kp_context* ctx, const Ctx& c, int p, int q, double* A1, double* A2, double* B1,
-               double* B2, const double* G, double* out, double sign, int* info,
-               int32_t* status) {
-  const Plan& P = c.P;
-  double* la = c.at(P.o_la);
-  double* lb = c.at(P.o_lb);
-  double* work = c.at(P.o_work);
-  KP_SOLVER_TRY(cusolverDnSetStream(ctx->solver, c.s));
-  KP_BLAS_TRY(cublasSetStream(ctx->blas, c.s));
-  KP_CUDA_TRY(cudaMemsetAsync(info, 0, 2 * sizeof(int), c.s));
-  // 1 x 1 factors (e.g. the h_out = 1 layer's B) are solved in closed form
-  if (p == 1) launch_gen_eig_1x1(A1, A2, 0.0, A1, la, info, c.s);
-  else KP_TRY(gen_eig(ctx->solver, p, A1, A2, la, work, (int)P.lwork, info));
-  if (q == 1) launch_gen_eig_1x1(B1, B2, 0.0, B1, lb, info + 1, c.s);
-  else KP_TRY(gen_eig(ctx->solver, q, B1, B2, lb, work, (int)P.lwork, info + 1));
-  launch_eig_status(la, p, lb, q, info, status, c.s);
-  return kron_combine(ctx->blas, c.s, p, q, A1, la, B1, lb, G, out, sign, c.at(P.o_T1),
-                      c.at(P.o_T2));
-}
-
-// Generalised eigenproblem of a mid-size pair (small_eig_max_n() < n <= mid_eig_max_n()),
-// entirely asynchronous on stream s (no host-blocking library call).  Warm start as in the
-// small solver: the pair is first congruence-transformed by the previous step's T (kept in
-// tp; the identity until a solve of this pair has succeeded, decided on the device by
-// *valid, so the same launches serve cold and warm steps and can be graph-captured):
-//   M_i' = Tp^T (F_i + lam I) Tp,  M2' = L L^T (potrf),  C = L^-1 M1' L^-T (two trsm),
-//   C = R^T R (potrf), one-sided Jacobi on R in an 8-CTA cluster (kp_eig_mid.cu) ->
-//   C V = V diag(ev),  T = Tp L^-T V, left in m1 (column-major, like sygvd's) and in tp.
-int gen_eig_mid(cusolverDnHandle_t hs, cublasHandle_t hb, cudaStream_t s, int n, const double* f1,
-                const double* f2, double lam, double* m1, double* m2, double* ev, double* work,
-                int lwork, int* info, int* chol_info, double* tp, double* w, int* valid) {
-  const double one = 1.0, zero = 0.0;
+// Generalised eigenproblem M1 x = lam M2 x of one factor pair (M_i = F_i + damping I) with
+// small_eig_max_n() < n, entirely on the device and asynchronous on stream s (no library
+// call, nothing blocks the host, graph-capturable).  Warm start as in the small solver: the
+// pair is first congruence-transformed by the previous step's T (tp holds T^T row-major, the
+// identity until a solve of this pair has succeeded, decided on the device by *valid, so the
+// same launches serve cold and warm steps):
+//   M_i' = T_p^T M_i T_p,  M2' = L L^T,  M1' = K K^T  (blocked Cholesky, kp_dense.cu),
+//   L_C = L^-1 K  (lower triangular: C = L^-1 M1' L^-T = L_C L_C^T, R = L_C^T),
+// then one-sided Jacobi on the rows of L_C (= the columns of R):
+//   n <= mid_eig_max_n(): R and V in a thread-block cluster's shared memory (kp_eig_mid.cu),
+//   larger:               R and V in L2, one 16-CTA cluster (kp_eig_large.cu);
+// T' = L^-T V, i.e. T'^T = V^T L^-1;
+// and T = T_p T'.  Out: tout = T^T row-major (= T column-major), lam = eigenvalues; the same
+// T^T is kept in tp for the next step.  chol_info[0..1]: Cholesky infos of M2', M1' (a failure
+// makes the eigensolver report info = n + 1: not positive definite).
+// scratch: pair_scratch_doubles(n) = 3 n^2; m2: n^2.
+int gen_eig_pair(cudaStream_t s, int n, const double* f1, const double* f2, double lam,
+                 double* tout, double* m2, double* ev, double* scratch, int* info, int* chol_info,
+                 double* tp, int* valid) {
+  const size_t nn = (size_t)n * n;
+  double* m1 = scratch;
+  double* s1 = scratch + nn;
+  double* s2 = scratch + 2 * nn;
   KP_CUDA_TRY(cudaMemsetAsync(chol_info, 0, 2 * sizeof(int), s));
   launch_damped_copy(f1, lam, n, m1, s);
   launch_damped_copy(f2, lam, n, m2, s);
   launch_warm_identity(tp, n, valid, s);
-  for (double* m : {m2, m1}) {
-    KP_BLAS_TRY(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, n, n, n, &one, m, n, tp, n, &zero, w, n));
-    KP_BLAS_TRY(cublasDgemm(hb, CUBLAS_OP_T, CUBLAS_OP_N, n, n, n, &one, tp, n, w, n, &zero, m, n));
+  for (double* m : {m2, m1}) {  // M' = Tp^T M Tp = tp M tp^T
+    launch_dense_gemm(DenseGemm{n, n, n, tp, n, false, m, n, false, s1, n, 1.0, 0.0, false}, s);
+    launch_dense_gemm(DenseGemm{n, n, n, s1, n, false, tp, n, true, m, n, 1.0, 0.0, false}, s);
   }
-  KP_SOLVER_TRY(cusolverDnDpotrf(hs, CUBLAS_FILL_MODE_LOWER, n, m2, n, work, lwork, chol_info));
-  KP_BLAS_TRY(cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N,
-                          CUBLAS_DIAG_NON_UNIT, n, n, &one, m2, n, m1, n));
-  KP_BLAS_TRY(cublasDtrsm(hb, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T,
-                          CUBLAS_DIAG_NON_UNIT, n, n, &one, m2, n, m1, n));
-  KP_SOLVER_TRY(cusolverDnDpotrf(hs, CUBLAS_FILL_MODE_UPPER, n, m1, n, work, lwork, chol_info + 1));
-  launch_eig_mid(n, m1, ev, info, chol_info, s, valid);
-  KP_BLAS_TRY(cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T,
-                          CUBLAS_DIAG_NON_UNIT, n, n, &one, m2, n, m1, n));
-  KP_BLAS_TRY(cublasDgemm(hb, CUBLAS_OP_N, CUBLAS_OP_N, n, n, n, &one, tp, n, m1, n, &zero, w, n));
-  KP_CUDA_TRY(cudaMemcpyAsync(m1, w, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s));
-  KP_CUDA_TRY(cudaMemcpyAsync(tp, w, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, s));
+  launch_cholesky(n, m2, n, chol_info, s);      // L
+  launch_cholesky(n, m1, n, chol_info + 1, s);  // K
+  launch_zero_upper(n, m1, n, s);
+  launch_trsm_lower(n, m2, n, s1, n, n, true, s);  // s1 = L^-1
+  launch_dense_gemm(DenseGemm{n, n, n, s1, n, false, m1, n, false, s2, n, 1.0, 0.0, false}, s);
+  double* vt = s2;
+  if (n <= mid_eig_max_n()) {
+    launch_eig_mid(n, s2, ev, info, chol_info, s, valid);  // s2 <- V^T
+  } else if (large_eig_accumulate_v()) {
+    launch_eig_large(n, s2, m1, ev, info, chol_info, s, valid);  // s2 <- U^T, m1 <- V^T
+    vt = m1;
+  } else {  // T' = K^-T U  (K^-T U = L^-T L_C^-T R V = L^-T V)
+    launch_eig_large(n, s2, nullptr, ev, info, chol_info, s, valid);  // s2 <- U^T
+    launch_trsm_lower(n, m1, n, s1, n, n, true, s);                   // s1 = K^-1
+  }
+  launch_dense_gemm(DenseGemm{n, n, n, vt, n, false, s1, n, false, m2, n, 1.0, 0.0, false}, s);
+  // T^T = T'^T T_p^T
+  launch_dense_gemm(DenseGemm{n, n, n, m2, n, false, tp, n, false, tout, n, 1.0, 0.0, false}, s);
+  launch_copy_matrix(tout, n, n, n, tp, n, s);
   return KP_OK;
+}
+
+// out (q x p row-major) = sign * T_B [(T_B^T G T_A) / (lb la^T + 1)] T_A^T  (the
+// two-term Kronecker-sum solution, linalg.py:168-173) from TtA = T_A^T (p x p) and
+// TtB = T_B^T (q x q), both row-major, and the q x p gradient G; t1, t2: q x p scratch.
+void kron_combine(cudaStream_t s, int p, int q, const double* TtA, const double* la,
+                  const double* TtB, const double* lb, const double* G, double* out, double sign,
+                  double* t1, double* t2) {
+  launch_dense_gemm(DenseGemm{q, p, q, TtB, q, false, G, p, false, t1, p, 1.0, 0.0, false}, s);
+  launch_dense_gemm(DenseGemm{q, p, p, t1, p, false, TtA, p, true, t2, p, 1.0, 0.0, false}, s);
+  launch_kron_scale(t2, la, p, lb, q, s);
+  launch_dense_gemm(DenseGemm{q, p, q, TtB, q, true, t2, p, false, t1, p, 1.0, 0.0, false}, s);
+  launch_dense_gemm(DenseGemm{q, p, p, t1, p, false, TtA, p, false, out, p, sign, 0.0, false}, s);
 }
 
 // `owned` (host, L flags) = nullptr: every layer's Kronecker solve runs here and the phase
@@ -994,10 +927,6 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
   const double ema = cfg->ema;
   kp_context* ctx = c.ctx;
   auto pair_small = [&](int l, int k) { return (k == 0 ? P.p[l] : P.q[l]) <= small_eig_max_n(); };
-  auto pair_mid = [&](int l, int k) {
-    const int n = k == 0 ? P.p[l] : P.q[l];
-    return n > small_eig_max_n() && n <= mid_eig_max_n();
-  };
   // early layers: their factors were completed (c.early: ctx->layer_ev) before the end of the
   // accumulate phase; their EMA and eigenproblems start on the side streams right then
   std::vector<char> early(P.L, 0);
@@ -1035,9 +964,10 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
   // factor pair of layer l on streams 2l and 2l+1), combine on 2l, join back.
   // Factor pairs up to small_eig_max_n(): on-device Cholesky + Jacobi solver, all of them in
   // one launch on the main stream (plus one combine launch for the layers whose two pairs are
-  // both small).  Larger pairs: cuSOLVER sygvd, which blocks the calling host thread, so each
-  // is issued from its own host thread (own handle + stream); a layer with a large pair is
-  // combined with cuBLAS on its side stream.
+  // both small).  Larger pairs: the device route of gen_eig_pair on the pair's own side
+  // stream (blocked Cholesky / triangular solves / DMMA GEMMs and a cluster Jacobi), all
+  // pairs concurrently; a layer with a larger pair is combined by DMMA GEMMs on its side
+  // stream.
   bool any_big = false;
   for (int l = 0; l < P.L; ++l)
     any_big |= (!owned || owned[l]) && (!pair_small(l, 0) || !pair_small(l, 1));
@@ -1049,12 +979,11 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
     KP_CUDA_TRY(cudaEventRecord(ready, c.s));
   }
   std::vector<int> big;  // layers with at least one pair outside the one-launch small solver
-  struct MidWarm {
+  struct PairWarm {
     double* t;
-    double* scratch;
     int* valid;
   };
-  std::vector<MidWarm> mid_warm(2 * P.L, MidWarm{nullptr, nullptr, nullptr});
+  std::vector<PairWarm> pair_warm(2 * P.L, PairWarm{nullptr, nullptr});
   // warm-start cache for the small pairs (re-keyed when shapes or factor buffers change)
   bool warm_reset = false;
   {
@@ -1069,7 +998,8 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
       put(&P.q[l], sizeof(int));
       for (int k = 0; k < 2; ++k) {
         const size_t nn = (size_t)(k == 0 ? P.p[l] : P.q[l]);
-        if (pair_small(l, k) || pair_mid(l, k)) need += 2 * nn * nn;
+        // small pairs keep T and a scratch matrix, the others their previous T^T
+        need += (pair_small(l, k) ? 2 : 1) * nn * nn;
       }
     }
     put(&st->a_int, sizeof(double*));
@@ -1091,7 +1021,7 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
       }
       KP_CUDA_TRY(cudaMemsetAsync(ctx->warm_flags, 0, sizeof(int) * 64, c.s));
       ctx->warm_key = key;
-      // the mid-size pairs read their flags on side streams that (for early layers) wait
+      // the larger pairs read their flags on side streams that (for early layers) wait
       // only on their own factors: order them after this reset
       if (!ctx->warm_ev) KP_CUDA_TRY(cudaEventCreateWithFlags(&ctx->warm_ev, cudaEventDisableTiming));
       KP_CUDA_TRY(cudaEventRecord(ctx->warm_ev, c.s));
@@ -1145,100 +1075,37 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
       else
         big.push_back(l);
     }
-    // warm-start slots of the mid-size pairs follow the small ones (owned or not: stable)
+    // warm-start slots of the larger pairs follow the small ones (owned or not: stable)
     for (int l = 0; l < P.L; ++l)
       for (int k = 0; k < 2; ++k) {
-        if (!pair_mid(l, k)) continue;
-        SmallEigJob tmp{};
-        tmp.n = k == 0 ? P.p[l] : P.q[l];
-        warm(tmp);
-        mid_warm[2 * l + k] = MidWarm{tmp.warm_t, tmp.warm_scratch, tmp.warm_valid};
+        if (pair_small(l, k)) continue;
+        const size_t n = (size_t)(k == 0 ? P.p[l] : P.q[l]);
+        pair_warm[2 * l + k] = PairWarm{ctx->warm_buf + woff, ctx->warm_flags + wjob++};
+        woff += n * n;
       }
     launch_gen_eig_small(ej, ne, maxn, out->status, c.s);
     if (any_big) KP_CUDA_TRY(cudaEventRecord(small_done, c.s));
     launch_kron_combine_small(cj, nc, c.s);
   }
-  // mid-size pairs: asynchronous route issued from this thread on the pair's side stream
+  // pairs above the one-launch small solver: the device route (gen_eig_pair) on the pair's
+  // side stream, then each such layer is combined on its A-side stream
   for (int l : big)
     for (int k = 0; k < 2; ++k) {
-      if (!pair_mid(l, k)) continue;
+      if (pair_small(l, k)) continue;
       cudaStream_t s = ctx->side[2 * l + k];
       KP_CUDA_TRY(cudaStreamWaitEvent(s, early[l] ? ctx->fin_ev[l] : ready, 0));
       if (warm_reset) KP_CUDA_TRY(cudaStreamWaitEvent(s, ctx->warm_ev, 0));
       int* info = reinterpret_cast<int*>(c.at(P.k_info[l])) + k;
       KP_CUDA_TRY(cudaMemsetAsync(info, 0, sizeof(int), s));
-      KP_TRY(gen_eig_mid(ctx->side_solver[2 * l + k], ctx->side_blas[2 * l + k], s,
-                         k == 0 ? P.p[l] : P.q[l],
-                         k == 0 ? st->a_int + P.fa[l] : st->b_int + P.fb[l],
-                         k == 0 ? st->a_bnd + P.fa[l] : st->b_bnd + P.fb[l], lam,
-                         c.at(k == 0 ? P.k_A1[l] : P.k_B1[l]), c.at(k == 0 ? P.k_A2[l] : P.k_B2[l]),
-                         c.at(k == 0 ? P.k_la[l] : P.k_lb[l]), c.at(k == 0 ? P.k_wa[l] : P.k_wb[l]),
-                         P.lw[l][k], info, reinterpret_cast<int*>(c.at(P.k_info[l])) + 2 + 2 * k,
-                         mid_warm[2 * l + k].t, mid_warm[2 * l + k].scratch,
-                         mid_warm[2 * l + k].valid));
+      KP_TRY(gen_eig_pair(s, k == 0 ? P.p[l] : P.q[l],
+                          k == 0 ? st->a_int + P.fa[l] : st->b_int + P.fb[l],
+                          k == 0 ? st->a_bnd + P.fa[l] : st->b_bnd + P.fb[l], lam,
+                          c.at(k == 0 ? P.k_A1[l] : P.k_B1[l]), c.at(k == 0 ? P.k_A2[l] : P.k_B2[l]),
+                          c.at(k == 0 ? P.k_la[l] : P.k_lb[l]), c.at(k == 0 ? P.k_wa[l] : P.k_wb[l]),
+                          info, reinterpret_cast<int*>(c.at(P.k_info[l])) + 2 + 2 * k,
+                          pair_warm[2 * l + k].t, pair_warm[2 * l + k].valid));
       KP_CUDA_TRY(cudaEventRecord(ctx->side_ev[2 * l + k], s));
     }
-  // Large pairs (n > mid_eig_max_n()): M2 = L L^T and C = L^-1 M1 L^-T are issued here
-  // (asynchronous); only the symmetric eigensolver (cuSOLVER syevd, which blocks its calling
-  // thread) runs on one host thread per pair, followed by T = L^-T V.  (Measured on c5's eight
-  // pairs: 42.6 ms vs 47.3 ms for sygvd per thread, tools/syevd_threads_bench.cu.)
-  auto big_pair = [&](int l, int k) { return !pair_small(l, k) && !pair_mid(l, k); };
-  for (int l : big)
-    for (int k = 0; k < 2; ++k) {
-      if (!big_pair(l, k)) continue;
-      cudaStream_t s = ctx->side[2 * l + k];
-      const int n = k == 0 ? P.p[l] : P.q[l];
-      int* iw = reinterpret_cast<int*>(c.at(P.k_info[l]));
-      const double one = 1.0;
-      double* m1 = c.at(k == 0 ? P.k_A1[l] : P.k_B1[l]);
-      double* m2 = c.at(k == 0 ? P.k_A2[l] : P.k_B2[l]);
-      KP_CUDA_TRY(cudaStreamWaitEvent(s, early[l] ? ctx->fin_ev[l] : ready, 0));
-      // info words must not depend on what the workspace held before
-      KP_CUDA_TRY(cudaMemsetAsync(iw + k, 0, sizeof(int), s));
-      KP_CUDA_TRY(cudaMemsetAsync(iw + 2 + 2 * k, 0, sizeof(int), s));
-      launch_damped_copy(k == 0 ? st->a_int + P.fa[l] : st->b_int + P.fb[l], lam, n, m1, s);
-      launch_damped_copy(k == 0 ? st->a_bnd + P.fa[l] : st->b_bnd + P.fb[l], lam, n, m2, s);
-      cublasHandle_t hb = ctx->side_blas[2 * l + k];
-      KP_SOLVER_TRY(cusolverDnDpotrf(ctx->side_solver[2 * l + k], CUBLAS_FILL_MODE_LOWER, n, m2, n,
-                                     c.at(k == 0 ? P.k_wa[l] : P.k_wb[l]), P.lw[l][k],
-                                     iw + 2 + 2 * k));
-      KP_BLAS_TRY(cublasDtrsm(hb, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N,
-                              CUBLAS_DIAG_NON_UNIT, n, n, &one, m2, n, m1, n));
-      KP_BLAS_TRY(cublasDtrsm(hb, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T,
-                              CUBLAS_DIAG_NON_UNIT, n, n, &one, m2, n, m1, n));
-    }
-  std::vector<int> rc(2 * P.L, KP_OK);
-  auto solve_pair = [&](int l, int k) {
-    cudaSetDevice(ctx->device);
-    cudaStream_t s = ctx->side[2 * l + k];
-    const int n = k == 0 ? P.p[l] : P.q[l];
-    int* iw = reinterpret_cast<int*>(c.at(P.k_info[l]));
-    double* m1 = c.at(k == 0 ? P.k_A1[l] : P.k_B1[l]);
-    double* m2 = c.at(k == 0 ? P.k_A2[l] : P.k_B2[l]);
-    const double one = 1.0;
-    if (cusolverDnDsyevd(ctx->side_solver[2 * l + k], CUSOLVER_EIG_MODE_VECTOR,
-                         CUBLAS_FILL_MODE_LOWER, n, m1, n, c.at(k == 0 ? P.k_la[l] : P.k_lb[l]),
-                         c.at(k == 0 ? P.k_wa[l] : P.k_wb[l]), P.lw[l][k],
-                         iw + k) != CUSOLVER_STATUS_SUCCESS) {
-      rc[2 * l + k] = KP_ERR_CUDA;
-      return;
-    }
-    launch_merge_chol_info(iw + 2 + 2 * k, iw + k, n, s);  // M2 not PD -> info > n
-    if (cublasDtrsm(ctx->side_blas[2 * l + k], CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T,
-                    CUBLAS_DIAG_NON_UNIT, n, n, &one, m2, n, m1, n) != CUBLAS_STATUS_SUCCESS) {
-      rc[2 * l + k] = KP_ERR_CUDA;
-      return;
-    }
-    cudaEventRecord(ctx->side_ev[2 * l + k], s);
-  };
-  if (!big.empty()) {
-    std::vector<std::thread> pool;
-    for (int l : big)
-      for (int k = 0; k < 2; ++k)
-        if (big_pair(l, k)) pool.emplace_back(solve_pair, l, k);
-    for (auto& t : pool) t.join();
-  }
-  for (int v : rc) KP_TRY(v);
   for (int l : big) {
     cudaStream_t s = ctx->side[2 * l];
     if (!pair_small(l, 1)) KP_CUDA_TRY(cudaStreamWaitEvent(s, ctx->side_ev[2 * l + 1], 0));
@@ -1246,9 +1113,9 @@ int phase_precondition(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, kp
     if (early[l]) KP_CUDA_TRY(cudaStreamWaitEvent(s, ready, 0));  // the finalized gradient
     launch_eig_status(c.at(P.k_la[l]), P.p[l], c.at(P.k_lb[l]), P.q[l],
                       reinterpret_cast<int*>(c.at(P.k_info[l])), out->status, s);
-    KP_TRY(kron_combine(ctx->side_blas[2 * l], s, P.p[l], P.q[l], c.at(P.k_A1[l]), c.at(P.k_la[l]),
-                        c.at(P.k_B1[l]), c.at(P.k_lb[l]), grad + P.th[l], delta + P.th[l], -1.0,
-                        c.at(P.k_T1[l]), c.at(P.k_T2[l])));
+    kron_combine(s, P.p[l], P.q[l], c.at(P.k_A1[l]), c.at(P.k_la[l]), c.at(P.k_B1[l]),
+                 c.at(P.k_lb[l]), grad + P.th[l], delta + P.th[l], -1.0, c.at(P.k_T1[l]),
+                 c.at(P.k_T2[l]));
     KP_CUDA_TRY(cudaEventRecord(ctx->side_ev[2 * l], s));
   }
   for (int l : big) KP_CUDA_TRY(cudaStreamWaitEvent(c.s, ctx->side_ev[2 * l], 0));
@@ -1473,7 +1340,7 @@ const char* kp_status_string(int32_t s) {
     case KP_ERR_NOT_PSD: return "matrix not positive (semi)definite";
     case KP_ERR_LINE_SEARCH: return "loss is non-finite at every line-search step size";
     case KP_ERR_NONFINITE: return "parameters became non-finite during the step";
-    case KP_ERR_CUDA: return "CUDA/cuSOLVER/cuBLAS failure";
+    case KP_ERR_CUDA: return "CUDA failure";
     case KP_ERR_EIG: return "eigensolver did not converge";
     case KP_ERR_WORKSPACE: return "workspace too small";
     default: return "unknown status";
@@ -1485,15 +1352,6 @@ int32_t kp_context_create(int32_t device, kp_context** out) {
   KP_CUDA_TRY(cudaSetDevice(device));
   kp_context* c = new kp_context();
   c->device = device;
-  if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS) {
-    delete c;
-    return KP_ERR_CUDA;
-  }
-  if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) {
-    cusolverDnDestroy(c->solver);
-    delete c;
-    return KP_ERR_CUDA;
-  }
   *out = c;
   return KP_OK;
 }
@@ -1514,16 +1372,12 @@ int32_t kp_context_destroy(kp_context* c) {
   if (c->cap_out) cudaEventDestroy(c->cap_out);
   for (size_t k = 0; k < c->side.size(); ++k) {
     cudaStreamSynchronize(c->side[k]);
-    cusolverDnDestroy(c->side_solver[k]);
-    cublasDestroy(c->side_blas[k]);
     cudaEventDestroy(c->side_ev[k]);
     cudaStreamDestroy(c->side[k]);
   }
   for (cudaEvent_t e : c->ev) cudaEventDestroy(e);
   for (cudaEvent_t e : c->layer_ev) cudaEventDestroy(e);
   for (cudaEvent_t e : c->fin_ev) cudaEventDestroy(e);
-  if (c->blas) cublasDestroy(c->blas);
-  if (c->solver) cusolverDnDestroy(c->solver);
   delete c;
   return KP_OK;
 }
@@ -1537,6 +1391,14 @@ int32_t kp_profile_enable(kp_context* c, int32_t enable) {
   c->ev_hbm_used = 0;
   c->prof_hbm_bytes = 0.0;
   c->prof_hbm_launches = 0;
+  return KP_OK;
+}
+
+int32_t kp_solver_sweeps(int32_t* small_max, int32_t* mid_max, int32_t* large_max,
+                         int32_t reset) {
+  if (small_max) *small_max = small_eig_sweeps_used(reset != 0);
+  if (mid_max) *mid_max = mid_eig_sweeps_used(reset != 0);
+  if (large_max) *large_max = large_eig_sweeps_used(reset != 0);
   return KP_OK;
 }
 
@@ -1853,8 +1715,7 @@ int32_t kp_kfac_star_step(kp_context* ctx, const kp_problem* prob, const kp_kfac
 
 
 // Whole step (KFAC or KFAC*) replayed from a CUDA graph captured on first use.  Only when
-// every layer's Kronecker solve runs on the device (no host-blocking cuSOLVER call) and
-// profiling is off; otherwise identical to kp_kfac_step / kp_kfac_star_step.  The graph is
+// every factor pair is within the device solvers' range (max_pair_n) and profiling is off; otherwise identical to kp_kfac_step / kp_kfac_star_step.  The graph is
 // keyed on every argument (pointers and configuration values are baked into the nodes).
 int32_t kp_kfac_step_graphed(kp_context* ctx, const kp_problem* prob, const kp_kfac_config* cfg,
                              kp_state* st, const kp_batch* bt, kp_step_out* out, void* ws,
@@ -1867,7 +1728,7 @@ int32_t kp_kfac_step_graphed(kp_context* ctx, const kp_problem* prob, const kp_k
   Plan P;
   KP_TRY(prepare(ctx, prob, P, ws_bytes));
   bool capturable = !ctx->profile;
-  for (int l = 0; l < P.L; ++l) capturable &= std::max(P.p[l], P.q[l]) <= mid_eig_max_n();
+  for (int l = 0; l < P.L; ++l) capturable &= std::max(P.p[l], P.q[l]) <= max_pair_n();
   if (!capturable) return plain();
   std::vector<unsigned char> key;
   auto put = [&](const void* p, size_t n) {
@@ -2009,20 +1870,11 @@ int32_t kp_evaluate_losses(kp_context* ctx, const kp_problem* prob, const double
 
 int32_t kp_kron_solve_workspace_bytes(kp_context* ctx, int32_t p, int32_t q, size_t* bytes) {
   if (!ctx || p < 1 || q < 1 || !bytes) return KP_ERR_INVALID;
-  kp_problem pr{};
-  pr.net.n_layers = 1;
-  pr.net.widths[0] = p - 1 > 0 ? p - 1 : 1;
-  pr.net.widths[1] = 1;
-  (void)pr;
-  int lw = 1;
-  for (int n : {p, q}) {
-    int w = 0;
-    KP_SOLVER_TRY(cusolverDnDsygvd_bufferSize(ctx->solver, CUSOLVER_EIG_TYPE_1,
-                                              CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n,
-                                              nullptr, n, nullptr, n, nullptr, &w));
-    lw = std::max(lw, w);
-  }
-  const int64_t doubles = 2LL * p * p + 2LL * q * q + p + q + 2LL * p * q + lw + 8 + 16 * 32;
+  // T^T (A, B), M2 (A, B), eigenvalues, two q x p combine buffers, infos, and per larger pair
+  // the solver scratch plus a warm-start T (identity: a standalone solve is cold)
+  int64_t doubles = 2LL * p * p + 2LL * q * q + p + q + 2LL * p * q + 8 + 16 * 32;
+  for (int n : {p, q})
+    if (n > small_eig_max_n()) doubles += pair_scratch_doubles(n) + (int64_t)n * n + 32;
   *bytes = (size_t)doubles * sizeof(double);
   return KP_OK;
 }
@@ -2051,8 +1903,6 @@ int32_t kp_kron_sum_solve(kp_context* ctx, int32_t p, int32_t q, const double* a
   P.o_T1 = take((int64_t)p * q);
   P.o_T2 = take((int64_t)p * q);
   P.o_info = take(8);
-  P.o_work = o;
-  P.lwork = (int64_t)(ws_bytes / sizeof(double)) - o;
   Ctx c{ctx, P, static_cast<double*>(ws), s};
   KP_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int32_t), s));
   if (std::max(p, q) <= small_eig_max_n()) {
@@ -2068,12 +1918,37 @@ int32_t kp_kron_sum_solve(kp_context* ctx, int32_t p, int32_t q, const double* a
     KP_CUDA_TRY(cudaGetLastError());
     return KP_OK;
   }
-  KP_CUDA_TRY(cudaMemcpyAsync(c.at(P.o_A1), a1, sizeof(double) * p * p, cudaMemcpyDeviceToDevice, s));
-  KP_CUDA_TRY(cudaMemcpyAsync(c.at(P.o_A2), a2, sizeof(double) * p * p, cudaMemcpyDeviceToDevice, s));
-  KP_CUDA_TRY(cudaMemcpyAsync(c.at(P.o_B1), b1, sizeof(double) * q * q, cudaMemcpyDeviceToDevice, s));
-  KP_CUDA_TRY(cudaMemcpyAsync(c.at(P.o_B2), b2, sizeof(double) * q * q, cudaMemcpyDeviceToDevice, s));
-  KP_TRY(kron_solve(ctx, c, p, q, c.at(P.o_A1), c.at(P.o_A2), c.at(P.o_B1), c.at(P.o_B2), g, x,
-                    1.0, reinterpret_cast<int*>(c.at(P.o_info)), status));
+  // at least one larger pair: device route per larger pair, the small solver for a small
+  // one (T written column-major = T^T row-major), then the DMMA combine
+  int* info = reinterpret_cast<int*>(c.at(P.o_info));
+  KP_CUDA_TRY(cudaMemsetAsync(info, 0, 8 * sizeof(int), s));
+  SmallEigJobs ej{};
+  int ne = 0;
+  int64_t o2 = o;
+  for (int k = 0; k < 2; ++k) {
+    const int n = k == 0 ? p : q;
+    const double* f1 = k == 0 ? a1 : b1;
+    const double* f2 = k == 0 ? a2 : b2;
+    double* t = c.at(k == 0 ? P.o_A1 : P.o_B1);
+    double* ev = c.at(k == 0 ? P.o_la : P.o_lb);
+    if (n <= small_eig_max_n()) {
+      ej.job[ne++] = SmallEigJob{n, f1, f2, 0.0, t, ev, info + k, 1};
+      continue;
+    }
+    double* scratch = c.at(o2);
+    o2 += pair_scratch_doubles(n);
+    double* tp = c.at(o2);
+    o2 += (int64_t)n * n;
+    int* valid = reinterpret_cast<int*>(c.at(o2));
+    o2 += 32;
+    KP_CUDA_TRY(cudaMemsetAsync(valid, 0, sizeof(int), s));
+    KP_TRY(gen_eig_pair(s, n, f1, f2, 0.0, t, c.at(k == 0 ? P.o_A2 : P.o_B2), ev, scratch,
+                        info + k, info + 2 + 2 * k, tp, valid));
+  }
+  if (ne > 0) launch_gen_eig_small(ej, ne, ej.job[0].n, status, s);
+  launch_eig_status(c.at(P.o_la), p, c.at(P.o_lb), q, info, status, s);
+  kron_combine(s, p, q, c.at(P.o_A1), c.at(P.o_la), c.at(P.o_B1), c.at(P.o_lb), g, x, 1.0,
+               c.at(P.o_T1), c.at(P.o_T2));
   KP_CUDA_TRY(cudaGetLastError());
   return KP_OK;
 }

@@ -221,7 +221,9 @@ def test_taylor_forward_matches_oracle():
 def test_kron_sum_solve_matches_dense():
     from paper_2405_15603_b200.engine import kron_sum_solve_device
     rng = np.random.default_rng(4)
-    for p, q in ((5, 3), (65, 64), (101, 1), (257, 256)):
+    # small (one-CTA), mid (cluster shared memory) and large (L2-resident cluster Jacobi)
+    # routes, and mixed small/large pairs
+    for p, q in ((5, 3), (65, 64), (101, 1), (257, 256), (513, 512), (769, 768), (300, 40)):
         mk = lambda k: (lambda a: a @ a.T / k + 0.3 * np.eye(k))(rng.standard_normal((k, k)))  # noqa: E731
         a1, a2, b1, b2 = mk(p), mk(p), mk(q), mk(q)
         g = rng.standard_normal((q, p))
@@ -415,8 +417,8 @@ def test_tiny_batches_match_oracle(n_int, n_bnd):
 
 @pytest.mark.parametrize("cluster", ["8", "0"], ids=["cluster8", "cusolver"])
 def test_mid_size_pairs_other_routes_match_reference(cluster):
-    """c4's mid-size factor pairs through the 8-CTA-cluster solver and through the cuSOLVER
-    fallback (taken when no cluster launch can be scheduled) match the reference goldens too
+    """c4's mid-size factor pairs through the 8-CTA-cluster solver and (KP_MID_CLUSTER=0)
+    through the L2-resident large-pair solver match the reference goldens too
     (KP_MID_CLUSTER is read once per process, hence the subprocess)."""
     import os
     import subprocess

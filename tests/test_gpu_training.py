@@ -29,8 +29,8 @@ def test_run_training_matches_reference_log(name, tmp_path):
     if cfg.optimizer == "kfac":
         assert np.array_equal(got[:, 5], ref[:, 5])                  # line-search alpha (exact)
     else:
-        assert np.allclose(got[:, 5:7], ref[:, 5:7], rtol=1e-7, atol=1e-12)
-    assert np.allclose(got[:, 1:5], ref[:, 1:5], rtol=1e-7, atol=0)  # losses, total, L2 error
+        assert np.allclose(got[:, 5:7], ref[:, 5:7], rtol=1e-8, atol=1e-12)
+    assert np.allclose(got[:, 1:5], ref[:, 1:5], rtol=1e-8, atol=0)  # losses, total, L2 error
     # the reference's file formats
     rows = list(csv.reader(l for l in open(tmp_path / "log.csv") if not l.startswith("#")))
     assert rows[0] == ["step", "wall_time_s", "loss_interior", "loss_boundary", "loss_total",

@@ -89,6 +89,10 @@ def main():
     res["workload"] = wl.name
     res["n_interior"] = a.n_interior
     res["chunk"] = int(eng.prob.chunk)
+    import ctypes as C
+    sw = [C.c_int32() for _ in range(3)]
+    eng.lib.kp_solver_sweeps(*[C.byref(v) for v in sw], 0)
+    res["max_sweeps"] = {"small": sw[0].value, "mid": sw[1].value, "large": sw[2].value}
     print(json.dumps(res))
 
 
