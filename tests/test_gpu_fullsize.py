@@ -26,9 +26,9 @@ from paper_2405_15603_b200.dist import make_rank_engine  # noqa: E402
 N, NB = 16384, 5461
 
 
-def _run(chunk, kind, steps):
+def _run(chunk, kind, steps, n=N, nb=NB):
     wl = cfgs.WORKLOADS["c5"]
-    prob, params, batch = wl.build(0, N, NB)
+    prob, params, batch = wl.build(0, n, nb)
     eng = make_rank_engine(wl.widths, batch, prob, 0, 1, ema=wl.ema, damping=wl.damping,
                            momentum=wl.momentum, chunk=chunk)
     eng.use_graph = False
@@ -69,3 +69,68 @@ def test_c5_n16384_four_chunks_equal_one_chunk(kind, steps):
             # step-1 factors are plain sums over points; the rest passes through the solves
             tol = 1e-12 if (t == 0 and key not in ("theta", "prev")) else 1e-10
             assert max_rel(b[key], a[key]) <= tol, (t, key, max_rel(b[key], a[key]))
+
+
+def test_c5_n65536_eight_point_shards_match_one_gpu():
+    """SURVEY.md §8(e) at BASELINE c5's largest sweep point (N_Omega = 65536, N_b = 21845):
+    eight point shards (one engine per emulated rank, exchange buffers summed on the host in
+    rank order, per-layer solves distributed by dist.layer_owners) take the same two KFAC
+    steps as one GPU with the whole batch: identical line-search alpha, losses and line-search
+    losses to 1e-12 / 1e-10, parameters to 1e-10 on every rank."""
+    from paper_2405_15603_b200.dist import layer_owners
+
+    n, nb, world = 65536, 21845, 8
+    one = _run(0, "kfac", 2, n, nb)
+    wl = cfgs.WORKLOADS["c5"]
+    prob, params, batch = wl.build(0, n, nb)
+    owners = layer_owners(wl.widths, world)
+    ranks = []
+    for r in range(world):
+        e = make_rank_engine(wl.widths, batch, prob, r, world, ema=wl.ema, damping=wl.damping,
+                             momentum=wl.momentum, chunk=1024)
+        e.use_graph = False
+        e.load_params(params)
+        e.init_factors(True)
+        ranks.append(e)
+
+    def all_reduce(bufs):
+        total = bufs[0].clone()
+        for b in bufs[1:]:
+            total += b
+        for b in bufs:
+            b.copy_(total)
+
+    try:
+        for t in range(2):
+            for e in ranks:
+                e.phase("accumulate")
+            all_reduce([e.reduce_buffer() for e in ranks])
+            for r, e in enumerate(ranks):
+                e.phase("precondition_owned", owned=[o == r for o in owners])
+            all_reduce([e.direction_buffer() for e in ranks])
+            for e in ranks:
+                e.phase("direction")
+                e.phase("linesearch")
+            all_reduce([e.linesearch_buffer() for e in ranks])
+            for e in ranks:
+                e.phase("update")
+            outs = []
+            for e in ranks:
+                sc, code = e.finish_step()
+                assert code == 0, (t, code)
+                outs.append(np.array([sc[0], sc[1], sc[2], sc[3]]))
+            assert all(np.array_equal(o, outs[0]) for o in outs)
+            ref = one[t]
+            tol = 1e-12 if t == 0 else 1e-10
+            assert outs[0][2] == ref["scalars"][2], (t, outs[0], ref["scalars"])  # alpha
+            assert max_rel(outs[0][:2], ref["scalars"][:2]) <= tol
+            thetas = [e.theta_numpy() for e in ranks]
+            assert all(np.array_equal(th, thetas[0]) for th in thetas[1:])
+            assert max_rel(thetas[0], ref["theta"]) <= 1e-10, (t, max_rel(thetas[0], ref["theta"]))
+            ls, lref = ranks[0].ls_losses.cpu().numpy(), ref["ls"]
+            tot = lref.reshape(-1, 2).sum(axis=1)
+            keep = np.isfinite(tot) & (tot <= 1e3 * np.nanmin(tot))
+            assert max_rel(ls.reshape(-1, 2)[keep], lref.reshape(-1, 2)[keep]) <= tol
+    finally:
+        for e in ranks:
+            e.close()
