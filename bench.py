@@ -345,9 +345,11 @@ def run_ours(args):
         eng.init_factors(identity=True)
 
     reset_state()
+    # the timed steps continue the warm-up run: steps W+1 .. W+K of one optimisation from
+    # identity factors (the Kronecker solves warm-start from the previous step's eigenbasis,
+    # as in a training run; the first steps after an identity start need more Jacobi sweeps)
     for _ in range(args.warmup):
         do_step()
-    reset_state()
     barrier()
     clocks = ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ else local)
     clocks.start()
@@ -435,6 +437,8 @@ def run_ours(args):
                        "n_boundary_per_gpu": nb_loc, "n_interior_total": n_glob,
                        "n_boundary_total": nb_glob, "chunk": chunk,
                        "parallelism": f"dp{world}",
+                       "timed_steps": f"steps {args.warmup + 1}..{args.warmup + args.steps} of one run "
+                                      "from identity factors (the warm-up steps come first)",
                        "l2": "working set (Taylor states, GBs) far larger than the 126 MB L2"},
             "kfac_steps_per_s": steps_per_s,
             "alg_tflops_per_s": f_step * steps_per_s / 1e12,

@@ -40,6 +40,9 @@ namespace kp {
 namespace {
 
 constexpr int MID_MAXN = 288;
+// Without V (U-only mode) a record is one column, so 16-CTA clusters hold columns up to
+// MID_MAXN_WIDE (c5's 512 / 513 pairs): 17 warps per CTA, 38 records of 544 doubles.
+constexpr int MID_MAXN_WIDE = 544;
 constexpr int MID_MAX_SWEEPS = 40;
 
 __device__ int g_mid_sweeps_max = 0;  // diagnostic: most sweeps used by any solve
@@ -64,12 +67,12 @@ __device__ __forceinline__ double warp_allsum(double v) {
 // outgoing columns (last top slot -> right neighbour, first bottom slot -> left neighbour)
 // also store them into the neighbour's landing record.  Between the two halves of the
 // cluster barrier each CTA writes the next round's slot table.
-template <int CL, int EF>
-__global__ void __launch_bounds__(((MID_MAXN / 2 + CL - 1) / CL) * 32, 1)
+template <int CL, int EF, bool ACCV, int MAXN = MID_MAXN>
+__global__ void __launch_bounds__(((MAXN / 2 + CL - 1) / CL) * 32, 1)
     k_eig_mid(int n, double* __restrict__ rv, double* __restrict__ lam, int* __restrict__ info,
               const int* __restrict__ chol_info, double tol, int* __restrict__ warm_valid,
               long long* prof) {
-  constexpr int MAXPPC = (MID_MAXN / 2 + CL - 1) / CL;
+  constexpr int MAXPPC = (MAXN / 2 + CL - 1) / CL;
   cg::cluster_group cluster = cg::this_cluster();
   long long t_rot = 0, t_sync = 0, t_upd = 0, t0 = 0;
   const int c = (int)cluster.block_rank();
@@ -83,7 +86,7 @@ __global__ void __launch_bounds__(((MID_MAXN / 2 + CL - 1) / CL) * 32, 1)
   extern __shared__ double msm[];
   const int ppc = mid_ppc(n, CL);
   const int m = 2 * CL * ppc;  // padded column count (columns >= n are zero)
-  const size_t cs2 = 2 * (size_t)n;  // one column record: R (n) then V (n)
+  const size_t cs2 = (ACCV ? 2 : 1) * (size_t)n;  // one column record: R (n) [then V (n)]
   double* buf = msm;  // 2 ppc + 4 records: the slots' columns and 4 landing records
   // land[dir][par]: the record a neighbour stores its handed-over column into in rounds of
   // parity par (dir 0: from the left, 1: from the right).  After the round the record joins
@@ -117,7 +120,7 @@ __global__ void __launch_bounds__(((MID_MAXN / 2 + CL - 1) / CL) * 32, 1)
     const int k = b < ppc ? b : b - ppc;
     const int col = 2 * (c * ppc + k) + (b < ppc ? 0 : 1);
     buf[b * cs2 + i] = (col < n && i <= col) ? rv[(size_t)col * n + i] : 0.0;
-    buf[b * cs2 + n + i] = (i == col) ? 1.0 : 0.0;
+    if (ACCV) buf[b * cs2 + n + i] = (i == col) ? 1.0 : 0.0;
   }
   cluster.sync();  // every CTA initialised before any remote store
 
@@ -179,19 +182,17 @@ __global__ void __launch_bounds__(((MID_MAXN / 2 + CL - 1) / CL) * 32, 1)
             const int i = lane + 32 * u;
             if (u < EF || tl) {
               const double xr = cs * x[u] - sn * y[u], yr = sn * x[u] + cs * y[u];
-              const double pu = vp[i], qu = vq[i];
-              const double xv = cs * pu - sn * qu, yv = sn * pu + cs * qu;
               rp[i] = xr;
               rq[i] = yr;
-              vp[i] = xv;
-              vq[i] = yv;
-              if (send_r) {
-                dr[i] = xr;
-                dr[n + i] = xv;
-              }
-              if (send_l) {
-                dl[i] = yr;
-                dl[n + i] = yv;
+              if (send_r) dr[i] = xr;
+              if (send_l) dl[i] = yr;
+              if (ACCV) {
+                const double pu = vp[i], qu = vq[i];
+                const double xv = cs * pu - sn * qu, yv = sn * pu + cs * qu;
+                vp[i] = xv;
+                vq[i] = yv;
+                if (send_r) dr[n + i] = xv;
+                if (send_l) dl[n + i] = yv;
               }
             }
           }
@@ -203,11 +204,11 @@ __global__ void __launch_bounds__(((MID_MAXN / 2 + CL - 1) / CL) * 32, 1)
             if (u < EF || tl) {
               if (send_r) {
                 dr[i] = x[u];
-                dr[n + i] = vp[i];
+                if (ACCV) dr[n + i] = vp[i];
               }
               if (send_l) {
                 dl[i] = y[u];
-                dl[n + i] = vq[i];
+                if (ACCV) dl[n + i] = vq[i];
               }
             }
           }
@@ -265,7 +266,7 @@ __global__ void __launch_bounds__(((MID_MAXN / 2 + CL - 1) / CL) * 32, 1)
     double a = 0.0;
     for (int i = lane; i < n; i += 32) {
       a = fma(r[i], r[i], a);
-      rv[(size_t)col * n + i] = r[n + i];
+      rv[(size_t)col * n + i] = ACCV ? r[n + i] : r[i];
     }
     a = warp_allsum(a);
     if (lane == 0) lam[col] = a;
@@ -285,30 +286,50 @@ __global__ void __launch_bounds__(((MID_MAXN / 2 + CL - 1) / CL) * 32, 1)
 }
 
 template <int CL>
-size_t mid_smem(int n) {
-  return (size_t)(2 * mid_ppc(n, CL) + 4) * 2 * n * sizeof(double);  // slots + landing records
+size_t mid_smem(int n, bool accv) {  // slots + landing records
+  return (size_t)(2 * mid_ppc(n, CL) + 4) * (accv ? 2 : 1) * n * sizeof(double);
 }
 
 // Cluster size: 16 when the device can co-schedule 16-CTA clusters of this kernel
 // (non-portable size), else 8.
 template <int CL>
 bool mid_setup() {
-  auto kern = k_eig_mid<CL, MID_MAXN / 32>;
   bool ok = true;
-  auto attrs = [&](auto k) {
+  auto attrs = [&](auto k, bool accv) {
     ok = ok && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)mid_smem<CL>(MID_MAXN)) == cudaSuccess;
+                                    (int)mid_smem<CL>(MID_MAXN, accv)) == cudaSuccess;
     if (CL > 8)
       ok = ok && cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
                      cudaSuccess;
   };
-  attrs(k_eig_mid<CL, 3>);
-  attrs(k_eig_mid<CL, 4>);
-  attrs(k_eig_mid<CL, 5>);
-  attrs(k_eig_mid<CL, 6>);
-  attrs(k_eig_mid<CL, 7>);
-  attrs(k_eig_mid<CL, 8>);
-  attrs(k_eig_mid<CL, 9>);
+#define KP_MID_ATTRS(E)               \
+  attrs(k_eig_mid<CL, E, true>, true); \
+  attrs(k_eig_mid<CL, E, false>, false);
+  KP_MID_ATTRS(3)
+  KP_MID_ATTRS(4)
+  KP_MID_ATTRS(5)
+  KP_MID_ATTRS(6)
+  KP_MID_ATTRS(7)
+  KP_MID_ATTRS(8)
+  KP_MID_ATTRS(9)
+#undef KP_MID_ATTRS
+  if (CL == 16) {  // wide U-only instances
+    auto wide = [&](auto k) {
+      ok = ok && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)mid_smem<16>(MID_MAXN_WIDE, false)) == cudaSuccess;
+      ok = ok && cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                     cudaSuccess;
+    };
+    wide(k_eig_mid<16, 9, false, MID_MAXN_WIDE>);
+    wide(k_eig_mid<16, 10, false, MID_MAXN_WIDE>);
+    wide(k_eig_mid<16, 11, false, MID_MAXN_WIDE>);
+    wide(k_eig_mid<16, 12, false, MID_MAXN_WIDE>);
+    wide(k_eig_mid<16, 13, false, MID_MAXN_WIDE>);
+    wide(k_eig_mid<16, 14, false, MID_MAXN_WIDE>);
+    wide(k_eig_mid<16, 15, false, MID_MAXN_WIDE>);
+    wide(k_eig_mid<16, 16, false, MID_MAXN_WIDE>);
+    wide(k_eig_mid<16, 17, false, MID_MAXN_WIDE>);
+  }
   if (!ok) {
     cudaGetLastError();
     return false;
@@ -316,7 +337,7 @@ bool mid_setup() {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(CL);
   cfg.blockDim = dim3(mid_ppc(MID_MAXN, CL) * 32);
-  cfg.dynamicSmemBytes = mid_smem<CL>(MID_MAXN);
+  cfg.dynamicSmemBytes = mid_smem<CL>(MID_MAXN, true);
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = CL;
@@ -325,7 +346,9 @@ bool mid_setup() {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   int nc = 0;
-  if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) != cudaSuccess || nc < 1) {
+  if (cudaOccupancyMaxActiveClusters(&nc, k_eig_mid<CL, MID_MAXN / 32, true>, &cfg) !=
+          cudaSuccess ||
+      nc < 1) {
     cudaGetLastError();
     return false;
   }
@@ -334,12 +357,12 @@ bool mid_setup() {
 
 template <int CL>
 void launch_mid(int n, double* rv, double* lam, int* info, const int* chol_info,
-                cudaStream_t s, int* warm_valid, long long* prof) {
+                cudaStream_t s, int* warm_valid, long long* prof, bool accv) {
   const double tol = fmax(1e-14, 2.0 * n * DBL_EPSILON);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(CL);
   cfg.blockDim = dim3(mid_ppc(n, CL) * 32);
-  cfg.dynamicSmemBytes = mid_smem<CL>(n);
+  cfg.dynamicSmemBytes = mid_smem<CL>(n, accv);
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -348,11 +371,37 @@ void launch_mid(int n, double* rv, double* lam, int* info, const int* chol_info,
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  if (n > MID_MAXN) {  // wide U-only instances (CL == 16 and !accv: see mid_eig_max_n)
+    switch (n / 32) {
+#define KP_MID_WIDE(E)                                                                        \
+  case E:                                                                                     \
+    cudaLaunchKernelEx(&cfg, k_eig_mid<16, E, false, MID_MAXN_WIDE>, n, rv, lam, info,        \
+                       chol_info, tol, warm_valid, prof);                                     \
+    break;
+      KP_MID_WIDE(9)
+      KP_MID_WIDE(10)
+      KP_MID_WIDE(11)
+      KP_MID_WIDE(12)
+      KP_MID_WIDE(13)
+      KP_MID_WIDE(14)
+      KP_MID_WIDE(15)
+      KP_MID_WIDE(16)
+      KP_MID_WIDE(17)
+#undef KP_MID_WIDE
+      default:
+        break;
+    }
+    return;
+  }
   switch (n / 32) {
-#define KP_MID_CASE(E)                                                                     \
-  case E:                                                                                  \
-    cudaLaunchKernelEx(&cfg, k_eig_mid<CL, E>, n, rv, lam, info, chol_info, tol, warm_valid, \
-                       prof);                                                              \
+#define KP_MID_CASE(E)                                                                        \
+  case E:                                                                                     \
+    if (accv)                                                                                 \
+      cudaLaunchKernelEx(&cfg, k_eig_mid<CL, E, true>, n, rv, lam, info, chol_info, tol,      \
+                         warm_valid, prof);                                                   \
+    else                                                                                      \
+      cudaLaunchKernelEx(&cfg, k_eig_mid<CL, E, false>, n, rv, lam, info, chol_info, tol,     \
+                         warm_valid, prof);                                                   \
     break;
     KP_MID_CASE(3)
     KP_MID_CASE(4)
@@ -371,6 +420,14 @@ int g_mid_cl = 0;  // 0: not chosen yet
 
 }  // namespace
 
+bool mid_eig_accumulate_v() {
+  static const bool acc = [] {
+    const char* e = getenv("KP_MID_ACCV");
+    return e && atoi(e) == 1;
+  }();
+  return acc;
+}
+
 int mid_eig_cluster_size() {
   if (g_mid_cl == 0) {
     const char* env = getenv("KP_MID_CLUSTER");
@@ -382,7 +439,11 @@ int mid_eig_cluster_size() {
 
 // 0 when no cluster launch of the kernel can be scheduled: the pairs then take the large-pair
 // route (kp_eig_large.cu).
-int mid_eig_max_n() { return mid_eig_cluster_size() > 0 ? MID_MAXN : 0; }
+int mid_eig_max_n() {
+  const int cl = mid_eig_cluster_size();
+  if (cl <= 0) return 0;
+  return (cl == 16 && !mid_eig_accumulate_v()) ? MID_MAXN_WIDE : MID_MAXN;
+}
 
 int mid_eig_sweeps_used(bool reset) {
   int v = 0;
@@ -396,14 +457,15 @@ int mid_eig_sweeps_used(bool reset) {
 
 void launch_eig_mid(int n, double* rv, double* lam, int* info, const int* chol_info,
                     cudaStream_t s, int* warm_valid, long long* prof) {
+  const bool accv = mid_eig_accumulate_v();
   count_launch();
   // 16-CTA clusters for the large pairs (the critical path); pairs up to 160 use 8 CTAs,
   // which leaves SMs (and whole GPCs) free for the large pairs' clusters (c4 precondition
   // 6.41 -> 5.68 ms)
   constexpr int kSmallN = 160;
   if (mid_eig_cluster_size() == 16 && n > kSmallN)
-    launch_mid<16>(n, rv, lam, info, chol_info, s, warm_valid, prof);
-  else launch_mid<8>(n, rv, lam, info, chol_info, s, warm_valid, prof);
+    launch_mid<16>(n, rv, lam, info, chol_info, s, warm_valid, prof, accv);
+  else launch_mid<8>(n, rv, lam, info, chol_info, s, warm_valid, prof, accv);
 }
 
 }  // namespace kp

@@ -17,6 +17,8 @@
 // Kronecker-sum system is unique, so it matches the reference's LAPACK route to
 // roundoff (tests/test_gpu_parity.py).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "../../include/kfac_pinn_b200.h"
 #include "kp_common.cuh"
@@ -38,6 +40,9 @@ constexpr double kJacobiTol = 1e-14;
 __host__ __device__ inline int eig_pitch(int n) { return ((n + 15) / 16) * 16 + 1; }
 
 __device__ int g_eig_sweeps_max = 0;  // diagnostic: most Jacobi sweeps used by any job
+// diagnostic (KP_EIG_TRACE=1): per sweep, print the largest |cos| between two rows and the
+// number of rotations applied
+__device__ int g_eig_trace = 0;
 
 __device__ __forceinline__ void set_status_dev(int32_t* status, int32_t code) {
   atomicCAS(status, 0, code);
@@ -62,8 +67,15 @@ __device__ __forceinline__ void jacobi_rows(double* G, double* W, int n, int ld,
   const int npair = m / 2;
   const bool active = k < npair;
   const double tol2 = tol * tol;
+  __shared__ unsigned long long tr_max;
+  __shared__ int tr_rot;
+  const bool trace = g_eig_trace != 0;
   for (int sweep = 0; sweep < EIG_MAX_SWEEPS; ++sweep) {
-    if (tid == 0) *flag = 0;
+    if (tid == 0) {
+      *flag = 0;
+      tr_max = 0ull;
+      tr_rot = 0;
+    }
     __syncthreads();
     int ia = k > 0 ? k - 1 : 0, ib = m - 2 - k;
     for (int round = 0; round < m - 1; ++round) {
@@ -92,9 +104,12 @@ __device__ __forceinline__ void jacobi_rows(double* G, double* W, int n, int ld,
             be += __shfl_xor_sync(hmask, be, o);
             ga += __shfl_xor_sync(hmask, ga, o);
           }
+          if (trace && hl == 0 && al > 0.0 && be > 0.0)
+            atomicMax(&tr_max, (unsigned long long)__double_as_longlong(fabs(ga) / sqrt(al * be)));
           if (ga * ga > tol2 * (al * be) && fabs(ga) > 1e-300) {
             double cs, sn;
             jacobi_angle(al, be, ga, cs, sn);
+            if (trace && hl == 0) atomicAdd(&tr_rot, 1);
             double* wp = W + p * ld + hl;
             double* wq = W + q * ld + hl;
 #pragma unroll
@@ -112,6 +127,9 @@ __device__ __forceinline__ void jacobi_rows(double* G, double* W, int n, int ld,
       __syncthreads();
     }
     const int rotated = *flag;
+    if (trace && tid == 0)
+      printf("[kp eig small] block %d n %d sweep %d max|cos| %.3e rotations %d\n", blockIdx.x, n,
+             sweep, __longlong_as_double((long long)tr_max), tr_rot);
     __syncthreads();
     if (rotated == 0) {
       if (tid == 0) atomicMax(&g_eig_sweeps_max, sweep + 1);
@@ -481,6 +499,11 @@ void launch_gen_eig_small(const SmallEigJobs& jobs, int njobs, int max_n, int32_
   if (!attr_set) {
     cudaFuncSetAttribute(k_gen_eig_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)small_eig_smem_bytes(EIG_MAXN));
+    const char* e = getenv("KP_EIG_TRACE");
+    if (e && atoi(e) == 1) {
+      const int one = 1;
+      cudaMemcpyToSymbol(g_eig_trace, &one, sizeof(int));
+    }
     attr_set = true;
   }
   count_launch();

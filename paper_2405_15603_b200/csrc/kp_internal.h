@@ -338,18 +338,24 @@ int mid_eig_max_n();
 int mid_eig_sweeps_used(bool reset = false);
 int small_eig_sweeps_used(bool reset = false);
 int mid_eig_cluster_size();  // 16, 8, or -1 when no cluster launch is possible
+// Rows out of launch_eig_mid: U = R V (default; the caller forms T'^T = U^T K^-1) or,
+// KP_MID_ACCV=1, the eigenvectors V accumulated in the kernel (T'^T = V^T L^-1)
+bool mid_eig_accumulate_v();
 void launch_eig_mid(int n, double* rv, double* lam, int* info, const int* chol_info,
                     cudaStream_t s, int* warm_valid = nullptr, long long* prof = nullptr);
 // kp_eig_large.cu: one-sided Jacobi with the vectors in L2, one 16-CTA cluster per pair, for
-// mid_eig_max_n() < n <= large_eig_max_n(); U (n x n row-major): the rows of L_C in,
+// mid_eig_max_n() < n <= large_eig_max_n(); U (n x n row-major, even pitch ld): the rows of L_C in,
 // orthogonalised rows out; V (n x n): the eigenvectors of C as rows
 int large_eig_max_n();
 // T^T = U^T K^-1 from the orthogonalised rows U (default), or KP_LARGE_ACCV=1: V accumulated
 // in the kernel and T^T = V^T L^-1
 bool large_eig_accumulate_v();
 int large_eig_sweeps_used(bool reset = false);
-void launch_eig_large(int n, double* U, double* V, double* lam, int* info, const int* chol_info,
-                      cudaStream_t s, int* warm_valid = nullptr);
+// gtail (optional, U-only): 16 (2 ceil(ceil(n/2)/16) + 4) (n - 512) doubles of scratch for
+// the split-record kernel (544 < n <= 800: record heads in smem, tails in L2)
+void launch_eig_large(int n, int ld, double* U, double* V, double* lam, int* info,
+                      const int* chol_info, cudaStream_t s, int* warm_valid = nullptr,
+                      double* gtail = nullptr);
 size_t small_eig_smem_bytes(int n);
 void launch_gen_eig_small(const SmallEigJobs& jobs, int njobs, int max_n, int32_t* status,
                           cudaStream_t s);

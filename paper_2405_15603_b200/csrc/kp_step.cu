@@ -149,8 +149,8 @@ struct Plan {
 };
 
 // Scratch of the device generalised eigensolver per factor pair (gen_eig_pair): M1 / K, and
-// two n x n work matrices.
-inline int64_t pair_scratch_doubles(int n) { return 3LL * n * n; }
+// two n x n work matrices (n x (n + 1) each: the large-pair Jacobi wants an even row pitch).
+inline int64_t pair_scratch_doubles(int n) { return 3LL * n * (n + 1); }
 
 // Largest factor size the device solvers handle (small / mid / large route).
 inline int max_pair_n() {
@@ -852,10 +852,12 @@ int phase_accumulate(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, cons
 // same launches serve cold and warm steps):
 //   M_i' = T_p^T M_i T_p,  M2' = L L^T,  M1' = K K^T  (blocked Cholesky, kp_dense.cu),
 //   L_C = L^-1 K  (lower triangular: C = L^-1 M1' L^-T = L_C L_C^T, R = L_C^T),
-// then one-sided Jacobi on the rows of L_C (= the columns of R):
-//   n <= mid_eig_max_n(): R and V in a thread-block cluster's shared memory (kp_eig_mid.cu),
-//   larger:               R and V in L2, one 16-CTA cluster (kp_eig_large.cu);
-// T' = L^-T V, i.e. T'^T = V^T L^-1;
+// then one-sided Jacobi on the rows of L_C (= the columns of R), U = R V with orthogonal
+// columns (C V = V diag(||u_i||^2)):
+//   n <= mid_eig_max_n(): R in a thread-block cluster's shared memory (kp_eig_mid.cu),
+//   larger:               R in L2, one 16-CTA cluster (kp_eig_large.cu);
+// T' = L^-T V = K^-T U (K^-T U = L^-T L_C^-T R V), i.e. T'^T = U^T K^-1, so V is never
+// accumulated (KP_MID_ACCV=1 / KP_LARGE_ACCV=1: the kernels rotate V too, T'^T = V^T L^-1);
 // and T = T_p T'.  Out: tout = T^T row-major (= T column-major), lam = eigenvalues; the same
 // T^T is kept in tp for the next step.  chol_info[0..1]: Cholesky infos of M2', M1' (a failure
 // makes the eigensolver report info = n + 1: not positive definite).
@@ -863,10 +865,11 @@ int phase_accumulate(const Ctx& c, const kp_kfac_config* cfg, kp_state* st, cons
 int gen_eig_pair(cudaStream_t s, int n, const double* f1, const double* f2, double lam,
                  double* tout, double* m2, double* ev, double* scratch, int* info, int* chol_info,
                  double* tp, int* valid) {
-  const size_t nn = (size_t)n * n;
+  const size_t region = (size_t)n * (n + 1);
+  const int ld2 = n + (n & 1);  // even row pitch of the Jacobi rows (16-byte aligned)
   double* m1 = scratch;
-  double* s1 = scratch + nn;
-  double* s2 = scratch + 2 * nn;
+  double* s1 = scratch + region;
+  double* s2 = scratch + 2 * region;
   KP_CUDA_TRY(cudaMemsetAsync(chol_info, 0, 2 * sizeof(int), s));
   launch_damped_copy(f1, lam, n, m1, s);
   launch_damped_copy(f2, lam, n, m2, s);
@@ -879,18 +882,26 @@ int gen_eig_pair(cudaStream_t s, int n, const double* f1, const double* f2, doub
   launch_cholesky(n, m1, n, chol_info + 1, s);  // K
   launch_zero_upper(n, m1, n, s);
   launch_trsm_lower(n, m2, n, s1, n, n, true, s);  // s1 = L^-1
-  launch_dense_gemm(DenseGemm{n, n, n, s1, n, false, m1, n, false, s2, n, 1.0, 0.0, false}, s);
-  double* vt = s2;
-  if (n <= mid_eig_max_n()) {
-    launch_eig_mid(n, s2, ev, info, chol_info, s, valid);  // s2 <- V^T
+  const bool mid = n <= mid_eig_max_n();
+  const int lu = mid ? n : ld2;  // pitch of the Jacobi rows
+  launch_dense_gemm(DenseGemm{n, n, n, s1, n, false, m1, n, false, s2, lu, 1.0, 0.0, false}, s);
+  const double* vt = s2;  // rows: V^T (eigenvectors accumulated) or U^T
+  int lv = lu;
+  bool u_rows = true;
+  if (mid) {
+    launch_eig_mid(n, s2, ev, info, chol_info, s, valid);
+    u_rows = !mid_eig_accumulate_v();
   } else if (large_eig_accumulate_v()) {
-    launch_eig_large(n, s2, m1, ev, info, chol_info, s, valid);  // s2 <- U^T, m1 <- V^T
+    launch_eig_large(n, ld2, s2, m1, ev, info, chol_info, s, valid);  // m1 <- V^T (pitch ld2)
     vt = m1;
-  } else {  // T' = K^-T U  (K^-T U = L^-T L_C^-T R V = L^-T V)
-    launch_eig_large(n, s2, nullptr, ev, info, chol_info, s, valid);  // s2 <- U^T
-    launch_trsm_lower(n, m1, n, s1, n, n, true, s);                   // s1 = K^-1
+    u_rows = false;
+  } else {
+    // s1 (L^-1) is dead until K^-1 is formed below: the split-record tails live there
+    launch_eig_large(n, ld2, s2, nullptr, ev, info, chol_info, s, valid, s1);
   }
-  launch_dense_gemm(DenseGemm{n, n, n, vt, n, false, s1, n, false, m2, n, 1.0, 0.0, false}, s);
+  // T'^T = U^T K^-1 (K^-T U = L^-T V) or V^T L^-1
+  if (u_rows) launch_trsm_lower(n, m1, n, s1, n, n, true, s);  // s1 = K^-1
+  launch_dense_gemm(DenseGemm{n, n, n, vt, lv, false, s1, n, false, m2, n, 1.0, 0.0, false}, s);
   // T^T = T'^T T_p^T
   launch_dense_gemm(DenseGemm{n, n, n, m2, n, false, tp, n, false, tout, n, 1.0, 0.0, false}, s);
   launch_copy_matrix(tout, n, n, n, tp, n, s);
@@ -1618,8 +1629,8 @@ int32_t kp_kfac_phase_update(kp_context* ctx, const kp_problem* prob, const kp_k
 }
 
 // Early preconditioning for single-call steps (Ctx::early): per-layer contractions (not the
-// grouped small-network launch) and at least one factor pair outside the one-launch small
-// solver.  KP_EARLY_PRECOND=0 turns it off (measurements).
+// grouped small-network launch), at least one factor pair outside the one-launch small
+// solver and none above 288 (c4).  KP_EARLY_PRECOND=0 turns it off (measurements).
 static int setup_early(Ctx& c) {
   static const bool enabled = [] {
     const char* e = getenv("KP_EARLY_PRECOND");
@@ -1628,9 +1639,15 @@ static int setup_early(Ctx& c) {
   const Plan& P = c.P;
   if (!enabled || P.tn_grouped) return KP_OK;
   bool any = false;
-  for (int l = 0; l < P.L; ++l)
+  int maxn = 0;
+  for (int l = 0; l < P.L; ++l) {
     any |= std::max(P.p[l], P.q[l]) > small_eig_max_n();
-  if (!any) return KP_OK;
+    maxn = std::max(maxn, std::max(P.p[l], P.q[l]));
+  }
+  // Pairs above 288 run 16-CTA clusters for tens of milliseconds (c5: 512-769); started
+  // during the accumulate phase they take SMs from its contractions and the step gets
+  // slower (c5 N = 16384: 4523 vs 4483 ms per step), so they wait for the phase to end.
+  if (!any || maxn > 288) return KP_OK;
   KP_TRY(ensure_side_streams(c.ctx, 2 * P.L + 2));
   c.early = true;
   return KP_OK;
@@ -1874,7 +1891,7 @@ int32_t kp_kron_solve_workspace_bytes(kp_context* ctx, int32_t p, int32_t q, siz
   // the solver scratch plus a warm-start T (identity: a standalone solve is cold)
   int64_t doubles = 2LL * p * p + 2LL * q * q + p + q + 2LL * p * q + 8 + 16 * 32;
   for (int n : {p, q})
-    if (n > small_eig_max_n()) doubles += pair_scratch_doubles(n) + (int64_t)n * n + 32;
+    if (n > small_eig_max_n()) doubles += pair_scratch_doubles(n) + (int64_t)n * n + 32 + 96;
   *bytes = (size_t)doubles * sizeof(double);
   return KP_OK;
 }
@@ -1935,12 +1952,14 @@ int32_t kp_kron_sum_solve(kp_context* ctx, int32_t p, int32_t q, const double* a
       ej.job[ne++] = SmallEigJob{n, f1, f2, 0.0, t, ev, info + k, 1};
       continue;
     }
-    double* scratch = c.at(o2);
-    o2 += pair_scratch_doubles(n);
-    double* tp = c.at(o2);
-    o2 += (int64_t)n * n;
-    int* valid = reinterpret_cast<int*>(c.at(o2));
-    o2 += 32;
+    auto take2 = [&](int64_t k) {  // 32-double (256-byte) aligned sub-allocations
+      double* at = c.at(o2);
+      o2 += (k + 31) / 32 * 32;
+      return at;
+    };
+    double* scratch = take2(pair_scratch_doubles(n));
+    double* tp = take2((int64_t)n * n);
+    int* valid = reinterpret_cast<int*>(take2(32));
     KP_CUDA_TRY(cudaMemsetAsync(valid, 0, sizeof(int), s));
     KP_TRY(gen_eig_pair(s, n, f1, f2, 0.0, t, c.at(k == 0 ? P.o_A2 : P.o_B2), ev, scratch,
                         info + k, info + 2 + 2 * k, tp, valid));
