@@ -42,7 +42,8 @@ namespace {
 
 constexpr int LG_CL = 16;            // cluster size (non-portable)
 constexpr int LG_MAX_SWEEPS = 60;
-constexpr int LG_MAXN = 1055;
+constexpr int LG_MAXN = 1087;      // register-cached kernels (k_eig_large)
+constexpr int LG_MAXN_ANY = 16383;  // streaming kernel: bounded only by memory
 
 __device__ int g_large_sweeps_max = 0;  // diagnostic: most sweeps used by any solve
 
@@ -179,6 +180,111 @@ __global__ void __launch_bounds__(W * 32, 1)
   // eigenvalues ||u_i||^2
   const int nthr_w = W * LG_CL;
   for (int i = c * W + warp; i < n; i += nthr_w) {
+    const double* ui = U + (size_t)i * ld;
+    double a = 0.0;
+    for (int e = lane; e < n; e += 32) {
+      const double v = __ldcg(ui + e);
+      a = fma(v, v, a);
+    }
+    a = warp_sum(a);
+    if (lane == 0) lam[i] = a;
+  }
+  if (c == 0 && threadIdx.x == 0) {
+    *info = converged ? 0 : 1;
+    if (warm_valid) *warm_valid = converged ? 1 : 0;
+    atomicMax(&g_large_sweeps_max, converged ? sweep + 1 : 1000 + sweep);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Any n (the fallback above 1087, where two rows no longer fit a warp's registers): the
+// same closed-form circle pairing with the rows in L2, two streaming passes per pair
+// (dot products, then rotation), 16-byte accesses, 16 warps per CTA.  No width limit other
+// than memory.
+__global__ void __launch_bounds__(16 * 32, 1)
+    k_eig_stream(int n, int ld, double* __restrict__ U, double* __restrict__ lam,
+                 int* __restrict__ info, const int* __restrict__ chol_info, double tol,
+                 int* __restrict__ warm_valid) {
+  constexpr int W = 16;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int c = (int)cluster.block_rank();
+  if (chol_info[0] != 0 || chol_info[1] != 0) {
+    if (c == 0 && threadIdx.x == 0) {
+      *info = n + 1;
+      if (warm_valid) *warm_valid = 0;
+    }
+    return;
+  }
+  __shared__ int rotated;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ppc = lg_ppc(n);
+  const int m = 2 * LG_CL * ppc;
+  const int n2 = n / 2;  // full double2 elements; an odd n leaves element n - 1 (lane 0)
+  const double tol2 = tol * tol;
+  int sweep = 0;
+  bool converged = false;
+  for (; sweep < LG_MAX_SWEEPS; ++sweep) {
+    if (threadIdx.x == 0) rotated = 0;
+    __syncthreads();
+    int any_local = 0;
+    for (int r = 0; r < m - 1; ++r) {
+      for (int k = c * ppc + warp; k < (c + 1) * ppc; k += W) {
+        const int cp = lg_col(k, r, m), cq = lg_col(m - 1 - k, r, m);
+        if (cp >= n || cq >= n) continue;
+        double* up = U + (size_t)cp * ld;
+        double* uq = U + (size_t)cq * ld;
+        double2* up2 = reinterpret_cast<double2*>(up);
+        double2* uq2 = reinterpret_cast<double2*>(uq);
+        double a = 0.0, b = 0.0, g = 0.0;
+        for (int j = lane; j < n2; j += 32) {
+          const double2 x = __ldcg(up2 + j), y = __ldcg(uq2 + j);
+          a = fma(x.x, x.x, fma(x.y, x.y, a));
+          b = fma(y.x, y.x, fma(y.y, y.y, b));
+          g = fma(x.x, y.x, fma(x.y, y.y, g));
+        }
+        if ((n & 1) && lane == 0) {
+          const double x = __ldcg(up + n - 1), y = __ldcg(uq + n - 1);
+          a = fma(x, x, a);
+          b = fma(y, y, b);
+          g = fma(x, y, g);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          a += __shfl_xor_sync(0xffffffffu, a, o);
+          b += __shfl_xor_sync(0xffffffffu, b, o);
+          g += __shfl_xor_sync(0xffffffffu, g, o);
+        }
+        if (g * g > tol2 * (a * b) && fabs(g) > 1e-300) {
+          double cs, sn;
+          jacobi_angle(a, b, g, cs, sn);
+          for (int j = lane; j < n2; j += 32) {
+            const double2 x = __ldcg(up2 + j), y = __ldcg(uq2 + j);
+            __stcg(up2 + j, make_double2(cs * x.x - sn * y.x, cs * x.y - sn * y.y));
+            __stcg(uq2 + j, make_double2(sn * x.x + cs * y.x, sn * x.y + cs * y.y));
+          }
+          if ((n & 1) && lane == 0) {
+            const double x = __ldcg(up + n - 1), y = __ldcg(uq + n - 1);
+            __stcg(up + n - 1, cs * x - sn * y);
+            __stcg(uq + n - 1, sn * x + cs * y);
+          }
+          any_local = 1;
+        }
+      }
+      asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+      asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    }
+    if (any_local && lane == 0) rotated = 1;
+    __syncthreads();
+    cluster.sync();
+    int any = 0;
+    for (int q = 0; q < LG_CL; ++q) any |= *cluster.map_shared_rank(&rotated, q);
+    cluster.sync();
+    if (!any) {
+      converged = true;
+      break;
+    }
+  }
+  for (int i = c * W + warp; i < n; i += W * LG_CL) {
     const double* ui = U + (size_t)i * ld;
     double a = 0.0;
     for (int e = lane; e < n; e += 32) {
@@ -502,6 +608,8 @@ int large_eig_max_n() {
   if (g_large_ok == 0) {
     bool ok = lg_attrs<6, 16>() && lg_attrs<8, 16>() && lg_attrs<10, 12>() &&
               lg_attrs<12, 12>() && lg_attrs<14, 12>() && lg_attrs<16, 12>();
+    ok = ok && cudaFuncSetAttribute(k_eig_stream, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                                    1) == cudaSuccess;
     g_split_ok = sp_attrs<1>() && sp_attrs<2>() && sp_attrs<3>() && sp_attrs<4>() &&
                  sp_attrs<5>();
     if (g_split_ok) {  // 16 CTAs of 800 threads and ~221 KB smem must be co-schedulable
@@ -537,7 +645,7 @@ int large_eig_max_n() {
     if (!ok) cudaGetLastError();
     g_large_ok = ok ? 1 : -1;
   }
-  return g_large_ok > 0 ? LG_MAXN : 0;
+  return g_large_ok > 0 ? LG_MAXN_ANY : 0;
 }
 
 bool large_eig_accumulate_v() {
@@ -547,6 +655,8 @@ bool large_eig_accumulate_v() {
   }();
   return acc;
 }
+
+int large_eig_accv_max_n() { return LG_MAXN; }
 
 int large_eig_sweeps_used(bool reset) {
   int v = 0;
@@ -570,7 +680,7 @@ bool large_eig_split_ok(int n) {
 void launch_eig_large(int n, int ld, double* U, double* V, double* lam, int* info,
                       const int* chol_info, cudaStream_t s, int* warm_valid, double* gtail) {
   count_launch();
-  const double tol = fmax(1e-14, 2.0 * n * DBL_EPSILON);
+  const double tol = fmax(jacobi_tol_floor(), 2.0 * n * DBL_EPSILON);
   if (!V && gtail && large_eig_split_ok(n)) {
     switch ((n - SP_H + 63) / 64) {
 #define KP_SP_CASE(E)                                                                    case E:                                                                                  sp_launch<E>(n, ld, U, lam, info, chol_info, tol, warm_valid, gtail, s);              return;
@@ -583,6 +693,21 @@ void launch_eig_large(int n, int ld, double* U, double* V, double* lam, int* inf
       default:
         break;
     }
+  }
+  if (n > LG_MAXN) {  // any width: the streaming kernel (U only)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(LG_CL);
+    cfg.blockDim = dim3(16 * 32);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = LG_CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_eig_stream, n, ld, U, lam, info, chol_info, tol, warm_valid);
+    return;
   }
   const int ef = n / 64;
   if (ef <= 6) lg_launch<6, 16>(n, ld, U, V, lam, info, chol_info, tol, warm_valid, s);

@@ -358,7 +358,7 @@ bool mid_setup() {
 template <int CL>
 void launch_mid(int n, double* rv, double* lam, int* info, const int* chol_info,
                 cudaStream_t s, int* warm_valid, long long* prof, bool accv) {
-  const double tol = fmax(1e-14, 2.0 * n * DBL_EPSILON);
+  const double tol = fmax(jacobi_tol_floor(), 2.0 * n * DBL_EPSILON);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(CL);
   cfg.blockDim = dim3(mid_ppc(n, CL) * 32);

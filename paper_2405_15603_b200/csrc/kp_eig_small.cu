@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(EIG_THREADS) k_gen_eig_small(const SmallEigJob
   }
   __syncthreads();
   {
-    const double tol = fmax(1e-14, 2.0 * n * 2.220446049250313e-16);
+    const double tol = fmax(jobs.tol_floor, 2.0 * n * 2.220446049250313e-16);
     switch (nr / 16) {
       case 1: jacobi_rows<1>(C, V, n, ld, &flag, tol); break;
       case 2: jacobi_rows<2>(C, V, n, ld, &flag, tol); break;
@@ -477,6 +477,14 @@ __global__ void __launch_bounds__(1024) k_kron_combine_small_smem(const SmallCom
 
 int small_eig_max_n() { return EIG_MAXN; }
 
+double jacobi_tol_floor() {
+  static const double v = [] {
+    const char* e = getenv("KP_JACOBI_TOL");
+    return e ? atof(e) : 1e-14;
+  }();
+  return v;
+}
+
 int small_eig_sweeps_used(bool reset) {
   int v = 0;
   cudaMemcpyFromSymbol(&v, g_eig_sweeps_max, sizeof(int));
@@ -507,7 +515,9 @@ void launch_gen_eig_small(const SmallEigJobs& jobs, int njobs, int max_n, int32_
     attr_set = true;
   }
   count_launch();
-  k_gen_eig_small<<<njobs, EIG_THREADS, smem, s>>>(jobs, status);
+  SmallEigJobs j = jobs;
+  j.tol_floor = jacobi_tol_floor();
+  k_gen_eig_small<<<njobs, EIG_THREADS, smem, s>>>(j, status);
 }
 
 void launch_kron_combine_small(const SmallCombineJobs& jobs, int njobs, cudaStream_t s) {

@@ -316,7 +316,11 @@ struct SmallEigJob {
 };
 struct SmallEigJobs {
   SmallEigJob job[32];
+  double tol_floor = 1e-14;  // set by the launcher (jacobi_tol_floor)
 };
+// Floor of the Jacobi rotation threshold |cos| > max(floor, 2 n eps) of every device
+// eigensolver: 1e-14, or KP_JACOBI_TOL (measurements of the accuracy / sweep trade-off).
+double jacobi_tol_floor();
 struct SmallCombineJob {
   int p, q;
   const double* g;   // q x p gradient
@@ -347,6 +351,7 @@ void launch_eig_mid(int n, double* rv, double* lam, int* info, const int* chol_i
 // mid_eig_max_n() < n <= large_eig_max_n(); U (n x n row-major, even pitch ld): the rows of L_C in,
 // orthogonalised rows out; V (n x n): the eigenvectors of C as rows
 int large_eig_max_n();
+int large_eig_accv_max_n();  // widest pair the V-accumulating variant handles
 // T^T = U^T K^-1 from the orthogonalised rows U (default), or KP_LARGE_ACCV=1: V accumulated
 // in the kernel and T^T = V^T L^-1
 bool large_eig_accumulate_v();

@@ -891,7 +891,7 @@ int gen_eig_pair(cudaStream_t s, int n, const double* f1, const double* f2, doub
   if (mid) {
     launch_eig_mid(n, s2, ev, info, chol_info, s, valid);
     u_rows = !mid_eig_accumulate_v();
-  } else if (large_eig_accumulate_v()) {
+  } else if (large_eig_accumulate_v() && n <= large_eig_accv_max_n()) {
     launch_eig_large(n, ld2, s2, m1, ev, info, chol_info, s, valid);  // m1 <- V^T (pitch ld2)
     vt = m1;
     u_rows = false;

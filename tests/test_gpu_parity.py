@@ -124,6 +124,8 @@ def _oracle_vs_device(widths, problem, n_int, n_bnd, steps, momentum=0.0, ema=0.
     ((3, 5, 9, 1), "poisson_norm2"),                # odd widths, K/N tails
     ((5, 33, 17, 65, 1), "heat4"),                  # partial Laplacian, ragged tiles
     ((10, 130, 70, 1), "poisson_harmonic_mixed"),   # > 128 wide, 10d
+    ((3, 600, 1), "poisson_norm2"),                 # split-record cluster Jacobi (n = 601, 600)
+    ((3, 1100, 1), "poisson_norm2"),                # > 1087: the streaming Jacobi
 ])
 def test_device_matches_oracle_various_shapes(widths, problem):
     if problem == "heat4":
@@ -223,7 +225,8 @@ def test_kron_sum_solve_matches_dense():
     rng = np.random.default_rng(4)
     # small (one-CTA), mid (cluster shared memory) and large (L2-resident cluster Jacobi)
     # routes, and mixed small/large pairs
-    for p, q in ((5, 3), (65, 64), (101, 1), (257, 256), (513, 512), (769, 768), (300, 40)):
+    for p, q in ((5, 3), (65, 64), (101, 1), (257, 256), (513, 512), (769, 768), (300, 40),
+                 (1201, 1100)):
         mk = lambda k: (lambda a: a @ a.T / k + 0.3 * np.eye(k))(rng.standard_normal((k, k)))  # noqa: E731
         a1, a2, b1, b2 = mk(p), mk(p), mk(q), mk(q)
         g = rng.standard_normal((q, p))
@@ -429,5 +432,23 @@ def test_mid_size_pairs_other_routes_match_reference(cluster):
                         os.path.join(here, "test_gpu_parity.py"), "-k",
                         "test_kfac_steps_match_reference_golden and c4"],
                        env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout and "failed" not in r.stdout, r.stdout[-500:]
+
+
+@pytest.mark.parametrize("env", [{"KP_LARGE_SPLIT": "0"}, {"KP_LARGE_ACCV": "1", "KP_MID_ACCV": "1"}])
+def test_c5_alternative_solver_routes_match_reference(env):
+    """c5 at the BASELINE size through the other eigensolver routes — the all-L2 Jacobi for the
+    768 / 769 pairs instead of the split-record one, and both cluster Jacobis accumulating V
+    (T^T = V^T L^-1) instead of T' = K^-T U — against the reference's goldens (the switches
+    are read once per process, hence the subprocess)."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_parity.py"), "-k",
+                        "test_kfac_steps_match_reference_golden and c5_full3"],
+                       env=dict(os.environ, **env), capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert " passed" in r.stdout and "failed" not in r.stdout, r.stdout[-500:]
