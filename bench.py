@@ -508,9 +508,10 @@ def run_e2e_sharded(args, wl, prob, params, batch, rank, world, eng, stepper):
 
     from paper_2405_15603_b200.dist import upload_shard
 
-    steps = args.e2e_steps or args.steps
-    eng.load_params(params)
-    eng.init_factors(True)
+    # continues the device-timed run (no reset: warm-started solves, as in the timed steps);
+    # at most 5 steps unless --e2e-steps says otherwise (strong scaling at 65536 points makes
+    # an N = 2 step ~9 s)
+    steps = args.e2e_steps or min(args.steps, 5)
     dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
