@@ -7,10 +7,10 @@
 //
 // For a pair (F1, F2) with damping lam (reference src/curvature.py:150-161):
 //   M1 = F1 + lam I, M2 = F2 + lam I
-//   M2 = L L^T (Cholesky; failure -> not positive definite, src/linalg.py:128-132)
-//   C  = L^-1 M1 L^-T (two forward substitutions, C symmetric)
-//   C  = G G^T (Cholesky), one-sided Jacobi on the rows of G -> C = V diag(lam) V^T
-//   T  = L^-T V           (so T^T M2 T = I, T^T M1 T = diag(lam))
+//   M2 = L L^T, M1 = K K^T (Cholesky; failure -> not positive definite, src/linalg.py:128-132)
+//   L_C = L^-1 K (one forward substitution; C = L^-1 M1 L^-T = L_C L_C^T, R = L_C^T)
+//   one-sided Jacobi on the rows of L_C -> U = R V with orthogonal columns, C V = V diag(lam)
+//   T  = K^-T U = L^-T V  (so T^T M2 T = I, T^T M1 T = diag(lam)); V is never accumulated
 // Combine (src/linalg.py:168-173 restated on the generalised basis):
 //   out = -T_B [(T_B^T G T_A) / (lb la^T + 1)] T_A^T.
 // One-sided Jacobi is accurate to a few ulps relative to each eigenpair; the solution of the
@@ -56,7 +56,7 @@ __device__ __forceinline__ void set_status_dev(int32_t* status, int32_t code) {
 // per lane; rows zero-padded to 16 EPL, so no bounds checks), forms the three dot products
 // with a 4-level shuffle reduction and rotates both rows of G and W.  Rows do not move,
 // only the pairing changes, so a round is one CTA barrier.
-template <int EPL>
+template <int EPL, bool ACCW>
 __device__ __forceinline__ void jacobi_rows(double* G, double* W, int n, int ld, int* flag,
                                             double tol) {
   const int tid = threadIdx.x, lane = tid & 31;
@@ -110,15 +110,17 @@ __device__ __forceinline__ void jacobi_rows(double* G, double* W, int n, int ld,
             double cs, sn;
             jacobi_angle(al, be, ga, cs, sn);
             if (trace && hl == 0) atomicAdd(&tr_rot, 1);
-            double* wp = W + p * ld + hl;
-            double* wq = W + q * ld + hl;
+            double* wp = ACCW ? W + p * ld + hl : nullptr;
+            double* wq = ACCW ? W + q * ld + hl : nullptr;
 #pragma unroll
             for (int u = 0; u < EPL; ++u) {
               gp[16 * u] = cs * x[u] - sn * y[u];
               gq[16 * u] = sn * x[u] + cs * y[u];
-              const double wx = wp[16 * u], wy = wq[16 * u];
-              wp[16 * u] = cs * wx - sn * wy;
-              wq[16 * u] = sn * wx + cs * wy;
+              if (ACCW) {
+                const double wx = wp[16 * u], wy = wq[16 * u];
+                wp[16 * u] = cs * wx - sn * wy;
+                wq[16 * u] = sn * wx + cs * wy;
+              }
             }
             if (hl == 0) *flag = 1;
           }
@@ -234,7 +236,7 @@ __global__ void __launch_bounds__(EIG_THREADS) k_gen_eig_small(const SmallEigJob
   double* L = esm;
   double* C = L + n * ld;
   double* V = C + n * ld;
-  double* invd = V + n * ld;  // 1 / diag of the Cholesky factor of M2
+  double* invd = V + n * ld;  // 1 / diag of the Cholesky factors of M2 (n) and M1 (n)
   __shared__ int flag;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -275,8 +277,13 @@ __global__ void __launch_bounds__(EIG_THREADS) k_gen_eig_small(const SmallEigJob
     }
   }
 
-  // Cholesky of M2 (lower triangle of L); failure -> info > n (second matrix not PD)
+  // M2 = L L^T and M1 = K K^T (Cholesky, lower triangles of L and C); a failure of M2's ->
+  // info > n (second matrix not PD), of M1's -> info = n + 1 (not PD either way)
   chol_lower(L, n, ld, &flag);
+  if (flag == 0) {
+    chol_lower(C, n, ld, &flag);
+    if (flag != 0) flag = n + 1;
+  }
   if (flag != 0) {
     if (tid == 0) {
       if (jb.info) *jb.info = flag;
@@ -285,80 +292,57 @@ __global__ void __launch_bounds__(EIG_THREADS) k_gen_eig_small(const SmallEigJob
     }
     return;
   }
-
-  // C <- L^-1 C (into V), then C <- L^-1 (L^-1 C)^T (from V back into C): right-looking
-  // triangular solves, warp per column (tri_solve_cols)
-  for (int i = tid; i < n; i += EIG_THREADS) invd[i] = 1.0 / L[i * ld + i];
+  // L_C = L^-1 K (lower triangular; C_sym = L^-1 M1 L^-T = L_C L_C^T, R = L_C^T), into V by
+  // right-looking warp-per-column triangular solves; one-sided Jacobi on the rows of L_C
+  // (the columns of R) leaves U = R V_eig with orthogonal columns, ||u_i||^2 the eigenvalues;
+  // then T = K^-T U (= L^-T L_C^-T R V_eig = L^-T V_eig): the eigenvectors are never
+  // accumulated (half the rotation work; the same route as the cluster solvers)
+  double* invk = invd + n;
+  for (int i = tid; i < n; i += EIG_THREADS) {
+    invd[i] = 1.0 / L[i * ld + i];
+    invk[i] = 1.0 / C[i * ld + i];
+  }
+  for (int e = tid; e < n * n; e += EIG_THREADS) {  // K's strict upper triangle still holds M1
+    const int i = e / n, j = e % n;
+    if (j > i) C[i * ld + j] = 0.0;
+  }
   __syncthreads();
   tri_solve_cols<false>(L, invd, C, false, V, n, ld);
   __syncthreads();
-  tri_solve_cols<false>(L, invd, V, true, C, n, ld);
-  __syncthreads();
-  // symmetrise (roundoff), C = G G^T (Cholesky, G lower; strictly upper part zeroed) and
-  // W = I; one-sided Jacobi on the rows of G (jacobi_rows): C W^T = W^T diag(||g_i||^2)
-  for (int e = tid; e < n * n; e += EIG_THREADS) {
-    const int i = e / n, j = e % n;
-    if (i < j) {
-      const double a = 0.5 * (C[i * ld + j] + C[j * ld + i]);
-      C[i * ld + j] = a;
-      C[j * ld + i] = a;
-    }
-    V[i * ld + j] = (i == j) ? 1.0 : 0.0;
-  }
-  __syncthreads();
-  chol_lower(C, n, ld, &flag);
-  if (flag != 0) {  // M1 not PD
-    if (tid == 0) {
-      if (jb.info) *jb.info = n + 1;
-      if (jb.warm_valid) *jb.warm_valid = 0;
-      set_status_dev(status, KP_ERR_NOT_PSD);
-    }
-    return;
-  }
   const int nr = ((n + 15) / 16) * 16;  // padded row length read by the Jacobi rounds
   for (int e = tid; e < n * nr; e += EIG_THREADS) {
     const int i = e / nr, j = e % nr;
-    if (j > i) C[i * ld + j] = 0.0;
-    if (j >= n) V[i * ld + j] = 0.0;
+    if (j > i) V[i * ld + j] = 0.0;  // exact zeros already for j < n; the padding too
   }
   __syncthreads();
   {
     const double tol = fmax(jobs.tol_floor, 2.0 * n * 2.220446049250313e-16);
     switch (nr / 16) {
-      case 1: jacobi_rows<1>(C, V, n, ld, &flag, tol); break;
-      case 2: jacobi_rows<2>(C, V, n, ld, &flag, tol); break;
-      case 3: jacobi_rows<3>(C, V, n, ld, &flag, tol); break;
-      case 4: jacobi_rows<4>(C, V, n, ld, &flag, tol); break;
-      case 5: jacobi_rows<5>(C, V, n, ld, &flag, tol); break;
-      default: jacobi_rows<6>(C, V, n, ld, &flag, tol); break;
+      case 1: jacobi_rows<1, false>(V, nullptr, n, ld, &flag, tol); break;
+      case 2: jacobi_rows<2, false>(V, nullptr, n, ld, &flag, tol); break;
+      case 3: jacobi_rows<3, false>(V, nullptr, n, ld, &flag, tol); break;
+      case 4: jacobi_rows<4, false>(V, nullptr, n, ld, &flag, tol); break;
+      case 5: jacobi_rows<5, false>(V, nullptr, n, ld, &flag, tol); break;
+      default: jacobi_rows<6, false>(V, nullptr, n, ld, &flag, tol); break;
     }
   }
 
-  // eigenvalues; V <- W^T (column j = eigenvector j); T = L^-T V (back substitution, warp per
-  // column) written to global
+  // eigenvalues ||u_i||^2; T = K^-T U (U[k][i] = V[i][k]: transposed read) into L
   for (int i = warp; i < n; i += NWARPS) {
     double a = 0.0;
-    for (int j = lane; j < n; j += 32) a = fma(C[i * ld + j], C[i * ld + j], a);
+    for (int j = lane; j < n; j += 32) a = fma(V[i * ld + j], V[i * ld + j], a);
     a = warp_sum(a);
     if (lane == 0) jb.lam[i] = a;
   }
-  for (int e = tid; e < n * n; e += EIG_THREADS) {
-    const int i = e / n, j = e % n;
-    if (i < j) {
-      const double a = V[i * ld + j];
-      V[i * ld + j] = V[j * ld + i];
-      V[j * ld + i] = a;
-    }
-  }
   __syncthreads();
-  tri_solve_cols<true>(L, invd, V, false, C, n, ld);  // C reused as T = L^-T V
+  tri_solve_cols<true>(C, invk, V, true, L, n, ld);
   __syncthreads();
-  const double* T = C;
-  if (warm) {  // T = T_prev T''  (T_prev from global, T'' in C; result in V)
+  const double* T = L;
+  if (warm) {  // T = T_prev T''  (T_prev from global, T'' in L; result in V)
     for (int e2 = tid; e2 < n * n; e2 += EIG_THREADS) {
       const int i = e2 / n, j = e2 % n;
       double a = 0.0;
-      for (int k = 0; k < n; ++k) a = fma(jb.warm_t[i * n + k], C[k * ld + j], a);
+      for (int k = 0; k < n; ++k) a = fma(jb.warm_t[i * n + k], L[k * ld + j], a);
       V[i * ld + j] = a;
     }
     __syncthreads();
@@ -496,7 +480,7 @@ int small_eig_sweeps_used(bool reset) {
 }
 
 size_t small_eig_smem_bytes(int n) {
-  return sizeof(double) * (3 * (size_t)n * eig_pitch(n) + (size_t)n);
+  return sizeof(double) * (3 * (size_t)n * eig_pitch(n) + 2 * (size_t)n);
 }
 
 void launch_gen_eig_small(const SmallEigJobs& jobs, int njobs, int max_n, int32_t* status,
