@@ -296,6 +296,15 @@ void launch_copy_matrix(const double* src, int64_t lds, int rows, int cols, doub
                         int64_t ldd, cudaStream_t s);
 void launch_zero_upper(int n, double* A, int64_t lda, cudaStream_t s);
 
+// ---- FP64 GEMM on the INT8 tensor cores, Ozaki scheme (kp_ozaki.cu; KP_OZAKI=1) ------
+bool ozaki_enabled();
+int ozaki_slices();
+bool ozaki_gemm_ok(int64_t M, int N, int K, int64_t lda, int64_t ldb);
+bool launch_ozaki_gemm(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                       int64_t ldc, int64_t M, int N, int K, const double* bias,
+                       int64_t bias_stride, int rows_per_sample, int8_t* a_planes, int* a_ex,
+                       int8_t* b_planes, int* b_ex, cudaStream_t s);
+
 // ---- small on-device generalised eigensolver + combine (kp_eig_small.cu) ---------
 struct SmallEigJob {
   int n;

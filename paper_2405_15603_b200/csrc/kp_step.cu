@@ -118,6 +118,7 @@ struct Plan {
   // workspace offsets, in doubles
   int64_t o_wT[MAXL] = {}, o_zval0 = 0, o_post[MAXL] = {}, o_pre[MAXL] = {}, o_gout[MAXL] = {};
   int64_t o_ping = 0, o_pong = 0;
+  int64_t o_ozEa = 0, o_ozB = 0, o_ozEb = 0;  // Ozaki line-search scratch (KP_OZAKI=1)
   int64_t o_bzval0 = 0, o_bpost[MAXL] = {}, o_bpre[MAXL] = {}, o_bg[MAXL] = {};
   int64_t o_bping = 0, o_bpong = 0, o_ones = 0;
   int64_t o_r = 0, o_rb = 0, o_rls = 0, o_rbls = 0, o_u = 0, o_upart = 0;
@@ -266,6 +267,11 @@ int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
   for (int l = 1; l + 1 < P.L; ++l) P.o_bpre[l] = take(P.Nb * P.h[l + 1]);
   for (int l = 0; l + 1 < P.L; ++l) P.o_bg[l] = take(P.Nb * P.h[l + 1]);
   P.o_bping = take(P.Bc * P.Nb * P.maxh);
+  if (ozaki_enabled()) {  // A planes alias the layer's stored-state buffer (idle in the line search)
+    P.o_ozEa = take(Mc / 2 + 1);
+    P.o_ozB = take((int64_t)P.maxh * P.maxh);
+    P.o_ozEb = take(P.maxh);
+  }
   P.o_bpong = take(P.Bc * P.Nb * P.maxh);
   P.o_ones = take(P.Nb);
   P.o_r = take(P.N);
@@ -579,6 +585,25 @@ void forward_loss(const Ctx& c, const double* theta, const double* wpad, const d
     double* a = ping;
     double* b = pong;
     for (int l = 1; l + 1 < L; ++l) {
+      // FP64 emulated on the INT8 tensor cores (KP_OZAKI=1): GEMM + bias, then the Taylor
+      // activation in place; the layer's stored-state buffer (idle during the line search)
+      // holds the input's slices.  The h_out = 1 output layer then runs unfused below.
+      if (batch == 1 && ozaki_gemm_ok(n * td.S, P.h[l + 1], P.h[l], P.h[l], P.h[l])) {
+        bool done = false;
+        prof_launch(c, 2.0 * (double)n * td.S * P.h[l] * P.h[l + 1], [&] {
+          done = launch_ozaki_gemm(a, P.h[l], wpad + wp.wo[l], P.h[l], b, P.h[l + 1], n * td.S,
+                                   P.h[l + 1], P.h[l], theta + P.th[l] + P.h[l], P.p[l], td.S,
+                                   reinterpret_cast<int8_t*>(c.at(P.o_post[l])),
+                                   reinterpret_cast<int*>(c.at(P.o_ozEa)),
+                                   reinterpret_cast<int8_t*>(c.at(P.o_ozB)),
+                                   reinterpret_cast<int*>(c.at(P.o_ozEb)), c.s);
+        });
+        if (done) {
+          launch_act_fwd(b, b, n, P.h[l + 1], td, cdiag, c.s);
+          std::swap(a, b);
+          continue;
+        }
+      }
       GemmAct ga{};
       ga.A = a;
       ga.lda = P.h[l];
