@@ -436,12 +436,14 @@ def test_mid_size_pairs_other_routes_match_reference(cluster):
     assert " passed" in r.stdout and "failed" not in r.stdout, r.stdout[-500:]
 
 
-@pytest.mark.parametrize("env", [{"KP_LARGE_SPLIT": "0"}, {"KP_LARGE_ACCV": "1", "KP_MID_ACCV": "1"}])
+@pytest.mark.parametrize("env", [{"KP_LARGE_SPLIT": "0"}, {"KP_LARGE_ACCV": "1", "KP_MID_ACCV": "1"},
+                                 {"KP_OZAKI": "1"}])
 def test_c5_alternative_solver_routes_match_reference(env):
-    """c5 at the BASELINE size through the other eigensolver routes — the all-L2 Jacobi for the
-    768 / 769 pairs instead of the split-record one, and both cluster Jacobis accumulating V
-    (T^T = V^T L^-1) instead of T' = K^-T U — against the reference's goldens (the switches
-    are read once per process, hence the subprocess)."""
+    """c5 at the BASELINE size through the other routes — the all-L2 Jacobi for the 768 / 769
+    pairs instead of the split-record one, both cluster Jacobis accumulating V (T^T = V^T L^-1)
+    instead of T' = K^-T U, and the line-search layers on the INT8 tensor cores (Ozaki
+    emulation of FP64) — against the reference's goldens (the switches are read once per
+    process, hence the subprocess)."""
     import os
     import subprocess
     import sys
