@@ -1672,7 +1672,11 @@ static int setup_early(Ctx& c) {
   // Pairs above 288 run 16-CTA clusters for tens of milliseconds (c5: 512-769); started
   // during the accumulate phase they take SMs from its contractions and the step gets
   // slower (c5 N = 16384: 4523 vs 4483 ms per step), so they wait for the phase to end.
-  if (!any || maxn > 288) return KP_OK;
+  static const bool force = [] {  // KP_EARLY_PRECOND=2: also for pairs above 288
+    const char* e = getenv("KP_EARLY_PRECOND");
+    return e && atoi(e) == 2;
+  }();
+  if (!any || (maxn > 288 && !force)) return KP_OK;
   KP_TRY(ensure_side_streams(c.ctx, 2 * P.L + 2));
   c.early = true;
   return KP_OK;
