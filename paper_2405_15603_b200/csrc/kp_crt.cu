@@ -1,0 +1,706 @@
+// Fused Taylor layer with the FP64 product emulated on the tcgen05 INT8 tensor cores by the
+// Chinese-remainder construction (Ozaki scheme II), sm_100a — the hidden layers of the
+// line-search forwards (reference src/taylor.py:134-169 inside src/optim.py:195-211: 31 of the
+// 32 forward passes of a KFAC step) for one-sample tiles (57 <= S <= 112: c5's S = 102).
+//
+// Exactness argument.  Every row of the states H (n*S x K) and of W (N x K) is scaled by a
+// power of two to a BETA-bit integer, a = rint(h 2^(BETA - e_r)) with max|h_r| < 2^e_r, so
+// |a| <= 2^BETA (and likewise b for W, exponent f_u).  The integer product P = sum_k a_k b_k
+// (|P| <= K 2^(2 BETA) < M / 2) is computed exactly modulo NMOD pairwise-coprime moduli
+// p_i <= 256 (M = prod p_i; 13 moduli: M ~ 2^102.5, BETA = 45): one int8 x int8 -> int32
+// tcgen05 GEMM of the symmetric residues per modulus, exact since K 128^2 <= 2^24.  With
+// q_i = M / p_i and s_i = q_i^-1 mod p_i folded into W's residues, t_i = acc_i mod p_i =
+// (s_i P) mod p_i and P = sum_i q_i t_i - k M for the integer k = round(sum / M).  The sum is
+// carried as an exact FP64 high part (q_i rounded down to a multiple of 2^E) plus an int32 low
+// part (the rest of q_i to 18 bits, error far below the 2^(BETA+5) input rounding);
+// z = P 2^(e_r + f_u - 2 BETA).  The only approximation is the rounding of h and w to BETA bits:
+// about 2e-14 of sum_k |h_k w_k| (DGEMM: ~2e-16; 12 moduli, BETA = 41: 16x larger for 6% less
+// time, not taken); the line search consumes these losses only
+// through the argmin over the step-size grid (tools/crt_check.py: candidate losses within
+// 2e-14 relative of the DMMA path, runner-up gaps >= 6e-3).  Constants: tools/crt_constants.py.
+//
+// Kernel (one persistent CTA per SM, 384 threads): warp 0 lane 0 = TMA producer (per modulus,
+// K in 128-byte chunks: W residues 128 units x 128 B, H residues 112 rows x 128 B, 128-byte
+// swizzle, six stages), warp 1 = TMEM allocator + MMA issuer (tcgen05.mma kind::i8, M 128
+// units, N 112 rows, K 32; two int32 accumulators of 112 columns), warps 4..11 = epilogue
+// (two per TMEM lane quadrant, 56 rows each; setmaxnreg 232): fold each modulus into the CRT
+// sums while the MMA computes the next one, then reconstruct, add the bias and apply the
+// Taylor activation (s0 on the value row, s1 g_i on the derivative rows, s1 l + s2 sum c_i g_i^2
+// on the operator row; the two halves of a sample exchange s1, s2 and the partial quadratic
+// form through shared memory).  ACT_LOSS writes the activations, ACT_LAST reduces them against
+// the output layer's weights into per-(row, unit tile) partial dots (k_last_from_partials).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "kp_common.cuh"
+#include "kp_internal.h"
+
+namespace kp {
+
+namespace {
+
+// 13 moduli, log2 M = 102.525, BETA = 45, E = 53, low part c2 * 2^35  (tools/crt_constants.py 13)
+constexpr int NMOD = 13;
+constexpr int BETA = 45;
+constexpr double CR_LOW_SCALE = 0x1.0000000000000p+35;
+__constant__ double cr_pd[NMOD] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211};
+__constant__ double cr_ipd[NMOD] = {1.0 / 256, 1.0 / 255, 1.0 / 253, 1.0 / 251, 1.0 / 247, 1.0 / 241, 1.0 / 239, 1.0 / 233, 1.0 / 229, 1.0 / 227, 1.0 / 223, 1.0 / 217, 1.0 / 211};
+__constant__ double cr_s[NMOD] = {195, 1, 238, 224, 245, 161, 24, 60, 112, 29, 185, 156, 46};
+__constant__ double cr_q1[NMOD] = {0x1.703d73109e800p+94, 0x1.71af2232d1000p+94, 0x1.749b44df3c000p+94, 0x1.779353b31e000p+94, 0x1.7da85e6211000p+94, 0x1.8728d7b42d000p+94, 0x1.8a6ececc2d800p+94, 0x1.9497047757000p+94, 0x1.9ba8302477000p+94, 0x1.9f48aedffe000p+94, 0x1.a6bba31685800p+94, 0x1.b26be29560000p+94, 0x1.bec64ef0fa800p+94};
+__constant__ uint32_t cr_c2[NMOD] = {40666u, 207364u, 148907u, 87430u, 95213u, 119339u, 55624u, 226944u, 75224u, 207536u, 172466u, 125289u, 70460u};
+constexpr uint32_t CR_C2H = 192308489u;  // sum c2_i floor(p_i / 2)
+constexpr double CR_M1 = 0x1.703d73109e938p+102, CR_M2 = 0x1.6d0683e4deb00p+52, CR_IM = 0x1.63f115f5d0b38p-103;
+__constant__ uint32_t cr_m[NMOD] = {2147483648u, 2155905153u, 2172947881u, 2190262207u, 2225732041u, 2281144456u, 2300233531u, 2359467013u, 2400680410u, 2421831780u, 2465272709u, 2533436931u, 2605477791u};
+__constant__ uint32_t cr_add[NMOD] = {16777344u, 16777597u, 16777568u, 16777467u, 16777351u, 16777576u, 16777441u, 16777514u, 16777341u, 16777456u, 16777516u, 16777463u, 16777348u};
+__constant__ uint32_t cr_pu[NMOD] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211};
+__constant__ double cr_hd[NMOD] = {0x1p52 + 128, 0x1p52 + 127, 0x1p52 + 126, 0x1p52 + 125, 0x1p52 + 123, 0x1p52 + 120, 0x1p52 + 119, 0x1p52 + 116, 0x1p52 + 114, 0x1p52 + 113, 0x1p52 + 111, 0x1p52 + 108, 0x1p52 + 105};
+
+#ifndef CRT_KB
+#define CRT_KB 128
+#endif
+#ifndef CRT_ST
+#define CRT_ST 6
+#endif
+// K bytes per pipeline stage (128: 128-byte swizzle, 29 KB stages; 64: 64-byte swizzle) and
+// stage count (measured, tools/crt_bench.cu: 64-byte stages x 13 are 15% slower than 128 x 6,
+// 128 x 7 no faster)
+constexpr int CM = 128, CN = 112, CKB = CRT_KB, CST = CRT_ST;
+constexpr int A_BYTES = CM * CKB, B_BYTES = CN * CKB, STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int EWQ = 2, NEW = 4 * EWQ, CPW = CN / EWQ;  // 56 rows per epilogue thread
+constexpr int THREADS = 32 * (4 + NEW);
+constexpr int TM_COLS = 256, ACC_STRIDE = 128;
+constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(CN >> 3) << 17) |
+                           ((uint32_t)(CM >> 4) << 24);
+constexpr size_t SMEM_BYTES = (size_t)CST * STAGE_BYTES + 1024;
+
+constexpr double MAGIC = 6755399441055744.0;  // 1.5 * 2^52: round-to-integer by addition
+
+__device__ __forceinline__ double pow2i(int e) { return __hiloint2double((e + 1023) << 20, 0); }
+
+__device__ __forceinline__ void tma3d(void* dst, const CUtensorMap* m, int x, int y, int z,
+                                      uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3, %4}], [%5];\n" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(x), "r"(y), "r"(z), "r"(smem_addr(b))
+      : "memory");
+}
+
+// K-major swizzled UMMA shared-memory descriptor: start >> 4, LBO 16 B (unused), SBO = 8 rows
+// x CKB bytes, version 1, layout SWIZZLE_128B (2) or SWIZZLE_64B (4)
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr) {
+  uint64_t d = (uint64_t)((addr >> 4) & 0x3fff);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)((8 * CKB) >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)(CKB == 128 ? 2 : 4) << 61;
+  return d;
+}
+
+template <int N>
+__device__ __forceinline__ void tm_ld(uint32_t ta, uint32_t* r);
+template <>
+__device__ __forceinline__ void tm_ld<32>(uint32_t ta, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(ta));
+}
+template <>
+__device__ __forceinline__ void tm_ld<16>(uint32_t ta, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(ta));
+}
+template <>
+__device__ __forceinline__ void tm_ld<8>(uint32_t ta, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "r"(ta));
+}
+__device__ __forceinline__ void tm_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
+// Folding one modulus (no conversion-unit instructions: I2F / F2F / FRND issue on the XU pipe
+// at a quarter of the FMA rate and bounded the first version): w = acc + add_i >= 0,
+// t' = w mod p_i in [0, p_i) by multiply-high (cr_m), t = t' - floor(p_i / 2) in [-128, 127];
+// x1 += q1_i t in FP64 (exact: t from the bits of 2^52 + t', q1_i a multiple of 2^E with
+// sum |q1_i t| < 2^(E+53)), x2 += c2_i t' in uint32 (< 2^31; offset CR_C2H removed at the end).
+struct FoldC {
+  uint32_t add, m, negp, c2;
+  double hd, q1;
+};
+
+__device__ __forceinline__ FoldC fold_consts(int i) {
+  return FoldC{cr_add[i], cr_m[i], 0u - cr_pu[i], cr_c2[i], cr_hd[i], cr_q1[i]};
+}
+
+// fold NC accumulator columns of one modulus into the CRT sums: x1 (FP64, exact high part),
+// x2 (uint32, low part)
+template <int NC>
+__device__ __forceinline__ void fold(const uint32_t* r, double* x1, uint32_t* x2, const FoldC& c) {
+#pragma unroll
+  for (int j = 0; j < NC; ++j) {
+    const uint32_t w = r[j] + c.add;
+    const uint32_t t = w + (__umulhi(w, c.m) >> 7) * c.negp;  // w mod p in [0, p)
+    x2[j] += t * c.c2;
+    x1[j] = fma(__hiloint2double(0x43300000, (int)t) - c.hd, c.q1, x1[j]);
+  }
+}
+
+// Moduli as compile-time constants for the state slicing: c1 = 2^15 mod p, c2 = 2^30 mod p
+// (centred), so that a = a2 2^30 + a1 2^15 + a0 reduces as y = a2 c2 + a1 c1 + a0, |y| < 2^23.
+__host__ __device__ constexpr int modulus(int i) {
+  return i == 0 ? 256 : i == 1 ? 255 : i == 2 ? 253 : i == 3 ? 251 : i == 4 ? 247 : i == 5 ? 241
+       : i == 6 ? 239 : i == 7 ? 233 : i == 8 ? 229 : i == 9 ? 227 : i == 10 ? 223 : i == 11 ? 217
+       : 211;
+}
+__host__ __device__ constexpr int cmod(long long v, int p) {
+  return (int)(v % p) > p / 2 ? (int)(v % p) - p : (int)(v % p);
+}
+constexpr float MAGICF = 12582912.0f;  // 1.5 * 2^23
+
+// Weight rows (once per layer and candidate): one warp per row, FP64 residue arithmetic with
+// s_i folded in, t_i = s_i a mod p_i.
+__global__ void __launch_bounds__(256)
+    k_crt_slice_w(const double* __restrict__ X, int64_t rows, int K, int64_t ldx,
+                  int8_t* __restrict__ planes, int64_t ps, int* __restrict__ ex) {
+  const int64_t row = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const double* x = X + row * ldx;
+  double m = 0.0;
+  for (int k = lane; k < K; k += 32) m = fmax(m, fabs(x[k]));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  int e = 0;
+  if (m > 0.0) frexp(m, &e);
+  if (lane == 0) ex[row] = e;
+  const double sc = pow2i(BETA - e);
+  for (int k = lane; k < K; k += 32) {
+    const double a = (x[k] * sc + MAGIC) - MAGIC;  // rint, |a| <= 2^45
+#pragma unroll
+    for (int i = 0; i < NMOD; ++i) {
+      const double p = cr_pd[i], ip = cr_ipd[i];
+      double r = fma(-(fma(a, ip, MAGIC) - MAGIC), p, a);  // exact, |r| <= p/2 + 1
+      r *= cr_s[i];
+      r = fma(-(fma(r, ip, MAGIC) - MAGIC), p, r);
+      int ri = __double2loint(r + MAGIC);
+      if (ri > 127) ri -= (int)p;
+      planes[i * ps + row * (int64_t)K + k] = (int8_t)ri;
+    }
+  }
+}
+
+// State rows: one warp per row, lane = 4 consecutive K entries per 128-wide chunk.  max|x| <
+// 2^e; a = rint(x 2^(BETA - e)) read from the bits of x 2^(BETA-e) + 1.5 2^52 (|a| <= 2^45),
+// split into 15-bit pieces held exactly in FP32; per modulus y = a2 c2 + a1 c1 + a0 (exact,
+// |y| < 2^23), r = y - p rint(y / p) (exact, |r| <= p/2 + 1; p = 255 folds r = 128 to -127),
+// stored as the low byte of r + 1.5 2^23.  p = 256 is the low byte of a.
+__global__ void __launch_bounds__(256)
+    k_crt_slice_h(const double* __restrict__ X, int64_t rows, int K, int64_t ldx,
+                  int8_t* __restrict__ planes, int64_t ps, int* __restrict__ ex) {
+  const int64_t row = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const double* x = X + row * ldx;
+  double m = 0.0;
+  for (int k = 4 * lane; k < K; k += 128) {
+    const double2 v0 = *reinterpret_cast<const double2*>(x + k);
+    const double2 v1 = *reinterpret_cast<const double2*>(x + k + 2);
+    m = fmax(m, fmax(fmax(fabs(v0.x), fabs(v0.y)), fmax(fabs(v1.x), fabs(v1.y))));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  int e = 0;
+  if (m > 0.0) frexp(m, &e);
+  if (lane == 0) ex[row] = e;
+  const double sc = pow2i(BETA - e);
+  const long long mb = __double_as_longlong(MAGIC);
+  for (int k = 4 * lane; k < K; k += 128) {
+    const double2 v0 = *reinterpret_cast<const double2*>(x + k);
+    const double2 v1 = *reinterpret_cast<const double2*>(x + k + 2);
+    const double xv[4] = {v0.x, v0.y, v1.x, v1.y};
+    float f0[4], f1[4], f2[4];
+    uint32_t low[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const long long a = __double_as_longlong(fma(xv[t], sc, MAGIC)) - mb;
+      const uint32_t lo = (uint32_t)a;
+      low[t] = lo;
+      f0[t] = __int_as_float(0x4B000000 | (lo & 0x7fffu)) - 8388608.0f;
+      f1[t] = __int_as_float(0x4B000000 | ((lo >> 15) & 0x7fffu)) - 8388608.0f;
+      f2[t] = __int_as_float(0x4B400000 + (int)(a >> 30)) - MAGICF;
+    }
+    int8_t* dst = planes + row * (int64_t)K + k;
+    *reinterpret_cast<uint32_t*>(dst) = __byte_perm(__byte_perm(low[0], low[1], 0x0040),
+                                                    __byte_perm(low[2], low[3], 0x0040), 0x5410);
+#pragma unroll
+    for (int i = 1; i < NMOD; ++i) {
+      const float p = (float)modulus(i), ip = 1.0f / (float)modulus(i);
+      const float c1 = (float)cmod(1LL << 15, modulus(i)), c2 = (float)cmod(1LL << 30, modulus(i));
+      int b[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float y = fmaf(f2[t], c2, fmaf(f1[t], c1, f0[t]));
+        float r = fmaf(-(fmaf(y, ip, MAGICF) - MAGICF), p, y);
+        if (modulus(i) == 255) r = r > 127.5f ? r - p : r;
+        b[t] = __float_as_int(r + MAGICF);
+      }
+      *reinterpret_cast<uint32_t*>(dst + i * ps) =
+          __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
+    }
+  }
+}
+
+// Tile schedule.  CL = 1: tile t -> unit tile t % UT, sample t / UT, CTAs striding by the grid.
+// CL = 4: 2 x 2 clusters; cluster tile ct -> unit tiles 2 (ct % (UT/2)) + cu and samples
+// 2 (ct / (UT/2)) + cs for the CTA of rank cu + 2 cs; the two CTAs of a unit tile share its
+// weight residues and the two CTAs of a sample its state residues, each loading one half with a
+// cluster multicast (half the L2 operand traffic).
+template <int CL>
+struct Sched {
+  int first, step, count;  // tile indices < 2^31 (n_samples * UT checked by the launcher)
+  int cu, cs, UT;
+  __device__ Sched(int64_t n_samples, int ut_count) : UT(ut_count) {
+    if (CL == 1) {
+      first = blockIdx.x;
+      step = gridDim.x;
+      count = (int)(n_samples * UT);
+      cu = cs = 0;
+    } else {
+      uint32_t rank, cid, ncl;
+      asm("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(rank));
+      asm("mov.u32 %0, %%clusterid.x;\n" : "=r"(cid));
+      asm("mov.u32 %0, %%nclusterid.x;\n" : "=r"(ncl));
+      first = cid;
+      step = ncl;
+      count = (int)((n_samples + 1) / 2 * (UT / 2));
+      cu = (int)(rank & 1);
+      cs = (int)(rank >> 1);
+    }
+  }
+  __device__ int ut(int t) const { return CL == 1 ? t % UT : 2 * (t % (UT / 2)) + cu; }
+  __device__ int64_t smp(int t) const { return CL == 1 ? t / UT : 2 * (int64_t)(t / (UT / 2)) + cs; }
+};
+
+__device__ __forceinline__ void tma3d_mc(void* dst, const CUtensorMap* m, int x, int y, int z,
+                                         uint64_t* b, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::"
+      "cluster [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(x), "r"(y), "r"(z), "r"(smem_addr(b)), "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
+                   : "memory");
+}
+
+template <int MODE, int CL>
+__global__ void __launch_bounds__(THREADS, 1)
+    k_crt_act(const __grid_constant__ CUtensorMap mW, const __grid_constant__ CUtensorMap mH,
+              const int* __restrict__ exw, const int* __restrict__ exh, GemmAct g, int UT) {
+  extern __shared__ __align__(1024) uint8_t crt_sm[];
+  uint8_t* base =
+      reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(crt_sm) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[CST], empty[CST], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_base;
+  __shared__ double xs1[CM], xs2[CM], xq[CM];  // value-row s1, s2 and half-0 quadratic form
+  __shared__ double red[4][CN];                // ACT_LAST: per-quadrant row partials
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S = g.S;
+  const Sched<CL> sch(g.n_samples, UT);
+  const int KC = g.K / CKB;
+  // multicast groups: same unit tile (weights) and same sample (states); the stage's consumers
+  // release it to every CTA that writes into it
+  const uint16_t mask_w = (uint16_t)((1u << sch.cu) | (1u << (sch.cu + 2)));
+  const uint16_t mask_h = (uint16_t)(3u << (2 * sch.cs));
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < CST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CL == 1 ? 1 : 3);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], NEW);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_addr(&tmem_base)),
+                 "r"(TM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (CL > 1) cluster_sync_all();  // peers' barriers initialised before any multicast
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tmem = tmem_base;
+
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n");
+    if (warp == 0 && lane == 0) {  // TMA producer
+      uint32_t it = 0;
+      for (int tile = sch.first; tile < sch.count; tile += sch.step) {
+        const int ut = sch.ut(tile);
+        const int row0 = (int)(sch.smp(tile) * S);
+        for (int i = 0; i < NMOD; ++i)
+          for (int kc = 0; kc < KC; ++kc, ++it) {
+            const uint32_t s = it % CST;
+            if (it >= CST) mbar_wait(&empty[s], ((it / CST) - 1) & 1);
+            uint8_t* a = base + s * STAGE_BYTES;
+            mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+            if (CL == 1) {
+              tma3d(a, &mW, kc * CKB, ut * CM, i, &full[s]);
+              tma3d(a + A_BYTES, &mH, kc * CKB, row0, i, &full[s]);
+            } else {  // my half of the unit tile's weights and of the sample's states
+              tma3d_mc(a + sch.cs * (CM / 2) * CKB, &mW, kc * CKB, ut * CM + sch.cs * (CM / 2), i,
+                       &full[s], mask_w);
+              tma3d_mc(a + A_BYTES + sch.cu * (CN / 2) * CKB, &mH, kc * CKB, row0 + sch.cu * (CN / 2),
+                       i, &full[s], mask_h);
+            }
+          }
+      }
+    } else if (warp == 1 && lane == 0) {  // MMA issuer
+      uint32_t it = 0, gm = 0;
+      for (int tile = sch.first; tile < sch.count; tile += sch.step) {
+        for (int i = 0; i < NMOD; ++i, ++gm) {
+          const uint32_t b = gm & 1;
+          if (gm >= 2) mbar_wait(&tempty[b], ((gm >> 1) - 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;\n");
+          const uint32_t acc_col = tmem + b * ACC_STRIDE;
+          for (int kc = 0; kc < KC; ++kc, ++it) {
+            const uint32_t s = it % CST;
+            mbar_wait(&full[s], (it / CST) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;\n");
+            const uint32_t a = smem_addr(base + s * STAGE_BYTES), bb = a + A_BYTES;
+#pragma unroll
+            for (int k = 0; k < CKB / 32; ++k) {
+              const uint64_t da = sdesc(a + 32 * k), db = sdesc(bb + 32 * k);
+              const uint32_t acc = (kc | k) ? 1u : 0u;
+#ifndef CRT_DBG_NOMMA  // (tools/crt_bench.cu timing variants)
+              asm volatile(
+                  "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                  "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(acc_col),
+                  "l"(da), "l"(db), "r"(IDESC), "r"(acc));
+#else
+              (void)da, (void)db, (void)acc, (void)acc_col;
+#endif
+            }
+            if (CL == 1)
+              asm volatile(
+                  "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                      smem_addr(&empty[s]))
+                  : "memory");
+            else
+              asm volatile(
+                  "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::"
+                  "cluster.b64 [%0], %1;\n" ::"r"(smem_addr(&empty[s])),
+                  "h"((uint16_t)(mask_w | mask_h))
+                  : "memory");
+          }
+          asm volatile(
+              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                  smem_addr(&tfull[b]))
+              : "memory");
+        }
+      }
+    }
+  } else {  // epilogue: quadrant q = TMEM lanes 32q..32q+31 = units, half h = rows 56h..56h+55
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n");
+    const int q = warp & 3, h = (warp - 4) >> 2;
+    const int c0 = h * CPW;
+    const int ul = 32 * q + lane;  // unit within the tile
+    const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
+    const int d = g.d;
+    uint32_t gm = 0;
+    for (int tile = sch.first; tile < sch.count; tile += sch.step) {
+      const int ut = sch.ut(tile);
+      const int64_t smp = sch.smp(tile);
+      const bool live = smp < g.n_samples;  // (CL = 4, odd n: the last pair's second sample)
+      const int64_t row0 = smp * S;
+      const int unit = ut * CM + ul;
+      double x1[CPW];
+      uint32_t x2[CPW];
+#pragma unroll
+      for (int j = 0; j < CPW; ++j) {
+        x1[j] = 0.0;
+        x2[j] = 0u;
+      }
+#pragma unroll 1
+      for (int i = 0; i < NMOD; ++i, ++gm) {
+        const uint32_t b = gm & 1;
+        mbar_wait(&tfull[b], (gm >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
+        const FoldC fc = fold_consts(i);
+        const uint32_t ta = lane_base + b * ACC_STRIDE;
+        uint32_t r[32];
+        tm_ld<32>(ta, r);
+        tm_wait();
+#ifndef CRT_DBG_NOFOLD
+        fold<32>(r, x1, x2, fc);
+#endif
+        tm_ld<16>(ta + 32, r);
+        tm_ld<8>(ta + 48, r + 16);
+        tm_wait();
+        asm volatile("tcgen05.fence::before_thread_sync;\n");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[b]);
+#ifndef CRT_DBG_NOFOLD
+        fold<24>(r, x1 + 32, x2 + 32, fc);
+#endif
+      }
+      // reconstruct z = P 2^(e_r + f_u - 2 BETA) in x1 (value row: + bias)
+      const double su = pow2i(exw[unit] - 2 * BETA);
+#pragma unroll
+      for (int j = 0; j < CPW; ++j) {
+        const int col = c0 + j;
+        double z = 0.0;
+        if (col < S && live) {
+          const double X2 = (double)(int)(x2[j] - CR_C2H) * CR_LOW_SCALE;
+          const double k = rint((x1[j] + X2) * CR_IM);
+          const double P = fma(-k, CR_M1, x1[j]) + fma(-k, CR_M2, X2);
+          z = P * su * pow2i(exh[row0 + col]);
+        }
+        x1[j] = z;
+      }
+      // Taylor activation (src/taylor.py:140-169): half 0 owns the value row and derivative
+      // rows 1..55, half 1 the remaining derivative rows and the operator row S - 1.
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, quad = 0.0;
+      if (h == 0) {
+        x1[0] += g.bias[(int64_t)unit * g.bias_stride];
+        const TanhD t = tanh_derivs(x1[0], false);
+        s0 = t.s0;
+        s1 = t.s1;
+        s2 = t.s2;
+#pragma unroll
+        for (int j = 1; j < CPW; ++j) quad += (x1[j] * g.cdiag[j - 1]) * x1[j];
+        xs1[ul] = s1;
+        xs2[ul] = s2;
+        xq[ul] = quad;
+      }
+      asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");
+      if (h == 1) {
+        s1 = xs1[ul];
+        s2 = xs2[ul];
+        quad = xq[ul];
+#pragma unroll
+        for (int j = 0; j < CPW; ++j) {
+          const int i = c0 + j;  // derivative index
+          if (i <= d) quad += (x1[j] * g.cdiag[i - 1]) * x1[j];
+        }
+      }
+      asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");  // xs*/xq reusable
+      // outputs in x1
+#pragma unroll
+      for (int j = 0; j < CPW; ++j) {
+        const int col = c0 + j;
+        double o;
+        if (col == 0) o = s0;
+        else if (col == S - 1) o = s1 * x1[j] + s2 * quad;
+        else o = s1 * x1[j];
+        x1[j] = o;
+      }
+      if (MODE == ACT_LOSS) {
+#pragma unroll
+        for (int j = 0; j < CPW; ++j) {
+          const int col = c0 + j;
+          if (col < S && live) g.post[(row0 + col) * g.ldo + unit] = x1[j];
+        }
+      } else {  // ACT_LAST: row partials over this tile's 128 units
+        const double wl = g.wlast[unit];
+#pragma unroll
+        for (int j = 0; j < CPW; ++j) {
+          double v = x1[j] * wl;
+#pragma unroll
+          for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+          if (lane == 0) red[q][c0 + j] = v;
+        }
+        asm volatile("bar.sync 5, 256;\n" ::: "memory");
+        for (int col = threadIdx.x - 128; live && col < S; col += 256)
+          g.upart[(row0 + col) * UT + ut] = ((red[0][col] + red[1][col]) + red[2][col]) + red[3][col];
+        asm volatile("bar.sync 5, 256;\n" ::: "memory");
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (CL > 1) cluster_sync_all();  // no peer still multicasts into this CTA's stages
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                 "r"(TM_COLS));
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 crt_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// residue planes (NMOD x rows x K int8) as a 3-D tensor map: box {128 bytes of K, box_rows,
+// one plane}, 128-byte swizzle; cached by geometry
+bool crt_map(CUtensorMap* m, const int8_t* planes, int64_t rows, int K, uint32_t box_rows) {
+  using Key = std::tuple<const int8_t*, int64_t, int, uint32_t>;
+  static std::map<Key, CUtensorMap> cache;
+  static std::mutex mu;
+  const Key key{planes, rows, K, box_rows};
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *m = it->second;
+    return true;
+  }
+  auto fn = crt_encode();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)K, (cuuint64_t)rows, (cuuint64_t)NMOD};
+  cuuint64_t strides[2] = {(cuuint64_t)K, (cuuint64_t)K * (cuuint64_t)rows};
+  cuuint32_t box[3] = {CKB, box_rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  if (fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(planes), dims, strides, box, es,
+         CU_TENSOR_MAP_INTERLEAVE_NONE,
+         CKB == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  if (cache.size() > 4096) cache.clear();
+  cache.emplace(key, *m);
+  return true;
+}
+
+int sm_count() {
+  static const int n = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+}  // namespace
+
+// On by default; KP_CRT=0 keeps every line-search layer on the FP64 DMMA kernel.
+bool crt_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("KP_CRT");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
+int crt_moduli() { return NMOD; }
+
+bool crt_act_ok(int S, int K, int N) {
+  return crt_enabled() && S > CPW && S <= CN && K % CKB == 0 && K >= CKB && K <= 1024 &&
+         N % CM == 0;
+}
+
+void launch_crt_slice(const double* X, int64_t rows, int K, int64_t ldx, int8_t* planes, int* ex,
+                      bool weights, cudaStream_t s) {
+  if (rows <= 0) return;
+  count_launch();
+  const unsigned blocks = (unsigned)ceil_div(rows, 8);
+  if (weights)
+    k_crt_slice_w<<<blocks, 256, 0, s>>>(X, rows, K, ldx, planes, rows * (int64_t)K, ex);
+  else
+    k_crt_slice_h<<<blocks, 256, 0, s>>>(X, rows, K, ldx, planes, rows * (int64_t)K, ex);
+}
+
+// Fused layer from residue planes: resH (NMOD x n*S x K, exponents exH), resW (NMOD x N x K,
+// exponents exW, sliced with weights = true).  ACT_LOSS: g.post / g.ldo; ACT_LAST: g.wlast,
+// g.upart ((n*S) x N/128 partial dots).
+bool launch_crt_act(const GemmAct& g, int mode, const int8_t* resH, const int* exH,
+                    const int8_t* resW, const int* exW, cudaStream_t s) {
+  if (g.n_samples <= 0) return true;
+  if (!crt_act_ok(g.S, g.K, g.N) || g.batch != 1 || !g.taylor || (mode != ACT_LOSS && mode != ACT_LAST) ||
+      g.n_samples * (g.N / CM) >= (int64_t(1) << 31) || g.n_samples * g.S >= (int64_t(1) << 31))
+    return false;
+  const int64_t rows = g.n_samples * g.S;
+  const int UT = g.N / CM;
+  static const int cl_env = [] {
+    const char* e = getenv("KP_CRT_CLUSTER");
+    return e ? atoi(e) : 4;
+  }();
+  const int CL = (cl_env == 4 && UT % 2 == 0 && g.n_samples >= 2) ? 4 : 1;
+  CUtensorMap mw, mh;
+  if (!crt_map(&mw, resW, g.N, g.K, CL == 4 ? CM / 2 : CM) ||
+      !crt_map(&mh, resH, rows, g.K, CL == 4 ? CN / 2 : CN))
+    return false;
+  void (*kern)(const CUtensorMap, const CUtensorMap, const int*, const int*, GemmAct, int);
+  if (mode == ACT_LAST) kern = CL == 4 ? k_crt_act<ACT_LAST, 4> : k_crt_act<ACT_LAST, 1>;
+  else kern = CL == 4 ? k_crt_act<ACT_LOSS, 4> : k_crt_act<ACT_LOSS, 1>;
+  static std::map<void*, int> max_clusters;  // co-resident 4-CTA clusters (persistent grid)
+  static std::mutex mu;
+  int grid_ctas;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = max_clusters.find((void*)kern);
+    if (it == max_clusters.end()) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+      int mc = sm_count();
+      if (CL == 4) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 4;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(4 * sm_count());
+        cfg.blockDim = dim3(THREADS);
+        cfg.dynamicSmemBytes = SMEM_BYTES;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        mc = 0;
+        if (cudaOccupancyMaxActiveClusters(&mc, (const void*)kern, &cfg) != cudaSuccess || mc <= 0)
+          mc = 0;
+      }
+      it = max_clusters.emplace((void*)kern, mc).first;
+    }
+    grid_ctas = CL == 4 ? 4 * it->second : it->second;
+  }
+  if (grid_ctas <= 0) return false;
+  const int64_t work = CL == 4 ? 4 * ((g.n_samples + 1) / 2 * (UT / 2)) : g.n_samples * UT;
+  grid_ctas = (int)std::min<int64_t>(grid_ctas, work);
+  count_launch();
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3((unsigned)grid_ctas);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = s;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, mw, mh, exW, exH, g, UT) == cudaSuccess;
+}
+
+}  // namespace kp

@@ -305,6 +305,15 @@ bool launch_ozaki_gemm(const double* A, int64_t lda, const double* B, int64_t ld
                        int64_t bias_stride, int rows_per_sample, int8_t* a_planes, int* a_ex,
                        int8_t* b_planes, int* b_ex, cudaStream_t s);
 
+// ---- fused Taylor layer, FP64 product on the INT8 tensor cores by the CRT (kp_crt.cu; KP_CRT=0 disables)
+bool crt_enabled();
+int crt_moduli();
+bool crt_act_ok(int S, int K, int N);
+void launch_crt_slice(const double* X, int64_t rows, int K, int64_t ldx, int8_t* planes, int* ex,
+                      bool weights, cudaStream_t s);
+bool launch_crt_act(const GemmAct& g, int mode, const int8_t* resH, const int* exH,
+                    const int8_t* resW, const int* exW, cudaStream_t s);
+
 // ---- small on-device generalised eigensolver + combine (kp_eig_small.cu) ---------
 struct SmallEigJob {
   int n;

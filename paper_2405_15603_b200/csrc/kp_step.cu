@@ -119,6 +119,7 @@ struct Plan {
   int64_t o_wT[MAXL] = {}, o_zval0 = 0, o_post[MAXL] = {}, o_pre[MAXL] = {}, o_gout[MAXL] = {};
   int64_t o_ping = 0, o_pong = 0;
   int64_t o_ozEa = 0, o_ozB = 0, o_ozEb = 0;  // Ozaki line-search scratch (KP_OZAKI=1)
+  int64_t o_crtH = 0, o_crtEH = 0, o_crtW = 0, o_crtEW = 0;  // CRT line-search residues
   int64_t o_bzval0 = 0, o_bpost[MAXL] = {}, o_bpre[MAXL] = {}, o_bg[MAXL] = {};
   int64_t o_bping = 0, o_bpong = 0, o_ones = 0;
   int64_t o_r = 0, o_rb = 0, o_rls = 0, o_rbls = 0, o_u = 0, o_upart = 0;
@@ -271,6 +272,12 @@ int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
     P.o_ozEa = take(Mc / 2 + 1);
     P.o_ozB = take((int64_t)P.maxh * P.maxh);
     P.o_ozEb = take(P.maxh);
+  }
+  if (crt_enabled()) {  // residue planes of one layer's states and weights (int8) + exponents
+    P.o_crtH = take(ceil_div((int64_t)crt_moduli() * Mc * P.maxh, 8));
+    P.o_crtEH = take(Mc / 2 + 1);
+    P.o_crtW = take(ceil_div((int64_t)crt_moduli() * P.maxh * P.maxh, 8));
+    P.o_crtEW = take(P.maxh / 2 + 1);
   }
   P.o_bpong = take(P.Bc * P.Nb * P.maxh);
   P.o_ones = take(P.Nb);
@@ -585,6 +592,49 @@ void forward_loss(const Ctx& c, const double* theta, const double* wpad, const d
     double* a = ping;
     double* b = pong;
     for (int l = 1; l + 1 < L; ++l) {
+      // FP64 product emulated on the INT8 tensor cores by the CRT construction (kp_crt.cu):
+      // slice the states and the candidate's weights into residue planes, then the fused
+      // layer (c5's one-sample tiles; the output layer folded in as in ACT_LAST below).
+      if (batch == 1 && td.taylor && crt_act_ok(td.S, P.h[l], P.h[l + 1])) {
+        int8_t* resH = reinterpret_cast<int8_t*>(c.at(P.o_crtH));
+        int* exH = reinterpret_cast<int*>(c.at(P.o_crtEH));
+        int8_t* resW = reinterpret_cast<int8_t*>(c.at(P.o_crtW));
+        int* exW = reinterpret_cast<int*>(c.at(P.o_crtEW));
+        launch_crt_slice(a, n * td.S, P.h[l], P.h[l], resH, exH, false, c.s);
+        launch_crt_slice(wpad + wp.wo[l], P.h[l + 1], P.h[l], P.h[l], resW, exW, true, c.s);
+        GemmAct ga{};
+        ga.bias = theta + P.th[l] + P.h[l];
+        ga.bias_stride = P.p[l];
+        ga.n_samples = n;
+        ga.S = td.S;
+        ga.d = td.d;
+        ga.taylor = true;
+        ga.N = P.h[l + 1];
+        ga.K = P.h[l];
+        ga.cdiag = cdiag;
+        const bool last = (l == L - 2 && u_out == nullptr);
+        if (last) {
+          ga.wlast = theta + P.th[L - 1];
+          ga.upart = c.at(P.o_upart);
+        } else {
+          ga.post = b;
+          ga.ldo = P.h[l + 1];
+        }
+        bool done = false;
+        prof_launch(c, 2.0 * (double)n * td.S * P.h[l] * P.h[l + 1], [&] {
+          done = launch_crt_act(ga, last ? ACT_LAST : ACT_LOSS, resH, exH, resW, exW, c.s);
+        });
+        if (done) {  // (a rejected launch falls through to the FP64 DMMA layer below)
+          if (last) {
+            launch_last_from_partials(c.at(P.o_upart), P.h[l + 1] / 128, n, td,
+                                      theta + P.th[L - 1] + P.h[L - 1], ri.r0, ri.seeds,
+                                      ri.targets, r, c.s, batch, P.D, r_bstride, ri.quad);
+            return;
+          }
+          std::swap(a, b);
+          continue;
+        }
+      }
       // FP64 emulated on the INT8 tensor cores (KP_OZAKI=1): GEMM + bias, then the Taylor
       // activation in place; the layer's stored-state buffer (idle during the line search)
       // holds the input's slices.  The h_out = 1 output layer then runs unfused below.
