@@ -11,24 +11,33 @@
 // tcgen05 GEMM of the symmetric residues per modulus, exact since K 128^2 <= 2^24.  With
 // q_i = M / p_i and s_i = q_i^-1 mod p_i folded into W's residues, t_i = acc_i mod p_i =
 // (s_i P) mod p_i and P = sum_i q_i t_i - k M for the integer k = round(sum / M).  The sum is
-// carried as an exact FP64 high part (q_i rounded down to a multiple of 2^E) plus an int32 low
-// part (the rest of q_i to 18 bits, error far below the 2^(BETA+5) input rounding);
+// carried as an exact FP64 high part (q_i rounded down to a multiple of 2^E) plus an FP32 low
+// part (the rest of q_i, accurate to 2^(BETA-1), far below the 2^(BETA+5) input rounding);
 // z = P 2^(e_r + f_u - 2 BETA).  The only approximation is the rounding of h and w to BETA bits:
 // about 2e-14 of sum_k |h_k w_k| (DGEMM: ~2e-16; 12 moduli, BETA = 41: 16x larger for 6% less
 // time, not taken); the line search consumes these losses only
 // through the argmin over the step-size grid (tools/crt_check.py: candidate losses within
-// 2e-14 relative of the DMMA path, runner-up gaps >= 6e-3).  Constants: tools/crt_constants.py.
+// 2e-14 relative of the DMMA path, runner-up gaps >= 6e-3).  Constants and the proof
+// obligations of the fold: tools/crt_constants.py (tests/test_crt_constants.py).
 //
 // Kernel (one persistent CTA per SM, 384 threads): warp 0 lane 0 = TMA producer (per modulus,
 // K in 128-byte chunks: W residues 128 units x 128 B, H residues 112 rows x 128 B, 128-byte
 // swizzle, six stages), warp 1 = TMEM allocator + MMA issuer (tcgen05.mma kind::i8, M 128
-// units, N 112 rows, K 32; two int32 accumulators of 112 columns), warps 4..11 = epilogue
-// (two per TMEM lane quadrant, 56 rows each; setmaxnreg 232): fold each modulus into the CRT
-// sums while the MMA computes the next one, then reconstruct, add the bias and apply the
-// Taylor activation (s0 on the value row, s1 g_i on the derivative rows, s1 l + s2 sum c_i g_i^2
-// on the operator row; the two halves of a sample exchange s1, s2 and the partial quadratic
-// form through shared memory).  ACT_LOSS writes the activations, ACT_LAST reduces them against
-// the output layer's weights into per-(row, unit tile) partial dots (k_last_from_partials).
+// units, N 112 rows, K 32; four int32 accumulators of 112 columns: the MMAs run up to four
+// moduli ahead of the fold, which covers the end-of-tile activation), warps 4..11 = epilogue
+// (two per TMEM lane quadrant, 56 rows each; setmaxnreg 232).  The fold of one modulus is
+// all FP32 / one DFMA per term (measured, tools/fold_bench.cu: integer multiply-high
+// reduction + DADD + DFMA with uniform-register constants 2278 clk per modulus and SM, this
+// form 2-3x less): t = f - p rint(f / p) on packed f32x2 pipes (FFMA2 / FADD2), the low CRT
+// part an FP32 FMA, the high part one DFMA against D = 1.5 +- t / 256, whose high word is the
+// bit pattern of an FP32 FMA result and whose low word is a register that stays zero; the
+// per-modulus constants are kept in vector registers (an FP64 instruction with a
+// uniform-register operand issues at a fraction of the rate).  Then reconstruct, add the
+// bias and apply the Taylor activation (s0 on the value row, s1 g_i on the derivative rows,
+// s1 l + s2 sum c_i g_i^2 on the operator row; the two halves of a sample exchange s1, s2 and
+// the partial quadratic form through shared memory), branch-free over a thread's 56 rows.
+// ACT_LOSS writes the activations, ACT_LAST reduces them against the output layer's weights
+// into per-(row, unit tile) partial dots (k_last_from_partials).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -44,21 +53,19 @@ namespace kp {
 
 namespace {
 
-// 13 moduli, log2 M = 102.525, BETA = 45, E = 53, low part c2 * 2^35  (tools/crt_constants.py 13)
+// 13 moduli, log2 M = 102.525, BETA = 45, E = 53  (tools/crt_constants.py 13)
 constexpr int NMOD = 13;
 constexpr int BETA = 45;
-constexpr double CR_LOW_SCALE = 0x1.0000000000000p+35;
 __constant__ double cr_pd[NMOD] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211};
 __constant__ double cr_ipd[NMOD] = {1.0 / 256, 1.0 / 255, 1.0 / 253, 1.0 / 251, 1.0 / 247, 1.0 / 241, 1.0 / 239, 1.0 / 233, 1.0 / 229, 1.0 / 227, 1.0 / 223, 1.0 / 217, 1.0 / 211};
 __constant__ double cr_s[NMOD] = {195, 1, 238, 224, 245, 161, 24, 60, 112, 29, 185, 156, 46};
-__constant__ double cr_q1[NMOD] = {0x1.703d73109e800p+94, 0x1.71af2232d1000p+94, 0x1.749b44df3c000p+94, 0x1.779353b31e000p+94, 0x1.7da85e6211000p+94, 0x1.8728d7b42d000p+94, 0x1.8a6ececc2d800p+94, 0x1.9497047757000p+94, 0x1.9ba8302477000p+94, 0x1.9f48aedffe000p+94, 0x1.a6bba31685800p+94, 0x1.b26be29560000p+94, 0x1.bec64ef0fa800p+94};
-__constant__ uint32_t cr_c2[NMOD] = {40666u, 207364u, 148907u, 87430u, 95213u, 119339u, 55624u, 226944u, 75224u, 207536u, 172466u, 125289u, 70460u};
-constexpr uint32_t CR_C2H = 192308489u;  // sum c2_i floor(p_i / 2)
+__constant__ float cr_npf[NMOD] = {-256.0f, -255.0f, -253.0f, -251.0f, -247.0f, -241.0f, -239.0f, -233.0f, -229.0f, -227.0f, -223.0f, -217.0f, -211.0f};
+__constant__ float cr_ipf[NMOD] = {0x1.0000000000000p-8f, 0x1.0101020000000p-8f, 0x1.03091c0000000p-8f, 0x1.0519800000000p-8f, 0x1.0953f40000000p-8f, 0x1.0fef020000000p-8f, 0x1.12358e0000000p-8f, 0x1.1945380000000p-8f, 0x1.1e2ef40000000p-8f, 0x1.20b4700000000p-8f, 0x1.25e2280000000p-8f, 0x1.2e025c0000000p-8f, 0x1.3698e00000000p-8f};
+__constant__ float cr_cl[NMOD] = {0x1.3db41a0000000p+50f, 0x1.9502080000000p+52f, 0x1.22d5880000000p+52f, 0x1.5585aa0000000p+51f, 0x1.73ed660000000p+51f, 0x1.d22a8c0000000p+51f, 0x1.b28fa40000000p+50f, 0x1.bb3fc00000000p+52f, 0x1.25d7d00000000p+51f, 0x1.9557fe0000000p+52f, 0x1.50d9000000000p+52f, 0x1.e9690e0000000p+51f, 0x1.133b840000000p+51f};
+__constant__ float cr_sg[NMOD] = {0x1.0000000000000p-11f, -0x1.0000000000000p-11f, 0x1.0000000000000p-11f, -0x1.0000000000000p-11f, 0x1.0000000000000p-11f, -0x1.0000000000000p-11f, 0x1.0000000000000p-11f, -0x1.0000000000000p-11f, 0x1.0000000000000p-11f, -0x1.0000000000000p-11f, 0x1.0000000000000p-11f, -0x1.0000000000000p-11f, 0x1.0000000000000p-11f};
+__constant__ double cr_sq[NMOD] = {0x1.703d73109e800p+102, -0x1.71af2232d1000p+102, 0x1.749b44df3c000p+102, -0x1.779353b31e000p+102, 0x1.7da85e6211000p+102, -0x1.8728d7b42d000p+102, 0x1.8a6ececc2d800p+102, -0x1.9497047757000p+102, 0x1.9ba8302477000p+102, -0x1.9f48aedffe000p+102, 0x1.a6bba31685800p+102, -0x1.b26be29560000p+102, 0x1.bec64ef0fa800p+102};
+constexpr double CR_C1 = 0x1.318a5ad26f400p+103;  // 384 sum sg_i q1_i
 constexpr double CR_M1 = 0x1.703d73109e938p+102, CR_M2 = 0x1.6d0683e4deb00p+52, CR_IM = 0x1.63f115f5d0b38p-103;
-__constant__ uint32_t cr_m[NMOD] = {2147483648u, 2155905153u, 2172947881u, 2190262207u, 2225732041u, 2281144456u, 2300233531u, 2359467013u, 2400680410u, 2421831780u, 2465272709u, 2533436931u, 2605477791u};
-__constant__ uint32_t cr_add[NMOD] = {16777344u, 16777597u, 16777568u, 16777467u, 16777351u, 16777576u, 16777441u, 16777514u, 16777341u, 16777456u, 16777516u, 16777463u, 16777348u};
-__constant__ uint32_t cr_pu[NMOD] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211};
-__constant__ double cr_hd[NMOD] = {0x1p52 + 128, 0x1p52 + 127, 0x1p52 + 126, 0x1p52 + 125, 0x1p52 + 123, 0x1p52 + 120, 0x1p52 + 119, 0x1p52 + 116, 0x1p52 + 114, 0x1p52 + 113, 0x1p52 + 111, 0x1p52 + 108, 0x1p52 + 105};
 
 #ifndef CRT_KB
 #define CRT_KB 128
@@ -73,12 +80,14 @@ constexpr int CM = 128, CN = 112, CKB = CRT_KB, CST = CRT_ST;
 constexpr int A_BYTES = CM * CKB, B_BYTES = CN * CKB, STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int EWQ = 2, NEW = 4 * EWQ, CPW = CN / EWQ;  // 56 rows per epilogue thread
 constexpr int THREADS = 32 * (4 + NEW);
-constexpr int TM_COLS = 256, ACC_STRIDE = 128;
+constexpr int NACC = 4, ACC_STRIDE = 128, TM_COLS = NACC * ACC_STRIDE;  // all of TMEM
+constexpr int ND = 4;  // zero-low FP64 scratch pairs of the fold
 constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(CN >> 3) << 17) |
                            ((uint32_t)(CM >> 4) << 24);
 constexpr size_t SMEM_BYTES = (size_t)CST * STAGE_BYTES + 1024;
 
 constexpr double MAGIC = 6755399441055744.0;  // 1.5 * 2^52: round-to-integer by addition
+constexpr float MAGICF = 12582912.0f;         // 1.5 * 2^23
 
 __device__ __forceinline__ double pow2i(int e) { return __hiloint2double((e + 1023) << 20, 0); }
 
@@ -137,30 +146,71 @@ __device__ __forceinline__ void tm_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
 
-// Folding one modulus (no conversion-unit instructions: I2F / F2F / FRND issue on the XU pipe
-// at a quarter of the FMA rate and bounded the first version): w = acc + add_i >= 0,
-// t' = w mod p_i in [0, p_i) by multiply-high (cr_m), t = t' - floor(p_i / 2) in [-128, 127];
-// x1 += q1_i t in FP64 (exact: t from the bits of 2^52 + t', q1_i a multiple of 2^E with
-// sum |q1_i t| < 2^(E+53)), x2 += c2_i t' in uint32 (< 2^31; offset CR_C2H removed at the end).
-struct FoldC {
-  uint32_t add, m, negp, c2;
-  double hd, q1;
-};
-
-__device__ __forceinline__ FoldC fold_consts(int i) {
-  return FoldC{cr_add[i], cr_m[i], 0u - cr_pu[i], cr_c2[i], cr_hd[i], cr_q1[i]};
+// Packed FP32 pairs (sm_100 f32x2 instructions: SASS FFMA2 / FADD2).
+__device__ __forceinline__ uint64_t pk2(float lo, float hi) {
+  uint64_t d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
+  return d;
+}
+__device__ __forceinline__ void unpk2(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// high word of the FP64 pair D <- bit pattern of fmaf(t, s, b); the low word (zero) stays
+__device__ __forceinline__ void set_hi(double& D, float t, float s, float b) {
+  asm("{\n.reg .b32 lo, hi;\nmov.b64 {lo, hi}, %0;\nfma.rn.f32 hi, %1, %2, %3;\nmov.b64 %0, {lo, hi};\n}"
+      : "+d"(D)
+      : "f"(t), "f"(s), "f"(b));
 }
 
-// fold NC accumulator columns of one modulus into the CRT sums: x1 (FP64, exact high part),
-// x2 (uint32, low part)
+// Per-modulus constants of the fold, in vector registers (`tz` is a zero the compiler cannot
+// prove uniform: constants it can prove uniform go to uniform registers, and FP64 / packed
+// instructions reading those issue far below their rate).
+struct FoldC {
+  float ip, np, cl, sg;
+  double sq;
+};
+__device__ __forceinline__ FoldC fold_consts(int i, uint32_t tz) {
+  FoldC c;
+  c.ip = __uint_as_float(__float_as_uint(cr_ipf[i]) | tz);
+  c.np = __uint_as_float(__float_as_uint(cr_npf[i]) | tz);
+  c.cl = __uint_as_float(__float_as_uint(cr_cl[i]) | tz);
+  c.sg = __uint_as_float(__float_as_uint(cr_sg[i]) | tz);
+  const double q = cr_sq[i];
+  c.sq = __hiloint2double(__double2hiint(q) | (int)tz, __double2loint(q) | (int)tz);
+  return c;
+}
+
+// Fold NC accumulator columns of one modulus into the CRT sums (tools/crt_constants.py):
+// f = float(acc) (exact), t = f - p rint(f / p) in [-128, 128] (magic-number rounding inside
+// the FMA), x2 += t cl (FP32 low part, packed pairs), x1 += (1.5 + sg t / 256) (sg 256 q1)
+// (exact FP64 high part; the constant 384 sg q1 is removed at the end).
 template <int NC>
-__device__ __forceinline__ void fold(const uint32_t* r, double* x1, uint32_t* x2, const FoldC& c) {
+__device__ __forceinline__ void fold(const uint32_t* r, double* x1, uint64_t* x2, const FoldC& c,
+                                     double* D, float bc) {
+  const uint64_t ip2 = pk2(c.ip, c.ip), np2 = pk2(c.np, c.np), cl2 = pk2(c.cl, c.cl);
+  const uint64_t mg = pk2(MAGICF, MAGICF), nmg = pk2(-MAGICF, -MAGICF);
 #pragma unroll
-  for (int j = 0; j < NC; ++j) {
-    const uint32_t w = r[j] + c.add;
-    const uint32_t t = w + (__umulhi(w, c.m) >> 7) * c.negp;  // w mod p in [0, p)
-    x2[j] += t * c.c2;
-    x1[j] = fma(__hiloint2double(0x43300000, (int)t) - c.hd, c.q1, x1[j]);
+  for (int j = 0; j < NC; j += 2) {
+    const uint64_t f2 = pk2(__int2float_rn((int)r[j]), __int2float_rn((int)r[j + 1]));
+    const uint64_t q2 = fadd2(ffma2(f2, ip2, mg), nmg);
+    const uint64_t t2 = ffma2(q2, np2, f2);
+    x2[j / 2] = ffma2(t2, cl2, x2[j / 2]);
+    float ta, tb;
+    unpk2(t2, ta, tb);
+    set_hi(D[j % ND], ta, c.sg, bc);
+    x1[j] = fma(D[j % ND], c.sq, x1[j]);
+    set_hi(D[(j + 1) % ND], tb, c.sg, bc);
+    x1[j + 1] = fma(D[(j + 1) % ND], c.sq, x1[j + 1]);
   }
 }
 
@@ -174,7 +224,6 @@ __host__ __device__ constexpr int modulus(int i) {
 __host__ __device__ constexpr int cmod(long long v, int p) {
   return (int)(v % p) > p / 2 ? (int)(v % p) - p : (int)(v % p);
 }
-constexpr float MAGICF = 12582912.0f;  // 1.5 * 2^23
 
 // Weight rows (once per layer and candidate): one warp per row, FP64 residue arithmetic with
 // s_i folded in, t_i = s_i a mod p_i.
@@ -321,10 +370,13 @@ __global__ void __launch_bounds__(THREADS, 1)
   extern __shared__ __align__(1024) uint8_t crt_sm[];
   uint8_t* base =
       reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(crt_sm) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t full[CST], empty[CST], tfull[2], tempty[2];
+  __shared__ uint64_t full[CST], empty[CST], tfull[NACC], tempty[NACC];
   __shared__ uint32_t tmem_base;
   __shared__ double xs1[CM], xs2[CM], xq[CM];  // value-row s1, s2 and half-0 quadratic form
   __shared__ double red[4][CN];                // ACT_LAST: per-quadrant row partials
+  __shared__ double sc_s[2][CN];               // row scales 2^e_r of the current / next tile
+  __shared__ double cw_s[CN];                  // c_i on derivative row i, 0 elsewhere
+  __shared__ uint32_t zero_s[32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = g.S;
   const Sched<CL> sch(g.n_samples, UT);
@@ -338,12 +390,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], CL == 1 ? 1 : 3);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NACC; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], NEW);
     }
     mbar_fence_init();
   }
+  if (threadIdx.x < 32) zero_s[threadIdx.x] = 0u;
+  for (int i = threadIdx.x; i < CN; i += THREADS) cw_s[i] = (i >= 1 && i <= g.d) ? g.cdiag[i - 1] : 0.0;
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
                      smem_addr(&tmem_base)),
@@ -384,8 +438,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint32_t it = 0, gm = 0;
       for (int tile = sch.first; tile < sch.count; tile += sch.step) {
         for (int i = 0; i < NMOD; ++i, ++gm) {
-          const uint32_t b = gm & 1;
-          if (gm >= 2) mbar_wait(&tempty[b], ((gm >> 1) - 1) & 1);
+          const uint32_t b = gm % NACC;
+          if (gm >= NACC) mbar_wait(&tempty[b], ((gm / NACC) - 1) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;\n");
           const uint32_t acc_col = tmem + b * ACC_STRIDE;
           for (int kc = 0; kc < KC; ++kc, ++it) {
@@ -430,58 +484,81 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int q = warp & 3, h = (warp - 4) >> 2;
     const int c0 = h * CPW;
     const int ul = 32 * q + lane;  // unit within the tile
+    const int te = threadIdx.x - 128;  // epilogue thread index
     const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c0;
     const int d = g.d;
-    uint32_t gm = 0;
-    for (int tile = sch.first; tile < sch.count; tile += sch.step) {
+    const int64_t rows_total = g.n_samples * S;
+    // a zero the compiler cannot prove uniform (volatile: not rematerialised)
+    uint32_t tz;
+    asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(tz) : "r"(smem_addr(&zero_s[lane])));
+    double D[ND];
+#pragma unroll
+    for (int j = 0; j < ND; ++j) D[j] = __hiloint2double((int)tz, (int)tz);
+    const float bc = __uint_as_float(0x3FF80000u | tz);  // 1.9375f: the high word of 1.5
+    const double c1 = __hiloint2double(__double2hiint(CR_C1) | (int)tz, __double2loint(CR_C1) | (int)tz);
+    uint32_t gm = 0, tcount = 0;
+    for (int tile = sch.first; tile < sch.count; tile += sch.step, ++tcount) {
       const int ut = sch.ut(tile);
       const int64_t smp = sch.smp(tile);
       const bool live = smp < g.n_samples;  // (CL = 4, odd n: the last pair's second sample)
       const int64_t row0 = smp * S;
       const int unit = ut * CM + ul;
-      double x1[CPW];
-      uint32_t x2[CPW];
-#pragma unroll
-      for (int j = 0; j < CPW; ++j) {
-        x1[j] = 0.0;
-        x2[j] = 0u;
+      double* sc = sc_s[tcount & 1];
+      if (te < CN) {  // this tile's row scales 2^e_r (rows past the end: clamped, never stored)
+        const int64_t r = row0 + te;
+        sc[te] = pow2i(exh[r < rows_total ? r : rows_total - 1]);
       }
+      double x1[CPW];
+      uint64_t x2[CPW / 2];
+#pragma unroll
+      for (int j = 0; j < CPW; ++j) x1[j] = 0.0;
+#pragma unroll
+      for (int j = 0; j < CPW / 2; ++j) x2[j] = 0ull;
 #pragma unroll 1
       for (int i = 0; i < NMOD; ++i, ++gm) {
-        const uint32_t b = gm & 1;
-        mbar_wait(&tfull[b], (gm >> 1) & 1);
+        const uint32_t b = gm % NACC;
+        const FoldC fc = fold_consts(i, tz);
+        mbar_wait(&tfull[b], (gm / NACC) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n");
-        const FoldC fc = fold_consts(i);
         const uint32_t ta = lane_base + b * ACC_STRIDE;
-        uint32_t r[32];
-        tm_ld<32>(ta, r);
+        uint32_t ra[16], rb[16];
+        tm_ld<16>(ta, ra);
         tm_wait();
+        tm_ld<16>(ta + 16, rb);
 #ifndef CRT_DBG_NOFOLD
-        fold<32>(r, x1, x2, fc);
+        fold<16>(ra, x1, x2, fc, D, bc);
 #endif
-        tm_ld<16>(ta + 32, r);
-        tm_ld<8>(ta + 48, r + 16);
+        tm_wait();
+        tm_ld<16>(ta + 32, ra);
+#ifndef CRT_DBG_NOFOLD
+        fold<16>(rb, x1 + 16, x2 + 8, fc, D, bc);
+#endif
+        tm_wait();
+        tm_ld<8>(ta + 48, rb);
+#ifndef CRT_DBG_NOFOLD
+        fold<16>(ra, x1 + 32, x2 + 16, fc, D, bc);
+#endif
         tm_wait();
         asm volatile("tcgen05.fence::before_thread_sync;\n");
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[b]);
 #ifndef CRT_DBG_NOFOLD
-        fold<24>(r, x1 + 32, x2 + 32, fc);
+        fold<8>(rb, x1 + 48, x2 + 24, fc, D, bc);
 #endif
       }
-      // reconstruct z = P 2^(e_r + f_u - 2 BETA) in x1 (value row: + bias)
+      asm volatile("bar.sync 5, 256;\n" ::: "memory");  // sc of this tile written
+      // reconstruct z = P 2^(e_r + f_u - 2 BETA) in x1, branch-free (rows past S: 0)
       const double su = pow2i(exw[unit] - 2 * BETA);
 #pragma unroll
       for (int j = 0; j < CPW; ++j) {
-        const int col = c0 + j;
-        double z = 0.0;
-        if (col < S && live) {
-          const double X2 = (double)(int)(x2[j] - CR_C2H) * CR_LOW_SCALE;
-          const double k = rint((x1[j] + X2) * CR_IM);
-          const double P = fma(-k, CR_M1, x1[j]) + fma(-k, CR_M2, X2);
-          z = P * su * pow2i(exh[row0 + col]);
-        }
-        x1[j] = z;
+        float lo, hi;
+        unpk2(x2[j / 2], lo, hi);
+        const double X1 = x1[j] - c1;
+        const double X2 = (double)((j & 1) ? hi : lo);
+        const double k = fma(X1 + X2, CR_IM, MAGIC) - MAGIC;
+        const double P = fma(-k, CR_M1, X1) + fma(-k, CR_M2, X2);
+        const double z = (P * su) * sc[c0 + j];
+        x1[j] = (c0 + j < S) ? z : 0.0;
       }
       // Taylor activation (src/taylor.py:140-169): half 0 owns the value row and derivative
       // rows 1..55, half 1 the remaining derivative rows and the operator row S - 1.
@@ -492,39 +569,40 @@ __global__ void __launch_bounds__(THREADS, 1)
         s0 = t.s0;
         s1 = t.s1;
         s2 = t.s2;
-#pragma unroll
-        for (int j = 1; j < CPW; ++j) quad += (x1[j] * g.cdiag[j - 1]) * x1[j];
-        xs1[ul] = s1;
-        xs2[ul] = s2;
-        xq[ul] = quad;
-      }
-      asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");
-      if (h == 1) {
+      } else {
+        asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");
         s1 = xs1[ul];
         s2 = xs2[ul];
         quad = xq[ul];
+      }
+      // quadratic form over this half's derivative rows (cw = 0 on every other row)
 #pragma unroll
-        for (int j = 0; j < CPW; ++j) {
-          const int i = c0 + j;  // derivative index
-          if (i <= d) quad += (x1[j] * g.cdiag[i - 1]) * x1[j];
-        }
+      for (int j = 0; j < CPW; ++j) quad += (x1[j] * cw_s[c0 + j]) * x1[j];
+      if (h == 0) {
+        xs1[ul] = s1;
+        xs2[ul] = s2;
+        xq[ul] = quad;
+        asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");
       }
       asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");  // xs*/xq reusable
       // outputs in x1
+      const double s2q = s2 * quad;
 #pragma unroll
       for (int j = 0; j < CPW; ++j) {
-        const int col = c0 + j;
-        double o;
-        if (col == 0) o = s0;
-        else if (col == S - 1) o = s1 * x1[j] + s2 * quad;
-        else o = s1 * x1[j];
-        x1[j] = o;
+        const double o = s1 * x1[j];
+        x1[j] = (c0 + j == S - 1) ? o + s2q : o;
       }
+      if (h == 0) x1[0] = s0;
       if (MODE == ACT_LOSS) {
+        double* out = g.post + row0 * g.ldo + unit;
 #pragma unroll
         for (int j = 0; j < CPW; ++j) {
-          const int col = c0 + j;
-          if (col < S && live) g.post[(row0 + col) * g.ldo + unit] = x1[j];
+          const uint32_t ok = (c0 + j < S) && live;
+          asm volatile(
+              "{\n.reg .pred p;\nsetp.ne.b32 p, %2, 0;\n@p st.global.f64 [%0], %1;\n}\n" ::"l"(
+                  out + (int64_t)(c0 + j) * g.ldo),
+              "d"(x1[j]), "r"(ok)
+              : "memory");
         }
       } else {  // ACT_LAST: row partials over this tile's 128 units
         const double wl = g.wlast[unit];
@@ -536,7 +614,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (lane == 0) red[q][c0 + j] = v;
         }
         asm volatile("bar.sync 5, 256;\n" ::: "memory");
-        for (int col = threadIdx.x - 128; live && col < S; col += 256)
+        for (int col = te; live && col < S; col += 256)
           g.upart[(row0 + col) * UT + ut] = ((red[0][col] + red[1][col]) + red[2][col]) + red[3][col];
         asm volatile("bar.sync 5, 256;\n" ::: "memory");
       }
