@@ -85,6 +85,14 @@ constexpr int ND = 4;  // zero-low FP64 scratch pairs of the fold
 constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(CN >> 3) << 17) |
                            ((uint32_t)(CM >> 4) << 24);
 constexpr size_t SMEM_BYTES = (size_t)CST * STAGE_BYTES + 1024;
+// CTA pair (CL = 2, tcgen05 cta_group::2): one MMA of M 256 units x N 112 rows spans the two
+// SMs of a TPC; each CTA stages its own 128 units of W and HALF of the sample's rows (the pair
+// shares B), so a stage is 23 KB and eight of them fit.
+constexpr int B2_BYTES = (CN / 2) * CKB, STAGE2_BYTES = A_BYTES + B2_BYTES, CST2 = 8;
+constexpr size_t SMEM2_BYTES = (size_t)CST2 * STAGE2_BYTES + 1024;
+constexpr uint32_t IDESC2 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(CN >> 3) << 17) |
+                            ((uint32_t)((2 * CM) >> 4) << 24);
+constexpr int CST_MAX = CST2 > CST ? CST2 : CST;
 
 constexpr double MAGIC = 6755399441055744.0;  // 1.5 * 2^52: round-to-integer by addition
 constexpr float MAGICF = 12582912.0f;         // 1.5 * 2^23
@@ -340,13 +348,21 @@ struct Sched {
       asm("mov.u32 %0, %%nclusterid.x;\n" : "=r"(ncl));
       first = cid;
       step = ncl;
-      count = (int)((n_samples + 1) / 2 * (UT / 2));
-      cu = (int)(rank & 1);
-      cs = (int)(rank >> 1);
+      if (CL == 2) {  // pair tile: unit tiles 2 (t % (UT/2)) + rank of sample t / (UT/2)
+        count = (int)(n_samples * (UT / 2));
+        cu = (int)rank;
+        cs = 0;
+      } else {
+        count = (int)((n_samples + 1) / 2 * (UT / 2));
+        cu = (int)(rank & 1);
+        cs = (int)(rank >> 1);
+      }
     }
   }
   __device__ int ut(int t) const { return CL == 1 ? t % UT : 2 * (t % (UT / 2)) + cu; }
-  __device__ int64_t smp(int t) const { return CL == 1 ? t / UT : 2 * (int64_t)(t / (UT / 2)) + cs; }
+  __device__ int64_t smp(int t) const {
+    return CL == 1 ? t / UT : CL == 2 ? t / (UT / 2) : 2 * (int64_t)(t / (UT / 2)) + cs;
+  }
 };
 
 __device__ __forceinline__ void tma3d_mc(void* dst, const CUtensorMap* m, int x, int y, int z,
@@ -358,10 +374,39 @@ __device__ __forceinline__ void tma3d_mc(void* dst, const CUtensorMap* m, int x,
       : "memory");
 }
 
+// CTA-pair load: the bytes are counted on the LEADER CTA's mbarrier (`lbar`: its
+// shared::cluster address)
+__device__ __forceinline__ void tma3d_2sm(void* dst, const CUtensorMap* m, int x, int y, int z,
+                                          uint32_t lbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(x), "r"(y), "r"(z), "r"(lbar)
+      : "memory");
+}
+// shared::cluster address of `p` in the CTA of rank `rank`
+__device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(smem_addr(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(addr) : "memory");
+}
+
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
                    : "memory");
 }
+
+#ifdef CRT_TIMING  // (tools/crt_bench.cu: where block 0's roles spend their cycles)
+__device__ long long crt_dbg[16];
+#define CRT_T0(v) const long long v = clock64()
+#define CRT_ACC(slot, v) dbg_acc[slot] += clock64() - (v)
+#else
+#define CRT_T0(v)
+#define CRT_ACC(slot, v)
+#endif
 
 template <int MODE, int CL>
 __global__ void __launch_bounds__(THREADS, 1)
@@ -370,11 +415,13 @@ __global__ void __launch_bounds__(THREADS, 1)
   extern __shared__ __align__(1024) uint8_t crt_sm[];
   uint8_t* base =
       reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(crt_sm) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t full[CST], empty[CST], tfull[NACC], tempty[NACC];
+  __shared__ uint64_t full[CST_MAX], empty[CST_MAX], tfull[NACC], tempty[NACC];
+  constexpr int NST = CL == 2 ? CST2 : CST;
+  constexpr int STB = CL == 2 ? STAGE2_BYTES : STAGE_BYTES;
   __shared__ uint32_t tmem_base;
   __shared__ double xs1[CM], xs2[CM], xq[CM];  // value-row s1, s2 and half-0 quadratic form
   __shared__ double red[4][CN];                // ACT_LAST: per-quadrant row partials
-  __shared__ double sc_s[2][CN];               // row scales 2^e_r of the current / next tile
+  __shared__ double sc_s[2][CN];               // row scales 2^(e_r - BETA) of the current / next tile
   __shared__ double cw_s[CN];                  // c_i on derivative row i, 0 elsewhere
   __shared__ uint32_t zero_s[32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -386,23 +433,30 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint16_t mask_w = (uint16_t)((1u << sch.cu) | (1u << (sch.cu + 2)));
   const uint16_t mask_h = (uint16_t)(3u << (2 * sch.cs));
   if (threadIdx.x == 0) {
-    for (int s = 0; s < CST; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CL == 1 ? 1 : 3);
+      mbar_init(&empty[s], CL == 4 ? 3 : 1);
     }
     for (int b = 0; b < NACC; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], NEW);
+      mbar_init(&tempty[b], CL == 2 ? 2 * NEW : NEW);  // pair: both CTAs' epilogues release
     }
     mbar_fence_init();
   }
   if (threadIdx.x < 32) zero_s[threadIdx.x] = 0u;
   for (int i = threadIdx.x; i < CN; i += THREADS) cw_s[i] = (i >= 1 && i <= g.d) ? g.cdiag[i - 1] : 0.0;
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
-                     smem_addr(&tmem_base)),
-                 "r"(TM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    if (CL == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                       smem_addr(&tmem_base)),
+                   "r"(TM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                       smem_addr(&tmem_base)),
+                   "r"(TM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n");
   __syncthreads();
@@ -414,15 +468,31 @@ __global__ void __launch_bounds__(THREADS, 1)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n");
     if (warp == 0 && lane == 0) {  // TMA producer
       uint32_t it = 0;
+#ifdef CRT_TIMING
+      long long dbg_acc[2] = {0, 0};
+      const long long dbg_t0 = clock64();
+#endif
+      const uint32_t lfull0 = CL == 2 ? mapa(&full[0], 0) : 0u;  // the leader's full[0]
       for (int tile = sch.first; tile < sch.count; tile += sch.step) {
         const int ut = sch.ut(tile);
         const int row0 = (int)(sch.smp(tile) * S);
         for (int i = 0; i < NMOD; ++i)
           for (int kc = 0; kc < KC; ++kc, ++it) {
-            const uint32_t s = it % CST;
-            if (it >= CST) mbar_wait(&empty[s], ((it / CST) - 1) & 1);
-            uint8_t* a = base + s * STAGE_BYTES;
-            mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+            const uint32_t s = it % NST;
+            {
+              CRT_T0(tw);
+              if (it >= NST) mbar_wait(&empty[s], ((it / NST) - 1) & 1);
+              CRT_ACC(0, tw);
+            }
+            uint8_t* a = base + s * STB;
+            if (CL == 2) {  // both CTAs' bytes are counted on the leader's barrier
+              if (sch.cu == 0) mbar_arrive_expect_tx(&full[s], 2 * STB);
+              const uint32_t lbar = lfull0 + s * (uint32_t)sizeof(uint64_t);
+              tma3d_2sm(a, &mW, kc * CKB, ut * CM, i, lbar);
+              tma3d_2sm(a + A_BYTES, &mH, kc * CKB, row0 + sch.cu * (CN / 2), i, lbar);
+              continue;
+            }
+            mbar_arrive_expect_tx(&full[s], STB);
             if (CL == 1) {
               tma3d(a, &mW, kc * CKB, ut * CM, i, &full[s]);
               tma3d(a + A_BYTES, &mH, kc * CKB, row0, i, &full[s]);
@@ -434,28 +504,52 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
           }
       }
-    } else if (warp == 1 && lane == 0) {  // MMA issuer
+#ifdef CRT_TIMING
+      if (blockIdx.x == 0) {
+        crt_dbg[0] = dbg_acc[0];
+        crt_dbg[1] = clock64() - dbg_t0;
+      }
+#endif
+    } else if (warp == 1 && lane == 0 && (CL != 2 || sch.cu == 0)) {  // MMA issuer (pair: leader)
       uint32_t it = 0, gm = 0;
+#ifdef CRT_TIMING
+      long long dbg_acc[2] = {0, 0};
+      const long long dbg_t0 = clock64();
+#endif
       for (int tile = sch.first; tile < sch.count; tile += sch.step) {
         for (int i = 0; i < NMOD; ++i, ++gm) {
           const uint32_t b = gm % NACC;
-          if (gm >= NACC) mbar_wait(&tempty[b], ((gm / NACC) - 1) & 1);
+          {
+            CRT_T0(tw);
+            if (gm >= NACC) mbar_wait(&tempty[b], ((gm / NACC) - 1) & 1);
+            CRT_ACC(0, tw);
+          }
           asm volatile("tcgen05.fence::after_thread_sync;\n");
           const uint32_t acc_col = tmem + b * ACC_STRIDE;
           for (int kc = 0; kc < KC; ++kc, ++it) {
-            const uint32_t s = it % CST;
-            mbar_wait(&full[s], (it / CST) & 1);
+            const uint32_t s = it % NST;
+            {
+              CRT_T0(tw);
+              mbar_wait(&full[s], (it / NST) & 1);
+              CRT_ACC(1, tw);
+            }
             asm volatile("tcgen05.fence::after_thread_sync;\n");
-            const uint32_t a = smem_addr(base + s * STAGE_BYTES), bb = a + A_BYTES;
+            const uint32_t a = smem_addr(base + s * STB), bb = a + A_BYTES;
 #pragma unroll
             for (int k = 0; k < CKB / 32; ++k) {
               const uint64_t da = sdesc(a + 32 * k), db = sdesc(bb + 32 * k);
               const uint32_t acc = (kc | k) ? 1u : 0u;
 #ifndef CRT_DBG_NOMMA  // (tools/crt_bench.cu timing variants)
-              asm volatile(
-                  "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                  "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(acc_col),
-                  "l"(da), "l"(db), "r"(IDESC), "r"(acc));
+              if (CL == 2)
+                asm volatile(
+                    "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                    "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(acc_col),
+                    "l"(da), "l"(db), "r"(IDESC2), "r"(acc));
+              else
+                asm volatile(
+                    "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(acc_col),
+                    "l"(da), "l"(db), "r"(IDESC), "r"(acc));
 #else
               (void)da, (void)db, (void)acc, (void)acc_col;
 #endif
@@ -465,6 +559,12 @@ __global__ void __launch_bounds__(THREADS, 1)
                   "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                       smem_addr(&empty[s]))
                   : "memory");
+            else if (CL == 2)
+              asm volatile(
+                  "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::"
+                  "cluster.b64 [%0], %1;\n" ::"r"(smem_addr(&empty[s])),
+                  "h"((uint16_t)3)
+                  : "memory");
             else
               asm volatile(
                   "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::"
@@ -472,12 +572,26 @@ __global__ void __launch_bounds__(THREADS, 1)
                   "h"((uint16_t)(mask_w | mask_h))
                   : "memory");
           }
-          asm volatile(
-              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                  smem_addr(&tfull[b]))
-              : "memory");
+          if (CL == 2)
+            asm volatile(
+                "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::"
+                "cluster.b64 [%0], %1;\n" ::"r"(smem_addr(&tfull[b])),
+                "h"((uint16_t)3)
+                : "memory");
+          else
+            asm volatile(
+                "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                    smem_addr(&tfull[b]))
+                : "memory");
         }
       }
+#ifdef CRT_TIMING
+      if (blockIdx.x == 0) {
+        crt_dbg[2] = dbg_acc[0];
+        crt_dbg[3] = dbg_acc[1];
+        crt_dbg[4] = clock64() - dbg_t0;
+      }
+#endif
     }
   } else {  // epilogue: quadrant q = TMEM lanes 32q..32q+31 = units, half h = rows 56h..56h+55
     asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n");
@@ -495,8 +609,17 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
     for (int j = 0; j < ND; ++j) D[j] = __hiloint2double((int)tz, (int)tz);
     const float bc = __uint_as_float(0x3FF80000u | tz);  // 1.9375f: the high word of 1.5
-    const double c1 = __hiloint2double(__double2hiint(CR_C1) | (int)tz, __double2loint(CR_C1) | (int)tz);
+    auto vreg = [tz](double v) {  // the constant in a vector register pair (see FoldC)
+      return __hiloint2double(__double2hiint(v) | (int)tz, __double2loint(v) | (int)tz);
+    };
+    const double c1 = vreg(CR_C1);
+    const double v_im = CR_IM, v_mg = MAGIC, v_m1 = CR_M1, v_m2 = CR_M2;
+    const uint32_t ltempty0 = CL == 2 ? mapa(&tempty[0], 0) : 0u;  // the leader's tempty[0]
     uint32_t gm = 0, tcount = 0;
+#ifdef CRT_TIMING
+    long long dbg_acc[7] = {0, 0, 0, 0, 0, 0, 0};
+    const long long dbg_t0 = clock64();
+#endif
     for (int tile = sch.first; tile < sch.count; tile += sch.step, ++tcount) {
       const int ut = sch.ut(tile);
       const int64_t smp = sch.smp(tile);
@@ -504,21 +627,25 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int64_t row0 = smp * S;
       const int unit = ut * CM + ul;
       double* sc = sc_s[tcount & 1];
-      if (te < CN) {  // this tile's row scales 2^e_r (rows past the end: clamped, never stored)
+      if (te < CN) {  // this tile's row scales 2^(e_r - BETA) (rows past the end: clamped, never stored)
         const int64_t r = row0 + te;
-        sc[te] = pow2i(exh[r < rows_total ? r : rows_total - 1]);
+        sc[te] = pow2i(exh[r < rows_total ? r : rows_total - 1] - BETA);
       }
       double x1[CPW];
       uint64_t x2[CPW / 2];
 #pragma unroll
-      for (int j = 0; j < CPW; ++j) x1[j] = 0.0;
+      for (int j = 0; j < CPW; ++j) x1[j] = -c1;  // the fold adds C1 = 384 sum sg_i q1_i
 #pragma unroll
       for (int j = 0; j < CPW / 2; ++j) x2[j] = 0ull;
 #pragma unroll 1
       for (int i = 0; i < NMOD; ++i, ++gm) {
         const uint32_t b = gm % NACC;
         const FoldC fc = fold_consts(i, tz);
-        mbar_wait(&tfull[b], (gm / NACC) & 1);
+        {
+          CRT_T0(tw);
+          mbar_wait(&tfull[b], (gm / NACC) & 1);
+          CRT_ACC(0, tw);
+        }
         asm volatile("tcgen05.fence::after_thread_sync;\n");
         const uint32_t ta = lane_base + b * ACC_STRIDE;
         uint32_t ra[16], rb[16];
@@ -541,31 +668,36 @@ __global__ void __launch_bounds__(THREADS, 1)
         tm_wait();
         asm volatile("tcgen05.fence::before_thread_sync;\n");
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[b]);
+        if (lane == 0) {
+          if (CL == 2) mbar_arrive_cluster(ltempty0 + b * (uint32_t)sizeof(uint64_t));
+          else mbar_arrive(&tempty[b]);
+        }
 #ifndef CRT_DBG_NOFOLD
         fold<8>(rb, x1 + 48, x2 + 24, fc, D, bc);
 #endif
       }
+      CRT_T0(ttail);
       asm volatile("bar.sync 5, 256;\n" ::: "memory");  // sc of this tile written
-      // reconstruct z = P 2^(e_r + f_u - 2 BETA) in x1, branch-free (rows past S: 0)
-      const double su = pow2i(exw[unit] - 2 * BETA);
+      CRT_ACC(2, ttail);
+      // reconstruct y = P 2^(e_r - BETA) (z = y su, su = 2^(f_u - BETA): folded into the
+      // activation's factors) in x1, branch-free (rows past S: 0).  x1 started at -C1.
+      const double su = pow2i(exw[unit] - BETA);
 #pragma unroll
       for (int j = 0; j < CPW; ++j) {
         float lo, hi;
         unpk2(x2[j / 2], lo, hi);
-        const double X1 = x1[j] - c1;
         const double X2 = (double)((j & 1) ? hi : lo);
-        const double k = fma(X1 + X2, CR_IM, MAGIC) - MAGIC;
-        const double P = fma(-k, CR_M1, X1) + fma(-k, CR_M2, X2);
-        const double z = (P * su) * sc[c0 + j];
-        x1[j] = (c0 + j < S) ? z : 0.0;
+        const double k = fma(x1[j] + X2, v_im, v_mg) - v_mg;
+        const double P = fma(-k, v_m1, x1[j]) + fma(-k, v_m2, X2);
+        const double y = P * sc[c0 + j];
+        x1[j] = (c0 + j < S) ? y : 0.0;
       }
+      CRT_ACC(3, ttail);
       // Taylor activation (src/taylor.py:140-169): half 0 owns the value row and derivative
       // rows 1..55, half 1 the remaining derivative rows and the operator row S - 1.
       double s0 = 0.0, s1 = 0.0, s2 = 0.0, quad = 0.0;
       if (h == 0) {
-        x1[0] += g.bias[(int64_t)unit * g.bias_stride];
-        const TanhD t = tanh_derivs(x1[0], false);
+        const TanhD t = tanh_derivs(fma(x1[0], su, g.bias[(int64_t)unit * g.bias_stride]), false);
         s0 = t.s0;
         s1 = t.s1;
         s2 = t.s2;
@@ -575,7 +707,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         s2 = xs2[ul];
         quad = xq[ul];
       }
-      // quadratic form over this half's derivative rows (cw = 0 on every other row)
+      // quadratic form over this half's derivative rows (cw = 0 on every other row), in
+      // units of su^2
 #pragma unroll
       for (int j = 0; j < CPW; ++j) quad += (x1[j] * cw_s[c0 + j]) * x1[j];
       if (h == 0) {
@@ -585,14 +718,16 @@ __global__ void __launch_bounds__(THREADS, 1)
         asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");
       }
       asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");  // xs*/xq reusable
+      CRT_ACC(4, ttail);
       // outputs in x1
-      const double s2q = s2 * quad;
+      const double s1u = s1 * su, s2q = s2 * (quad * (su * su));
 #pragma unroll
       for (int j = 0; j < CPW; ++j) {
-        const double o = s1 * x1[j];
+        const double o = s1u * x1[j];
         x1[j] = (c0 + j == S - 1) ? o + s2q : o;
       }
       if (h == 0) x1[0] = s0;
+      CRT_ACC(5, ttail);
       if (MODE == ACT_LOSS) {
         double* out = g.post + row0 * g.ldo + unit;
 #pragma unroll
@@ -618,14 +753,31 @@ __global__ void __launch_bounds__(THREADS, 1)
           g.upart[(row0 + col) * UT + ut] = ((red[0][col] + red[1][col]) + red[2][col]) + red[3][col];
         asm volatile("bar.sync 5, 256;\n" ::: "memory");
       }
+      CRT_ACC(1, ttail);
     }
+#ifdef CRT_TIMING
+    if (blockIdx.x == 0 && threadIdx.x == 128) {
+      crt_dbg[5] = dbg_acc[0];
+      crt_dbg[6] = dbg_acc[1];
+      crt_dbg[7] = dbg_acc[2];
+      crt_dbg[8] = clock64() - dbg_t0;
+      crt_dbg[9] = dbg_acc[3];
+      crt_dbg[10] = dbg_acc[4];
+      crt_dbg[11] = dbg_acc[5];
+    }
+#endif
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n");
   __syncthreads();
   if (CL > 1) cluster_sync_all();  // no peer still multicasts into this CTA's stages
-  if (warp == 1)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
-                 "r"(TM_COLS));
+  if (warp == 1) {
+    if (CL == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                   "r"(TM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                   "r"(TM_COLS));
+  }
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 crt_encode() {
@@ -720,38 +872,47 @@ bool launch_crt_act(const GemmAct& g, int mode, const int8_t* resH, const int* e
     return false;
   const int64_t rows = g.n_samples * g.S;
   const int UT = g.N / CM;
+  // KP_CRT_CLUSTER: 1 = independent CTAs (the default: fastest, 5649 pts/s on c5), 2 = CTA
+  // pairs (tcgen05 cta_group::2 MMA of 256 units, the pair sharing the sample's rows: 23% less
+  // L2 and shared-memory fill traffic, but 5483 pts/s), 4 = 2 x 2 clusters of single-CTA MMAs
+  // with multicast loads (half the L2 traffic, 5646 pts/s).  Both cluster forms lose to the
+  // lock-step of their CTAs what they save in traffic.
   static const int cl_env = [] {
     const char* e = getenv("KP_CRT_CLUSTER");
-    return e ? atoi(e) : 4;
+    return e ? atoi(e) : 1;
   }();
-  const int CL = (cl_env == 4 && UT % 2 == 0 && g.n_samples >= 2) ? 4 : 1;
+  int CL = 1;
+  if (cl_env == 2 && UT % 2 == 0) CL = 2;
+  if (cl_env == 4 && UT % 2 == 0 && g.n_samples >= 2) CL = 4;
   CUtensorMap mw, mh;
   if (!crt_map(&mw, resW, g.N, g.K, CL == 4 ? CM / 2 : CM) ||
-      !crt_map(&mh, resH, rows, g.K, CL == 4 ? CN / 2 : CN))
+      !crt_map(&mh, resH, rows, g.K, CL == 1 ? CN : CN / 2))
     return false;
   void (*kern)(const CUtensorMap, const CUtensorMap, const int*, const int*, GemmAct, int);
-  if (mode == ACT_LAST) kern = CL == 4 ? k_crt_act<ACT_LAST, 4> : k_crt_act<ACT_LAST, 1>;
-  else kern = CL == 4 ? k_crt_act<ACT_LOSS, 4> : k_crt_act<ACT_LOSS, 1>;
-  static std::map<void*, int> max_clusters;  // co-resident 4-CTA clusters (persistent grid)
+  if (mode == ACT_LAST)
+    kern = CL == 4 ? k_crt_act<ACT_LAST, 4> : CL == 2 ? k_crt_act<ACT_LAST, 2> : k_crt_act<ACT_LAST, 1>;
+  else
+    kern = CL == 4 ? k_crt_act<ACT_LOSS, 4> : CL == 2 ? k_crt_act<ACT_LOSS, 2> : k_crt_act<ACT_LOSS, 1>;
+  const size_t smem = CL == 2 ? SMEM2_BYTES : SMEM_BYTES;
+  static std::map<void*, int> max_clusters;  // co-resident clusters (persistent grid)
   static std::mutex mu;
   int grid_ctas;
   {
     std::lock_guard<std::mutex> lock(mu);
     auto it = max_clusters.find((void*)kern);
     if (it == max_clusters.end()) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       int mc = sm_count();
-      if (CL == 4) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (CL > 1) {
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = 4;
+        at[0].val.clusterDim.x = CL;
         at[0].val.clusterDim.y = 1;
         at[0].val.clusterDim.z = 1;
-        cfg.gridDim = dim3(4 * sm_count());
+        cfg.gridDim = dim3(CL * sm_count());
         cfg.blockDim = dim3(THREADS);
-        cfg.dynamicSmemBytes = SMEM_BYTES;
+        cfg.dynamicSmemBytes = smem;
         cfg.attrs = at;
         cfg.numAttrs = 1;
         mc = 0;
@@ -760,10 +921,12 @@ bool launch_crt_act(const GemmAct& g, int mode, const int8_t* resH, const int* e
       }
       it = max_clusters.emplace((void*)kern, mc).first;
     }
-    grid_ctas = CL == 4 ? 4 * it->second : it->second;
+    grid_ctas = CL * it->second;
   }
   if (grid_ctas <= 0) return false;
-  const int64_t work = CL == 4 ? 4 * ((g.n_samples + 1) / 2 * (UT / 2)) : g.n_samples * UT;
+  const int64_t work = CL == 4   ? 4 * ((g.n_samples + 1) / 2 * (UT / 2))
+                       : CL == 2 ? 2 * (g.n_samples * (UT / 2))
+                                 : g.n_samples * UT;
   grid_ctas = (int)std::min<int64_t>(grid_ctas, work);
   count_launch();
   cudaLaunchConfig_t cfg = {};
@@ -774,7 +937,7 @@ bool launch_crt_act(const GemmAct& g, int mode, const int8_t* resH, const int* e
   at[0].val.clusterDim.z = 1;
   cfg.gridDim = dim3((unsigned)grid_ctas);
   cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cfg.attrs = at;
   cfg.numAttrs = 1;

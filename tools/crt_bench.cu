@@ -124,6 +124,23 @@ int main(int argc, char** argv) {
   printf("crt LOSS %.3f ms = %.1f FP64-equiv TFLOP/s\n", best[2], fl / best[2] / 1e9);
   printf("crt LAST %.3f ms\n", best[3]);
   printf("dmma LOSS %.3f ms = %.1f TFLOP/s\n", best[4], fl / best[4] / 1e9);
+#if defined(CRT_INLINE) && defined(CRT_TIMING)
+  {  // one more launch per mode, then block 0's cycle counters
+    for (int mode = 0; mode < 2; ++mode) {
+      g.post = mode == 0 ? o1 : nullptr;
+      g.upart = mode == 0 ? nullptr : up1;
+      kp::launch_crt_act(g, mode == 0 ? kp::ACT_LOSS : kp::ACT_LAST, rH, eH, rW, eW, 0);
+      CK(cudaDeviceSynchronize());
+      long long h[16];
+      CK(cudaMemcpyFromSymbol(h, kp::crt_dbg, sizeof(h)));
+      printf("block 0 (%s), kilo-clocks: producer wait-empty %lld of %lld | mma wait-tempty %lld wait-full %lld "
+             "of %lld | epilogue warp 4: wait-tfull %lld, tail %lld (cumulative: barrier %lld, reconstruct %lld, "
+             "activation %lld, outputs %lld) of %lld\n",
+             mode == 0 ? "LOSS" : "LAST", h[0] / 1000, h[1] / 1000, h[2] / 1000, h[3] / 1000, h[4] / 1000,
+             h[5] / 1000, h[6] / 1000, h[7] / 1000, h[9] / 1000, h[10] / 1000, h[11] / 1000, h[8] / 1000);
+    }
+  }
+#endif
   // compare activations row by row (relative to the row's max |.|) on a sample of rows
   std::vector<double> a((size_t)N), b((size_t)N);
   double worst = 0;

@@ -15,9 +15,9 @@ epilogue does it:
                                            FP32 1.9375 + sg_i t 2^-11, low word 0)
     high += D * (sg_i 256 q1_i)           FP64, q1_i = q_i - (q_i mod 2^E); adds q1_i t +
                                            384 sg_i q1_i, sg_i = +-1 alternating
-so high - C1 (C1 = 384 sum sg_i q1_i) = sum q1_i t_i exactly: every partial sum is a multiple
+so, started at -C1 (C1 = 384 sum sg_i q1_i), high = sum q1_i t_i exactly: every partial sum is a multiple
 of 2^E below 2^(E+53) (`derive` picks E for that; the alternating signs keep the 384 q1_i
-offsets from piling up).  P = high - C1 + low - k M with k = rint((high - C1 + low) / M).  The
+offsets from piling up).  P = high + low - k M with k = rint((high + low) / M).  The
 FP32 low part is accurate to 2^(BETA - 1), far below the 2^(BETA + 5) rounding of the inputs.
 """
 import math
@@ -54,7 +54,8 @@ def derive(n):
 
     def worst_partial(E):
         q1 = [(x >> E) << E for x in q]
-        worst, const, mag = 0, 0, 0
+        c1 = 384 * sum(a * b for a, b in zip(sg, q1))
+        worst, const, mag = abs(c1), -c1, 0  # the kernel starts the high part at -C1
         for a, b in zip(sg, q1):
             const += 384 * a * b
             mag += 128 * b

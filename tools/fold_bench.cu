@@ -239,6 +239,65 @@ void run(const char* name, int iters, double* out, long long* cyc) {
          avg / ((double)iters * NMOD), cudaGetErrorString(e));
 }
 
+// reconstruction tail of kp_crt.cu in isolation: 56 columns per thread, 8 warps per SM.
+// CV = 0: F2F.F64.F32 for the FP32 low part, 1: integer bit manipulation, 2: no conversion
+template <int CV>
+__global__ void __launch_bounds__(256, 1) k_tail(int iters, double* out, long long* cyc) {
+  __shared__ double sc[128];
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) sc[i] = 1.0 + i * 0x1p-20;
+  __syncthreads();
+  double x1[CPW];
+  float x2[CPW];
+#pragma unroll
+  for (int j = 0; j < CPW; ++j) {
+    x1[j] = 0x1p+100 * (1 + j + threadIdx.x);
+    x2[j] = 0x1p+60f * (1 + j);
+  }
+  const double IM = 0x1.63f115f5d0b38p-103, MG = 6755399441055744.0, M1 = 0x1.703d73109e938p+102,
+               M2 = 0x1.6d0683e4deb00p+52;
+  const long long t0 = clock64();
+#pragma unroll 1
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int j = 0; j < CPW; ++j) {
+      double X2;
+      if (CV == 0) {
+        X2 = (double)x2[j];
+      } else if (CV == 1) {
+        const uint32_t b = __float_as_uint(x2[j]);
+        const uint32_t mag = b & 0x7fffffffu;
+        const uint32_t hi = (b & 0x80000000u) | ((mag >> 3) + (mag ? 0x38000000u : 0u));
+        X2 = __hiloint2double((int)hi, (int)(b << 29));
+      } else {
+        X2 = __hiloint2double(__float_as_int(x2[j]), 0);
+      }
+      const double k = fma(x1[j] + X2, IM, MG) - MG;
+      const double P = fma(-k, M1, x1[j]) + fma(-k, M2, X2);
+      const double y = P * sc[(j + it) & 127];
+      x1[j] = y * 0x1p+40 + 0x1p+100;
+      x2[j] = x2[j] * 1.0000001f;
+    }
+  }
+  const long long t1 = clock64();
+  double s = 0.0;
+#pragma unroll
+  for (int j = 0; j < CPW; ++j) s += x1[j] + x2[j];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+template <int CV>
+void run_tail(const char* name, int iters, double* out, long long* cyc) {
+  k_tail<CV><<<148, 256>>>(2, out, cyc);
+  cudaDeviceSynchronize();
+  k_tail<CV><<<148, 256>>>(iters, out, cyc);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h[148];
+  cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
+  double avg = 0;
+  for (int i = 0; i < 148; ++i) avg += (double)h[i];
+  printf("%-50s %8.0f clk per 56-column reconstruction per SM  [%s]\n", name, avg / 148.0 / iters, cudaGetErrorString(e));
+}
+
 template <int F>
 void run8(const char* name, int iters, double* out, long long* cyc) {
   k_fold8<F><<<148, 256>>>(2, out, cyc);
@@ -303,5 +362,8 @@ int main() {
   run8<2>("8 ... without the D construction and DFMA", iters, out, cyc);
   run8<3>("8 ... without I2FP, D, DFMA", iters, out, cyc);
   run8<8>("8 ... DFMA on stale D (no scalar FFMA)", iters, out, cyc);
+  run_tail<0>("tail, F2F.F64.F32 conversion", 400, out, cyc);
+  run_tail<1>("tail, integer conversion", 400, out, cyc);
+  run_tail<2>("tail, no conversion", 400, out, cyc);
   return 0;
 }
