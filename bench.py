@@ -17,10 +17,14 @@ interior and ``--n-total // 3`` boundary points split contiguously across the ra
 gradient and line-search losses are all-reduced; the per-layer Kronecker solves are
 distributed across ranks.
 
-Printed JSON also carries: ``roofline`` for the dominant kernel (the FP64 DMMA
-forward GEMM, k_gemm_nt) measured with CUDA events inside the timed region;
-``roofline_hbm`` for the HBM-bound activation adjoint (k_act_bwd), also timed with
-CUDA events in the timed region; ``cpu_baseline`` (the CPU oracle restating the
+Printed JSON also carries: ``roofline`` for the dominant kernel -- with KFAC the line
+search's fused layer on the INT8 tensor cores (k_crt_act, the FP64 product emulated exactly
+by the CRT; int8 tensor operations against the measured tcgen05 int8 peak, the
+FP64-equivalent rate alongside), otherwise the FP64 DMMA forward GEMM (k_gemm_act), which
+is ``roofline_dmma`` when it is not the dominant one -- measured with CUDA events inside
+the timed region; ``roofline_hbm`` for the HBM-bound activation adjoint (k_act_bwd) and
+``roofline_hbm_slice`` for the residue slicing, also timed with CUDA events in the timed
+region; ``cpu_baseline`` (the CPU oracle restating the
 reference, timed on this host at two bounded sample sizes and extrapolated to the
 arm's N with a fixed + per-point cost fit); ``e2e`` (the public optimizer_step API with host numpy buffers,
 H2D of the batch and D2H of parameters + StepInfo inside the timed region);
@@ -42,6 +46,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FP64_DMMA_PEAK_TFLOPS = 37.1  # measured, profiles/r01_fp64_peaks.txt (register-only DMMA, 1965 MHz)
+INT8_UMMA_PEAK_TOPS = 4570.0   # measured tcgen05 kind::i8 issue peak, profiles/r02_umma_i8_peak.txt
+CRT_MODULI = 13               # csrc/kp_crt.cu NMOD
 HBM_COPY_PEAK_GBS = 6552.6    # measured copy bandwidth (profiles/r01_fp64_peaks.txt) when
                               # MEASURED_PEAKS.json is absent
 CPU_SAMPLE_POINTS = 128       # mean interior points per CPU-oracle step: the steps alternate
@@ -368,6 +374,8 @@ def run_ours(args):
     ms_total = e0.elapsed_time(e1)
     gemm_ms, gemm_flops, gemm_launches, k1 = eng.profile_read()
     hbm_ms, hbm_bytes, hbm_launches = eng.profile_read_hbm()
+    crt_ms, crt_flops, crt_launches = eng.profile_read_cat(0)
+    slice_ms, slice_bytes, slice_launches = eng.profile_read_cat(1)
     eng.profile(False)
     n_loc, nb_loc = eng.n_interior, eng.n_boundary
     clk = clocks.stop()
@@ -409,21 +417,70 @@ def run_ours(args):
         samples, cores = cpu_reference_fit(wl, cpu_sizes(args), args.optimizer)
         cpu = cpu_line(samples, cores, n_glob, nb_glob, wl, args.optimizer, "one")
 
-    traffic, traffic_note = None, None
-    tp = os.path.join(ROOT, "profiles", "gemm_act_traffic.json")
-    if os.path.exists(tp):
+    def stored_traffic(fname):
+        """DRAM bytes per launch from a stored ncu --set full capture (profiles/<fname>): only
+        valid for the workload it was captured on (bytes scale with N)."""
+        tp = os.path.join(ROOT, "profiles", fname)
+        if not os.path.exists(tp):
+            return None, None
         try:
             tj = json.load(open(tp))
-            # only valid for the workload it was captured on (bytes scale with N)
             if tj.get("n_interior") == args.n_interior and tj.get("workload") == wl.name:
-                traffic = tj.get("dram_bytes_per_launch")
-                traffic_note = {"launch": tj.get("kernel"),
-                                "algorithmic_bytes_per_launch": tj.get("algorithmic_bytes_per_launch"),
-                                "source": "stored ncu --set full capture of the same launch "
-                                          "(profiles/gemm_act_traffic.json), not measured in "
-                                          "this run"}
+                return tj.get("dram_bytes_per_launch"), {
+                    "launch": tj.get("kernel"),
+                    "algorithmic_bytes_per_launch": tj.get("algorithmic_bytes_per_launch"),
+                    "source": f"stored ncu --set full capture of the same launch (profiles/{fname}), "
+                              "not measured in this run"}
         except (OSError, ValueError):
-            traffic = None
+            pass
+        return None, None
+
+    traffic, traffic_note = stored_traffic("gemm_act_traffic.json")
+    per_step = max(args.steps, 1)
+    dmma_roof = {"bound": "tensor", "kernel": "k_gemm_act (TMA-fed FP64 DMMA forward GEMM fused with the Taylor "
+                                              "activation: the stored forward pass, and every line-search layer "
+                                              "with KP_CRT=0)",
+                 "achieved": achieved_tflops, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                 "frac": (achieved_tflops / FP64_DMMA_PEAK_TFLOPS) if achieved_tflops else None,
+                 "traffic": traffic, "traffic_of": traffic_note,
+                 "launches_per_step": gemm_launches // per_step,
+                 "share_of_step": gemm_ms / ms_total if ms_total else None,
+                 "peak_source": "measured DMMA issue peak, profiles/r01_fp64_peaks.txt "
+                                "(MEASURED_PEAKS.json has no FP64 entry; cuBLAS DGEMM 35.4)"}
+    crt_roof = None
+    if crt_ms > 0:
+        # every FP64-equivalent multiply-add is one int8 multiply-add per modulus (13)
+        crt_tops = CRT_MODULI * crt_flops / (crt_ms / 1e3) / 1e12
+        ctraffic, ctraffic_note = stored_traffic("crt_act_traffic.json")
+        crt_roof = {"bound": "tensor",
+                    "kernel": "k_crt_act (line-search hidden layers: FP64 product emulated exactly on the INT8 "
+                              "tensor cores by the CRT over 13 moduli, tcgen05.mma kind::i8 fed by TMA, fold + "
+                              "Taylor activation in the epilogue; src/taylor.py:134-169 in src/optim.py:195-211)",
+                    "achieved": crt_tops, "peak": INT8_UMMA_PEAK_TOPS, "unit": "TFLOP/s",
+                    "unit_note": "int8 tensor operations (2 per multiply-add), 13 per FP64 multiply-add",
+                    "frac": crt_tops / INT8_UMMA_PEAK_TOPS,
+                    "fp64_equivalent_tflops": crt_tops / CRT_MODULI,
+                    "fp64_equivalent_vs_dmma_peak": crt_tops / CRT_MODULI / FP64_DMMA_PEAK_TFLOPS,
+                    "traffic": ctraffic, "traffic_of": ctraffic_note,
+                    "launches_per_step": crt_launches // per_step,
+                    "share_of_step": crt_ms / ms_total if ms_total else None,
+                    "limit": "shared-memory bandwidth: a 128-unit x 112-row x 32-byte MMA reads 7.5 KB of operands "
+                             "while TMA writes 7.5 KB for a later one, 15 KB per 56 tensor clocks against 128 B/clk "
+                             "(measured 121 clk per MMA, DESIGN.md section 5); the fold state (12 B per output) "
+                             "fills the register file, so the tile cannot grow",
+                    "peak_source": "measured tcgen05 kind::i8 issue peak, tools/umma_i8_peak.cu "
+                                   "(profiles/r02_umma_i8_peak.txt: 4570 TOPS at N = 128/256, 4257 at N = 112); "
+                                   "MEASURED_PEAKS.json has no int8 entry (its bf16 burst figure x 2 = 3308)"}
+    slice_roof = None
+    if slice_ms > 0:
+        sl_gbs = slice_bytes / (slice_ms / 1e3) / 1e9
+        slice_roof = {"bound": "hbm", "kernel": "k_crt_slice_h (FP64 states -> 13 int8 residue planes + row exponents)",
+                      "achieved": sl_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": sl_gbs / hbm_peak,
+                      "traffic": None, "launches_per_step": slice_launches // per_step,
+                      "share_of_step": slice_ms / ms_total if ms_total else None,
+                      "peak_source": hbm_peak_src,
+                      "bytes": "algorithmic: 8 B read + 13 B written per state element"}
+    main_roof = crt_roof if (crt_roof and crt_ms > gemm_ms) else dmma_roof
 
     if rank == 0:
         line = {
@@ -443,14 +500,11 @@ def run_ours(args):
             "kfac_steps_per_s": steps_per_s,
             "alg_tflops_per_s": f_step * steps_per_s / 1e12,
             "alg_frac_fp64_peak": f_step * steps_per_s / 1e12 / (FP64_DMMA_PEAK_TFLOPS * world),
-            "roofline": {"bound": "tensor", "kernel": "k_gemm_act (TMA-fed FP64 DMMA forward GEMM fused with the Taylor activation; hidden-layer forwards)",
-                         "achieved": achieved_tflops, "peak": FP64_DMMA_PEAK_TFLOPS,
-                         "unit": "TFLOP/s",
-                         "frac": (achieved_tflops / FP64_DMMA_PEAK_TFLOPS) if achieved_tflops else None,
-                         "traffic": traffic, "traffic_of": traffic_note, "launches_per_step": gemm_launches // max(args.steps, 1),
-                         "share_of_step": gemm_ms / ms_total if ms_total else None,
-                         "peak_source": "measured DMMA issue peak, profiles/r01_fp64_peaks.txt "
-                                        "(MEASURED_PEAKS.json has no FP64 entry; cuBLAS DGEMM 35.4)"},
+            "alg_frac_note": "algorithmic FP64 flops of the step / measured FP64 DMMA peak; above 1 when the line "
+                             "search runs its products on the INT8 tensor cores (roofline)",
+            "roofline": main_roof,
+            "roofline_dmma": dmma_roof if main_roof is not dmma_roof else None,
+            "roofline_hbm_slice": slice_roof,
             "roofline_hbm": {"bound": "hbm", "kernel": "k_act_bwd (activation adjoint, src/taylor.py:206-239)",
                              "achieved": hbm_gbs, "peak": hbm_peak, "unit": "GB/s",
                              "frac": (hbm_gbs / hbm_peak) if hbm_gbs else None,

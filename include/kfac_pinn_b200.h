@@ -143,6 +143,13 @@ int32_t kp_profile_read(kp_context* ctx, double* gemm_ms, double* gemm_flops, in
 /* The same for the HBM-bound activation adjoint (k_act_bwd, src/taylor.py:206-239): summed
  * CUDA-event time, algorithmic DRAM bytes and launches since kp_profile_enable. */
 int32_t kp_profile_read_hbm(kp_context* ctx, double* ms, double* bytes, int64_t* launches);
+/* Further timed categories since kp_profile_enable.  cat 0: the line search's hidden layers on
+ * the INT8 tensor cores (the CRT fused layer, src/taylor.py:134-169 inside
+ * src/optim.py:195-211), work = FP64-equivalent flops 2 rows K N; cat 1: the residue slicing
+ * that feeds them, work = algorithmic DRAM bytes (8 B read + one byte per modulus written per
+ * state element). */
+int32_t kp_profile_read_cat(kp_context* ctx, int32_t cat, double* ms, double* work,
+                            int64_t* launches);
 /* Diagnostics: the most Jacobi sweeps any solve of each device eigensolver route used in this
  * process since the last reset (small: one CTA, mid: cluster shared memory, large:
  * L2-resident cluster); 1000 + s marks a solve that did not converge in s sweeps.  Call after

@@ -65,6 +65,8 @@ _SIGS = {
                                     P(C.c_int64)]),
     "kp_solver_sweeps": (C.c_int32, [P(C.c_int32), P(C.c_int32), P(C.c_int32), C.c_int32]),
     "kp_profile_read_hbm": (C.c_int32, [C.c_void_p, P(C.c_double), P(C.c_double), P(C.c_int64)]),
+    "kp_profile_read_cat": (C.c_int32, [C.c_void_p, C.c_int32, P(C.c_double), P(C.c_double),
+                                        P(C.c_int64)]),
     "kp_param_count": (C.c_int64, [P(kp_net)]),
     "kp_factor_count": (C.c_int64, [P(kp_net), C.c_int32]),
     "kp_workspace_bytes": (C.c_int32, [C.c_void_p, P(kp_problem), P(C.c_size_t)]),

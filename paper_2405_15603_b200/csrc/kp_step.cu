@@ -53,6 +53,13 @@ struct kp_context {
   size_t ev_hbm_used = 0;
   double prof_hbm_bytes = 0.0;
   int64_t prof_hbm_launches = 0;
+  // further categories (kp_profile_read_cat): 0 = the INT8 tensor-core (CRT) fused layers of
+  // the line search (work = FP64-equivalent flops), 1 = their residue slicing (work =
+  // algorithmic DRAM bytes)
+  std::vector<cudaEvent_t> ev_cat[2];
+  size_t ev_cat_used[2] = {0, 0};
+  double prof_cat_work[2] = {0.0, 0.0};
+  int64_t prof_cat_launches[2] = {0, 0};
   // side streams for the per-layer Kronecker-sum solves (2 per layer: A and B factor pairs)
   std::vector<cudaStream_t> side;
   std::vector<cudaEvent_t> side_ev;
@@ -448,6 +455,31 @@ void prof_hbm_launch(const Ctx& c, double bytes, F&& launch) {
   ctx->prof_hbm_launches += 1;
 }
 
+// CUDA-event timing of category `cat` (kp_context::ev_cat): CRT layers / residue slicing.
+template <typename F>
+void prof_cat_launch(const Ctx& c, int cat, double work, F&& launch) {
+  kp_context* ctx = c.ctx;
+  if (!ctx->profile) {
+    launch();
+    return;
+  }
+  auto& ev = ctx->ev_cat[cat];
+  size_t& used = ctx->ev_cat_used[cat];
+  if (used + 2 > ev.size()) {
+    for (int k = 0; k < 64; ++k) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev.push_back(e);
+    }
+  }
+  cudaEventRecord(ev[used], c.s);
+  launch();
+  cudaEventRecord(ev[used + 1], c.s);
+  used += 2;
+  ctx->prof_cat_work[cat] += work;
+  ctx->prof_cat_launches[cat] += 1;
+}
+
 // Algorithmic bytes of one k_act_bwd launch per (sample, unit): the stored pre-activation
 // state (S rows, or the one value row of layer 0), the incoming adjoint (S rows, or the
 // per-sample rank-1 seed, negligible) and the outgoing adjoint (S rows).
@@ -600,7 +632,10 @@ void forward_loss(const Ctx& c, const double* theta, const double* wpad, const d
         int* exH = reinterpret_cast<int*>(c.at(P.o_crtEH));
         int8_t* resW = reinterpret_cast<int8_t*>(c.at(P.o_crtW));
         int* exW = reinterpret_cast<int*>(c.at(P.o_crtEW));
-        launch_crt_slice(a, n * td.S, P.h[l], P.h[l], resH, exH, false, c.s);
+        // slicing: 8 B read + one byte per modulus written per state element
+        prof_cat_launch(c, 1, (8.0 + crt_moduli()) * (double)n * td.S * P.h[l], [&] {
+          launch_crt_slice(a, n * td.S, P.h[l], P.h[l], resH, exH, false, c.s);
+        });
         launch_crt_slice(wpad + wp.wo[l], P.h[l + 1], P.h[l], P.h[l], resW, exW, true, c.s);
         GemmAct ga{};
         ga.bias = theta + P.th[l] + P.h[l];
@@ -621,7 +656,7 @@ void forward_loss(const Ctx& c, const double* theta, const double* wpad, const d
           ga.ldo = P.h[l + 1];
         }
         bool done = false;
-        prof_launch(c, 2.0 * (double)n * td.S * P.h[l] * P.h[l + 1], [&] {
+        prof_cat_launch(c, 0, 2.0 * (double)n * td.S * P.h[l] * P.h[l + 1], [&] {
           done = launch_crt_act(ga, last ? ACT_LAST : ACT_LOSS, resH, exH, resW, exW, c.s);
         });
         if (done) {  // (a rejected launch falls through to the FP64 DMMA layer below)
@@ -1477,6 +1512,30 @@ int32_t kp_profile_enable(kp_context* c, int32_t enable) {
   c->ev_hbm_used = 0;
   c->prof_hbm_bytes = 0.0;
   c->prof_hbm_launches = 0;
+  for (int k = 0; k < 2; ++k) {
+    c->ev_cat_used[k] = 0;
+    c->prof_cat_work[k] = 0.0;
+    c->prof_cat_launches[k] = 0;
+  }
+  return KP_OK;
+}
+
+int32_t kp_profile_read_cat(kp_context* c, int32_t cat, double* ms_out, double* work,
+                            int64_t* launches) {
+  if (!c || cat < 0 || cat > 1) return KP_ERR_INVALID;
+  double ms = 0.0;
+  for (size_t k = 0; k + 1 < c->ev_cat_used[cat]; k += 2) {
+    KP_CUDA_TRY(cudaEventSynchronize(c->ev_cat[cat][k + 1]));
+    float t = 0.f;
+    KP_CUDA_TRY(cudaEventElapsedTime(&t, c->ev_cat[cat][k], c->ev_cat[cat][k + 1]));
+    ms += t;
+  }
+  if (ms_out) *ms_out = ms;
+  if (work) *work = c->prof_cat_work[cat];
+  if (launches) *launches = c->prof_cat_launches[cat];
+  c->ev_cat_used[cat] = 0;
+  c->prof_cat_work[cat] = 0.0;
+  c->prof_cat_launches[cat] = 0;
   return KP_OK;
 }
 

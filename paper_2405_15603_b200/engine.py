@@ -394,6 +394,15 @@ class KfacEngine:
         raise_for_status(self.lib.kp_profile_read_hbm(self.ctx, C.byref(ms), C.byref(by), C.byref(n)))
         return ms.value, by.value, n.value
 
+    def profile_read_cat(self, cat: int):
+        """(ms, work, launches) of category ``cat`` since enable: 0 = the line search's INT8
+        tensor-core (CRT) layers (work: FP64-equivalent flops), 1 = their residue slicing
+        (work: algorithmic DRAM bytes)."""
+        ms, wk, n = C.c_double(), C.c_double(), C.c_int64()
+        raise_for_status(self.lib.kp_profile_read_cat(self.ctx, int(cat), C.byref(ms), C.byref(wk),
+                                                      C.byref(n)))
+        return ms.value, wk.value, n.value
+
     def close(self):
         if getattr(self, "ctx", None) is not None and self.ctx.value:
             self.stream.synchronize()

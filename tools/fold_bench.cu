@@ -239,6 +239,61 @@ void run(const char* name, int iters, double* out, long long* cyc) {
          avg / ((double)iters * NMOD), cudaGetErrorString(e));
 }
 
+// variant 12: 64-bit fixed-point fold: acc64 += bits * round(2^64 / p) (IMAD.WIDE.U32 + IMAD),
+// bits = 0x4B400000 + t from the packed FP32 reduction; no FP64, two registers per column
+__global__ void __launch_bounds__(256, 1) k_fold12(int iters, double* out, long long* cyc) {
+  __shared__ uint32_t acc[CPW * 32 + 64];
+  __shared__ uint32_t zs[32];
+  for (int i = threadIdx.x; i < CPW * 32 + 64; i += blockDim.x) acc[i] = (i * 2654435761u) >> 9;
+  if (threadIdx.x < 32) zs[threadIdx.x] = 0;
+  __syncthreads();
+  uint64_t x[CPW];
+#pragma unroll
+  for (int j = 0; j < CPW; ++j) x[j] = 0ull;
+  const int lane = threadIdx.x & 31;
+  uint32_t tz;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(tz) : "r"((uint32_t)__cvta_generic_to_shared(&zs[lane])));
+  const float MAGICF = 12582912.0f;
+  const long long t0 = clock64();
+#pragma unroll 1
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll 1
+    for (int i = 0; i < NMOD; ++i) {
+      const float ipf = __uint_as_float(__float_as_uint(c_ipf[i]) | tz);
+      const float npf = __uint_as_float(__float_as_uint(-c_pf[i]) | tz);
+      const uint64_t ip2 = pk(ipf, ipf), np2 = pk(npf, npf);
+      const uint64_t mg = pk(MAGICF, MAGICF), nmg = pk(-MAGICF, -MAGICF);
+      const uint32_t clo = c_m[i] | tz, chi = c_add[i] | tz;
+      uint32_t r[CPW];
+#pragma unroll
+      for (int j = 0; j < CPW; j += 4) {
+        const uint4 v = *reinterpret_cast<const uint4*>(&acc[((j * 8 + lane * 4 + it) & 1023) & ~3]);
+        r[j] = v.x;
+        r[j + 1] = v.y;
+        r[j + 2] = v.z;
+        r[j + 3] = v.w;
+      }
+#pragma unroll
+      for (int j = 0; j < CPW; j += 2) {
+        const uint64_t f2 = pk(__int2float_rn((int)r[j]), __int2float_rn((int)r[j + 1]));
+        const uint64_t q2 = fadd2(ffma2(f2, ip2, mg), nmg);
+        const uint64_t b2 = fadd2(ffma2(q2, np2, f2), mg);
+        const uint32_t ba = (uint32_t)b2, bb = (uint32_t)(b2 >> 32);
+        asm("mad.wide.u32 %0, %1, %2, %0;" : "+l"(x[j]) : "r"(ba), "r"(clo));
+        asm("{\n.reg .b32 lo, hi;\nmov.b64 {lo, hi}, %0;\nmad.lo.u32 hi, %1, %2, hi;\nmov.b64 %0, {lo, hi};\n}" : "+l"(x[j]) : "r"(ba), "r"(chi));
+        asm("mad.wide.u32 %0, %1, %2, %0;" : "+l"(x[j + 1]) : "r"(bb), "r"(clo));
+        asm("{\n.reg .b32 lo, hi;\nmov.b64 {lo, hi}, %0;\nmad.lo.u32 hi, %1, %2, hi;\nmov.b64 %0, {lo, hi};\n}" : "+l"(x[j + 1]) : "r"(bb), "r"(chi));
+      }
+    }
+  }
+  const long long t1 = clock64();
+  double s = 0.0;
+#pragma unroll
+  for (int j = 0; j < CPW; ++j) s += (double)(long long)x[j];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
 // reconstruction tail of kp_crt.cu in isolation: 56 columns per thread, 8 warps per SM.
 // CV = 0: F2F.F64.F32 for the FP32 low part, 1: integer bit manipulation, 2: no conversion
 template <int CV>
@@ -362,6 +417,17 @@ int main() {
   run8<2>("8 ... without the D construction and DFMA", iters, out, cyc);
   run8<3>("8 ... without I2FP, D, DFMA", iters, out, cyc);
   run8<8>("8 ... DFMA on stale D (no scalar FFMA)", iters, out, cyc);
+  {
+    k_fold12<<<148, 256>>>(2, out, cyc);
+    cudaDeviceSynchronize();
+    k_fold12<<<148, 256>>>(iters, out, cyc);
+    cudaError_t e = cudaDeviceSynchronize();
+    long long h[148];
+    cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
+    double avg = 0;
+    for (int i = 0; i < 148; ++i) avg += (double)h[i];
+    printf("%-50s %8.0f clk per modulus step per SM  [%s]\n", "12 fixed-point 64-bit fold (no FP64)", avg / 148.0 / ((double)iters * NMOD), cudaGetErrorString(e));
+  }
   run_tail<0>("tail, F2F.F64.F32 conversion", 400, out, cyc);
   run_tail<1>("tail, integer conversion", 400, out, cyc);
   run_tail<2>("tail, no conversion", 400, out, cyc);
