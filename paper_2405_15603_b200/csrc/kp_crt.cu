@@ -294,6 +294,7 @@ __global__ void __launch_bounds__(256)
     const double2 v0 = *reinterpret_cast<const double2*>(x + k);
     const double2 v1 = *reinterpret_cast<const double2*>(x + k + 2);
     const double xv[4] = {v0.x, v0.y, v1.x, v1.y};
+    // pieces of the four elements as two packed FP32 pairs each (f32x2 arithmetic below)
     float f0[4], f1[4], f2[4];
     uint32_t low[4];
 #pragma unroll
@@ -301,9 +302,18 @@ __global__ void __launch_bounds__(256)
       const long long a = __double_as_longlong(fma(xv[t], sc, MAGIC)) - mb;
       const uint32_t lo = (uint32_t)a;
       low[t] = lo;
-      f0[t] = __int_as_float(0x4B000000 | (lo & 0x7fffu)) - 8388608.0f;
-      f1[t] = __int_as_float(0x4B000000 | ((lo >> 15) & 0x7fffu)) - 8388608.0f;
-      f2[t] = __int_as_float(0x4B400000 + (int)(a >> 30)) - MAGICF;
+      f0[t] = __int_as_float(0x4B000000 | (lo & 0x7fffu));
+      f1[t] = __int_as_float(0x4B000000 | ((lo >> 15) & 0x7fffu));
+      f2[t] = __int_as_float(0x4B400000 + (int)(a >> 30));
+    }
+    const uint64_t n23 = pk2(-8388608.0f, -8388608.0f), nmg = pk2(-MAGICF, -MAGICF),
+                   mg = pk2(MAGICF, MAGICF);
+    uint64_t g0[2], g1[2], g2[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      g0[u] = fadd2(pk2(f0[2 * u], f0[2 * u + 1]), n23);
+      g1[u] = fadd2(pk2(f1[2 * u], f1[2 * u + 1]), n23);
+      g2[u] = fadd2(pk2(f2[2 * u], f2[2 * u + 1]), nmg);
     }
     int8_t* dst = planes + row * (int64_t)K + k;
     *reinterpret_cast<uint32_t*>(dst) = __byte_perm(__byte_perm(low[0], low[1], 0x0040),
@@ -312,16 +322,25 @@ __global__ void __launch_bounds__(256)
     for (int i = 1; i < NMOD; ++i) {
       const float p = (float)modulus(i), ip = 1.0f / (float)modulus(i);
       const float c1 = (float)cmod(1LL << 15, modulus(i)), c2 = (float)cmod(1LL << 30, modulus(i));
-      int b[4];
+      const uint64_t c1p = pk2(c1, c1), c2p = pk2(c2, c2), ipp = pk2(ip, ip), npp = pk2(-p, -p);
+      uint32_t bb[4];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const float y = fmaf(f2[t], c2, fmaf(f1[t], c1, f0[t]));
-        float r = fmaf(-(fmaf(y, ip, MAGICF) - MAGICF), p, y);
-        if (modulus(i) == 255) r = r > 127.5f ? r - p : r;
-        b[t] = __float_as_int(r + MAGICF);
+      for (int u = 0; u < 2; ++u) {
+        const uint64_t y = ffma2(g2[u], c2p, ffma2(g1[u], c1p, g0[u]));
+        uint64_t r = ffma2(fadd2(ffma2(y, ipp, mg), nmg), npp, y);
+        if (modulus(i) == 255) {  // r = 128 does not fit a byte: 128 = -127 (mod 255)
+          float ra, rb;
+          unpk2(r, ra, rb);
+          ra = ra > 127.5f ? ra - p : ra;
+          rb = rb > 127.5f ? rb - p : rb;
+          r = pk2(ra, rb);
+        }
+        const uint64_t bq = fadd2(r, mg);
+        bb[2 * u] = (uint32_t)bq;
+        bb[2 * u + 1] = (uint32_t)(bq >> 32);
       }
       *reinterpret_cast<uint32_t*>(dst + i * ps) =
-          __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
+          __byte_perm(__byte_perm(bb[0], bb[1], 0x0040), __byte_perm(bb[2], bb[3], 0x0040), 0x5410);
     }
   }
 }
