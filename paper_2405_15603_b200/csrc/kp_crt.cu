@@ -430,7 +430,8 @@ __device__ long long crt_dbg[16];
 template <int MODE, int CL>
 __global__ void __launch_bounds__(THREADS, 1)
     k_crt_act(const __grid_constant__ CUtensorMap mW, const __grid_constant__ CUtensorMap mH,
-              const int* __restrict__ exw, const int* __restrict__ exh, GemmAct g, int UT) {
+              const int* __restrict__ exw, const int* __restrict__ exh, GemmAct g, int UT,
+              int* __restrict__ tile_counter) {
   extern __shared__ __align__(1024) uint8_t crt_sm[];
   uint8_t* base =
       reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(crt_sm) + 1023) & ~uintptr_t(1023));
@@ -443,6 +444,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   __shared__ double sc_s[2][CN];               // row scales 2^(e_r - BETA) of the current / next tile
   __shared__ double cw_s[CN];                  // c_i on derivative row i, 0 elsewhere
   __shared__ uint32_t zero_s[32];
+  // tile queue: the producer announces tile k (or -1: no more) in slot k % 8; with a tile
+  // counter (independent CTAs) tiles are handed out in order, so the CTAs working on one
+  // sample's unit tiles stay within a tile of each other and its residues are read from HBM once
+  __shared__ int tq[8];
+  __shared__ uint64_t tready[8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = g.S;
   const Sched<CL> sch(g.n_samples, UT);
@@ -456,6 +462,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], CL == 4 ? 3 : 1);
     }
+    for (int b = 0; b < 8; ++b) mbar_init(&tready[b], 1);
     for (int b = 0; b < NACC; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], CL == 2 ? 2 * NEW : NEW);  // pair: both CTAs' epilogues release
@@ -492,7 +499,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       const long long dbg_t0 = clock64();
 #endif
       const uint32_t lfull0 = CL == 2 ? mapa(&full[0], 0) : 0u;  // the leader's full[0]
-      for (int tile = sch.first; tile < sch.count; tile += sch.step) {
+      const uint32_t hrows = (uint32_t)((S + 7) & ~7);
+      for (uint32_t tk = 0;; ++tk) {
+        int tile = (CL == 1 && tile_counter) ? atomicAdd(tile_counter, 1)
+                                              : sch.first + (int)tk * sch.step;
+        if (tile >= sch.count) tile = -1;
+        tq[tk & 7] = tile;
+        mbar_arrive(&tready[tk & 7]);
+        if (tile < 0) break;
         const int ut = sch.ut(tile);
         const int row0 = (int)(sch.smp(tile) * S);
         for (int i = 0; i < NMOD; ++i)
@@ -511,11 +525,13 @@ __global__ void __launch_bounds__(THREADS, 1)
               tma3d_2sm(a + A_BYTES, &mH, kc * CKB, row0 + sch.cu * (CN / 2), i, lbar);
               continue;
             }
-            mbar_arrive_expect_tx(&full[s], STB);
-            if (CL == 1) {
+            if (CL == 1) {  // only the sample's rows (to a multiple of 8): the rest of the
+                            // 112-row operand is stale shared memory feeding unused columns
+              mbar_arrive_expect_tx(&full[s], A_BYTES + hrows * CKB);
               tma3d(a, &mW, kc * CKB, ut * CM, i, &full[s]);
               tma3d(a + A_BYTES, &mH, kc * CKB, row0, i, &full[s]);
-            } else {  // my half of the unit tile's weights and of the sample's states
+            } else {
+              mbar_arrive_expect_tx(&full[s], STB);  // my half of the unit tile's weights and of the sample's states
               tma3d_mc(a + sch.cs * (CM / 2) * CKB, &mW, kc * CKB, ut * CM + sch.cs * (CM / 2), i,
                        &full[s], mask_w);
               tma3d_mc(a + A_BYTES + sch.cu * (CN / 2) * CKB, &mH, kc * CKB, row0 + sch.cu * (CN / 2),
@@ -535,7 +551,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       long long dbg_acc[2] = {0, 0};
       const long long dbg_t0 = clock64();
 #endif
-      for (int tile = sch.first; tile < sch.count; tile += sch.step) {
+      for (uint32_t tk = 0;; ++tk) {
+        mbar_wait(&tready[tk & 7], (tk >> 3) & 1);
+        if (tq[tk & 7] < 0) break;
         for (int i = 0; i < NMOD; ++i, ++gm) {
           const uint32_t b = gm % NACC;
           {
@@ -639,7 +657,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     long long dbg_acc[7] = {0, 0, 0, 0, 0, 0, 0};
     const long long dbg_t0 = clock64();
 #endif
-    for (int tile = sch.first; tile < sch.count; tile += sch.step, ++tcount) {
+    for (;; ++tcount) {
+      mbar_wait(&tready[tcount & 7], (tcount >> 3) & 1);
+      const int tile = tq[tcount & 7];
+      if (tile < 0) break;
       const int ut = sch.ut(tile);
       const int64_t smp = sch.smp(tile);
       const bool live = smp < g.n_samples;  // (CL = 4, odd n: the last pair's second sample)
@@ -706,7 +727,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         float lo, hi;
         unpk2(x2[j / 2], lo, hi);
         const double X2 = (double)((j & 1) ? hi : lo);
-        const double k = fma(x1[j] + X2, v_im, v_mg) - v_mg;
+        // (|low| < 2^65 cannot move the rounding: |P| < M / 2.4 keeps high / M off the ties)
+        const double k = fma(x1[j], v_im, v_mg) - v_mg;
         const double P = fma(-k, v_m1, x1[j]) + fma(-k, v_m2, X2);
         const double y = P * sc[c0 + j];
         x1[j] = (c0 + j < S) ? y : 0.0;
@@ -715,26 +737,24 @@ __global__ void __launch_bounds__(THREADS, 1)
       // Taylor activation (src/taylor.py:140-169): half 0 owns the value row and derivative
       // rows 1..55, half 1 the remaining derivative rows and the operator row S - 1.
       double s0 = 0.0, s1 = 0.0, s2 = 0.0, quad = 0.0;
+      // quadratic form over this half's derivative rows (cw = 0 on every other row), in
+      // units of su^2; the two halves' parts are summed in a fixed order (half 0 + half 1)
+#pragma unroll
+      for (int j = 0; j < CPW; ++j) quad += (x1[j] * cw_s[c0 + j]) * x1[j];
       if (h == 0) {
         const TanhD t = tanh_derivs(fma(x1[0], su, g.bias[(int64_t)unit * g.bias_stride]), false);
         s0 = t.s0;
         s1 = t.s1;
         s2 = t.s2;
-      } else {
-        asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");
-        s1 = xs1[ul];
-        s2 = xs2[ul];
-        quad = xq[ul];
-      }
-      // quadratic form over this half's derivative rows (cw = 0 on every other row), in
-      // units of su^2
-#pragma unroll
-      for (int j = 0; j < CPW; ++j) quad += (x1[j] * cw_s[c0 + j]) * x1[j];
-      if (h == 0) {
         xs1[ul] = s1;
         xs2[ul] = s2;
         xq[ul] = quad;
-        asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");
+      }
+      asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");
+      if (h == 1) {
+        s1 = xs1[ul];
+        s2 = xs2[ul];
+        quad = xq[ul] + quad;
       }
       asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");  // xs*/xq reusable
       CRT_ACC(4, ttail);
@@ -905,9 +925,9 @@ bool launch_crt_act(const GemmAct& g, int mode, const int8_t* resH, const int* e
   if (cl_env == 4 && UT % 2 == 0 && g.n_samples >= 2) CL = 4;
   CUtensorMap mw, mh;
   if (!crt_map(&mw, resW, g.N, g.K, CL == 4 ? CM / 2 : CM) ||
-      !crt_map(&mh, resH, rows, g.K, CL == 1 ? CN : CN / 2))
+      !crt_map(&mh, resH, rows, g.K, CL == 1 ? (uint32_t)((g.S + 7) & ~7) : CN / 2))
     return false;
-  void (*kern)(const CUtensorMap, const CUtensorMap, const int*, const int*, GemmAct, int);
+  void (*kern)(const CUtensorMap, const CUtensorMap, const int*, const int*, GemmAct, int, int*);
   if (mode == ACT_LAST)
     kern = CL == 4 ? k_crt_act<ACT_LAST, 4> : CL == 2 ? k_crt_act<ACT_LAST, 2> : k_crt_act<ACT_LAST, 1>;
   else
@@ -960,7 +980,32 @@ bool launch_crt_act(const GemmAct& g, int mode, const int8_t* resH, const int* e
   cfg.stream = s;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, mw, mh, exW, exH, g, UT) == cudaSuccess;
+  // tile counter of the in-order schedule (independent CTAs): a ring of 64 counters per
+  // device, one per launch (launches on different streams never share one), zeroed here
+  int* counter = nullptr;
+  if (CL == 1) {
+    static std::map<int, std::pair<int*, unsigned>> counters;  // per device: ring, next slot
+    static std::mutex cmu;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+      std::lock_guard<std::mutex> lock(cmu);
+      auto it = counters.find(dev);
+      if (it == counters.end()) {
+        int* pcnt = nullptr;
+        if (cudaMalloc(&pcnt, 64 * sizeof(int)) != cudaSuccess) pcnt = nullptr;
+        it = counters.emplace(dev, std::make_pair(pcnt, 0u)).first;
+      }
+      if (it->second.first) counter = it->second.first + (it->second.second++ % 64);
+    }
+    static const bool dyn = [] {
+      const char* e = getenv("KP_CRT_DYNAMIC");
+      return !(e && atoi(e) == 0);
+    }();
+    if (!dyn) counter = nullptr;
+    if (counter && cudaMemsetAsync(counter, 0, sizeof(int), s) != cudaSuccess) return false;
+  }
+  return cudaLaunchKernelEx(&cfg, kern, mw, mh, exW, exH, g, UT, counter) == cudaSuccess;
 }
 
 }  // namespace kp
