@@ -265,6 +265,62 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Residues of four consecutive elements of one row: a = rint(x sc) read from the bits of
+// x sc + 1.5 2^52 (|a| <= 2^45), split into 15-bit pieces held exactly in FP32; per modulus
+// y = a2 c2 + a1 c1 + a0 (exact, |y| < 2^23), r = y - p rint(y / p) (exact, |r| <= p/2 + 1;
+// p = 255 folds r = 128 to -127), stored as the low byte of r + 1.5 2^23 (packed f32x2
+// arithmetic: two elements per instruction).  p = 256 is the low byte of a.
+__device__ __forceinline__ void slice4(const double (&xv)[4], double sc, int8_t* dst, int64_t ps) {
+  const long long mb = __double_as_longlong(MAGIC);
+  // pieces of the four elements as two packed FP32 pairs each (f32x2 arithmetic below)
+  float f0[4], f1[4], f2[4];
+  uint32_t low[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const long long a = __double_as_longlong(fma(xv[t], sc, MAGIC)) - mb;
+    const uint32_t lo = (uint32_t)a;
+    low[t] = lo;
+    f0[t] = __int_as_float(0x4B000000 | (lo & 0x7fffu));
+    f1[t] = __int_as_float(0x4B000000 | ((lo >> 15) & 0x7fffu));
+    f2[t] = __int_as_float(0x4B400000 + (int)(a >> 30));
+  }
+  const uint64_t n23 = pk2(-8388608.0f, -8388608.0f), nmg = pk2(-MAGICF, -MAGICF),
+                 mg = pk2(MAGICF, MAGICF);
+  uint64_t g0[2], g1[2], g2[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    g0[u] = fadd2(pk2(f0[2 * u], f0[2 * u + 1]), n23);
+    g1[u] = fadd2(pk2(f1[2 * u], f1[2 * u + 1]), n23);
+    g2[u] = fadd2(pk2(f2[2 * u], f2[2 * u + 1]), nmg);
+  }
+  *reinterpret_cast<uint32_t*>(dst) = __byte_perm(__byte_perm(low[0], low[1], 0x0040),
+                                                  __byte_perm(low[2], low[3], 0x0040), 0x5410);
+#pragma unroll
+  for (int i = 1; i < NMOD; ++i) {
+    const float p = (float)modulus(i), ip = 1.0f / (float)modulus(i);
+    const float c1 = (float)cmod(1LL << 15, modulus(i)), c2 = (float)cmod(1LL << 30, modulus(i));
+    const uint64_t c1p = pk2(c1, c1), c2p = pk2(c2, c2), ipp = pk2(ip, ip), npp = pk2(-p, -p);
+    uint32_t bb[4];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint64_t y = ffma2(g2[u], c2p, ffma2(g1[u], c1p, g0[u]));
+      uint64_t r = ffma2(fadd2(ffma2(y, ipp, mg), nmg), npp, y);
+      if (modulus(i) == 255) {  // r = 128 does not fit a byte: 128 = -127 (mod 255)
+        float ra, rb;
+        unpk2(r, ra, rb);
+        ra = ra > 127.5f ? ra - p : ra;
+        rb = rb > 127.5f ? rb - p : rb;
+        r = pk2(ra, rb);
+      }
+      const uint64_t bq = fadd2(r, mg);
+      bb[2 * u] = (uint32_t)bq;
+      bb[2 * u + 1] = (uint32_t)(bq >> 32);
+    }
+    *reinterpret_cast<uint32_t*>(dst + i * ps) =
+        __byte_perm(__byte_perm(bb[0], bb[1], 0x0040), __byte_perm(bb[2], bb[3], 0x0040), 0x5410);
+  }
+}
+
 // State rows: one warp per row, lane = 4 consecutive K entries per 128-wide chunk.  max|x| <
 // 2^e; a = rint(x 2^(BETA - e)) read from the bits of x 2^(BETA-e) + 1.5 2^52 (|a| <= 2^45),
 // split into 15-bit pieces held exactly in FP32; per modulus y = a2 c2 + a1 c1 + a0 (exact,
@@ -289,59 +345,76 @@ __global__ void __launch_bounds__(256)
   if (m > 0.0) frexp(m, &e);
   if (lane == 0) ex[row] = e;
   const double sc = pow2i(BETA - e);
-  const long long mb = __double_as_longlong(MAGIC);
   for (int k = 4 * lane; k < K; k += 128) {
     const double2 v0 = *reinterpret_cast<const double2*>(x + k);
     const double2 v1 = *reinterpret_cast<const double2*>(x + k + 2);
     const double xv[4] = {v0.x, v0.y, v1.x, v1.y};
-    // pieces of the four elements as two packed FP32 pairs each (f32x2 arithmetic below)
-    float f0[4], f1[4], f2[4];
-    uint32_t low[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const long long a = __double_as_longlong(fma(xv[t], sc, MAGIC)) - mb;
-      const uint32_t lo = (uint32_t)a;
-      low[t] = lo;
-      f0[t] = __int_as_float(0x4B000000 | (lo & 0x7fffu));
-      f1[t] = __int_as_float(0x4B000000 | ((lo >> 15) & 0x7fffu));
-      f2[t] = __int_as_float(0x4B400000 + (int)(a >> 30));
+    slice4(xv, sc, planes + row * (int64_t)K + k, ps);
+  }
+}
+
+// Layer 0 straight to residue planes (no FP64 states written or re-read): the activations of
+// the first layer are rank-one in the sample (src/taylor.py:124-169 with the linear input:
+// value row tanh(z_u), derivative row i: s1(z_u) W0[u, i], operator row: s2(z_u) q_u with
+// q_u = sum_i c_i W0[u, i]^2).  One CTA per sample at a time: tanh and its derivatives of the
+// sample's h1 pre-activations go to shared memory, then each warp takes rows of the sample and
+// treats them like k_crt_slice_h (lane = 4 consecutive units per 128-wide chunk; maximum,
+// then slicing), forming the row's entries on the fly from W0^T (d x h1, L2-resident) and q.
+constexpr int FIRST_WARPS = 8, FIRST_MAXH = 1024;
+__global__ void __launch_bounds__(FIRST_WARPS * 32)
+    k_crt_first(const double* __restrict__ zval, int64_t n, int h1, int S, int d,
+                const double* __restrict__ w0t, const double* __restrict__ q0,
+                int8_t* __restrict__ planes, int64_t ps, int* __restrict__ ex) {
+  __shared__ double sv[3][FIRST_MAXH];  // s0, s1, s2 of the current sample
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t smp = blockIdx.x; smp < n; smp += gridDim.x) {
+    for (int u = threadIdx.x; u < h1; u += blockDim.x) {
+      const TanhD td = tanh_derivs(zval[smp * h1 + u], false);
+      sv[0][u] = td.s0;
+      sv[1][u] = td.s1;
+      sv[2][u] = td.s2;
     }
-    const uint64_t n23 = pk2(-8388608.0f, -8388608.0f), nmg = pk2(-MAGICF, -MAGICF),
-                   mg = pk2(MAGICF, MAGICF);
-    uint64_t g0[2], g1[2], g2[2];
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      g0[u] = fadd2(pk2(f0[2 * u], f0[2 * u + 1]), n23);
-      g1[u] = fadd2(pk2(f1[2 * u], f1[2 * u + 1]), n23);
-      g2[u] = fadd2(pk2(f2[2 * u], f2[2 * u + 1]), nmg);
-    }
-    int8_t* dst = planes + row * (int64_t)K + k;
-    *reinterpret_cast<uint32_t*>(dst) = __byte_perm(__byte_perm(low[0], low[1], 0x0040),
-                                                    __byte_perm(low[2], low[3], 0x0040), 0x5410);
-#pragma unroll
-    for (int i = 1; i < NMOD; ++i) {
-      const float p = (float)modulus(i), ip = 1.0f / (float)modulus(i);
-      const float c1 = (float)cmod(1LL << 15, modulus(i)), c2 = (float)cmod(1LL << 30, modulus(i));
-      const uint64_t c1p = pk2(c1, c1), c2p = pk2(c2, c2), ipp = pk2(ip, ip), npp = pk2(-p, -p);
-      uint32_t bb[4];
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const uint64_t y = ffma2(g2[u], c2p, ffma2(g1[u], c1p, g0[u]));
-        uint64_t r = ffma2(fadd2(ffma2(y, ipp, mg), nmg), npp, y);
-        if (modulus(i) == 255) {  // r = 128 does not fit a byte: 128 = -127 (mod 255)
-          float ra, rb;
-          unpk2(r, ra, rb);
-          ra = ra > 127.5f ? ra - p : ra;
-          rb = rb > 127.5f ? rb - p : rb;
-          r = pk2(ra, rb);
+    __syncthreads();
+    for (int i = warp; i < S; i += FIRST_WARPS) {
+      const double* coef = i == 0 ? sv[0] : (i <= d ? sv[1] : sv[2]);
+      const double* data = i == 0 ? nullptr : (i <= d ? w0t + (int64_t)(i - 1) * h1 : q0);
+      auto load4 = [&](int k, double (&xv)[4]) {
+        const double2 c0 = *reinterpret_cast<const double2*>(coef + k);
+        const double2 c1 = *reinterpret_cast<const double2*>(coef + k + 2);
+        if (data == nullptr) {
+          xv[0] = c0.x;
+          xv[1] = c0.y;
+          xv[2] = c1.x;
+          xv[3] = c1.y;
+        } else {
+          const double2 w0 = *reinterpret_cast<const double2*>(data + k);
+          const double2 w1 = *reinterpret_cast<const double2*>(data + k + 2);
+          xv[0] = c0.x * w0.x;
+          xv[1] = c0.y * w0.y;
+          xv[2] = c1.x * w1.x;
+          xv[3] = c1.y * w1.y;
         }
-        const uint64_t bq = fadd2(r, mg);
-        bb[2 * u] = (uint32_t)bq;
-        bb[2 * u + 1] = (uint32_t)(bq >> 32);
+      };
+      double m = 0.0;
+      for (int k = 4 * lane; k < h1; k += 128) {
+        double xv[4];
+        load4(k, xv);
+        m = fmax(m, fmax(fmax(fabs(xv[0]), fabs(xv[1])), fmax(fabs(xv[2]), fabs(xv[3]))));
       }
-      *reinterpret_cast<uint32_t*>(dst + i * ps) =
-          __byte_perm(__byte_perm(bb[0], bb[1], 0x0040), __byte_perm(bb[2], bb[3], 0x0040), 0x5410);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      int e = 0;
+      if (m > 0.0) frexp(m, &e);
+      const int64_t row = smp * S + i;
+      if (lane == 0) ex[row] = e;
+      const double sc = pow2i(BETA - e);
+      for (int k = 4 * lane; k < h1; k += 128) {
+        double xv[4];
+        load4(k, xv);
+        slice4(xv, sc, planes + row * (int64_t)h1 + k, ps);
+      }
     }
+    __syncthreads();  // sv is rewritten for the next sample
   }
 }
 
@@ -884,6 +957,16 @@ bool crt_enabled() {
 
 int crt_moduli() { return NMOD; }
 
+// Layer 0 straight to residue planes (k_crt_first); KP_CRT_FIRST=0 writes the FP64 state and
+// slices it like the other layers.
+bool crt_first_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("KP_CRT_FIRST");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
 bool crt_act_ok(int S, int K, int N) {
   return crt_enabled() && S > CPW && S <= CN && K % CKB == 0 && K >= CKB && K <= 1024 &&
          N % CM == 0;
@@ -900,11 +983,25 @@ void launch_crt_slice(const double* X, int64_t rows, int K, int64_t ldx, int8_t*
     k_crt_slice_h<<<blocks, 256, 0, s>>>(X, rows, K, ldx, planes, rows * (int64_t)K, ex);
 }
 
+// Layer 0 (given z = x W0^T + b0) straight to the residue planes the first hidden CRT layer
+// reads; false when the shape is outside the kernel's (h1 a multiple of 128 up to 1024).
+bool launch_crt_first(const double* zval, int64_t n, int h1, int S, int d, const double* w0t,
+                      const double* q0, int8_t* planes, int* ex, cudaStream_t s) {
+  if (n <= 0) return true;
+  if (h1 % 128 != 0 || h1 > FIRST_MAXH || S != d + 2) return false;
+  count_launch();
+  const unsigned blocks = (unsigned)std::min<int64_t>(n, (int64_t)sm_count() * 8);
+  k_crt_first<<<blocks, FIRST_WARPS * 32, 0, s>>>(zval, n, h1, S, d, w0t, q0, planes,
+                                                   n * S * (int64_t)h1, ex);
+  return true;
+}
+
 // Fused layer from residue planes: resH (NMOD x n*S x K, exponents exH), resW (NMOD x N x K,
 // exponents exW, sliced with weights = true).  ACT_LOSS: g.post / g.ldo; ACT_LAST: g.wlast,
-// g.upart ((n*S) x N/128 partial dots).
+// g.upart ((n*S) x N/128 partial dots).  tile_counter: one device int owned by the caller for
+// the in-order tile schedule (nullptr: static striding); not shared by concurrent launches.
 bool launch_crt_act(const GemmAct& g, int mode, const int8_t* resH, const int* exH,
-                    const int8_t* resW, const int* exW, cudaStream_t s) {
+                    const int8_t* resW, const int* exW, cudaStream_t s, int* tile_counter) {
   if (g.n_samples <= 0) return true;
   if (!crt_act_ok(g.S, g.K, g.N) || g.batch != 1 || !g.taylor || (mode != ACT_LOSS && mode != ACT_LAST) ||
       g.n_samples * (g.N / CM) >= (int64_t(1) << 31) || g.n_samples * g.S >= (int64_t(1) << 31))
@@ -980,29 +1077,15 @@ bool launch_crt_act(const GemmAct& g, int mode, const int8_t* resH, const int* e
   cfg.stream = s;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  // tile counter of the in-order schedule (independent CTAs): a ring of 64 counters per
-  // device, one per launch (launches on different streams never share one), zeroed here
+  // tile counter of the in-order schedule (independent CTAs): caller-owned (workspace), zeroed
+  // here on the launch's stream; KP_CRT_DYNAMIC=0 keeps the static striding
   int* counter = nullptr;
-  if (CL == 1) {
-    static std::map<int, std::pair<int*, unsigned>> counters;  // per device: ring, next slot
-    static std::mutex cmu;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    {
-      std::lock_guard<std::mutex> lock(cmu);
-      auto it = counters.find(dev);
-      if (it == counters.end()) {
-        int* pcnt = nullptr;
-        if (cudaMalloc(&pcnt, 64 * sizeof(int)) != cudaSuccess) pcnt = nullptr;
-        it = counters.emplace(dev, std::make_pair(pcnt, 0u)).first;
-      }
-      if (it->second.first) counter = it->second.first + (it->second.second++ % 64);
-    }
+  if (CL == 1 && tile_counter) {
     static const bool dyn = [] {
       const char* e = getenv("KP_CRT_DYNAMIC");
       return !(e && atoi(e) == 0);
     }();
-    if (!dyn) counter = nullptr;
+    if (dyn) counter = tile_counter;
     if (counter && cudaMemsetAsync(counter, 0, sizeof(int), s) != cudaSuccess) return false;
   }
   return cudaLaunchKernelEx(&cfg, kern, mw, mh, exW, exH, g, UT, counter) == cudaSuccess;

@@ -143,6 +143,7 @@ struct TaylorDims {
 // post-activation state (n*S x h1) -> post.  Derivative rows of the pre-activation
 // are W0[:, i] and its operator row is 0 (reference taylor.py:124-131).
 // batch > 1: parameter sets theta0 + kk*D; zval/post/w0t/q0 stacked per entry.
+// post == nullptr: zval only.
 void launch_first_layer(const double* x, int64_t n, int d, const double* theta0, int h1,
                         TaylorDims td, const double* w0t, const double* q0, double* zval,
                         double* post, cudaStream_t s, int batch = 1, int64_t D = 0);
@@ -308,11 +309,15 @@ bool launch_ozaki_gemm(const double* A, int64_t lda, const double* B, int64_t ld
 // ---- fused Taylor layer, FP64 product on the INT8 tensor cores by the CRT (kp_crt.cu; KP_CRT=0 disables)
 bool crt_enabled();
 int crt_moduli();
+bool crt_first_enabled();
 bool crt_act_ok(int S, int K, int N);
 void launch_crt_slice(const double* X, int64_t rows, int K, int64_t ldx, int8_t* planes, int* ex,
                       bool weights, cudaStream_t s);
+bool launch_crt_first(const double* zval, int64_t n, int h1, int S, int d, const double* w0t,
+                      const double* q0, int8_t* planes, int* ex, cudaStream_t s);
 bool launch_crt_act(const GemmAct& g, int mode, const int8_t* resH, const int* exH,
-                    const int8_t* resW, const int* exW, cudaStream_t s);
+                    const int8_t* resW, const int* exW, cudaStream_t s,
+                    int* tile_counter = nullptr);
 
 // ---- small on-device generalised eigensolver + combine (kp_eig_small.cu) ---------
 struct SmallEigJob {

@@ -56,6 +56,7 @@ struct kp_context {
   // further categories (kp_profile_read_cat): 0 = the INT8 tensor-core (CRT) fused layers of
   // the line search (work = FP64-equivalent flops), 1 = their residue slicing (work =
   // algorithmic DRAM bytes)
+  unsigned crt_seq = 0;  // next slot of the CRT layer's tile-counter ring
   std::vector<cudaEvent_t> ev_cat[2];
   size_t ev_cat_used[2] = {0, 0};
   double prof_cat_work[2] = {0.0, 0.0};
@@ -127,6 +128,7 @@ struct Plan {
   int64_t o_ping = 0, o_pong = 0;
   int64_t o_ozEa = 0, o_ozB = 0, o_ozEb = 0;  // Ozaki line-search scratch (KP_OZAKI=1)
   int64_t o_crtH = 0, o_crtEH = 0, o_crtW = 0, o_crtEW = 0;  // CRT line-search residues
+  int64_t o_crtCnt = 0;                                      // ring of 64 tile counters
   int64_t o_bzval0 = 0, o_bpost[MAXL] = {}, o_bpre[MAXL] = {}, o_bg[MAXL] = {};
   int64_t o_bping = 0, o_bpong = 0, o_ones = 0;
   int64_t o_r = 0, o_rb = 0, o_rls = 0, o_rbls = 0, o_u = 0, o_upart = 0;
@@ -285,6 +287,7 @@ int make_plan(kp_context* ctx, const kp_problem* pr, Plan& P) {
     P.o_crtEH = take(Mc / 2 + 1);
     P.o_crtW = take(ceil_div((int64_t)crt_moduli() * P.maxh * P.maxh, 8));
     P.o_crtEW = take(P.maxh / 2 + 1);
+    P.o_crtCnt = take(32);
   }
   P.o_bpong = take(P.Bc * P.Nb * P.maxh);
   P.o_ones = take(P.Nb);
@@ -619,8 +622,23 @@ void forward_loss(const Ctx& c, const double* theta, const double* wpad, const d
     }
   } else {
     double* zs = td.taylor ? c.at(P.o_zval0) : c.at(P.o_bzval0);
-    launch_first_layer(x, n, P.d, theta + P.th[0], P.h[1], td, c.at(cand ? P.o_w0tc : P.o_w0t),
-                       c.at(cand ? P.o_q0c : P.o_q0), zs, ping, c.s, batch, P.D);
+    const double* w0t = c.at(cand ? P.o_w0tc : P.o_w0t);
+    const double* q0 = c.at(cand ? P.o_q0c : P.o_q0);
+    // When the first hidden layer runs on the INT8 tensor cores, layer 0 goes straight to its
+    // residue planes (k_crt_first): the FP64 state is neither written nor read back.
+    bool first_sliced = false;
+    if (L > 2 && batch == 1 && td.taylor && crt_act_ok(td.S, P.h[1], P.h[2]) && crt_first_enabled()) {
+      launch_first_layer(x, n, P.d, theta + P.th[0], P.h[1], td, w0t, q0, zs, nullptr, c.s, 1, P.D);
+      prof_cat_launch(c, 1, (double)crt_moduli() * (double)n * td.S * P.h[1], [&] {
+        first_sliced = launch_crt_first(zs, n, P.h[1], td.S, td.d, w0t, q0,
+                                        reinterpret_cast<int8_t*>(c.at(P.o_crtH)),
+                                        reinterpret_cast<int*>(c.at(P.o_crtEH)), c.s);
+      });
+      if (!first_sliced)  // shape outside the fused kernel: expand z the usual way
+        launch_first_layer(x, n, P.d, theta + P.th[0], P.h[1], td, w0t, q0, zs, ping, c.s, 1, P.D);
+    } else {
+      launch_first_layer(x, n, P.d, theta + P.th[0], P.h[1], td, w0t, q0, zs, ping, c.s, batch, P.D);
+    }
     double* a = ping;
     double* b = pong;
     for (int l = 1; l + 1 < L; ++l) {
@@ -633,9 +651,10 @@ void forward_loss(const Ctx& c, const double* theta, const double* wpad, const d
         int8_t* resW = reinterpret_cast<int8_t*>(c.at(P.o_crtW));
         int* exW = reinterpret_cast<int*>(c.at(P.o_crtEW));
         // slicing: 8 B read + one byte per modulus written per state element
-        prof_cat_launch(c, 1, (8.0 + crt_moduli()) * (double)n * td.S * P.h[l], [&] {
-          launch_crt_slice(a, n * td.S, P.h[l], P.h[l], resH, exH, false, c.s);
-        });
+        if (!(l == 1 && first_sliced))
+          prof_cat_launch(c, 1, (8.0 + crt_moduli()) * (double)n * td.S * P.h[l], [&] {
+            launch_crt_slice(a, n * td.S, P.h[l], P.h[l], resH, exH, false, c.s);
+          });
         launch_crt_slice(wpad + wp.wo[l], P.h[l + 1], P.h[l], P.h[l], resW, exW, true, c.s);
         GemmAct ga{};
         ga.bias = theta + P.th[l] + P.h[l];
@@ -657,8 +676,13 @@ void forward_loss(const Ctx& c, const double* theta, const double* wpad, const d
         }
         bool done = false;
         prof_cat_launch(c, 0, 2.0 * (double)n * td.S * P.h[l] * P.h[l + 1], [&] {
-          done = launch_crt_act(ga, last ? ACT_LAST : ACT_LOSS, resH, exH, resW, exW, c.s);
+          int* cnt = reinterpret_cast<int*>(c.at(P.o_crtCnt)) + (c.ctx->crt_seq++ % 64);
+          done = launch_crt_act(ga, last ? ACT_LAST : ACT_LOSS, resH, exH, resW, exW, c.s, cnt);
         });
+        if (!done && l == 1 && first_sliced) {  // the DMMA layer below needs layer 0's FP64 state
+          launch_first_layer(x, n, P.d, theta + P.th[0], P.h[1], td, w0t, q0, zs, ping, c.s, 1, P.D);
+          first_sliced = false;
+        }
         if (done) {  // (a rejected launch falls through to the FP64 DMMA layer below)
           if (last) {
             launch_last_from_partials(c.at(P.o_upart), P.h[l + 1] / 128, n, td,

@@ -160,6 +160,7 @@ void launch_first_layer(const double* x, int64_t n, int d, const double* theta0,
   g.sBias = D;
   g.sC = n * h1;
   launch_gemm_nt(g, s);
+  if (post == nullptr) return;  // z only (the caller expands it: kp_crt.cu k_crt_first)
   const unsigned tiles = (unsigned)ceil_div(h1, 32);
   // about 8 blocks per SM over the whole (tiles x groups x candidates) grid
   const int64_t groups = std::max<int64_t>(

@@ -90,6 +90,8 @@ int main(int argc, char** argv) {
   g.cdiag = dcd;
   g.ldo = N;
   g.wlast = dwl;
+  int* dcnt;
+  CK(cudaMalloc(&dcnt, 64 * sizeof(int)));
   cudaEvent_t ev[6];
   for (auto& ee : ev) CK(cudaEventCreate(&ee));
   float best[5] = {1e30f, 1e30f, 1e30f, 1e30f, 1e30f};
@@ -100,11 +102,11 @@ int main(int argc, char** argv) {
     kp::launch_crt_slice(dW, N, K, K, rW, eW, true, 0);
     CK(cudaEventRecord(ev[2]));
     g.post = o1;
-    if (!kp::launch_crt_act(g, kp::ACT_LOSS, rH, eH, rW, eW, 0)) printf("crt LOSS rejected\n");
+    if (!kp::launch_crt_act(g, kp::ACT_LOSS, rH, eH, rW, eW, 0, dcnt)) printf("crt LOSS rejected\n");
     CK(cudaEventRecord(ev[3]));
     g.post = nullptr;
     g.upart = up1;
-    if (!kp::launch_crt_act(g, kp::ACT_LAST, rH, eH, rW, eW, 0)) printf("crt LAST rejected\n");
+    if (!kp::launch_crt_act(g, kp::ACT_LAST, rH, eH, rW, eW, 0, dcnt + 1)) printf("crt LAST rejected\n");
     CK(cudaEventRecord(ev[4]));
     g.upart = nullptr;
     g.post = o2;
@@ -129,7 +131,7 @@ int main(int argc, char** argv) {
     for (int mode = 0; mode < 2; ++mode) {
       g.post = mode == 0 ? o1 : nullptr;
       g.upart = mode == 0 ? nullptr : up1;
-      kp::launch_crt_act(g, mode == 0 ? kp::ACT_LOSS : kp::ACT_LAST, rH, eH, rW, eW, 0);
+      kp::launch_crt_act(g, mode == 0 ? kp::ACT_LOSS : kp::ACT_LAST, rH, eH, rW, eW, 0, dcnt + 2);
       CK(cudaDeviceSynchronize());
       long long h[16];
       CK(cudaMemcpyFromSymbol(h, kp::crt_dbg, sizeof(h)));
