@@ -14,3 +14,6 @@ python tools/phase_timing.py --workload c5 --n-interior 16384 --reps 4 >> $OUT/p
 python tools/solve_timing.py --workload c5 --steps 2 --reps 2 > $OUT/solve_c5.jsonl 2>&1
 python tools/solve_timing.py --workload c4 --steps 2 --reps 2 > $OUT/solve_c4.jsonl 2>&1
 ls -la $OUT
+python bench.py --n-interior 3000 --no-cpu > $OUT/bench_c5_n3000.json 2>> $OUT/bench.err
+python bench.py --n-interior 65536 --no-cpu --steps 2 --warmup 3 > $OUT/bench_c5_n65536.json 2>> $OUT/bench.err
+KP_CRT=0 python bench.py --no-cpu --no-e2e > $OUT/bench_c5_n16384_crt0.json 2>> $OUT/bench.err
