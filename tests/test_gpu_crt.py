@@ -17,9 +17,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 pytestmark = pytest.mark.gpu
 
 
-def _run(tmp_path, crt, n, steps, cluster=1):
-    out = tmp_path / f"crt{crt}_{n}_{cluster}.json"
-    env = dict(os.environ, KP_CRT=str(crt), KP_CRT_CLUSTER=str(cluster))
+def _run(tmp_path, crt, n, steps, cluster=1, **switches):
+    tag = "_".join(f"{k}{v}" for k, v in sorted(switches.items()))
+    out = tmp_path / f"crt{crt}_{n}_{cluster}_{tag}.json"
+    env = dict(os.environ, KP_CRT=str(crt), KP_CRT_CLUSTER=str(cluster),
+               **{k: str(v) for k, v in switches.items()})
     subprocess.run([sys.executable, os.path.join(ROOT, "tools", "crt_check.py"), "--workload", "c5",
                     "--n-interior", str(n), "--steps", str(steps), "--out", str(out)],
                    env=env, check=True, cwd=ROOT, timeout=900)
@@ -39,3 +41,18 @@ def test_c5_linesearch_crt_matches_fp64_layers(tmp_path, n, cluster):
         assert np.array_equal(fin, np.isfinite(lb))
         worst = max(worst, float(np.max(np.abs(la[fin] - lb[fin]) / np.abs(la[fin]))))
     assert 0.0 < worst < 1e-12, worst
+
+
+def test_crt_organisations_are_bitwise_equivalent(tmp_path):
+    """The CTA organisation (independent CTAs / cta_group::2 pairs / multicast clusters), the
+    tile order (in-order queue / static striding) and the way layer 0 reaches its residue planes
+    (fused k_crt_first / FP64 state + slicing) change the schedule, never the arithmetic: the
+    line-search losses of three c5 steps are bitwise identical across all of them."""
+    ref = _run(tmp_path, 1, 1000, 3)
+    variants = [dict(cluster=2), dict(cluster=4), dict(KP_CRT_DYNAMIC=0), dict(KP_CRT_FIRST=0)]
+    for v in variants:
+        other = _run(tmp_path, 1, 1000, 3, **v)
+        for sa, sb in zip(ref["steps"], other["steps"]):
+            assert sa["code"] == sb["code"] == 0, v
+            assert sa["alpha"] == sb["alpha"], v
+            assert sa["ls"] == sb["ls"], v
