@@ -265,44 +265,54 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// Residues of four consecutive elements of one row: a = rint(x sc) read from the bits of
-// x sc + 1.5 2^52 (|a| <= 2^45), split into 15-bit pieces held exactly in FP32; per modulus
+// Residues of NE = 4 or 8 consecutive elements of one row: a = rint(x sc) read from the bits
+// of x sc + 1.5 2^52 (|a| <= 2^45), split into 15-bit pieces held exactly in FP32; per modulus
 // y = a2 c2 + a1 c1 + a0 (exact, |y| < 2^23), r = y - p rint(y / p) (exact, |r| <= p/2 + 1;
 // p = 255 folds r = 128 to -127), stored as the low byte of r + 1.5 2^23 (packed f32x2
-// arithmetic: two elements per instruction).  p = 256 is the low byte of a.
-__device__ __forceinline__ void slice4(const double (&xv)[4], double sc, int8_t* dst, int64_t ps) {
+// arithmetic: two elements per instruction; eight elements per call amortise the per-modulus
+// constants, which the compiler rematerialises per use).  p = 256 is the low byte of a.
+template <int NE>
+__device__ __forceinline__ void slice_n(const double (&xv)[NE], double sc, int8_t* dst, int64_t ps) {
+  constexpr int NP = NE / 2;
   const long long mb = __double_as_longlong(MAGIC);
-  // pieces of the four elements as two packed FP32 pairs each (f32x2 arithmetic below)
-  float f0[4], f1[4], f2[4];
-  uint32_t low[4];
-#pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    const long long a = __double_as_longlong(fma(xv[t], sc, MAGIC)) - mb;
-    const uint32_t lo = (uint32_t)a;
-    low[t] = lo;
-    f0[t] = __int_as_float(0x4B000000 | (lo & 0x7fffu));
-    f1[t] = __int_as_float(0x4B000000 | ((lo >> 15) & 0x7fffu));
-    f2[t] = __int_as_float(0x4B400000 + (int)(a >> 30));
-  }
   const uint64_t n23 = pk2(-8388608.0f, -8388608.0f), nmg = pk2(-MAGICF, -MAGICF),
                  mg = pk2(MAGICF, MAGICF);
-  uint64_t g0[2], g1[2], g2[2];
+  uint64_t g0[NP], g1[NP], g2[NP];
+  uint32_t low[NE];
 #pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    g0[u] = fadd2(pk2(f0[2 * u], f0[2 * u + 1]), n23);
-    g1[u] = fadd2(pk2(f1[2 * u], f1[2 * u + 1]), n23);
-    g2[u] = fadd2(pk2(f2[2 * u], f2[2 * u + 1]), nmg);
+  for (int u = 0; u < NP; ++u) {
+    float f0[2], f1[2], f2[2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const long long a = __double_as_longlong(fma(xv[2 * u + t], sc, MAGIC)) - mb;
+      const uint32_t lo = (uint32_t)a;
+      low[2 * u + t] = lo;
+      f0[t] = __int_as_float(0x4B000000 | (lo & 0x7fffu));
+      f1[t] = __int_as_float(0x4B000000 | ((lo >> 15) & 0x7fffu));
+      f2[t] = __int_as_float(0x4B400000 + (int)(a >> 30));
+    }
+    g0[u] = fadd2(pk2(f0[0], f0[1]), n23);
+    g1[u] = fadd2(pk2(f1[0], f1[1]), n23);
+    g2[u] = fadd2(pk2(f2[0], f2[1]), nmg);
   }
-  *reinterpret_cast<uint32_t*>(dst) = __byte_perm(__byte_perm(low[0], low[1], 0x0040),
-                                                  __byte_perm(low[2], low[3], 0x0040), 0x5410);
+  auto store = [&](int8_t* d, const uint32_t (&w)[NE]) {
+    uint32_t q[NE / 4];
+#pragma unroll
+    for (int v = 0; v < NE / 4; ++v)
+      q[v] = __byte_perm(__byte_perm(w[4 * v], w[4 * v + 1], 0x0040),
+                         __byte_perm(w[4 * v + 2], w[4 * v + 3], 0x0040), 0x5410);
+    if (NE == 8) *reinterpret_cast<uint2*>(d) = make_uint2(q[0], q[NE / 4 - 1]);
+    else *reinterpret_cast<uint32_t*>(d) = q[0];
+  };
+  store(dst, low);
 #pragma unroll
   for (int i = 1; i < NMOD; ++i) {
     const float p = (float)modulus(i), ip = 1.0f / (float)modulus(i);
     const float c1 = (float)cmod(1LL << 15, modulus(i)), c2 = (float)cmod(1LL << 30, modulus(i));
     const uint64_t c1p = pk2(c1, c1), c2p = pk2(c2, c2), ipp = pk2(ip, ip), npp = pk2(-p, -p);
-    uint32_t bb[4];
+    uint32_t bb[NE];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < NP; ++u) {
       const uint64_t y = ffma2(g2[u], c2p, ffma2(g1[u], c1p, g0[u]));
       uint64_t r = ffma2(fadd2(ffma2(y, ipp, mg), nmg), npp, y);
       if (modulus(i) == 255) {  // r = 128 does not fit a byte: 128 = -127 (mod 255)
@@ -316,9 +326,11 @@ __device__ __forceinline__ void slice4(const double (&xv)[4], double sc, int8_t*
       bb[2 * u] = (uint32_t)bq;
       bb[2 * u + 1] = (uint32_t)(bq >> 32);
     }
-    *reinterpret_cast<uint32_t*>(dst + i * ps) =
-        __byte_perm(__byte_perm(bb[0], bb[1], 0x0040), __byte_perm(bb[2], bb[3], 0x0040), 0x5410);
+    store(dst + i * ps, bb);
   }
+}
+__device__ __forceinline__ void slice4(const double (&xv)[4], double sc, int8_t* dst, int64_t ps) {
+  slice_n<4>(xv, sc, dst, ps);
 }
 
 // State rows: one warp per row, lane = 4 consecutive K entries per 128-wide chunk.  max|x| <
@@ -345,7 +357,19 @@ __global__ void __launch_bounds__(256)
   if (m > 0.0) frexp(m, &e);
   if (lane == 0) ex[row] = e;
   const double sc = pow2i(BETA - e);
-  for (int k = 4 * lane; k < K; k += 128) {
+  const int K8 = K & ~255;
+  for (int k = 8 * lane; k < K8; k += 256) {
+    double xv[8];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const double2 v = *reinterpret_cast<const double2*>(x + k + 2 * t);
+      xv[2 * t] = v.x;
+      xv[2 * t + 1] = v.y;
+    }
+    slice_n<8>(xv, sc, planes + row * (int64_t)K + k, ps);
+  }
+  if (K8 < K) {  // K = 128 (mod 256): one 128-wide chunk, four elements per lane
+    const int k = K8 + 4 * lane;
     const double2 v0 = *reinterpret_cast<const double2*>(x + k);
     const double2 v1 = *reinterpret_cast<const double2*>(x + k + 2);
     const double xv[4] = {v0.x, v0.y, v1.x, v1.y};
@@ -408,10 +432,18 @@ __global__ void __launch_bounds__(FIRST_WARPS * 32)
       const int64_t row = smp * S + i;
       if (lane == 0) ex[row] = e;
       const double sc = pow2i(BETA - e);
-      for (int k = 4 * lane; k < h1; k += 128) {
+      const int h8 = h1 & ~255;
+      for (int k = 8 * lane; k < h8; k += 256) {
+        double xa[4], xb[4];
+        load4(k, xa);
+        load4(k + 4, xb);
+        const double xv[8] = {xa[0], xa[1], xa[2], xa[3], xb[0], xb[1], xb[2], xb[3]};
+        slice_n<8>(xv, sc, planes + row * (int64_t)h1 + k, ps);
+      }
+      if (h8 < h1) {
         double xv[4];
-        load4(k, xv);
-        slice4(xv, sc, planes + row * (int64_t)h1 + k, ps);
+        load4(h8 + 4 * lane, xv);
+        slice4(xv, sc, planes + row * (int64_t)h1 + h8 + 4 * lane, ps);
       }
     }
     __syncthreads();  // sv is rewritten for the next sample
