@@ -3,8 +3,9 @@
     python tools/sass_histogram.py > profiles/r02_sass_histogram.md
 
 Disassembles paper_2405_15603_b200/libkfac_pinn_b200.so with cuobjdump -sass and counts, per
-kernel, the instructions that prove the FP64 tensor-core / TMA / cluster paths: DMMA
-(mma.sync .f64), UTMALDG (TMA tensor loads), UBLKCP (bulk copies), SYNCS (mbarrier
+kernel, the instructions that prove the FP64 tensor-core / tcgen05 / TMA / cluster paths: DMMA
+(mma.sync .f64), UTCIMMA (tcgen05.mma kind::i8), LDTM (tcgen05.ld from TMEM), UTCBAR
+(tcgen05.commit), FFMA2 (packed f32x2 FMA), UTMALDG (TMA tensor loads), UBLKCP (bulk copies), SYNCS (mbarrier
 arrive/wait), DFMA, LDGSTS (cp.async), UCGABAR (cluster barrier arrive/wait), BAR (CTA
 barrier), and the total instruction count.
 """
@@ -16,7 +17,8 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_2405_15603_b200", "libkfac_pinn_b200.so")
-OPS = ("DMMA", "UTMALDG", "UBLKCP", "SYNCS", "DFMA", "LDGSTS", "UCGABAR", "BAR")
+OPS = ("DMMA", "UTCIMMA", "LDTM", "UTMALDG", "UTCBAR", "UBLKCP", "SYNCS", "DFMA", "FFMA2", "LDGSTS",
+       "UCGABAR", "BAR")
 
 
 def demangle(names):
