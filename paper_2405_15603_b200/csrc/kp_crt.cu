@@ -544,7 +544,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   constexpr int NST = CL == 2 ? CST2 : CST;
   constexpr int STB = CL == 2 ? STAGE2_BYTES : STAGE_BYTES;
   __shared__ uint32_t tmem_base;
-  __shared__ double xs1[CM], xs2[CM], xq[CM];  // value-row s1, s2 and half-0 quadratic form
+  __shared__ double xs1[2][CM], xs2[2][CM], xq[2][CM];  // value-row s1, s2 and half-0 quadratic form (by tile parity)
   __shared__ double red[4][CN];                // ACT_LAST: per-quadrant row partials
   __shared__ double sc_s[2][CN];               // row scales 2^(e_r - BETA) of the current / next tile
   __shared__ double cw_s[CN];                  // c_i on derivative row i, 0 elsewhere
@@ -827,8 +827,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       // reconstruct y = P 2^(e_r - BETA) (z = y su, su = 2^(f_u - BETA): folded into the
       // activation's factors) in x1, branch-free (rows past S: 0).  x1 started at -C1.
       const double su = pow2i(exw[unit] - BETA);
-#pragma unroll
-      for (int j = 0; j < CPW; ++j) {
+      auto recon = [&](int j) {
         float lo, hi;
         unpk2(x2[j / 2], lo, hi);
         const double X2 = (double)((j & 1) ? hi : lo);
@@ -836,61 +835,118 @@ __global__ void __launch_bounds__(THREADS, 1)
         const double k = fma(x1[j], v_im, v_mg) - v_mg;
         const double P = fma(-k, v_m1, x1[j]) + fma(-k, v_m2, X2);
         const double y = P * sc[c0 + j];
-        x1[j] = (c0 + j < S) ? y : 0.0;
-      }
-      CRT_ACC(3, ttail);
+        return (c0 + j < S) ? y : 0.0;
+      };
       // Taylor activation (src/taylor.py:140-169): half 0 owns the value row and derivative
-      // rows 1..55, half 1 the remaining derivative rows and the operator row S - 1.
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, quad = 0.0;
-      // quadratic form over this half's derivative rows (cw = 0 on every other row), in
-      // units of su^2; the two halves' parts are summed in a fixed order (half 0 + half 1)
-#pragma unroll
-      for (int j = 0; j < CPW; ++j) quad += (x1[j] * cw_s[c0 + j]) * x1[j];
+      // rows 1..55, half 1 the remaining derivative rows and the operator row S - 1 (S > 56).
+      // Half 0 never waits: it publishes s1, s2 as soon as the value row is reconstructed
+      // (named barrier 1 + q, arrive only) and its part of the quadratic form after its rows
+      // (barrier 6 + q); half 1 needs the first for every row and the second for the operator
+      // row only.  xs1 / xs2 / xq are double-buffered by tile parity (half 0 can be at most
+      // the accumulators' depth, less than a tile, ahead of half 1).
+      const int par = (int)(tcount & 1);
+      double s0 = 0.0, s1, s2, quad = 0.0;
       if (h == 0) {
+        x1[0] = recon(0);
         const TanhD t = tanh_derivs(fma(x1[0], su, g.bias[(int64_t)unit * g.bias_stride]), false);
         s0 = t.s0;
         s1 = t.s1;
         s2 = t.s2;
-        xs1[ul] = s1;
-        xs2[ul] = s2;
-        xq[ul] = quad;
-      }
-      asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");
-      if (h == 1) {
-        s1 = xs1[ul];
-        s2 = xs2[ul];
-        quad = xq[ul] + quad;
-      }
-      asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");  // xs*/xq reusable
-      CRT_ACC(4, ttail);
-      // outputs in x1
-      const double s1u = s1 * su, s2q = s2 * (quad * (su * su));
+        xs1[par][ul] = s1;
+        xs2[par][ul] = s2;
+        asm volatile("bar.arrive %0, 64;\n" ::"r"(1 + q) : "memory");
 #pragma unroll
-      for (int j = 0; j < CPW; ++j) {
-        const double o = s1u * x1[j];
-        x1[j] = (c0 + j == S - 1) ? o + s2q : o;
+        for (int j = 1; j < CPW; ++j) x1[j] = recon(j);
+        CRT_ACC(3, ttail);
+        // quadratic form over this half's derivative rows (cw = 0 on every other row), in
+        // units of su^2; the two halves' parts are summed in a fixed order (half 0 + half 1)
+#pragma unroll
+        for (int j = 1; j < CPW; ++j) quad += (x1[j] * cw_s[c0 + j]) * x1[j];
+        xq[par][ul] = quad;
+        asm volatile("bar.arrive %0, 64;\n" ::"r"(6 + q) : "memory");
+      } else {
+#pragma unroll
+        for (int j = 0; j < CPW; ++j) x1[j] = recon(j);
+        CRT_ACC(3, ttail);
+#pragma unroll
+        for (int j = 0; j < CPW; ++j) quad += (x1[j] * cw_s[c0 + j]) * x1[j];
+        asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");
+        s1 = xs1[par][ul];
+        s2 = xs2[par][ul];
       }
+      CRT_ACC(4, ttail);
+      // outputs in x1 (the operator row's s2 term: below, once half 0's quadratic form is in)
+      const double s1u = s1 * su;
+#pragma unroll
+      for (int j = 0; j < CPW; ++j) x1[j] = s1u * x1[j];
       if (h == 0) x1[0] = s0;
+      double s2q = 0.0;
+      if (MODE == ACT_LAST && h == 1) {  // (the row reduction below needs the complete row)
+        asm volatile("bar.sync %0, 64;\n" ::"r"(6 + q) : "memory");
+        s2q = s2 * ((xq[par][ul] + quad) * (su * su));
+#pragma unroll
+        for (int j = 0; j < CPW; ++j) x1[j] = (c0 + j == S - 1) ? x1[j] + s2q : x1[j];
+      }
       CRT_ACC(5, ttail);
       if (MODE == ACT_LOSS) {
         double* out = g.post + row0 * g.ldo + unit;
 #pragma unroll
         for (int j = 0; j < CPW; ++j) {
-          const uint32_t ok = (c0 + j < S) && live;
+          const uint32_t ok = (c0 + j < S) && live && !(h == 1 && c0 + j == S - 1);
           asm volatile(
               "{\n.reg .pred p;\nsetp.ne.b32 p, %2, 0;\n@p st.global.f64 [%0], %1;\n}\n" ::"l"(
                   out + (int64_t)(c0 + j) * g.ldo),
               "d"(x1[j]), "r"(ok)
               : "memory");
         }
+        if (h == 1) {  // the operator row, with half 0's part of the quadratic form
+          asm volatile("bar.sync %0, 64;\n" ::"r"(6 + q) : "memory");
+          s2q = s2 * ((xq[par][ul] + quad) * (su * su));
+          double op = 0.0;
+#pragma unroll
+          for (int j = 0; j < CPW; ++j) op = (c0 + j == S - 1) ? x1[j] : op;
+          if (live) out[(int64_t)(S - 1) * g.ldo] = op + s2q;
+        }
       } else {  // ACT_LAST: row partials over this tile's 128 units
         const double wl = g.wlast[unit];
+        // sums over the warp's 32 units of all 56 rows by recursive halving: at distance 16
+        // a lane keeps one half of the rows and hands the other half to its partner, and so
+        // on (28, 14, 7 -> 8, 4, 2 rows: 55 exchanges instead of 56 five-step butterflies);
+        // lane l ends with rows 28 b4 + 14 b3 + 7 b2 + 4 b1 + 2 b0 + {0, 1} (b = bits of l)
+        double v[CPW];
 #pragma unroll
-        for (int j = 0; j < CPW; ++j) {
-          double v = x1[j] * wl;
+        for (int j = 0; j < CPW; ++j) v[j] = x1[j] * wl;
+        auto halve = [&](int len, int off) {  // v[0..len) -> v[0..len/2)
+          const bool up = (lane & off) != 0;
 #pragma unroll
-          for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-          if (lane == 0) red[q][c0 + j] = v;
+          for (int i = 0; i < CPW / 2; ++i) {
+            if (i < len / 2) {
+              const double send = up ? v[i] : v[i + len / 2];
+              const double keep = up ? v[i + len / 2] : v[i];
+              v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+            }
+          }
+        };
+        halve(56, 16);
+        halve(28, 8);
+        v[7] = 0.0;  // 14 -> 7 + 7: pad each half to 8 with a zero (slot 7 of the kept half)
+        {
+          const bool up = (lane & 4) != 0;
+#pragma unroll
+          for (int i = 0; i < 7; ++i) {
+            const double send = up ? v[i] : v[i + 7];
+            const double keep = up ? v[i + 7] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+          }
+          v[7] = 0.0;
+        }
+        halve(8, 2);
+        halve(4, 1);
+        {
+          const int sub = ((lane & 2) ? 4 : 0) + ((lane & 1) ? 2 : 0);  // within the 7-row group
+          const int base = ((lane & 16) ? 28 : 0) + ((lane & 8) ? 14 : 0) + ((lane & 4) ? 7 : 0) + sub;
+          if (sub < 7) red[q][c0 + base] = v[0];
+          if (sub + 1 < 7) red[q][c0 + base + 1] = v[1];
         }
         asm volatile("bar.sync 5, 256;\n" ::: "memory");
         for (int col = te; live && col < S; col += 256)
