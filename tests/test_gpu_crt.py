@@ -56,3 +56,27 @@ def test_crt_organisations_are_bitwise_equivalent(tmp_path):
             assert sa["code"] == sb["code"] == 0, v
             assert sa["alpha"] == sb["alpha"], v
             assert sa["ls"] == sb["ls"], v
+
+
+def test_c5_graph_replay_with_crt_layers_is_bit_identical():
+    """c5 KFAC steps replayed from a captured CUDA graph (the INT8 tensor-core layers, their
+    tile-counter resets and residue slicing inside the graph) equal the plain calls bit for bit."""
+    torch = pytest.importorskip("torch")
+    from paper_2405_15603_b200 import configs
+    from paper_2405_15603_b200.dist import make_rank_engine
+
+    wl = configs.WORKLOADS["c5"]
+    prob, params, batch = wl.build(0, 1000, 333)
+    runs = []
+    for graph in (False, True):
+        eng = make_rank_engine(wl.widths, batch, prob, 0, 1, ema=wl.ema, damping=wl.damping,
+                               momentum=wl.momentum)
+        eng.use_graph = graph
+        eng.load_params(params)
+        eng.init_factors(True)
+        outs = [tuple(eng.step()) for _ in range(4)]
+        runs.append((outs, eng.theta_numpy()))
+        eng.close()
+    assert runs[0][0] == runs[1][0]
+    assert np.array_equal(runs[0][1], runs[1][1])
+    torch.cuda.synchronize()
