@@ -503,7 +503,10 @@ def run_ours(args):
                        "parallelism": f"dp{world}",
                        "timed_steps": f"steps {args.warmup + 1}..{args.warmup + args.steps} of one run "
                                       "from identity factors (the warm-up steps come first)",
-                       "l2": "working set (Taylor states, GBs) far larger than the 126 MB L2"},
+                       "l2": "working set (Taylor states, GBs) far larger than the 126 MB L2",
+                       "line_search_layers": ("INT8 tensor cores, FP64 products emulated by the CRT "
+                                              "(13 moduli, 45-bit operands: within 2e-14 of sum|h w|)"
+                                              if crt_launches > 0 else "FP64 DMMA")},
             "kfac_steps_per_s": steps_per_s,
             "alg_tflops_per_s": f_step * steps_per_s / 1e12,
             "alg_frac_fp64_peak": f_step * steps_per_s / 1e12 / (FP64_DMMA_PEAK_TFLOPS * world),
