@@ -138,6 +138,17 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def crt_smem_roof(int8_tops, clk):
+    """Shared-memory traffic of k_crt_act against the 128 B/clk/SM port: every M 128 x N 112 x
+    K 32 MMA reads 4096 + 3584 B of operands and TMA writes 4096 + 3328 B (104 of the 112 rows)
+    for a later one, for 2 * 128 * 102 * 32 algorithmic int8 operations."""
+    bytes_per_op = (4096 + 3584 + 4096 + 3328) / (2.0 * 128 * 102 * 32)
+    mhz = (clk or {}).get("sm_mhz") or (clk or {}).get("sm_max_mhz") or 1965.0
+    per_clk = int8_tops * 1e12 * bytes_per_op / 148.0 / (mhz * 1e6)
+    return {"bytes_per_clk_per_sm": per_clk, "peak": 128.0, "frac": per_clk / 128.0,
+            "at_sm_mhz": mhz, "bytes_per_int8_op": bytes_per_op}
+
+
 def oracle_step_fn(optimizer):
     """The oracle's step for --optimizer (reference src/optim.py:251-263 / :266-320)."""
     from oracle import kfac_oracle as orc
@@ -471,6 +482,7 @@ def run_ours(args):
                     "traffic": ctraffic, "traffic_of": ctraffic_note,
                     "launches_per_step": crt_launches // per_step,
                     "share_of_step": crt_ms / ms_total if ms_total else None,
+                    "smem": crt_smem_roof(crt_tops, clk),
                     "limit": "shared-memory bandwidth: a 128-unit x 112-row x 32-byte MMA reads 7.5 KB of operands "
                              "while TMA writes 7.5 KB for a later one, 15 KB per 56 tensor clocks against 128 B/clk "
                              "(measured 121 clk per MMA, DESIGN.md section 5); the fold state (12 B per output) "
